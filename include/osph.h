@@ -1,0 +1,113 @@
+/*
+ * osph.h -- C ABI of libosph.so, the B200 (sm_100a) forward/inverse spherical
+ * harmonic transform on the optimal-dimensionality L^2-sample grid.
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (optisph, pure Python) has no C ABI of its own; its callers bind the Python
+ * functions re-exported from optisph/__init__.py:39-48.  Each entry point
+ * below replaces one of them:
+ *
+ *   osph_plan_create   <- the per-band-limit precomputation the reference
+ *                         caches implicitly: _packed_tables / _ring_roots_flat
+ *                         (pkg/src/optisph/transform.py:268-301) plus the grid
+ *                         co-latitudes ColatitudeGrid.thetas (sampling.py:46-79)
+ *   osph_inverse       <- inverse_sht(coeffs, grid)      (transform.py:347-357)
+ *   osph_forward       <- forward_sht(samples, grid, method, check, stats)
+ *                                                        (transform.py:360-393)
+ *   osph_stats         <- TransformStats                 (transform.py:106-112)
+ *   OSPH_ERR_*         <- BandLimitError / IllConditionedSolveError(order, kappa)
+ *                         (errors.py:8-36; raised at transform.py:134-136 and
+ *                         blocks.py:113-115)
+ *
+ * Data layouts are the reference's flat layouts, so host<->device copies are
+ * plain memcpys:
+ *   coefficients  complex128 [B][L*L], index l*l + l + m   (transform.py:41-43)
+ *   samples       complex128 [B][L*L], ring k at [k*k, (k+1)*(k+1)),
+ *                 sample j of ring k at phi_j = 2*pi*j/(2k+1)  (transform.py:87-96)
+ * Complex values are interleaved (re, im) doubles, identical to numpy complex128.
+ *
+ * Conventions: a plan is bound to one CUDA device and is used by one host
+ * thread at a time; concurrent plans are allowed.  Inputs are never modified.
+ * All calls are host-blocking (results valid on return) unless OSPH_ASYNC is
+ * set together with OSPH_DEVICE, in which case work is enqueued on the plan's
+ * stream and the caller synchronises.  Every entry point returns an OSPH_*
+ * code; osph_last_error() gives a thread-local message for the last failure.
+ */
+#ifndef OSPH_H
+#define OSPH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OSPH_ABI_VERSION 1
+
+/* return codes */
+#define OSPH_OK 0
+#define OSPH_ERR_ARG 1        /* band-limit mismatch / bad argument (BandLimitError, ValueError) */
+#define OSPH_ERR_ILLCOND 2    /* per-order block numerically singular (IllConditionedSolveError) */
+#define OSPH_ERR_CUDA 3       /* CUDA runtime failure (no device, launch error, OOM) */
+#define OSPH_ERR_NCCL 4       /* reserved for the multi-GPU order-sharded path */
+
+/* pointer kinds / flags for osph_inverse / osph_forward */
+#define OSPH_HOST 0   /* host pointers: the library copies in and out (pinned memory is fastest) */
+#define OSPH_DEVICE 1 /* device pointers on the plan's device */
+#define OSPH_ASYNC 2  /* with OSPH_DEVICE: enqueue on the plan stream and return immediately */
+
+typedef struct osph_plan osph_plan;
+
+/* Mirrors optisph.transform.TransformStats (transform.py:106-112) plus the
+ * failure payload of IllConditionedSolveError (errors.py:28-36). */
+typedef struct osph_stats {
+  double solve_seconds;   /* device time of the per-order solve stage (factor + sweep) */
+  int32_t orders;         /* number of orders processed (= L) */
+  int32_t failed_order;   /* highest order whose block failed the check, -1 if none */
+  double failed_kappa;    /* infinity-norm condition estimate of that block */
+  double factor_seconds;  /* device time of the batched per-order factorisation */
+  double sweep_seconds;   /* device time of the order-peeling sweep */
+  double total_seconds;   /* device time of the whole call */
+} osph_stats;
+
+/* Create a plan for band limit L on `device`.  thetas[L] are the ring
+ * co-latitudes (ColatitudeGrid.thetas, ring k = ring with 2k+1 samples).
+ * max_batch bounds B in later calls (workspace is sized for it). */
+int osph_plan_create(int L, const double* thetas, int max_batch, int device, osph_plan** out);
+int osph_plan_destroy(osph_plan* plan);
+
+/* Use `stream` (a cudaStream_t) for all work of this plan; NULL = plan-owned stream. */
+int osph_plan_set_stream(osph_plan* plan, void* stream);
+
+/* Band limit / batch capacity of a plan. */
+int osph_plan_info(const osph_plan* plan, int* L, int* max_batch);
+
+/* inverse_sht for B maps: flm [B][L*L] complex128 -> samples [B][L*L] complex128. */
+int osph_inverse(osph_plan* plan, int B, const void* flm, void* samples, int ptr_kind);
+
+/* forward_sht for B maps: samples [B][L*L] -> flm [B][L*L].
+ * check != 0 refuses numerically singular per-order blocks (OSPH_ERR_ILLCOND,
+ * stats->failed_order / failed_kappa filled).  stats may be NULL. */
+int osph_forward(osph_plan* plan, int B, const void* samples, void* flm, int ptr_kind, int check,
+                 osph_stats* stats);
+
+/* ring_analysis(ring_values, m) (transform.py:115-131) for one host ring of odd
+ * length n: out[0..1] = delta * sum_j v_j e^{-i m phi_j} (re, im),
+ * out[2..3] = delta * sum_j v_j e^{+i m phi_j}, delta = 2 pi / n.  Refuses
+ * |m| > (n-1)/2 (AliasingError) and even n with OSPH_ERR_ARG. */
+int osph_ring_analysis(const double* ring, int n, int m, double* out, int device);
+
+/* Number of kernel launches enqueued by the last osph_inverse/osph_forward call. */
+int osph_last_launch_count(const osph_plan* plan);
+
+/* Thread-local description of the last error (empty string if none). */
+const char* osph_last_error(void);
+
+/* ABI version (OSPH_ABI_VERSION) -- lets bindings refuse a mismatched library. */
+int osph_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OSPH_H */

@@ -1,0 +1,40 @@
+// common.cuh -- shared definitions for libosph (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define OSPH_PI 3.141592653589793238462643383279502884
+#define OSPH_TWO_PI 6.283185307179586476925286766559005768
+
+// Rescaling window of the Legendre recurrence: |mantissa| kept in
+// [2^-500, 2^500], shifts of 2^1000 (pkg/src/optisph/legendre.py:31-36).
+#define OSPH_BIG 0x1p500
+#define OSPH_TINY 0x1p-500
+#define OSPH_UP 0x1p1000
+#define OSPH_DOWN 0x1p-1000
+
+// Ring DFTs with n <= OSPH_DIRECT_MAX use a direct O(n^2) DFT; longer rings
+// use Bluestein with a power-of-two FFT of size >= 2n-1 held in shared memory.
+#define OSPH_DIRECT_MAX 63
+#define OSPH_FFT_MAX 8192  // largest in-smem FFT (complex double: 128 KB)
+
+// Position of (order m, ring/degree offset i) in order-major packed storage:
+// sum_{m'<m} (L - m') + i   (same packing as transform.py:268-291 offsets).
+__host__ __device__ __forceinline__ int64_t packed_pos(int L, int m, int i) {
+  return (int64_t)m * L - ((int64_t)m * (m - 1)) / 2 + i;
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 conj2(double2 a) { return make_double2(a.x, -a.y); }
+
+// m8n8k4 fp64 tensor-core MMA (SASS DMMA.8x8x4): D = A(8x4,row) * B(4x8,col) + C.
+// Fragment layout (lane = 4*g + t): A[g][t], B[t][g], C/D[g][2t], C/D[g][2t+1].
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}

@@ -1,0 +1,393 @@
+// plan.cu -- C ABI of libosph (include/osph.h): plan life cycle and the
+// forward / inverse transform pipelines.
+//
+//   osph_inverse = inverse_sht   (pkg/src/optisph/transform.py:347-357):
+//       pack (flm -> per-order columns) -> synth (Legendre sums, G) ->
+//       ring inverse DFTs (fold + Bluestein)
+//   osph_forward = forward_sht   (transform.py:360-467, spectral method):
+//       ring forward DFTs -> per-order factorisation (data independent) ->
+//       order-peeling sweep
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+
+#include "../../include/osph.h"
+#include "plan.cuh"
+
+static thread_local std::string g_last_error;
+
+void osph_set_error(const std::string& msg) { g_last_error = msg; }
+
+void plan_dft_layout(osph_plan* p, std::vector<int>& bluestein_rings);  // tables.cu
+
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess) {                                                                  \
+      osph_set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));                     \
+      return OSPH_ERR_CUDA;                                                                   \
+    }                                                                                         \
+  } while (0)
+
+template <typename T>
+static cudaError_t dalloc(T** ptr, size_t count) {
+  return cudaMalloc(reinterpret_cast<void**>(ptr), sizeof(T) * std::max<size_t>(count, 1));
+}
+
+template <typename T>
+static cudaError_t upload(T** ptr, const T* host, size_t count, cudaStream_t st) {
+  cudaError_t e = dalloc(ptr, count);
+  if (e != cudaSuccess) return e;
+  if (count) e = cudaMemcpyAsync(*ptr, host, sizeof(T) * count, cudaMemcpyHostToDevice, st);
+  return e;
+}
+
+static void plan_free(osph_plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  void* ptrs[] = {p->d_cos, p->d_sin, p->d_rec, p->d_ls, p->d_pstart, p->d_ring_order, p->d_fft_n,
+                  p->d_chirp_off, p->d_bhat_off, p->d_chirp, p->d_bhat, p->d_tw, p->d_roots,
+                  p->d_bluestein_rings, p->d_ainv_off, p->d_pb_off, p->d_ainv, p->d_pbelow, p->d_piv,
+                  p->d_norms, p->d_kappa, p->d_status, p->d_fpack, p->d_g, p->d_r, p->d_x, p->d_in,
+                  p->d_out};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  for (cudaEvent_t& e : p->ev)
+    if (e) cudaEventDestroy(e);
+  if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+}
+
+extern "C" int osph_abi_version(void) { return OSPH_ABI_VERSION; }
+
+extern "C" const char* osph_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int osph_plan_create(int L, const double* thetas, int max_batch, int device, osph_plan** out) {
+  g_last_error.clear();
+  if (!out) {
+    osph_set_error("osph_plan_create: out is NULL");
+    return OSPH_ERR_ARG;
+  }
+  *out = nullptr;
+  if (L < 1 || L > 4096) {
+    osph_set_error("band limit must be in [1, 4096], got " + std::to_string(L));
+    return OSPH_ERR_ARG;
+  }
+  if (max_batch < 1) {
+    osph_set_error("max_batch must be positive");
+    return OSPH_ERR_ARG;
+  }
+  if (!thetas) {
+    osph_set_error("thetas is NULL");
+    return OSPH_ERR_ARG;
+  }
+  for (int k = 0; k < L; ++k) {
+    if (!(thetas[k] > 0.0 && thetas[k] <= OSPH_PI)) {  // ColatitudeGrid invariant (sampling.py:69-70)
+      osph_set_error("co-latitudes must lie in (0, pi]");
+      return OSPH_ERR_ARG;
+    }
+  }
+  int ndev = 0;
+  cudaError_t e0 = cudaGetDeviceCount(&ndev);
+  if (e0 != cudaSuccess || ndev == 0) {
+    osph_set_error(std::string("no CUDA device available: ") + cudaGetErrorString(e0));
+    return OSPH_ERR_CUDA;
+  }
+  if (device < 0 || device >= ndev) {
+    osph_set_error("device ordinal out of range");
+    return OSPH_ERR_ARG;
+  }
+  osph_plan* p = new osph_plan();
+  p->L = L;
+  p->device = device;
+  p->max_batch = max_batch;
+  auto fail = [&](int code) {
+    plan_free(p);
+    return code;
+  };
+#define PLAN_TRY(expr)                                                    \
+  do {                                                                    \
+    cudaError_t _e = (expr);                                              \
+    if (_e != cudaSuccess) {                                              \
+      osph_set_error(std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+      return fail(OSPH_ERR_CUDA);                                         \
+    }                                                                     \
+  } while (0)
+  PLAN_TRY(cudaSetDevice(device));
+  PLAN_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+  p->own_stream = true;
+  for (cudaEvent_t& e : p->ev) PLAN_TRY(cudaEventCreate(&e));
+  cudaStream_t st = p->stream;
+
+  std::vector<double> c(L), s(L);
+  for (int k = 0; k < L; ++k) {
+    c[k] = std::cos(thetas[k]);
+    s[k] = std::sin(thetas[k]);
+  }
+  PLAN_TRY(upload(&p->d_cos, c.data(), L, st));
+  PLAN_TRY(upload(&p->d_sin, s.data(), L, st));
+  std::vector<int> order(L);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return s[a] < s[b]; });
+  PLAN_TRY(upload(&p->d_ring_order, order.data(), L, st));
+  const size_t npacked = (size_t)L * (L + 1) / 2;
+  PLAN_TRY(dalloc(&p->d_rec, npacked));
+  PLAN_TRY(dalloc(&p->d_ls, (size_t)L * L));
+  PLAN_TRY(dalloc(&p->d_pstart, (size_t)L * L));
+
+  std::vector<int> brings;
+  plan_dft_layout(p, brings);
+  PLAN_TRY(upload(&p->d_fft_n, p->h_fft_n.data(), L, st));
+  PLAN_TRY(upload(&p->d_chirp_off, p->h_chirp_off.data(), L, st));
+  PLAN_TRY(upload(&p->d_bhat_off, p->h_bhat_off.data(), L, st));
+  PLAN_TRY(upload(&p->d_bluestein_rings, brings.data(), brings.size(), st));
+  PLAN_TRY(dalloc(&p->d_chirp, (size_t)p->h_chirp_off[L]));
+  PLAN_TRY(dalloc(&p->d_bhat, (size_t)p->h_bhat_off[L]));
+  PLAN_TRY(dalloc(&p->d_tw, 8192));
+  PLAN_TRY(dalloc(&p->d_roots, (size_t)(OSPH_DIRECT_MAX + 1) * (OSPH_DIRECT_MAX + 1) / 4 + 64));
+  for (int k = 0; k < L; ++k) {
+    if (p->h_fft_n[k] > OSPH_FFT_MAX) {
+      osph_set_error("ring DFT length exceeds the in-shared-memory FFT (L > 2048 not supported yet)");
+      return fail(OSPH_ERR_ARG);
+    }
+  }
+  PLAN_TRY(launch_tables(p));
+  PLAN_TRY(cudaStreamSynchronize(st));
+  *out = p;
+  return OSPH_OK;
+#undef PLAN_TRY
+}
+
+extern "C" int osph_plan_destroy(osph_plan* plan) {
+  plan_free(plan);
+  return OSPH_OK;
+}
+
+extern "C" int osph_plan_set_stream(osph_plan* p, void* stream) {
+  if (!p) {
+    osph_set_error("plan is NULL");
+    return OSPH_ERR_ARG;
+  }
+  CUDA_TRY(cudaSetDevice(p->device));
+  if (!stream && p->own_stream) return OSPH_OK;  // already on a plan-owned stream
+  if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+  p->own_stream = false;
+  p->stream = (cudaStream_t)stream;
+  if (!stream) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    p->own_stream = true;
+  }
+  return OSPH_OK;
+}
+
+extern "C" int osph_plan_info(const osph_plan* p, int* L, int* max_batch) {
+  if (!p) {
+    osph_set_error("plan is NULL");
+    return OSPH_ERR_ARG;
+  }
+  if (L) *L = p->L;
+  if (max_batch) *max_batch = p->max_batch;
+  return OSPH_OK;
+}
+
+extern "C" int osph_last_launch_count(const osph_plan* p) { return p ? p->launches : 0; }
+
+static int ensure_io(osph_plan* p) {
+  if (p->d_in) return OSPH_OK;
+  const size_t n = (size_t)p->max_batch * p->L * p->L;
+  CUDA_TRY(dalloc(&p->d_in, n));
+  CUDA_TRY(dalloc(&p->d_out, n));
+  return OSPH_OK;
+}
+
+static int ensure_inverse(osph_plan* p) {
+  if (p->inv_ready) return OSPH_OK;
+  const int L = p->L;
+  const size_t B = p->max_batch;
+  CUDA_TRY(dalloc(&p->d_fpack, (size_t)L * (L + 1) / 2 * 4 * B));
+  CUDA_TRY(dalloc(&p->d_g, (size_t)L * L * 4 * B));
+  p->inv_ready = true;
+  return OSPH_OK;
+}
+
+static int ensure_forward(osph_plan* p) {
+  if (p->fwd_ready) return OSPH_OK;
+  const int L = p->L;
+  if (L > 2048) {
+    osph_set_error("forward transform supports L <= 2048 in this build");
+    return OSPH_ERR_ARG;
+  }
+  const size_t B = p->max_batch;
+  p->h_ainv_off.assign(L + 1, 0);
+  p->h_pb_off.assign(L + 1, 0);
+  for (int m = 0; m < L; ++m) {
+    const int64_t n = L - m;
+    p->h_ainv_off[m + 1] = p->h_ainv_off[m] + n * n;
+    p->h_pb_off[m + 1] = p->h_pb_off[m] + n * m;
+  }
+  cudaStream_t st = p->stream;
+  CUDA_TRY(upload(&p->d_ainv_off, p->h_ainv_off.data(), L + 1, st));
+  CUDA_TRY(upload(&p->d_pb_off, p->h_pb_off.data(), L + 1, st));
+  CUDA_TRY(dalloc(&p->d_ainv, (size_t)p->h_ainv_off[L]));
+  CUDA_TRY(dalloc(&p->d_pbelow, (size_t)p->h_pb_off[L]));
+  CUDA_TRY(dalloc(&p->d_piv, (size_t)L * (L + 1) / 2));
+  CUDA_TRY(dalloc(&p->d_norms, (size_t)2 * L));
+  CUDA_TRY(dalloc(&p->d_kappa, (size_t)L));
+  CUDA_TRY(dalloc(&p->d_status, (size_t)L));
+  CUDA_TRY(dalloc(&p->d_r, (size_t)L * (L + 1) * B));
+  CUDA_TRY(dalloc(&p->d_x, (size_t)(B + 3) * 4 * L));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  p->fwd_ready = true;
+  return OSPH_OK;
+}
+
+static int check_call(osph_plan* p, int B, const void* a, void* b, int kind) {
+  if (!p) {
+    osph_set_error("plan is NULL");
+    return OSPH_ERR_ARG;
+  }
+  if (B < 1 || B > p->max_batch) {
+    osph_set_error("batch " + std::to_string(B) + " outside [1, max_batch=" + std::to_string(p->max_batch) + "]");
+    return OSPH_ERR_ARG;
+  }
+  if (!a || !b) {
+    osph_set_error("NULL data pointer");
+    return OSPH_ERR_ARG;
+  }
+  if (kind & ~(OSPH_DEVICE | OSPH_ASYNC)) {
+    osph_set_error("unknown ptr_kind flags");
+    return OSPH_ERR_ARG;
+  }
+  if ((kind & OSPH_ASYNC) && !(kind & OSPH_DEVICE)) {
+    osph_set_error("OSPH_ASYNC requires OSPH_DEVICE pointers");
+    return OSPH_ERR_ARG;
+  }
+  return OSPH_OK;
+}
+
+extern "C" int osph_inverse(osph_plan* p, int B, const void* flm, void* samples, int kind) {
+  g_last_error.clear();
+  int rc = check_call(p, B, flm, samples, kind);
+  if (rc) return rc;
+  CUDA_TRY(cudaSetDevice(p->device));
+  if ((rc = ensure_inverse(p))) return rc;
+  const bool host = !(kind & OSPH_DEVICE);
+  if (host && (rc = ensure_io(p))) return rc;
+  const size_t bytes = sizeof(double2) * (size_t)B * p->L * p->L;
+  cudaStream_t st = p->stream;
+  p->launches = 0;
+  const double2* in = (const double2*)flm;
+  double2* out = (double2*)samples;
+  if (host) {
+    CUDA_TRY(cudaMemcpyAsync(p->d_in, flm, bytes, cudaMemcpyHostToDevice, st));
+    in = p->d_in;
+    out = p->d_out;
+  }
+  CUDA_TRY(launch_pack(p, B, in));
+  CUDA_TRY(launch_synth(p, B));
+  CUDA_TRY(launch_ring_inverse(p, B, out));
+  if (host) CUDA_TRY(cudaMemcpyAsync(samples, p->d_out, bytes, cudaMemcpyDeviceToHost, st));
+  if (!(kind & OSPH_ASYNC)) CUDA_TRY(cudaStreamSynchronize(st));
+  return OSPH_OK;
+}
+
+extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm, int kind, int check,
+                            osph_stats* stats) {
+  g_last_error.clear();
+  int rc = check_call(p, B, samples, flm, kind);
+  if (rc) return rc;
+  if ((kind & OSPH_ASYNC) && check) {
+    osph_set_error("check=1 needs a host-blocking call (drop OSPH_ASYNC or pass check=0)");
+    return OSPH_ERR_ARG;
+  }
+  CUDA_TRY(cudaSetDevice(p->device));
+  if ((rc = ensure_forward(p))) return rc;
+  const bool host = !(kind & OSPH_DEVICE);
+  if (host && (rc = ensure_io(p))) return rc;
+  const int L = p->L;
+  const size_t bytes = sizeof(double2) * (size_t)B * L * L;
+  cudaStream_t st = p->stream;
+  p->launches = 0;
+  const double2* in = (const double2*)samples;
+  double2* out = (double2*)flm;
+  if (host) {
+    CUDA_TRY(cudaMemcpyAsync(p->d_in, samples, bytes, cudaMemcpyHostToDevice, st));
+    in = p->d_in;
+    out = p->d_out;
+  }
+  CUDA_TRY(cudaEventRecord(p->ev[0], st));
+  CUDA_TRY(launch_ring_forward(p, B, in));
+  CUDA_TRY(cudaEventRecord(p->ev[1], st));
+  CUDA_TRY(launch_factor(p));
+  CUDA_TRY(cudaEventRecord(p->ev[2], st));
+  CUDA_TRY(launch_sweep(p, B, out));
+  CUDA_TRY(cudaEventRecord(p->ev[3], st));
+  if (host) CUDA_TRY(cudaMemcpyAsync(flm, p->d_out, bytes, cudaMemcpyDeviceToHost, st));
+  if (kind & OSPH_ASYNC) return OSPH_OK;
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (stats) {
+    float t01 = 0, t12 = 0, t23 = 0;
+    cudaEventElapsedTime(&t01, p->ev[0], p->ev[1]);
+    cudaEventElapsedTime(&t12, p->ev[1], p->ev[2]);
+    cudaEventElapsedTime(&t23, p->ev[2], p->ev[3]);
+    stats->factor_seconds = t12 * 1e-3;
+    stats->sweep_seconds = t23 * 1e-3;
+    stats->solve_seconds = (t12 + t23) * 1e-3;
+    stats->total_seconds = (t01 + t12 + t23) * 1e-3;
+    stats->orders = L;
+    stats->failed_order = -1;
+    stats->failed_kappa = 0.0;
+  }
+  if (check) {
+    std::vector<double> kappa(L);
+    std::vector<int> status(L);
+    CUDA_TRY(cudaMemcpy(kappa.data(), p->d_kappa, sizeof(double) * L, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(status.data(), p->d_status, sizeof(int) * L, cudaMemcpyDeviceToHost));
+    for (int m = L - 1; m >= 0; --m) {  // the reference raises at the first failing order of its sweep
+      if (status[m] || !(kappa[m] <= 2.0e14)) {
+        if (stats) {
+          stats->failed_order = m;
+          stats->failed_kappa = status[m] ? INFINITY : kappa[m];
+        }
+        char buf[160];
+        snprintf(buf, sizeof buf, "order %d system is numerically singular (condition number %.3e)", m,
+                 status[m] ? INFINITY : kappa[m]);
+        osph_set_error(buf);
+        return OSPH_ERR_ILLCOND;
+      }
+    }
+  }
+  return OSPH_OK;
+}
+
+extern "C" int osph_ring_analysis(const double* ring, int n, int m, double* out, int device) {
+  g_last_error.clear();
+  if (!ring || !out) {
+    osph_set_error("NULL pointer");
+    return OSPH_ERR_ARG;
+  }
+  if (n < 1 || n % 2 == 0) {
+    osph_set_error("ring length must be odd, got " + std::to_string(n));
+    return OSPH_ERR_ARG;
+  }
+  const int k = (n - 1) / 2;
+  if (m > k || -m > k) {
+    osph_set_error("frequency " + std::to_string(m) + " is not resolvable on a ring of index " + std::to_string(k));
+    return OSPH_ERR_ARG;
+  }
+  CUDA_TRY(cudaSetDevice(device));
+  double2* d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, sizeof(double2) * (n + 2)));
+  cudaError_t e = cudaMemcpy(d, ring, sizeof(double2) * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = launch_ring_pair(n, m, d, d + n, 0);
+  if (e == cudaSuccess) e = cudaMemcpy(out, d + n, sizeof(double2) * 2, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) {
+    osph_set_error(std::string("ring analysis: ") + cudaGetErrorString(e));
+    return OSPH_ERR_CUDA;
+  }
+  return OSPH_OK;
+}

@@ -1,0 +1,75 @@
+// plan.cuh -- internal plan object and kernel launchers of libosph.
+#pragma once
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+struct osph_plan {
+  int L = 0;
+  int device = 0;
+  int max_batch = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int launches = 0;  // kernels enqueued by the last transform call
+
+  // ---- grid + recurrence tables (O(L^2), built once per plan) ----
+  double* d_cos = nullptr;  // [L] cos(theta_k)
+  double* d_sin = nullptr;  // [L] sin(theta_k)
+  double2* d_rec = nullptr;   // packed (m, l): {a_lm, 1/a_(l+1)m}
+  int* d_ls = nullptr;        // [m][k] first degree whose value is in the double range
+  double2* d_pstart = nullptr;  // [m][k] {P_(ls-1)m, P_(ls)m} (true values)
+  int* d_ring_order = nullptr;  // [L] rings sorted by sin(theta), for warp-coherent skipping
+
+  // ---- ring DFT tables ----
+  std::vector<int> h_fft_n;          // [L] Bluestein FFT size per ring (0 = direct DFT)
+  std::vector<int64_t> h_chirp_off;  // [L] offset of chirp table (n entries)
+  std::vector<int64_t> h_bhat_off;   // [L] offset of FFT(kernel) tables (2N entries: fwd, inv)
+  int* d_fft_n = nullptr;
+  int64_t* d_chirp_off = nullptr;
+  int64_t* d_bhat_off = nullptr;
+  double2* d_chirp = nullptr;  // e^{i pi t^2 / n}
+  double2* d_bhat = nullptr;   // FFT_N of the conjugate chirp kernel (per direction, / N)
+  double2* d_tw = nullptr;     // e^{-2 pi i j / OSPH_FFT_MAX}, j < OSPH_FFT_MAX/2
+  double2* d_roots = nullptr;  // small rings: e^{2 pi i r / n} at k*k + r (k*k < direct limit)
+  int n_bluestein_rings = 0;
+  int* d_bluestein_rings = nullptr;  // ring ids that use Bluestein, largest first
+  int n_direct_rings = 0;
+
+  // ---- forward factor storage (per call, data independent) ----
+  std::vector<int64_t> h_ainv_off;  // [L+1] offset of order m's n x n inverse
+  std::vector<int64_t> h_pb_off;    // [L+1] offset of order m's (m x n) below-block
+  int64_t* d_ainv_off = nullptr;
+  int64_t* d_pb_off = nullptr;
+  double* d_ainv = nullptr;
+  double* d_pbelow = nullptr;
+  int* d_piv = nullptr;          // [pos(m, j)] row permutation of order m's inverse
+  unsigned long long* d_norms = nullptr;  // [2L] ||A_m||_1, ||A_m^-1||_1 (as ordered bits)
+  double* d_kappa = nullptr;     // [L] 1-norm condition estimate per order
+  int* d_status = nullptr;       // [L] 0 ok, 1 zero/non-finite pivot
+  bool fwd_ready = false;        // forward buffers allocated
+  bool inv_ready = false;        // inverse buffers allocated
+
+  // ---- per-call workspaces (sized for max_batch) ----
+  double* d_fpack = nullptr;  // inverse: packed coefficients [pos(m,l)][4B]
+  double* d_g = nullptr;      // inverse: G [m][k][4B]
+  double2* d_r = nullptr;     // forward: order-major ring spectra [pos(m,k-m)][2][B]
+  double* d_x = nullptr;      // forward sweep scratch
+  double2* d_in = nullptr;    // device staging of host inputs  [B][L^2]
+  double2* d_out = nullptr;   // device staging of host outputs [B][L^2]
+
+  cudaEvent_t ev[6] = {};
+};
+
+// last-error plumbing (plan.cu)
+void osph_set_error(const std::string& msg);
+
+// ---- launchers (each returns cudaError_t of the launch) ----
+cudaError_t launch_tables(osph_plan* p);                                   // tables.cu
+cudaError_t launch_ring_inverse(osph_plan* p, int B, double2* samples);    // ringdft.cu
+cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples);  // ringdft.cu
+cudaError_t launch_pack(osph_plan* p, int B, const double2* flm);          // synth.cu
+cudaError_t launch_synth(osph_plan* p, int B);                             // synth.cu
+cudaError_t launch_factor(osph_plan* p);                                   // factor.cu
+cudaError_t launch_sweep(osph_plan* p, int B, double2* flm);               // sweep.cu
+cudaError_t launch_ring_pair(int n, int m, const double2* v, double2* out, cudaStream_t st);  // ringdft.cu

@@ -1,0 +1,246 @@
+// synth.cu -- inverse Legendre synthesis G_(+-m)(theta_k) = sum_l P_lm(theta_k) f_l(+-m).
+//
+// Reference: _synthesis_g / _g_accumulate (pkg/src/optisph/transform.py:143-201,
+// 310-331): for every ring i and order m the recurrence of
+// legendre.py:64-96 is fused with a four-stream dot product
+// [Re f_m, Im f_m, Re f_-m, Im f_-m].  Here the 4 streams of all B maps form
+// the C = 4B columns of a per-order product
+//     G_m[k][c] = sum_l P_m[k][l] * F_m[l][c]
+// with P_m generated on the fly by the upward recurrence (never stored) and
+// started at the precomputed first in-range degree ls(m,k) (tables.cu), so
+// the hot loops carry no rescaling branches.  2*pi and (-1)^m are applied by
+// the ring kernels.  Two kernels:
+//   * k_synth_fma  (C <= 8): one thread per (ring, order), FMA pipe;
+//   * k_synth_dmma (C >= 16): 64x64 output tiles on fp64 tensor cores
+//     (mma.sync m8n8k4 -> SASS DMMA.8x8x4); P tiles generated into shared
+//     memory by two warps while the others stage F.
+#include "plan.cuh"
+
+// flm [B][L^2] complex -> F [pos(m, l-m)][4B] doubles:
+// c = 4b + {0: Re f_lm, 1: Im f_lm, 2: Re f_l,-m, 3: Im f_l,-m}.
+__global__ void k_pack(int L, int B, const double2* __restrict__ flm, double* __restrict__ F) {
+  const int m = blockIdx.y;
+  const int n = L - m;
+  const int64_t total = (int64_t)n * B;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(t % B);
+    const int i = (int)(t / B);
+    const int64_t l = m + i;
+    const double2* f = flm + (int64_t)b * L * L + l * l + l;
+    const double2 fp = __ldg(f + m);
+    const double2 fn = __ldg(f - m);
+    double4* dst = reinterpret_cast<double4*>(F + (packed_pos(L, m, i) * B + b) * 4);
+    *dst = make_double4(fp.x, fp.y, fn.x, fn.y);
+  }
+}
+
+cudaError_t launch_pack(osph_plan* p, int B, const double2* flm) {
+  const int L = p->L;
+  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(((int64_t)L * B + 255) / 256, 64)), L);
+  k_pack<<<grid, 256, 0, p->stream>>>(L, B, flm, p->d_fpack);
+  p->launches++;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// FMA path: C <= 8 columns (B <= 2 maps).
+
+#define SYN_FMA_THREADS 128
+#define SYN_FMA_CHUNK 256
+
+template <int C>
+__global__ void __launch_bounds__(SYN_FMA_THREADS) k_synth_fma(
+    int L, const double* __restrict__ costh, const double2* __restrict__ rec, const int* __restrict__ ls_tab,
+    const double2* __restrict__ pstart, const int* __restrict__ ring_order, const double* __restrict__ F,
+    double* __restrict__ G) {
+  __shared__ double Fs[SYN_FMA_CHUNK * C];
+  __shared__ double2 Rs[SYN_FMA_CHUNK];
+  const int m = blockIdx.y;
+  const int idx = blockIdx.x * SYN_FMA_THREADS + threadIdx.x;
+  const bool active = idx < L;
+  const int k = active ? ring_order[idx] : 0;
+  const int64_t t = (int64_t)m * L + k;
+  int ls = active ? ls_tab[t] : L;
+  double2 pp = active ? pstart[t] : make_double2(0.0, 0.0);
+  double p0 = pp.x, p1 = pp.y;
+  const double x = costh[k];
+  double acc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) acc[c] = 0.0;
+  // block-wide first useful degree
+  int lmin = ls;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lmin = min(lmin, __shfl_xor_sync(0xffffffffu, lmin, o));
+  __shared__ int wmin[SYN_FMA_THREADS / 32];
+  if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = lmin;
+  __syncthreads();
+  lmin = wmin[0];
+  for (int w = 1; w < SYN_FMA_THREADS / 32; ++w) lmin = min(lmin, wmin[w]);
+  const double* Fm = F + packed_pos(L, m, 0) * C;
+  const double2* recm = rec + packed_pos(L, m, 0);
+  for (int cs = lmin; cs < L; cs += SYN_FMA_CHUNK) {
+    const int ce = min(L, cs + SYN_FMA_CHUNK);
+    __syncthreads();
+    for (int i = threadIdx.x; i < (ce - cs) * C; i += SYN_FMA_THREADS) Fs[i] = __ldg(Fm + (int64_t)(cs - m) * C + i);
+    for (int i = threadIdx.x; i < ce - cs; i += SYN_FMA_THREADS) Rs[i] = __ldg(recm + (cs - m) + i);
+    __syncthreads();
+    for (int l = max(cs, ls); l < ce; ++l) {
+      const int j = l - cs;
+#pragma unroll
+      for (int c = 0; c < C; ++c) acc[c] = fma(p1, Fs[j * C + c], acc[c]);
+      const double2 ar = Rs[j];
+      const double nxt = fma(x, p1, -ar.x * p0) * ar.y;
+      p0 = p1;
+      p1 = nxt;
+    }
+  }
+  if (active) {
+    double* g = G + ((int64_t)m * L + k) * C;
+#pragma unroll
+    for (int c = 0; c < C; ++c) g[c] = acc[c];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// DMMA path: C >= 16.  Block tile 64 rings x 64 columns, K chunks of 16 degrees.
+
+#define SYN_TM 64
+#define SYN_TN 64
+#define SYN_TK 16
+#define SYN_THREADS 256
+#define SYN_PAD 8
+
+__global__ void __launch_bounds__(SYN_THREADS, 2) k_synth_dmma(
+    int L, int C, const double* __restrict__ costh, const double2* __restrict__ rec,
+    const int* __restrict__ ls_tab, const double2* __restrict__ pstart, const int* __restrict__ ring_order,
+    const double* __restrict__ F, double* __restrict__ G) {
+  __shared__ __align__(16) double Ps[2][SYN_TK][SYN_TM + SYN_PAD];
+  __shared__ __align__(16) double Fs[2][SYN_TK][SYN_TN + SYN_PAD];
+  __shared__ int s_lmin[2];
+  const int m = blockIdx.z;
+  const int row0 = blockIdx.y * SYN_TM;
+  const int col0 = blockIdx.x * SYN_TN;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tq = lane & 3;
+
+  // generator state: threads 0..63 own one ring each
+  int ls = L, kring = 0;
+  double p0 = 0.0, p1 = 0.0, x = 0.0;
+  if (tid < SYN_TM) {
+    const int r = row0 + tid;
+    if (r < L) {
+      kring = ring_order[r];
+      const int64_t t = (int64_t)m * L + kring;
+      ls = ls_tab[t];
+      const double2 pp = pstart[t];
+      p0 = pp.x;
+      p1 = pp.y;
+      x = costh[kring];
+    }
+  }
+  if (tid < 2) s_lmin[tid] = L;
+  __syncthreads();
+  if (tid < SYN_TM) atomicMin(&s_lmin[0], ls);
+  __syncthreads();
+  const int lstart = s_lmin[0];
+  // chunk grid aligned to m so F loads stay aligned to the packed order start
+  const int kfirst = m + ((lstart - m) / SYN_TK) * SYN_TK;
+  const double* Fm = F + packed_pos(L, m, 0) * (int64_t)C;
+  const double2* recm = rec + packed_pos(L, m, 0);
+
+  // warp tile: 16 rows x 32 cols -> 2 x 4 m8n8 tiles
+  const int wr = (warp & 3) * 16;
+  const int wc = (warp >> 2) * 32;
+  double acc[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto produce = [&](int buf, int ks) {
+    if (tid < SYN_TM) {
+      for (int j = 0; j < SYN_TK; ++j) {
+        const int l = ks + j;
+        double v = 0.0;
+        if (l < L && l >= ls) {
+          v = p1;
+          const double2 ar = __ldg(recm + (l - m));
+          const double nxt = fma(x, p1, -ar.x * p0) * ar.y;
+          p0 = p1;
+          p1 = nxt;
+        }
+        Ps[buf][j][tid] = v;
+      }
+    } else {
+      for (int i = tid - SYN_TM; i < SYN_TK * SYN_TN / 2; i += SYN_THREADS - SYN_TM) {
+        const int j = i / (SYN_TN / 2);
+        const int c2 = (i % (SYN_TN / 2)) * 2;
+        const int l = ks + j;
+        const int c = col0 + c2;
+        double2 v = make_double2(0.0, 0.0);
+        if (l < L) {
+          const double* src = Fm + (int64_t)(l - m) * C + c;
+          if (c + 1 < C) v = __ldg(reinterpret_cast<const double2*>(src));
+          else if (c < C) v.x = __ldg(src);
+        }
+        *reinterpret_cast<double2*>(&Fs[buf][j][c2]) = v;
+      }
+    }
+  };
+
+  int buf = 0;
+  if (kfirst < L) produce(0, kfirst);
+  __syncthreads();
+  for (int ks = kfirst; ks < L; ks += SYN_TK) {
+    if (ks + SYN_TK < L) produce(buf ^ 1, ks + SYN_TK);
+#pragma unroll
+    for (int kk = 0; kk < SYN_TK; kk += 4) {
+      double a[2], b[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) a[i] = Ps[buf][kk + tq][wr + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Fs[buf][kk + tq][wc + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+  // store: C fragment rows = ring positions, cols = 2tq, 2tq+1
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = row0 + wr + i * 8 + g;
+    if (r >= L) continue;
+    const int k = ring_order[r];
+    double* grow = G + ((int64_t)m * L + k) * C;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = col0 + wc + j * 8 + 2 * tq;
+      if (c + 1 < C) *reinterpret_cast<double2*>(grow + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+      else if (c < C) grow[c] = acc[i][j][0];
+    }
+  }
+}
+
+cudaError_t launch_synth(osph_plan* p, int B) {
+  const int L = p->L;
+  const int C = 4 * B;
+  if (C <= 8) {
+    dim3 grid((L + SYN_FMA_THREADS - 1) / SYN_FMA_THREADS, L);
+    if (C == 4)
+      k_synth_fma<4><<<grid, SYN_FMA_THREADS, 0, p->stream>>>(L, p->d_cos, p->d_rec, p->d_ls, p->d_pstart,
+                                                            p->d_ring_order, p->d_fpack, p->d_g);
+    else
+      k_synth_fma<8><<<grid, SYN_FMA_THREADS, 0, p->stream>>>(L, p->d_cos, p->d_rec, p->d_ls, p->d_pstart,
+                                                            p->d_ring_order, p->d_fpack, p->d_g);
+  } else {
+    dim3 grid((C + SYN_TN - 1) / SYN_TN, (L + SYN_TM - 1) / SYN_TM, L);
+    k_synth_dmma<<<grid, SYN_THREADS, 0, p->stream>>>(L, C, p->d_cos, p->d_rec, p->d_ls, p->d_pstart,
+                                                     p->d_ring_order, p->d_fpack, p->d_g);
+  }
+  p->launches++;
+  return cudaGetLastError();
+}
