@@ -1,0 +1,378 @@
+"""Benchmark: fwd+inv SHT transforms/s (fp64) on the L^2-sample grid.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+Metric (BASELINE.json): forward+inverse transforms per second, whole job.  One
+"transform" = one map taken through inverse_sht then forward_sht (a round
+trip); a step = one inverse + one forward over a batch of B maps.  Default
+workload = BASELINE configs[1]: L=256, B=64 complex fp64 maps, flm ~ complex
+N(0,1) * sqrt(C_l), C_l = 1/(l(l+1)), C_0 = 1, on the reference's
+condition-minimised L=256 grid.  Inputs are seeded synthetic data of that
+shape/distribution (no dataset exists for this path).
+
+Multi-GPU (N > 1, torchrun): maps are independent, so every rank runs its own
+batch of B maps ("scaling": "weak"); no collective on the data path.  Timing
+is CUDA events on the launching stream, max over ranks.
+
+--impl reference times the CPU implementation of the same path: the oracle
+port of the reference (oracle/, C + numpy/scipy exactly as optisph does it) on
+the box's host cores, a bounded sample of maps per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "fwd+inv SHT transforms/s (fp64)"
+UNIT = "transforms/s"
+FP64_PEAK_TFLOPS = 37.15  # measured DMMA.8x8x4 issue rate on this pool's B200 (profiles/fp64_peak_r01.txt)
+
+CONFIGS = {
+    1: dict(L=64, B=1, spectrum="white", real=False, grid="grid-L64-uniform-condmin.txt"),
+    2: dict(L=256, B=64, spectrum="cmb", real=False, grid="grid-L256-uniform-condmin.txt"),
+    3: dict(L=512, B=256, spectrum="cmb", real=True, grid="grid-L512-uniform-condmin.txt"),
+}
+
+
+def make_coefficients(L: int, B: int, seed: int, spectrum: str, real: bool) -> np.ndarray:
+    """BASELINE recipes: per map Re[L^2] then Im[L^2] ~ N(0,1), l^2+l+m order."""
+    rng = np.random.default_rng(seed)
+    n = L * L
+    ells = np.floor(np.sqrt(np.arange(n))).astype(np.int64)
+    ms = np.arange(n) - ells * ells - ells
+    out = np.empty((B, n), dtype=np.complex128)
+    for b in range(B):
+        f = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        if real:
+            f[ms == 0] = f[ms == 0].real
+            neg = np.nonzero(ms < 0)[0]
+            pos = ells[neg] ** 2 + ells[neg] - ms[neg]
+            sgn = np.where((-ms[neg]) % 2 == 1, -1.0, 1.0)
+            f[neg] = sgn * np.conj(f[pos])
+        if spectrum == "cmb":
+            cl = np.ones(n)
+            nz = ells >= 1
+            cl[nz] = 1.0 / (ells[nz] * (ells[nz] + 1.0))
+            f = f * np.sqrt(cl)
+        out[b] = f
+    return out
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work, used for the roofline fields
+
+
+def flops(L: int, B: int) -> dict:
+    """Dense algorithmic fp64 flop counts per step (complex-map count)."""
+    ring_fft = sum(5.0 * (2 * k + 1) * np.log2(2 * k + 1) for k in range(1, L))
+    f_inv = 4.0 * B * L**3 + 1.5 * L**3 + B * ring_fft
+    f_lu = sum((2.0 / 3.0) * n**3 for n in range(1, L + 1))
+    f_fwd = f_lu + (8.0 / 3.0) * B * L**3 + (4.0 / 3.0) * B * L**3 + 1.5 * L**3 + B * ring_fft
+    return {
+        "inverse": f_inv,
+        "forward": f_fwd,
+        "synth": 8.0 * B * L * L * (L + 1) / 2.0,  # Legendre GEMM: 2 flops x 4B columns per (k, m, l)
+        "factor_gj": sum(2.0 * n**3 for n in range(1, L + 1)),  # explicit inverse per order
+        "sweep": sum(2.0 * 4 * B * ((L - m) ** 2 + m * (L - m)) for m in range(L)),
+    }
+
+
+# ---------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle port of the reference)
+
+
+def _cpu_worker(args):
+    L, seed, spectrum, real, grid_path, nmaps = args
+    from oracle import optisph_oracle as O
+
+    _, _, thetas = O.load_grid_file(grid_path)
+    flm = make_coefficients(L, nmaps, seed, spectrum, real)
+    t0 = time.perf_counter()
+    for b in range(nmaps):
+        s = O.inverse_sht(flm[b], thetas)
+        O.forward_sht(s, thetas, method="direct", check=False)  # the reference benchmark's protocol
+    return nmaps, time.perf_counter() - t0
+
+
+def cpu_round_trips(cfg: dict, procs: int, maps_per_proc: int, seed: int) -> tuple[float, float]:
+    """(maps, wall seconds) for procs processes x maps_per_proc round trips each."""
+    import multiprocessing as mp
+
+    env_threads = {"OPENBLAS_NUM_THREADS": "1", "OMP_NUM_THREADS": "1", "MKL_NUM_THREADS": "1"}
+    os.environ.update(env_threads)
+    grid_path = str(ROOT / "tests" / "golden" / "grids" / cfg["grid"])
+    jobs = [(cfg["L"], seed + i, cfg["spectrum"], cfg["real"], grid_path, maps_per_proc) for i in range(procs)]
+    from oracle import optisph_oracle as O
+
+    O.build()
+    t0 = time.perf_counter()
+    if procs == 1:
+        res = [_cpu_worker(jobs[0])]
+    else:
+        ctx = mp.get_context("fork")
+        with ctx.Pool(procs) as pool:
+            res = pool.map(_cpu_worker, jobs)
+    wall = time.perf_counter() - t0
+    return float(sum(r[0] for r in res)), wall
+
+
+# ---------------------------------------------------------------------------
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    procs = os.cpu_count() or 1
+    maps_per_proc = 1
+    times = []
+    total_maps = 0.0
+    for step in range(args.warmup + args.steps):
+        maps, wall = cpu_round_trips(cfg, procs, maps_per_proc, seed=14034661 + 100 * step)
+        if step >= args.warmup:
+            times.append(wall)
+            total_maps += maps
+    value = total_maps / sum(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(cfg, args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
+                         "sample": f"{procs} processes x {maps_per_proc} map round trip(s) per step "
+                                   f"(oracle port: C kernels + numpy.fft + scipy gelsy, 1 thread each)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg, args):
+    return {"workload": f"L={cfg['L']}, B={cfg['B']} {'real' if cfg['real'] else 'complex'} fp64 maps, "
+                        f"{'sqrt(C_l)-scaled' if cfg['spectrum'] == 'cmb' else 'unit'} complex Gaussian flm, "
+                        f"inverse then forward per step",
+            "L": cfg["L"], "maps_per_gpu": cfg["B"], "global_batch": cfg["B"] * args.gpus,
+            "grid": cfg["grid"], "parallelism": f"maps sharded over {args.gpus} GPU(s)",
+            "l2": "flushed (256 MiB write) before every timed step"}
+
+
+def run_ours(args, cfg):
+    import torch
+
+    import paper_1403_4661_b200 as osp
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    L, B = cfg["L"], cfg["B"]
+    grid = osp.load_grid(ROOT / "tests" / "golden" / "grids" / cfg["grid"])
+    flm_h = make_coefficients(L, B, 14034661 + 2 + 1000 * rank, cfg["spectrum"], cfg["real"])
+    flm = torch.from_numpy(flm_h).to(dev)
+    samples = torch.empty_like(flm)
+    back = torch.empty_like(flm)
+    plan = osp.get_plan(grid, B, local)
+    stream = torch.cuda.current_stream(dev)
+    plan.set_stream(osp.transform.torch_stream_handle(stream))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    kind = 1 | 2  # OSPH_DEVICE | OSPH_ASYNC
+
+    def step():
+        plan.inverse_raw(B, flm.data_ptr(), samples.data_ptr(), kind)
+        inv_launch = plan.last_launch_count()
+        plan.forward_raw(B, samples.data_ptr(), back.data_ptr(), kind, False)
+        return inv_launch + plan.last_launch_count()
+
+    # correctness guard on the measured data (not timed)
+    step()
+    torch.cuda.synchronize()
+    err = (back - flm).abs().max().item()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stage_i = np.zeros(3)
+    stage_f = np.zeros(3)
+    total_ms = 0.0
+    launches = 0
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            if world > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            nl = step()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            total_ms += ev0.elapsed_time(ev1)
+            t6 = plan.last_stage_times()
+            ti, tf = t6[:3], t6[3:]
+            stage_i += ti
+            stage_f += tf
+            launches += nl
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * B * args.steps / (total_ms * 1e-3)
+
+    # e2e: public API with pinned host buffers, H2D + D2H inside the timed region
+    flm_pin = torch.from_numpy(flm_h).pin_memory()
+    s_pin = torch.empty_like(flm_pin).pin_memory()
+    b_pin = torch.empty_like(flm_pin).pin_memory()
+    fn, sn, bn = flm_pin.numpy(), s_pin.numpy(), b_pin.numpy()
+    osp.inverse_sht_batch(fn, grid, out=sn, device=local)
+    osp.forward_sht_batch(sn, grid, out=bn, check=False, device=local)
+    e2e_t = []
+    for _ in range(max(1, min(args.steps, 5))):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        osp.inverse_sht_batch(fn, grid, out=sn, device=local)
+        osp.forward_sht_batch(sn, grid, out=bn, check=True, device=local)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_err = float(np.abs(bn - fn).max())
+    if world > 1:
+        t = torch.tensor([float(np.mean(e2e_t))], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_mean = float(t.item())
+    else:
+        e2e_mean = float(np.mean(e2e_t))
+    e2e_value = world * B / e2e_mean
+
+    if rank == 0:
+        fl = flops(L, B)
+        st_i = stage_i / args.steps
+        st_f = stage_f / args.steps
+        stages = {"pack": st_i[0], "synth": st_i[1], "ring_inverse": st_i[2],
+                  "ring_forward": st_f[0], "factor": st_f[1], "sweep": st_f[2]}
+        top = max(stages, key=stages.get)
+        alg = {"synth": fl["synth"], "factor": fl["factor_gj"], "sweep": fl["sweep"]}
+        roof = None
+        if top in alg:
+            achieved = alg[top] / stages[top] / 1e12
+            roof = {"bound": "tensor", "kernel": top, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                    "peak_source": "own fp64 DMMA microbenchmark (MEASURED_PEAKS.json has no fp64 entry)"}
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            procs = 1
+            maps, wall = cpu_round_trips(cfg, procs, args.cpu_maps, seed=99)
+            cpu = {"value": maps / wall, "unit": UNIT, "cores": procs, "kind": "port",
+                   "sample": f"{args.cpu_maps} map round trip(s), L={L}, 1 core, oracle port "
+                             f"(C kernels + numpy.fft + scipy gelsy), check=False as experiments.benchmark"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(cfg, args),
+            "stage_ms": {k: v * 1e3 for k, v in stages.items()},
+            "achieved_tflops": {"inverse": fl["inverse"] / (st_i.sum()) / 1e12,
+                                "forward": fl["forward"] / (st_f.sum()) / 1e12},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(2 * B * L * L * 16),
+                    "d2h_bytes_per_step": int(2 * B * L * L * 16)},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "roundtrip_max_err": max(err, e2e_err),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-maps", type=int, default=8)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -76,7 +76,8 @@ typedef struct osph_stats {
 int osph_plan_create(int L, const double* thetas, int max_batch, int device, osph_plan** out);
 int osph_plan_destroy(osph_plan* plan);
 
-/* Use `stream` (a cudaStream_t) for all work of this plan; NULL = plan-owned stream. */
+/* Use `stream` (a cudaStream_t) for all work of this plan; NULL = plan-owned
+ * stream (pass cudaStreamLegacy, i.e. (void*)1, for the legacy default stream). */
 int osph_plan_set_stream(osph_plan* plan, void* stream);
 
 /* Band limit / batch capacity of a plan. */
@@ -96,6 +97,12 @@ int osph_forward(osph_plan* plan, int B, const void* samples, void* flm, int ptr
  * out[2..3] = delta * sum_j v_j e^{+i m phi_j}, delta = 2 pi / n.  Refuses
  * |m| > (n-1)/2 (AliasingError) and even n with OSPH_ERR_ARG. */
 int osph_ring_analysis(const double* ring, int n, int m, double* out, int device);
+
+/* Device time of the stages of the last inverse and the last forward call, in
+ * seconds: seconds[0..2] = inverse {pack, Legendre synthesis, ring inverse DFTs},
+ * seconds[3..5] = forward {ring forward DFTs, per-order factorisation, sweep}
+ * (0 for a direction not yet run).  Blocks until that work has finished. */
+int osph_last_stage_times(const osph_plan* plan, double* seconds /* [6] */);
 
 /* Number of kernel launches enqueued by the last osph_inverse/osph_forward call. */
 int osph_last_launch_count(const osph_plan* plan);

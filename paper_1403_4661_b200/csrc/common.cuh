@@ -24,6 +24,20 @@ __host__ __device__ __forceinline__ int64_t packed_pos(int L, int m, int i) {
   return (int64_t)m * L - ((int64_t)m * (m - 1)) / 2 + i;
 }
 
+// Chunk-major 8-row tiling of the sweep operands (X_m and the below-block
+// Pb_m): columns are grouped in chunks of OSPH_TILE_KC, rows in tiles of 8;
+// element (r, k) of a matrix with nrt row tiles lives at
+//   ((k / KC) * nrt + r / 8) * KC * 8 + (k % KC) * 8 + r % 8,
+// so one chunk of a contiguous row-tile range is one contiguous block (a
+// single bulk copy).  Padding rows / columns are zero.
+#define OSPH_TILE_KC 32
+__host__ __device__ __forceinline__ int64_t tile_index(int r, int k, int nrt) {
+  return ((((int64_t)(k >> 5)) * nrt + (r >> 3)) << 8) + ((k & 31) << 3) + (r & 7);
+}
+__host__ __device__ __forceinline__ int64_t tile_size(int rows, int cols) {
+  return (int64_t)((cols + OSPH_TILE_KC - 1) / OSPH_TILE_KC) * ((rows + 7) / 8) * OSPH_TILE_KC * 8;
+}
+
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }

@@ -26,9 +26,13 @@
 // Also written: the "below" block 2pi Y_lm(theta_k), k < m (the k<m
 // correction matrix of transform.py:425-428), used by the sweep.
 //
-// Storage per order m (n = L-m): X column-major, element (i, j) at j*n + i
-// (i = degree l-m, j = pivoted ring row); perm[packed_pos(L,m,j)] = ring
-// offset feeding column j; Pb[(l-m)*m + k] for rings k < m.
+// Storage per order m (n = L-m): X column-major workspace, element (i, j) at
+// j*n + i (i = degree l-m, j = pivoted ring row); perm[packed_pos(L,m,j)] =
+// ring offset feeding column j.  For the sweep, X is re-emitted in 8-row
+// tiles Xt[((i/8)*n + j)*8 + i%8] (rows padded to a multiple of 8 with zeros)
+// and Pb is written directly in 8-ring tiles Pb[((k/8)*n + l-m)*8 + k%8], so
+// a CTA's row slice of either matrix is a run of contiguous 64-byte columns
+// that the sweep streams with bulk (TMA) copies.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -52,7 +56,9 @@ __global__ void __launch_bounds__(FAC_THREADS, 1) k_factor_gj(
     int L, int m_first, const double* __restrict__ costh, const double2* __restrict__ rec,
     const int* __restrict__ ls_tab, const double2* __restrict__ pstart, const int64_t* __restrict__ ainv_off,
     const int64_t* __restrict__ pb_off, double* __restrict__ ainv, double* __restrict__ pbelow,
-    int* __restrict__ perm_all, unsigned long long* __restrict__ norms, int* __restrict__ status_out) {
+    int* __restrict__ perm_all, unsigned long long* __restrict__ norms, int* __restrict__ status_out,
+    int* __restrict__ jstar_out, double* __restrict__ beta_out, double* __restrict__ xt_all,
+    const int64_t* __restrict__ xt_off) {
   cg::cluster_group cluster = cg::this_cluster();
   const int CS = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
@@ -95,7 +101,7 @@ __global__ void __launch_bounds__(FAC_THREADS, 1) k_factor_gj(
         p1 = nxt;
       }
       if (k >= m) A[(int64_t)(l - m) * n + (k - m)] = v;
-      else Pb[(int64_t)(l - m) * m + k] = v;
+      else Pb[tile_index(k, l - m, (m + 7) >> 3)] = v;  // chunk-major 8-ring tiles
     }
   }
   if (rank == 0)
@@ -315,6 +321,45 @@ __global__ void __launch_bounds__(FAC_THREADS, 1) k_factor_gj(
   }
   if (tid == 0 && s_bad) atomicOr(status_out + m, 1);
   (void)s_cmax;
+
+  // own columns of X -> 8-row tiles for the sweep (padding rows zero)
+  {
+    double* Xt = xt_all + xt_off[m];
+    const int npad = (n + 7) & ~7;
+    const int nrt = npad >> 3;
+    // the owner of the last columns also zero-fills the padding columns of the last chunk
+    const int cend = (cown1 == n) ? (n + OSPH_TILE_KC - 1) / OSPH_TILE_KC * OSPH_TILE_KC : cown1;
+    for (int col = cown0; col < cend; ++col)
+      for (int i = tid; i < npad; i += FAC_THREADS)
+        Xt[tile_index(i, col, nrt)] = (i < n && col < n) ? __ldcg(A + (int64_t)col * n + i) : 0.0;
+  }
+
+  // ---- 4. sweep chain constants (rank 0): j* = column of X fed by ring m
+  // (perm[j*] = 0) and beta_m = Pb_m[ring m-1, :] . X[:, j*], the coupling of
+  // order m's late right-hand-side entry into ring m-1 of order m-1.
+  if (rank == 0) {
+    __shared__ int s_jstar;
+    __shared__ double s_beta[FAC_THREADS / 32];
+    for (int j = tid; j < n; j += FAC_THREADS)
+      if (__ldcg(perm + j) == 0) s_jstar = j;
+    __syncthreads();
+    const int js = s_jstar;
+    double acc = 0.0;
+    if (m >= 1)
+      for (int l = tid; l < n; l += FAC_THREADS)
+        acc += __ldcg(Pb + tile_index(m - 1, l, (m + 7) >> 3)) *
+               __ldcg(A + (int64_t)js * n + l);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) s_beta[warp] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double b = 0.0;
+      for (int w = 0; w < FAC_THREADS / 32; ++w) b += s_beta[w];
+      beta_out[m] = b;
+      jstar_out[m] = js;
+    }
+  }
 }
 
 // Finalise kappa per order once every cluster has finished.
@@ -359,7 +404,7 @@ static cudaError_t launch_class(osph_plan* p, int m_first, int m_last, int cs) {
   e = cudaLaunchKernelEx(&cfg, kern, L, m_first, (const double*)p->d_cos, (const double2*)p->d_rec,
                          (const int*)p->d_ls, (const double2*)p->d_pstart, (const int64_t*)p->d_ainv_off,
                          (const int64_t*)p->d_pb_off, p->d_ainv, p->d_pbelow, p->d_piv, p->d_norms,
-                         p->d_status);
+                         p->d_status, p->d_jstar, p->d_beta, p->d_xt, (const int64_t*)p->d_xt_off);
   p->launches++;
   return e;
 }

@@ -51,8 +51,9 @@ static void plan_free(osph_plan* p) {
   void* ptrs[] = {p->d_cos, p->d_sin, p->d_rec, p->d_ls, p->d_pstart, p->d_ring_order, p->d_fft_n,
                   p->d_chirp_off, p->d_bhat_off, p->d_chirp, p->d_bhat, p->d_tw, p->d_roots,
                   p->d_bluestein_rings, p->d_ainv_off, p->d_pb_off, p->d_ainv, p->d_pbelow, p->d_piv,
-                  p->d_norms, p->d_kappa, p->d_status, p->d_fpack, p->d_g, p->d_r, p->d_x, p->d_in,
-                  p->d_out};
+                  p->d_norms, p->d_kappa, p->d_status, p->d_jstar, p->d_beta, p->d_xt_off, p->d_xt,
+                  p->d_fpack, p->d_g, p->d_r,
+                  p->d_in, p->d_out};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (cudaEvent_t& e : p->ev)
@@ -223,22 +224,30 @@ static int ensure_forward(osph_plan* p) {
   const size_t B = p->max_batch;
   p->h_ainv_off.assign(L + 1, 0);
   p->h_pb_off.assign(L + 1, 0);
+  p->h_xt_off.assign(L + 1, 0);
   for (int m = 0; m < L; ++m) {
     const int64_t n = L - m;
     p->h_ainv_off[m + 1] = p->h_ainv_off[m] + n * n;
-    p->h_pb_off[m + 1] = p->h_pb_off[m] + n * m;
+    p->h_pb_off[m + 1] = p->h_pb_off[m] + tile_size(m, (int)n);  // chunk-major 8-ring tiles
+    p->h_xt_off[m + 1] = p->h_xt_off[m] + tile_size((int)n, (int)n);  // chunk-major 8-row tiles
   }
   cudaStream_t st = p->stream;
   CUDA_TRY(upload(&p->d_ainv_off, p->h_ainv_off.data(), L + 1, st));
   CUDA_TRY(upload(&p->d_pb_off, p->h_pb_off.data(), L + 1, st));
+  CUDA_TRY(upload(&p->d_xt_off, p->h_xt_off.data(), L + 1, st));
   CUDA_TRY(dalloc(&p->d_ainv, (size_t)p->h_ainv_off[L]));
   CUDA_TRY(dalloc(&p->d_pbelow, (size_t)p->h_pb_off[L]));
+  CUDA_TRY(dalloc(&p->d_xt, (size_t)p->h_xt_off[L]));
+  // padding of the tiled operands stays zero forever (the kernels write only real entries)
+  CUDA_TRY(cudaMemsetAsync(p->d_pbelow, 0, sizeof(double) * (size_t)p->h_pb_off[L], st));
+  CUDA_TRY(cudaMemsetAsync(p->d_xt, 0, sizeof(double) * (size_t)p->h_xt_off[L], st));
   CUDA_TRY(dalloc(&p->d_piv, (size_t)L * (L + 1) / 2));
   CUDA_TRY(dalloc(&p->d_norms, (size_t)2 * L));
   CUDA_TRY(dalloc(&p->d_kappa, (size_t)L));
   CUDA_TRY(dalloc(&p->d_status, (size_t)L));
+  CUDA_TRY(dalloc(&p->d_jstar, (size_t)L));
+  CUDA_TRY(dalloc(&p->d_beta, (size_t)L));
   CUDA_TRY(dalloc(&p->d_r, (size_t)L * (L + 1) * B));
-  CUDA_TRY(dalloc(&p->d_x, (size_t)(B + 3) * 4 * L));
   CUDA_TRY(cudaStreamSynchronize(st));
   p->fwd_ready = true;
   return OSPH_OK;
@@ -286,9 +295,14 @@ extern "C" int osph_inverse(osph_plan* p, int B, const void* flm, void* samples,
     in = p->d_in;
     out = p->d_out;
   }
+  CUDA_TRY(cudaEventRecord(p->ev[0], st));
   CUDA_TRY(launch_pack(p, B, in));
+  CUDA_TRY(cudaEventRecord(p->ev[1], st));
   CUDA_TRY(launch_synth(p, B));
+  CUDA_TRY(cudaEventRecord(p->ev[2], st));
   CUDA_TRY(launch_ring_inverse(p, B, out));
+  CUDA_TRY(cudaEventRecord(p->ev[3], st));
+  p->have_inv = true;
   if (host) CUDA_TRY(cudaMemcpyAsync(samples, p->d_out, bytes, cudaMemcpyDeviceToHost, st));
   if (!(kind & OSPH_ASYNC)) CUDA_TRY(cudaStreamSynchronize(st));
   return OSPH_OK;
@@ -318,21 +332,22 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
     in = p->d_in;
     out = p->d_out;
   }
-  CUDA_TRY(cudaEventRecord(p->ev[0], st));
+  CUDA_TRY(cudaEventRecord(p->ev[4], st));
   CUDA_TRY(launch_ring_forward(p, B, in));
-  CUDA_TRY(cudaEventRecord(p->ev[1], st));
+  CUDA_TRY(cudaEventRecord(p->ev[5], st));
   CUDA_TRY(launch_factor(p));
-  CUDA_TRY(cudaEventRecord(p->ev[2], st));
+  CUDA_TRY(cudaEventRecord(p->ev[6], st));
   CUDA_TRY(launch_sweep(p, B, out));
-  CUDA_TRY(cudaEventRecord(p->ev[3], st));
+  CUDA_TRY(cudaEventRecord(p->ev[7], st));
+  p->have_fwd = true;
   if (host) CUDA_TRY(cudaMemcpyAsync(flm, p->d_out, bytes, cudaMemcpyDeviceToHost, st));
   if (kind & OSPH_ASYNC) return OSPH_OK;
   CUDA_TRY(cudaStreamSynchronize(st));
   if (stats) {
     float t01 = 0, t12 = 0, t23 = 0;
-    cudaEventElapsedTime(&t01, p->ev[0], p->ev[1]);
-    cudaEventElapsedTime(&t12, p->ev[1], p->ev[2]);
-    cudaEventElapsedTime(&t23, p->ev[2], p->ev[3]);
+    cudaEventElapsedTime(&t01, p->ev[4], p->ev[5]);
+    cudaEventElapsedTime(&t12, p->ev[5], p->ev[6]);
+    cudaEventElapsedTime(&t23, p->ev[6], p->ev[7]);
     stats->factor_seconds = t12 * 1e-3;
     stats->sweep_seconds = t23 * 1e-3;
     stats->solve_seconds = (t12 + t23) * 1e-3;
@@ -388,6 +403,25 @@ extern "C" int osph_ring_analysis(const double* ring, int n, int m, double* out,
   if (e != cudaSuccess) {
     osph_set_error(std::string("ring analysis: ") + cudaGetErrorString(e));
     return OSPH_ERR_CUDA;
+  }
+  return OSPH_OK;
+}
+
+extern "C" int osph_last_stage_times(const osph_plan* p, double* seconds) {
+  if (!p || !seconds) {
+    osph_set_error("NULL argument");
+    return OSPH_ERR_ARG;
+  }
+  for (int d = 0; d < 2; ++d) {
+    const bool have = d == 0 ? p->have_inv : p->have_fwd;
+    for (int i = 0; i < 3; ++i) {
+      float ms = 0.f;
+      if (have) {
+        CUDA_TRY(cudaEventSynchronize(p->ev[4 * d + 3]));
+        CUDA_TRY(cudaEventElapsedTime(&ms, p->ev[4 * d + i], p->ev[4 * d + i + 1]));
+      }
+      seconds[3 * d + i] = ms * 1e-3;
+    }
   }
   return OSPH_OK;
 }

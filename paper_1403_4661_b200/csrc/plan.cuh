@@ -47,6 +47,11 @@ struct osph_plan {
   unsigned long long* d_norms = nullptr;  // [2L] ||A_m||_1, ||A_m^-1||_1 (as ordered bits)
   double* d_kappa = nullptr;     // [L] 1-norm condition estimate per order
   int* d_status = nullptr;       // [L] 0 ok, 1 zero/non-finite pivot
+  int* d_jstar = nullptr;        // [L] column of X_m fed by ring m (perm[j*] = 0)
+  double* d_beta = nullptr;      // [L] beta_m = Pb_m[m-1, :] . X_m[:, j*]
+  std::vector<int64_t> h_xt_off;  // [L+1] offset of order m's 8-row-tiled inverse
+  int64_t* d_xt_off = nullptr;
+  double* d_xt = nullptr;         // X_m in 8-row tiles (sweep operand)
   bool fwd_ready = false;        // forward buffers allocated
   bool inv_ready = false;        // inverse buffers allocated
 
@@ -54,11 +59,11 @@ struct osph_plan {
   double* d_fpack = nullptr;  // inverse: packed coefficients [pos(m,l)][4B]
   double* d_g = nullptr;      // inverse: G [m][k][4B]
   double2* d_r = nullptr;     // forward: order-major ring spectra [pos(m,k-m)][2][B]
-  double* d_x = nullptr;      // forward sweep scratch
   double2* d_in = nullptr;    // device staging of host inputs  [B][L^2]
   double2* d_out = nullptr;   // device staging of host outputs [B][L^2]
 
-  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev[8] = {};  // [0..3] last inverse stages, [4..7] last forward stages
+  bool have_inv = false, have_fwd = false;
 };
 
 // last-error plumbing (plan.cu)

@@ -11,170 +11,700 @@
 // which the bin update is simply R[target] -= G and the RHS of order m is the
 // contiguous slab R[pos(m, 0..n)].
 //
-// A "team" (one thread-block cluster) owns a group of maps and runs the whole
-// sweep with cluster barriers only; teams are independent, so a batch fills
-// the GPU with teams (maps) and a single map gets one 16-CTA team.  Per order:
-//   phase 1: x = X * (P rhs)   rows of X split over the team   (solve)
-//   phase 2: G = Pb * x        rings k < m split over the team (correction)
+// Pipelining.  The solution of order s splits as
+//   x_s = x'_s + w_s L_s,  x'_s = X_s P rhs_s (late entry zeroed),  w_s = X_s[:, j*_s],
+// where L_s, the right-hand-side entry of ring s, is the only entry that
+// depends on order s+1.  It follows from a scalar chain
+//   G+-_{s+1}(theta_s) = a+-_s + beta_{s+1} L+-_{s+1},  a_s = Pb_{s+1}[s, :] . x'_{s+1},
+// so all bulk work of a step is independent of the chain and a step needs ONE
+// cluster barrier.  Step t (t = L-1 .. 0):
+//   (a) chain -> L_t                                 (shared memory only)
+//   (b) x_t = x'_t + w_t L_t on own rows -> flm, DSMEM broadcast to the team
+//   (c) CORR(t+1): corrections of order t+1 (x_{t+1} complete) on own rings
+//   (d) BULK(t-1): x'_{t-1} on own rows, chain partial a_{t-2} -> DSMEM
+// x'_s is computed one step before it is used; the corrections of order s+1
+// are applied one step after x_{s+1} is known -- both fit the alias
+// dependency structure (orders >= s+3 feed the non-late entries of order s).
+//
+// Streaming.  CORR and BULK are row-sliced GEMMs (rows of the team split
+// over its CTAs, K = n) on the fp64 tensor cores (mma.sync m8n8k4 ->
+// DMMA.8x8x4).  Their A operands (8-row tiles of Pb_s / X_s, written by
+// factor.cu) do not depend on the data, so one producer thread streams them
+// with bulk async copies (cp.async.bulk + mbarrier complete_tx, the TMA
+// engine) through an S-stage ring that runs ahead across jobs and steps;
+// only the small B operands (x, gathered right-hand sides) wait on the chain.
+//
+// A "team" = one thread-block cluster owning a group of maps; teams are
+// independent, so a batch fills the GPU with teams and a single map gets one
+// wide team.
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
 
 #include "plan.cuh"
 
 namespace cg = cooperative_groups;
 
 #define SWEEP_THREADS 256
+#define SWEEP_WARPS 8
+#define SWEEP_IPW 4     // max accumulator tiles per warp
+#define SWEEP_UMAX 8    // max gathered right-hand-side entries per thread
+#define SWEEP_KC 32     // K columns per streamed chunk
+
+// ---------------------------------------------------------------------------
+// mbarrier / bulk-copy PTX
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// -DOSPH_SWEEP_PROF: per-phase cycle counts of CTA 0 (debug builds only)
+#ifdef OSPH_SWEEP_PROF
+#define PROF_DECL            \
+  long long _pt = clock64(); \
+  long long _acc[5] = {0, 0, 0, 0, 0};
+#define PROF_MARK(i)                \
+  do {                              \
+    __syncthreads();                \
+    const long long _n = clock64(); \
+    _acc[i] += _n - _pt;            \
+    _pt = _n;                       \
+  } while (0)
+#define PROF_DUMP()                                                                                  \
+  if (blockIdx.x == 0 && threadIdx.x == 0)                                                           \
+  printf("sweep prof (cycles): chain+axpy %lld  corr %lld  gather %lld  bulk %lld  barrier %lld  "   \
+         "| mbar wait %lld over %lld chunks, compute %lld sync %lld issue %lld\n",                     \
+         _acc[0], _acc[1], _acc[2], _acc[3], _acc[4], prof_wait, prof_chunks, prof_compute, prof_sync, \
+         prof_issue)
+#else
+#define PROF_DECL
+#define PROF_MARK(i)
+#define PROF_DUMP()
+#endif
+
+// ---------------------------------------------------------------------------
+// configuration and shared-memory layout
+
+struct SweepCfg {
+  int L, T, CC, KC, S;
+  int tpc;  // max 8-row tiles of one job on one CTA
+  int ldx, ldr;
+  size_t xfull, bt, xp, wv, prow, apart, part, late, rch, stage, bar, total;  // offsets in doubles
+  __host__ __device__ SweepCfg(int L_, int T_, int CC_, int KC_, int S_) : L(L_), T(T_), CC(CC_), KC(KC_), S(S_) {
+    tpc = ((L + 7) / 8 + T - 1) / T;
+    ldx = ((L + 15) / 16) * 16 + 4;
+    ldr = 8 * tpc + 4;
+    size_t o = 0;
+    xfull = o; o += (size_t)2 * (CC + 1) * ldx;  // x_s of the whole team, transposed, by parity (+ zero row)
+    bt = o;    o += (size_t)(CC + 1) * ldx;  // permuted right-hand side (BULK B operand), transposed (+ zero row)
+    xp = o;    o += (size_t)2 * CC * ldr;   // own rows of x'_s, transposed, by parity of s
+    wv = o;    o += (size_t)2 * ldr;        // own rows of w_s, by parity of s
+    prow = o;  o += (size_t)ldr;            // own entries of Pb_s[s-1, :] (chain partial)
+    apart = o; o += (size_t)4 * T * CC;     // chain partials a_s from every rank, slot s % 4
+    part = o;  o += (size_t)SWEEP_WARPS * 64;
+    late = o;  o += (size_t)2 * CC;         // late right-hand-side entries L_s, by parity
+    rch = o;   o += (size_t)2 * CC;         // prefetched R(+-)[s][0], by parity
+    o = (o + 15) & ~(size_t)15;             // 128-byte aligned stages
+    stage = o; o += (size_t)S * tpc * KC * 8;
+    bar = o;   o += (size_t)S;
+    total = o;
+  }
+};
+
+// Job = one row-sliced GEMM of a step.  type 0: BULK(s) (A = X_s tiles),
+// type 1: CORR(s) (A = Pb_s tiles, rings k < s-1).
+struct Job {
+  int type, s, K;   // K = n_s
+  int rt0, rt1;     // own 8-row tiles
+  int nch;          // chunks of KC columns (0 = nothing to do on this CTA)
+  const double* A;  // operand base (X tiles or Pb tiles)
+  int64_t off;      // this CTA's row-tile range inside chunk 0 (chunk-major tiles, common.cuh)
+  int64_t cstride;  // doubles between consecutive chunks
+};
+
+__device__ __forceinline__ Job make_job(int type, int s, int L, int T, int rank, int KC, const double* xt,
+                                        const int64_t* xt_off, const double* pbt, const int64_t* pb_off) {
+  Job j;
+  j.type = type;
+  j.s = s;
+  j.K = L - s;
+  const int rows = type == 0 ? j.K : s - 1;   // CORR skips ring s-1 (the chain)
+  const int mrows = type == 0 ? j.K : s;      // rows of the stored matrix
+  const int nt = (rows + 7) / 8;
+  j.rt0 = (rank * nt) / T;
+  j.rt1 = ((rank + 1) * nt) / T;
+  j.nch = (j.rt1 > j.rt0 && rows > 0) ? (j.K + KC - 1) / KC : 0;
+  j.cstride = (int64_t)((mrows + 7) / 8) * KC * 8;
+  j.A = type == 0 ? xt : pbt;  // base; the offset below is consumed only at issue time
+  j.off = (type == 0 ? xt_off[s] : pb_off[s]) + (int64_t)j.rt0 * KC * 8;
+  return j;
+}
+
+// Job sequence: BULK(L-1) (prologue), then per step t = L-1..0:
+// CORR(t+1) if 1 <= t <= L-2, BULK(t-1) if t >= 1.  Cursor (t, ph).
+__device__ __forceinline__ bool next_job_id(int L, int& t, int& ph, int& type, int& s) {
+  while (t >= 0) {
+    if (ph == 0) {
+      ph = 1;
+      if (t >= 1 && t <= L - 2) {
+        type = 1;
+        s = t + 1;
+        return true;
+      }
+    } else {
+      const int tt = t;
+      ph = 0;
+      --t;
+      if (tt >= 1) {
+        type = 0;
+        s = tt - 1;
+        return true;
+      }
+    }
+  }
+  return false;
+}
+
+// Producer (thread 0): issues chunk after chunk of the job sequence.
+struct Producer {
+  int t, ph;       // job cursor
+  Job job, nxt;    // current job, next job (decoded ahead)
+  int ch;          // next chunk of the current job
+  bool has, has_nxt;
+  int st;          // stage receiving the next chunk
+};
 
 template <int CC>
-__global__ void __launch_bounds__(SWEEP_THREADS) k_sweep(
-    int L, int B, int maps_per_team, const double* __restrict__ ainv, const int64_t* __restrict__ ainv_off,
-    const int* __restrict__ perm_all, const double* __restrict__ pbelow, const int64_t* __restrict__ pb_off,
-    double2* __restrict__ R, double* __restrict__ xs_all, double2* __restrict__ flm) {
+__global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(
+    int L, int B, int maps_per_team, int KC, int S, const double* __restrict__ xt, const int64_t* __restrict__ xt_off,
+    const int* __restrict__ perm_all, const int* __restrict__ jstar_all, const double* __restrict__ beta_all,
+    const double* __restrict__ pbt, const int64_t* __restrict__ pb_off, double2* __restrict__ R,
+    double2* __restrict__ flm) {
   cg::cluster_group cluster = cg::this_cluster();
   const int T = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
   const int team = (int)(blockIdx.x / T);
   const int b0 = team * maps_per_team;
   const int gm = min(maps_per_team, B - b0);
-  const int tid = threadIdx.x;
-  extern __shared__ __align__(16) double vec[];  // [L][CC]: rhs in phase 1, x in phase 2
-  double* xg = xs_all + (int64_t)team * L * CC;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  constexpr int NCT = (CC + 7) / 8;
+  constexpr int NB4 = CC / 4;  // map slots of the team
 
-  for (int m = L - 1; m >= 0; --m) {
-    const int n = L - m;
-    const double sgn = (m & 1) ? -1.0 : 1.0;
-    const int64_t pm = packed_pos(L, m, 0);
-    const int* perm = perm_all + pm;
-    // ---- phase 1: permuted right-hand side -> smem
-    for (int idx = tid; idx < n * (CC / 4); idx += SWEEP_THREADS) {
-      const int i = idx / (CC / 4), bl = idx - i * (CC / 4);
-      double4 v = make_double4(0.0, 0.0, 0.0, 0.0);
-      if (bl < gm) {
-        const int64_t base = ((pm + perm[i]) * 2) * B + b0 + bl;
-        const double2 rp = __ldcg(R + base);
-        const double2 rn = __ldcg(R + base + B);
-        v = make_double4(rp.x, rp.y, sgn * rn.x, sgn * rn.y);
+  extern __shared__ __align__(128) double smem[];
+  const SweepCfg cfg(L, T, CC, KC, S);
+  const int ldx = cfg.ldx, ldr = cfg.ldr, tpc = cfg.tpc;
+  double* xfull = smem + cfg.xfull;
+  double* Bt = smem + cfg.bt;
+  double* xp = smem + cfg.xp;
+  double* wv = smem + cfg.wv;
+  double* prowb = smem + cfg.prow;
+  double* apart = smem + cfg.apart;
+  double* part = smem + cfg.part;
+  double* late = smem + cfg.late;
+  double* rch = smem + cfg.rch;
+  double* stages = smem + cfg.stage;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + cfg.bar);
+  const size_t stage_elems = (size_t)tpc * KC * 8;
+#ifdef OSPH_SWEEP_PROF
+  long long prof_wait = 0, prof_chunks = 0, prof_compute = 0, prof_sync = 0, prof_issue = 0;
+#endif
+
+  // ---- producer
+  Producer pr;
+  // The producer keeps the job after the current one decoded ahead of time so
+  // the offset-table loads of make_job never stall a chunk issue.
+  auto find_next = [&](Job& out) -> bool {
+    int type, s;
+    while (next_job_id(L, pr.t, pr.ph, type, s)) {
+      out = make_job(type, s, L, T, rank, SWEEP_KC, xt, xt_off, pbt, pb_off);
+      if (out.nch > 0) return true;
+    }
+    return false;
+  };
+  auto prod_advance = [&]() {
+    pr.job = pr.nxt;
+    pr.has = pr.has_nxt;
+    pr.ch = 0;
+    if (pr.has) pr.has_nxt = find_next(pr.nxt);
+  };
+  auto prod_issue = [&]() {  // thread 0 only: one chunk into stage next % S
+    if (!pr.has) return;
+    const Job& j = pr.job;
+    uint64_t* bar = bars + pr.st;
+    const uint32_t bytes = (uint32_t)((j.rt1 - j.rt0) * KC * 64);
+    mbar_arrive_expect_tx(bar, bytes);
+    bulk_g2s(stages + pr.st * stage_elems, j.A + j.off + pr.ch * j.cstride, bytes, bar);  // one contiguous block
+    if (++pr.st == S) pr.st = 0;
+    if (++pr.ch == j.nch) prod_advance();
+  };
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) mbar_init(bars + i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    pr.t = L;
+    pr.ph = 1;
+    pr.st = 0;
+    pr.has_nxt = find_next(pr.nxt);
+    prod_advance();
+    for (int i = 0; i < S; ++i) prod_issue();
+  }
+  for (int i = tid; i < ldx; i += SWEEP_THREADS) {  // zero rows: B operand of padding columns
+    xfull[(size_t)CC * ldx + i] = 0.0;
+    xfull[(size_t)(2 * CC + 1) * ldx + i] = 0.0;
+    Bt[(size_t)CC * ldx + i] = 0.0;
+  }
+  __syncthreads();
+
+  // ---- consumer: one job through the chunk ring
+  int cst = 0;           // stage of the next chunk to consume
+  uint32_t cphase = 0;   // its mbarrier phase parity
+  // Warp w owns output tiles w, w+8, ... (8 rows x 8 columns each) for the
+  // whole job; K is streamed in chunks of SWEEP_KC columns, two independent
+  // accumulator sets per tile (even / odd k-steps) for DMMA latency hiding.
+  auto run_job = [&](const Job& j, const double* Bsrc, int ldb, auto emit) {
+    if (j.nch == 0) return;
+    const int ntile = j.rt1 - j.rt0;
+    const int items = ntile * NCT;
+    int nmine = 0;
+    int aoff[SWEEP_IPW], boff[SWEEP_IPW];
+#pragma unroll
+    for (int u = 0; u < SWEEP_IPW; ++u) {
+      const int it = warp + u * SWEEP_WARPS;
+      const bool ok = it < items;
+      nmine += ok ? 1 : 0;
+      const int rtl = ok ? it % ntile : 0, ct = ok ? it / ntile : 0;
+      aoff[u] = rtl * SWEEP_KC * 8 + g;
+      const int col = ct * 8 + g;
+      boff[u] = (ok && col < CC ? col : CC) * ldb;  // row CC of Bsrc is a zero row
+    }
+    double acc[SWEEP_IPW][2][2];
+#pragma unroll
+    for (int u = 0; u < SWEEP_IPW; ++u) acc[u][0][0] = acc[u][0][1] = acc[u][1][0] = acc[u][1][1] = 0.0;
+    for (int ch = 0; ch < j.nch; ++ch) {
+#ifdef OSPH_SWEEP_PROF
+      const long long _w0 = clock64();
+      mbar_wait(bars + cst, cphase);
+      prof_wait += clock64() - _w0;
+      ++prof_chunks;
+#else
+      mbar_wait(bars + cst, cphase);
+#endif
+      const double* sA = stages + cst * stage_elems + tq * 8;
+      const int kb = ch * SWEEP_KC;
+      const double* Bk = Bsrc + kb + tq;
+      // Columns past K are zero in the tiled operand and finite in Bsrc, so a
+      // ragged last chunk needs no guard.  Branch once per chunk on the warp's
+      // tile count so no predicated-off DMMA slots are issued.
+      auto chunk = [&](auto NM) {
+        constexpr int nm = decltype(NM)::value;
+#pragma unroll
+        for (int ks = 0; ks < SWEEP_KC / 4; ++ks) {
+#pragma unroll
+          for (int u = 0; u < nm; ++u) {
+            const double a = sA[aoff[u] + ks * 32];
+            const double b = Bk[boff[u] + ks * 4];
+            dmma_8x8x4(acc[u][ks & 1][0], acc[u][ks & 1][1], a, b);
+          }
+        }
+      };
+      switch (nmine) {
+        case 1: chunk(std::integral_constant<int, 1>{}); break;
+        case 2: chunk(std::integral_constant<int, 2>{}); break;
+        case 3: chunk(std::integral_constant<int, 3>{}); break;
+        case 4: chunk(std::integral_constant<int, 4>{}); break;
+        default: break;
       }
-      *reinterpret_cast<double4*>(vec + (size_t)i * CC + 4 * bl) = v;
+      if (++cst == S) {
+        cst = 0;
+        cphase ^= 1u;
+      }
+#ifdef OSPH_SWEEP_PROF
+      const long long _c1 = clock64();
+      prof_compute += _c1 - _w0;
+      __syncthreads();  // stage free
+      const long long _c2 = clock64();
+      prof_sync += _c2 - _c1;
+      if (tid == 0) prod_issue();
+      prof_issue += clock64() - _c2;
+#else
+      __syncthreads();  // stage free
+      if (tid == 0) prod_issue();
+#endif
+    }
+#pragma unroll
+    for (int u = 0; u < SWEEP_IPW; ++u) {
+      const int it = warp + u * SWEEP_WARPS;
+      if (u < nmine) {
+        const int rtl = it % ntile, ct = it / ntile;
+        const int c = ct * 8 + 2 * tq;
+        if (c < CC) emit(8 * (j.rt0 + rtl) + g, c, acc[u][0][0] + acc[u][1][0], acc[u][0][1] + acc[u][1][1]);
+      }
+    }
+  };
+
+  // ---- gathered right-hand side of order s: registers (issued early) -> Bt
+  int pidx[SWEEP_UMAX];
+  double2 grp[SWEEP_UMAX], grn[SWEEP_UMAX];
+  auto load_perm = [&](int s) {  // data independent: one step ahead
+    const int ns = L - s;
+    const int* perm = perm_all + packed_pos(L, s, 0);
+#pragma unroll
+    for (int u = 0; u < SWEEP_UMAX; ++u) {
+      const int idx = tid + u * SWEEP_THREADS;
+      const int jj = idx / NB4;
+      pidx[u] = (jj < ns) ? __ldg(perm + jj) : -1;
+    }
+  };
+  auto gather_issue = [&](int s) {
+    const int64_t ps = packed_pos(L, s, 0);
+#pragma unroll
+    for (int u = 0; u < SWEEP_UMAX; ++u) {
+      const int idx = tid + u * SWEEP_THREADS;
+      const int bl = idx % NB4;
+      grp[u] = grn[u] = make_double2(0.0, 0.0);
+      if (pidx[u] > 0 && bl < gm) {
+        const int64_t base = ((ps + pidx[u]) * 2) * B + b0 + bl;
+        grp[u] = __ldcg(R + base);
+        grn[u] = __ldcg(R + base + B);
+      }
+    }
+  };
+  auto gather_store = [&](int s) {
+    const int ns = L - s;
+    const double sg = (s & 1) ? -1.0 : 1.0;
+#pragma unroll
+    for (int u = 0; u < SWEEP_UMAX; ++u) {
+      const int idx = tid + u * SWEEP_THREADS;
+      const int jj = idx / NB4, bl = idx % NB4;
+      if (jj < ns) {
+        Bt[(size_t)(4 * bl + 0) * ldx + jj] = grp[u].x;
+        Bt[(size_t)(4 * bl + 1) * ldx + jj] = grp[u].y;
+        Bt[(size_t)(4 * bl + 2) * ldx + jj] = sg * grn[u].x;
+        Bt[(size_t)(4 * bl + 3) * ldx + jj] = sg * grn[u].y;
+      }
+    }
+  };
+
+  auto load_rch = [&](int s) {  // R(+-)[s][0] of every map -> rch[s & 1]
+    if (tid < NB4) {
+      double2 rp = make_double2(0.0, 0.0), rn = rp;
+      if (tid < gm) {
+        const int64_t base = (packed_pos(L, s, 0) * 2) * B + b0 + tid;
+        rp = __ldcg(R + base);
+        rn = __ldcg(R + base + B);
+      }
+      double* d = rch + (size_t)(s & 1) * CC + 4 * tid;
+      d[0] = rp.x;
+      d[1] = rp.y;
+      d[2] = rn.x;
+      d[3] = rn.y;
+    }
+  };
+
+  // BULK(s): x'_s on own rows, w_s, chain partial a_{s-1}
+  auto bulk = [&](int s) {
+    const Job j = make_job(0, s, L, T, rank, KC, xt, xt_off, pbt, pb_off);
+    const int ns = j.K;
+    const int r0 = 8 * j.rt0, r1 = min(ns, 8 * j.rt1);
+    // data-independent side loads, consumed after the GEMM
+    double wl = 0.0, pl = 0.0;
+    if (tid < r1 - r0) {
+      const int l = r0 + tid;
+      const double* X = xt + xt_off[s];
+      wl = __ldg(X + tile_index(l, __ldg(jstar_all + s), (ns + 7) >> 3));
+      if (s >= 1) pl = __ldg(pbt + pb_off[s] + tile_index(s - 1, l, (s + 7) >> 3));
+    }
+    double* xps = xp + (size_t)(s & 1) * CC * ldr;
+    run_job(j, Bt, ldx, [&](int l, int c, double v0, double v1) {
+      if (l < ns) {
+        xps[(size_t)c * ldr + (l - r0)] = v0;
+        xps[(size_t)(c + 1) * ldr + (l - r0)] = v1;
+      }
+    });
+    if (tid < r1 - r0) {
+      wv[(size_t)(s & 1) * ldr + tid] = wl;
+      prowb[tid] = pl;
     }
     __syncthreads();
-    const double* X = ainv + ainv_off[m];
-    const int r0 = (rank * n) / T, r1 = ((rank + 1) * n) / T;
-    for (int l = r0 + tid; l < r1; l += SWEEP_THREADS) {
-      double acc[CC];
+    if (s >= 1) {
+      for (int c = warp; c < CC; c += SWEEP_WARPS) {
+        double acc = 0.0;
+        for (int l = lane; l < r1 - r0; l += 32) acc += prowb[l] * xps[(size_t)c * ldr + l];
 #pragma unroll
-      for (int c = 0; c < CC; ++c) acc[c] = 0.0;
-      const double* xc = X + l;
-      for (int i = 0; i < n; ++i) {
-        const double a = __ldg(xc + (int64_t)i * n);
-        const double* rv = vec + (size_t)i * CC;
-#pragma unroll
-        for (int c = 0; c < CC; ++c) acc[c] = fma(a, rv[c], acc[c]);
-      }
-#pragma unroll
-      for (int c = 0; c < CC; ++c) xg[(size_t)l * CC + c] = acc[c];
-      const int64_t ell = m + l;
-      for (int bl = 0; bl < gm; ++bl) {
-        double2* f = flm + (int64_t)(b0 + bl) * L * L + ell * ell + ell;
-        f[m] = make_double2(acc[4 * bl], acc[4 * bl + 1]);
-        if (m > 0) f[-m] = make_double2(acc[4 * bl + 2], acc[4 * bl + 3]);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane < T) *cluster.map_shared_rank(apart + ((s - 1) & 3) * T * CC + rank * CC + c, lane) = acc;
       }
     }
-    cluster.sync();
-    if (m == 0) break;
-    // ---- phase 2: corrections for rings k < m
-    for (int idx = tid; idx < n * CC; idx += SWEEP_THREADS) vec[idx] = __ldcg(xg + idx);
+  };
+
+  // ---- prologue: x'_{L-1}, a_{L-2}, R[L-1][0]
+  load_perm(L - 1);
+  gather_issue(L - 1);
+  gather_store(L - 1);
+  __syncthreads();
+  bulk(L - 1);
+  load_rch(L - 1);
+  if (L >= 2) load_perm(L - 2);
+  cluster.sync();
+
+  PROF_DECL
+  double beta_next = L >= 2 ? __ldg(beta_all + L - 1) : 0.0;  // beta_{t+1} of the coming step
+  for (int t = L - 1; t >= 0; --t) {
+    const int nt = L - t;
+    const double st = (t & 1) ? -1.0 : 1.0;
+    const double bt = beta_next;
+    if (t >= 1) beta_next = __ldg(beta_all + t);  // consumed one step later
+    // right-hand side of order t-1 is final now: start its gather
+    if (t >= 1) gather_issue(t - 1);
+    if (t == 0) load_rch(0);  // order-2 corrections to ring 0 land one step earlier
     __syncthreads();
-    const double* Pb = pbelow + pb_off[m];
-    const int k0 = (rank * m) / T, k1 = ((rank + 1) * m) / T;
-    for (int k = k0 + tid; k < k1; k += SWEEP_THREADS) {
-      double acc[CC];
+    // ---- (a) chain: late entries L_t of every map
+    if (tid < NB4 && tid < gm) {
+      const int b = tid;
+      double gp_r = 0.0, gp_i = 0.0, gm_r = 0.0, gm_i = 0.0;  // G+_{t+1}(theta_t), G-_{t+1}(theta_t)
+      if (t < L - 1) {
+        const double s1 = ((t + 1) & 1) ? -1.0 : 1.0;
+        double a[4] = {0.0, 0.0, 0.0, 0.0};
+        const double* ap = apart + (size_t)(t & 3) * T * CC + 4 * b;
+        for (int q = 0; q < T; ++q)
 #pragma unroll
-      for (int c = 0; c < CC; ++c) acc[c] = 0.0;
-      for (int l = 0; l < n; ++l) {
-        const double a = __ldg(Pb + (int64_t)l * m + k);
-        const double* xv = vec + (size_t)l * CC;
-#pragma unroll
-        for (int c = 0; c < CC; ++c) acc[c] = fma(a, xv[c], acc[c]);
+          for (int u = 0; u < 4; ++u) a[u] += ap[(size_t)q * CC + u];
+        const double* ln = late + (size_t)((t + 1) & 1) * CC + 4 * b;
+        gp_r = a[0] + bt * ln[0];
+        gp_i = a[1] + bt * ln[1];
+        gm_r = s1 * (a[2] + bt * ln[2]);
+        gm_i = s1 * (a[3] + bt * ln[3]);
       }
-      const int nk = 2 * k + 1;
-      const int r = m % nk;
-      int tm, tp_slot, tn_slot;  // target order; R slot receiving G+ and G-
-      if (r == 0) {
-        tm = 0;
-        tp_slot = 0;
-        tn_slot = 0;
-      } else if (r <= k) {
-        tm = r;
-        tp_slot = 0;
-        tn_slot = 1;
+      const double* rr = rch + (size_t)(t & 1) * CC + 4 * b;
+      double* lt = late + (size_t)(t & 1) * CC + 4 * b;
+      if (t == 0) {
+        lt[0] = rr[0] - gp_r - gm_r;
+        lt[1] = rr[1] - gp_i - gm_i;
+        lt[2] = 0.0;
+        lt[3] = 0.0;
       } else {
-        tm = nk - r;
-        tp_slot = 1;
-        tn_slot = 0;
+        lt[0] = rr[0] - gm_r;
+        lt[1] = rr[1] - gm_i;
+        lt[2] = st * (rr[2] - gp_r);
+        lt[3] = st * (rr[3] - gp_i);
       }
-      const int64_t tbase = packed_pos(L, tm, k - tm) * 2 * B + b0;
-      for (int bl = 0; bl < gm; ++bl) {
-        const double2 gp = make_double2(acc[4 * bl], acc[4 * bl + 1]);
-        const double2 gn = make_double2(sgn * acc[4 * bl + 2], sgn * acc[4 * bl + 3]);
-        double2* rp = R + tbase + tp_slot * B + bl;
-        double2 v = __ldcg(rp);
-        v.x -= gp.x;
-        v.y -= gp.y;
-        if (tn_slot == tp_slot) {
-          v.x -= gn.x;
-          v.y -= gn.y;
-          *rp = v;
-        } else {
-          *rp = v;
-          double2* rn = R + tbase + tn_slot * B + bl;
-          double2 w = __ldcg(rn);
-          w.x -= gn.x;
-          w.y -= gn.y;
-          *rn = w;
+    }
+    __syncthreads();
+    // ---- (b) x_t = x'_t + w_t L_t on own rows -> flm and every rank's xfull
+    {
+      const int nrt = (nt + 7) / 8;
+      const int r0 = 8 * ((rank * nrt) / T), r1 = min(nt, 8 * (((rank + 1) * nrt) / T));
+      const double* xps = xp + (size_t)(t & 1) * CC * ldr;
+      const double* wvs = wv + (size_t)(t & 1) * ldr;
+      const double* lt = late + (size_t)(t & 1) * CC;
+      double* xf = xfull + (size_t)(t & 1) * (CC + 1) * ldx;
+      for (int idx = tid; idx < (r1 - r0) * (CC / 2); idx += SWEEP_THREADS) {
+        const int l = r0 + idx / (CC / 2), c = 2 * (idx % (CC / 2));
+        const double wl = wvs[l - r0];
+        const double v0 = xps[(size_t)c * ldr + (l - r0)] + wl * lt[c];
+        const double v1 = xps[(size_t)(c + 1) * ldr + (l - r0)] + wl * lt[c + 1];
+        for (int q = 0; q < T; ++q) {
+          *cluster.map_shared_rank(xf + (size_t)c * ldx + l, q) = v0;
+          *cluster.map_shared_rank(xf + (size_t)(c + 1) * ldx + l, q) = v1;
+        }
+        const int bl = c >> 2;
+        if (bl < gm) {
+          const int64_t ell = t + l;
+          double2* f = flm + (int64_t)(b0 + bl) * L * L + ell * ell + ell;
+          if ((c & 2) == 0) f[t] = make_double2(v0, v1);
+          else if (t > 0) f[-t] = make_double2(v0, v1);
         }
       }
     }
+    PROF_MARK(0);
+    // ---- (c) CORR(t+1): corrections of order s = t+1 on own rings k < t
+    if (t >= 1 && t + 1 <= L - 1) {
+      const int s = t + 1;
+      const double ss = (s & 1) ? -1.0 : 1.0;
+      const Job j = make_job(1, s, L, T, rank, KC, xt, xt_off, pbt, pb_off);
+      run_job(j, xfull + (size_t)(s & 1) * (CC + 1) * ldx, ldx, [&](int k, int c, double v0, double v1) {
+        const int bl = c >> 2;
+        if (k >= s - 1 || bl >= gm) return;  // ring s-1 is the chain
+        const bool plus = (c & 2) == 0;
+        const double gr = plus ? v0 : ss * v0, gi = plus ? v1 : ss * v1;
+        const int nk = 2 * k + 1;
+        const int r = s % nk;
+        int tm, slot;
+        if (r == 0) {
+          tm = 0;
+          slot = 0;
+        } else if (r <= k) {
+          tm = r;
+          slot = plus ? 0 : 1;
+        } else {
+          tm = nk - r;
+          slot = plus ? 1 : 0;
+        }
+        // fire-and-forget reductions (RED.ADD.F64): no load latency on the step's
+        // critical path; at most two tones (r == 0) hit one bin per step
+        double2* rp = R + (packed_pos(L, tm, k - tm) * 2 + slot) * B + b0 + bl;
+        atomicAdd(&rp->x, -gr);
+        atomicAdd(&rp->y, -gi);
+      });
+    }
+    PROF_MARK(1);
+    // ---- (d) BULK(t-1): x'_{t-1}, a_{t-2}; prefetch R[t-1][0] and the next permutation
+    if (t >= 1) {
+      gather_store(t - 1);
+      if (t >= 2) load_perm(t - 2);
+      __syncthreads();
+      PROF_MARK(2);
+      bulk(t - 1);
+      if (t >= 2) load_rch(t - 1);
+    }
+    PROF_MARK(3);
     cluster.sync();
+    PROF_MARK(4);
   }
+  PROF_DUMP();
 }
 
+static size_t sweep_smem_bytes(const SweepCfg& c) { return sizeof(double) * c.total; }
+
 template <int CC>
-static cudaError_t launch_sweep_cc(osph_plan* p, int B, int g, int T, double2* flm) {
+static cudaError_t launch_sweep_cc(osph_plan* p, int B, int g, int T, int KC, int S, double2* flm) {
   const int L = p->L;
   const int teams = (B + g - 1) / g;
-  const size_t smem = sizeof(double) * (size_t)L * CC;
+  const SweepCfg cfg(L, T, CC, KC, S);
+  const size_t smem = sweep_smem_bytes(cfg);
   auto kern = k_sweep<CC>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (T > 8 && (e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
     return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(teams * T));
-  cfg.blockDim = dim3(SWEEP_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = p->stream;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)(teams * T));
+  lc.blockDim = dim3(SWEEP_THREADS);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = p->stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = T;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, L, B, g, (const double*)p->d_ainv, (const int64_t*)p->d_ainv_off,
-                         (const int*)p->d_piv, (const double*)p->d_pbelow, (const int64_t*)p->d_pb_off, p->d_r,
-                         p->d_x, flm);
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  if (getenv("OSPH_DEBUG")) {
+    int nclusters = -1;
+    cudaOccupancyMaxActiveClusters(&nclusters, (void*)kern, &lc);
+    fprintf(stderr, "[osph] sweep L=%d B=%d maps/team=%d teams=%d T=%d KC=%d S=%d smem=%zu maxActiveClusters=%d\n", L,
+            B, g, teams, T, KC, S, smem, nclusters);
+  }
+  e = cudaLaunchKernelEx(&lc, kern, L, B, g, KC, S, (const double*)p->d_xt, (const int64_t*)p->d_xt_off,
+                         (const int*)p->d_piv, (const int*)p->d_jstar, (const double*)p->d_beta,
+                         (const double*)p->d_pbelow, (const int64_t*)p->d_pb_off, p->d_r, flm);
   p->launches++;
   return e;
 }
 
+template <int CC>
+static int max_active_clusters(int L, int T, int KC, int S) {
+  const size_t smem = sweep_smem_bytes(SweepCfg(L, T, CC, KC, S));
+  auto kern = k_sweep<CC>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+  if (T > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)T);
+  lc.blockDim = dim3(SWEEP_THREADS);
+  lc.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = T;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, (void*)kern, &lc) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 cudaError_t launch_sweep(osph_plan* p, int B, double2* flm) {
-  const int g = B >= 4 ? 4 : B;
-  const int teams = (B + g - 1) / g;
+  const int L = p->L;
+  const size_t cap = 220 * 1024;
+  // maps per team: 4 (16 columns) / 2 / 1, limited by the register-held
+  // gather (L * CC/4 <= 8 * 256) and by shared memory
+  int g = B >= 3 ? 4 : B;
+  while (g > 1 && (size_t)L * g > (size_t)SWEEP_UMAX * SWEEP_THREADS) g /= 2;
   int T = 1;
-  while (T < 16 && teams * T * 2 <= 148 && T * 32 < p->L) T *= 2;
-  if (g == 4 || B == 3) return launch_sweep_cc<16>(p, B, 4, T, flm);
-  if (g == 2) return launch_sweep_cc<8>(p, B, 2, T, flm);
-  return launch_sweep_cc<4>(p, B, 1, T, flm);
+  while (T < 16 && ((B + g - 1) / g) * T * 2 <= 148 * 2 && T * 32 < L) T *= 2;
+  const int KC = SWEEP_KC;
+  int S = 8;
+  // a job's tiles must fit one row of threads (side loads) and the per-warp accumulators
+  auto tiles_ok = [&](int gg, int TT) {
+    const int tpc = ((L + 7) / 8 + TT - 1) / TT;
+    return tpc <= 32 && tpc * ((4 * gg + 7) / 8) <= SWEEP_WARPS * SWEEP_IPW;
+  };
+  auto fits = [&](int gg, int TT, int kc, int ss) { return sweep_smem_bytes(SweepCfg(L, TT, 4 * gg, kc, ss)) <= cap; };
+  auto mac = [&](int gg, int TT, int kc, int ss) {
+    return gg == 4 ? max_active_clusters<16>(L, TT, kc, ss)
+                   : gg == 2 ? max_active_clusters<8>(L, TT, kc, ss) : max_active_clusters<4>(L, TT, kc, ss);
+  };
+  T = env_int("OSPH_SWEEP_T", T);
+  for (int iter = 0; iter < 16; ++iter) {
+    while (T < 16 && !tiles_ok(g, T)) T *= 2;
+    while (!fits(g, T, KC, S)) {
+      if (S > 3) --S;
+      else if (T < 16) T *= 2;
+      else if (g > 1) g /= 2;
+      else break;
+    }
+    // keep every team resident at once (teams never wait on each other, but
+    // a second wave doubles the sweep's latency-bound wall time)
+    const int teams = (B + g - 1) / g;
+    if (T > 1 && tiles_ok(g, T / 2) && fits(g, T / 2, KC, S) && !getenv("OSPH_SWEEP_T") &&
+        mac(g, T, KC, S) < teams)
+      T /= 2;
+    else
+      break;
+  }
+  S = env_int("OSPH_SWEEP_S", S);
+  if (g == 4) return launch_sweep_cc<16>(p, B, 4, T, KC, S, flm);
+  if (g == 2) return launch_sweep_cc<8>(p, B, 2, T, KC, S, flm);
+  return launch_sweep_cc<4>(p, B, 1, T, KC, S, flm);
 }

@@ -152,6 +152,12 @@ class Plan:
     def last_launch_count(self) -> int:
         return int(self._lib.osph_last_launch_count(self._h))
 
+    def last_stage_times(self) -> np.ndarray:
+        """Device seconds: last inverse's 3 stages, then last forward's 3 (osph_last_stage_times)."""
+        out = np.zeros(6)
+        _lib.raise_for(self._lib.osph_last_stage_times(self._h, out.ctypes.data_as(ctypes.c_void_p)))
+        return out
+
     # raw calls -----------------------------------------------------------
     def inverse_raw(self, B: int, src: int, dst: int, kind: int) -> None:
         _lib.raise_for(self._lib.osph_inverse(self._h, B, ctypes.c_void_p(src), ctypes.c_void_p(dst), kind))
@@ -194,6 +200,13 @@ def clear_plans() -> None:
 # batched entry points
 
 
+def torch_stream_handle(stream) -> int:
+    """cudaStream_t of a torch stream; torch's default stream (handle 0) maps to
+    cudaStreamLegacy (1), since NULL means "plan-owned stream" in the C ABI."""
+    h = int(stream.cuda_stream)
+    return h if h != 0 else 1
+
+
 def _is_torch_cuda(x) -> bool:
     return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
 
@@ -215,7 +228,7 @@ def _run(direction: str, data, grid, out=None, check: bool = True, device: int =
         y = out if out is not None else torch.empty_like(x)
         plan = get_plan(grid, B, dev)
         with plan.lock:
-            plan.set_stream(torch.cuda.current_stream(x.device).cuda_stream)
+            plan.set_stream(torch_stream_handle(torch.cuda.current_stream(x.device)))
             if direction == "inverse":
                 plan.inverse_raw(B, x.data_ptr(), y.data_ptr(), _lib.OSPH_DEVICE)
                 return y, None
