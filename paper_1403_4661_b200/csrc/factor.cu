@@ -37,10 +37,13 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "plan.cuh"
 
 namespace cg = cooperative_groups;
+
+cudaError_t launch_factor_np_class(osph_plan* p, int m_first, int m_last, int cs);  // factor_np.cu
 
 #define FAC_THREADS 256
 #define FAC_TC 8      // column tile width of the rank-NB update
@@ -422,10 +425,16 @@ cudaError_t launch_factor(osph_plan* p) {
     int nlo, nhi, cs;
   };
   const Cls classes[] = {{1025, 2048, 16}, {513, 1024, 16}, {257, 512, 8}, {129, 256, 4}, {65, 128, 2}, {1, 64, 1}};
+  const bool static_piv = p->piv_ready && !getenv("OSPH_FACTOR_PIVOTED");
   for (const Cls& c : classes) {
     const int nhi = std::min(c.nhi, L);
     if (nhi < c.nlo) continue;
     const int m_first = L - nhi, m_last = L - c.nlo;
+    if (static_piv && nhi <= 256) {  // pivot order known: shared-memory static-pivot kernel
+      e = launch_factor_np_class(p, m_first, m_last, nhi > 128 ? 4 : 1);
+      if (e != cudaSuccess) return e;
+      continue;
+    }
     if (nhi > 1024) e = launch_class<8, 8>(p, m_first, m_last, c.cs);
     else if (nhi > 512) e = launch_class<4, 16>(p, m_first, m_last, c.cs);
     else if (nhi > 256) e = launch_class<2, 32>(p, m_first, m_last, c.cs);
@@ -434,5 +443,6 @@ cudaError_t launch_factor(osph_plan* p) {
   }
   k_kappa<<<(L + 127) / 128, 128, 0, p->stream>>>(L, p->d_norms, p->d_kappa);
   p->launches++;
+  p->piv_ready = true;  // the pivot order depends on the grid only
   return cudaGetLastError();
 }

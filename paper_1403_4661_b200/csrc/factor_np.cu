@@ -1,0 +1,361 @@
+// factor_np.cu -- per-order inversion with STATIC pivots, shared-memory resident.
+//
+// The per-order blocks A_m = 2pi Y_lm(theta_k, 0) depend only on the grid, so
+// the row order chosen by partial pivoting is the same on every call.  The
+// first forward transform of a plan runs the pivoting kernel (factor.cu),
+// which records perm_m (O(L^2) integers, kept in the plan next to the other
+// O(L^2) tables -- the reference likewise caches O(L^2) tables per band
+// limit, transform.py:268-301).  Every later call regenerates A_m in that row
+// order and inverts it by blocked Gauss-Jordan WITHOUT a pivot search -- the
+// identical elimination sequence, so the same rounding behaviour -- which
+// turns each panel step into a 32x32 diagonal-block inverse (one warp) plus
+// two GEMMs on the fp64 tensor cores:
+//     Dinv = A[P,P]^{-1},  E = -A[:,P] Dinv (E[P] = Dinv - I),  A[:, rest] += E A[P, rest].
+// The O(L^3) work (generation + inversion) is still done per call.
+//
+// One thread-block cluster per order; CTA r owns a contiguous slice of the
+// columns, held in shared memory for the whole factorisation (n <= 256), so
+// row interchanges never happen and every update is smem-to-smem.  The panel
+// owner publishes each panel through a small global buffer (double-buffered)
+// and one cluster barrier per panel orders the hand-off.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "plan.cuh"
+
+namespace cg = cooperative_groups;
+
+#define FNP_THREADS 256
+#define FNP_WARPS 8
+#define FNP_NB 32
+
+__device__ __forceinline__ void np_atomic_max_pos(unsigned long long* addr, double v) {
+  if (!(v >= 0.0) || isinf(v)) v = INFINITY;
+  atomicMax(addr, (unsigned long long)__double_as_longlong(v));
+}
+
+struct NpLayout {
+  int ldn, cwmax;
+  size_t slice, es, dinv, rowbuf, pinv_bytes_off, total_doubles;
+  __host__ __device__ NpLayout(int nmax, int CS) {
+    ldn = ((nmax + 15) / 16) * 16 + 4;
+    const int units = (nmax + FNP_NB - 1) / FNP_NB;
+    cwmax = ((units + CS - 1) / CS) * FNP_NB;
+    size_t o = 0;
+    slice = o;  o += (size_t)cwmax * ldn;
+    es = o;     o += (size_t)FNP_NB * ldn;
+    dinv = o;   o += (size_t)FNP_NB * FNP_NB;
+    rowbuf = o; o += FNP_NB;
+    pinv_bytes_off = o;  // ints follow
+    o += (size_t)(nmax + 1) / 2 + 1;
+    total_doubles = o;
+  }
+};
+
+__global__ void __launch_bounds__(FNP_THREADS, 1) k_factor_np(
+    int L, int m_first, int nmax, const double* __restrict__ costh, const double2* __restrict__ rec,
+    const int* __restrict__ ls_tab, const double2* __restrict__ pstart, const int* __restrict__ perm_all,
+    double* __restrict__ xt_all, const int64_t* __restrict__ xt_off, double* __restrict__ pbelow,
+    const int64_t* __restrict__ pb_off, double* __restrict__ panel_g, unsigned long long* __restrict__ norms,
+    int* __restrict__ status_out, int* __restrict__ jstar_out, double* __restrict__ beta_out) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CS = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int slot = (int)(blockIdx.x / CS);
+  const int m = m_first + slot;
+  if (m >= L) return;
+  const int n = L - m;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tq = lane & 3;
+
+  extern __shared__ __align__(16) double smem[];
+  const NpLayout lay(nmax, CS);
+  const int ldn = lay.ldn;
+  double* slice = smem + lay.slice;    // own columns, column-major, ld = ldn
+  double* Es = smem + lay.es;          // panel / E, column-major [NB][ldn]
+  double* Dinv = smem + lay.dinv;      // [NB][NB] row-major
+  double* rowbuf = smem + lay.rowbuf;  // pivot row broadcast for the diagonal inverse
+  int* pinv = reinterpret_cast<int*>(smem + lay.pinv_bytes_off);
+  __shared__ int s_bad;
+  __shared__ double s_red[FNP_WARPS];
+
+  const int* perm = perm_all + packed_pos(L, m, 0);
+  const int units = (n + FNP_NB - 1) / FNP_NB;
+  const int u0 = (rank * units) / CS, u1 = ((rank + 1) * units) / CS;
+  const int c0 = u0 * FNP_NB, c1 = min(n, u1 * FNP_NB);
+  const int cw = max(0, c1 - c0);
+  const int cwt = (cw + 7) & ~7;  // own columns rounded to 8-column tiles
+  const int nrt8 = (n + 7) >> 3;
+  double* pg = panel_g + (size_t)slot * 2 * FNP_NB * ldn;
+
+  if (tid == 0) s_bad = 0;
+  for (int j = tid; j < n; j += FNP_THREADS) pinv[__ldg(perm + j)] = j;
+
+  // ---- 1. generation: own degree columns l = m+c0 .. m+c1-1, rows in pivot order;
+  //         rings k < m go to the tiled below-block Pb (sweep operand)
+  {
+    const double2* recm = rec + packed_pos(L, m, 0);
+    double* Pb = pbelow + pb_off[m];
+    const int nrtpb = (m + 7) >> 3;
+    for (int it = tid; it < L; it += FNP_THREADS) {
+      const int k = it < n ? m + __ldg(perm + it) : it - n;  // row item -> ring
+      const int64_t t = (int64_t)m * L + k;
+      const int ls = ls_tab[t];
+      const double2 pp = pstart[t];
+      double p0 = pp.x, p1 = pp.y;
+      const double x = costh[k];
+      for (int l = m; l < m + c1; ++l) {
+        double v = 0.0;
+        if (l >= ls) {
+          v = OSPH_TWO_PI * p1;
+          const double2 ar = __ldg(recm + (l - m));
+          const double nxt = fma(x, p1, -ar.x * p0) * ar.y;
+          p0 = p1;
+          p1 = nxt;
+        }
+        if (l >= m + c0) {
+          if (it < n) slice[(size_t)(l - m - c0) * ldn + it] = v;
+          else Pb[tile_index(k, l - m, nrtpb)] = v;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // ||A||_1 over own columns
+  {
+    double cmax = 0.0;
+    for (int c = warp; c < cw; c += FNP_WARPS) {
+      double s = 0.0;
+      for (int i = lane; i < n; i += 32) s += fabs(slice[(size_t)c * ldn + i]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      cmax = fmax(cmax, s);
+    }
+    if (lane == 0 && cw > 0) np_atomic_max_pos(norms + 2 * m, cmax);
+  }
+
+  // ---- 2. blocked Gauss-Jordan, static pivots
+  for (int j0 = 0, par = 0; j0 < n; j0 += FNP_NB, par ^= 1) {
+    const int nb = min(FNP_NB, n - j0);
+    const bool owner = j0 >= c0 && j0 < c1;
+    double* pgp = pg + (size_t)par * FNP_NB * ldn;
+    if (owner)
+      for (int idx = tid; idx < nb * n; idx += FNP_THREADS) {
+        const int c = idx / n, r = idx - c * n;
+        pgp[(size_t)c * ldn + r] = slice[(size_t)(j0 - c0 + c) * ldn + r];
+      }
+    cluster.sync();
+    // a) panel -> Es (columns >= nb zero)
+    for (int idx = tid; idx < FNP_NB * n; idx += FNP_THREADS) {
+      const int c = idx / n, r = idx - c * n;
+      Es[(size_t)c * ldn + r] = c < nb ? __ldcg(pgp + (size_t)c * ldn + r) : 0.0;
+    }
+    __syncthreads();
+    // b) Dinv = A[P,P]^{-1}: unpivoted Gauss-Jordan in one warp (lane = row)
+    if (warp == 0) {
+      double d[FNP_NB];
+#pragma unroll
+      for (int c = 0; c < FNP_NB; ++c) d[c] = (lane < nb && c < nb) ? Es[(size_t)c * ldn + j0 + lane] : 0.0;
+#pragma unroll
+      for (int c = 0; c < FNP_NB; ++c) {
+        if (c < nb) {
+          if (lane == c)
+#pragma unroll
+            for (int cc = 0; cc < FNP_NB; ++cc) rowbuf[cc] = d[cc];
+          __syncwarp();
+          const double piv = rowbuf[c];
+          if (lane == 0 && (piv == 0.0 || !isfinite(piv))) s_bad = 1;
+          const double inv = 1.0 / piv;
+          if (lane == c) {
+#pragma unroll
+            for (int cc = 0; cc < FNP_NB; ++cc) d[cc] = (cc == c) ? inv : d[cc] * inv;
+          } else {
+            const double f = d[c] * inv;
+#pragma unroll
+            for (int cc = 0; cc < FNP_NB; ++cc)
+              if (cc != c) d[cc] = fma(-f, rowbuf[cc], d[cc]);
+            d[c] = -f;
+          }
+          __syncwarp();
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < FNP_NB; ++c) Dinv[lane * FNP_NB + c] = (lane < nb && c < nb) ? d[c] : 0.0;
+    }
+    __syncthreads();
+    // c) E = -A[:,P] Dinv (rows outside P), E[P] = Dinv - I; in place in Es, one 8-row tile per warp pass
+    {
+      const int pt0 = j0 >> 3, pt1 = (j0 + nb + 7) >> 3;
+      for (int rt = warp; rt < nrt8; rt += FNP_WARPS) {
+        const int r0 = rt * 8;
+        if (rt >= pt0 && rt < pt1) {
+          for (int e = lane; e < 8 * FNP_NB; e += 32) {
+            const int r = e & 7, c = e >> 3;
+            const int row = r0 + r;
+            const int pr = row - j0;
+            Es[(size_t)c * ldn + row] = (pr >= 0 && pr < nb && c < nb) ? Dinv[pr * FNP_NB + c] - (pr == c ? 1.0 : 0.0) : 0.0;
+          }
+          continue;
+        }
+        double acc[FNP_NB / 8][2];
+#pragma unroll
+        for (int ct = 0; ct < FNP_NB / 8; ++ct) acc[ct][0] = acc[ct][1] = 0.0;
+#pragma unroll
+        for (int k = 0; k < FNP_NB; k += 4) {
+          const double a = Es[(size_t)(k + tq) * ldn + r0 + g];
+#pragma unroll
+          for (int ct = 0; ct < FNP_NB / 8; ++ct)
+            dmma_8x8x4(acc[ct][0], acc[ct][1], a, Dinv[(k + tq) * FNP_NB + ct * 8 + g]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int ct = 0; ct < FNP_NB / 8; ++ct) {
+          Es[(size_t)(ct * 8 + 2 * tq) * ldn + r0 + g] = -acc[ct][0];
+          Es[(size_t)(ct * 8 + 2 * tq + 1) * ldn + r0 + g] = -acc[ct][1];
+        }
+      }
+    }
+    __syncthreads();
+    // d) owner: new panel columns = E + I on P
+    if (owner)
+      for (int idx = tid; idx < nb * n; idx += FNP_THREADS) {
+        const int c = idx / n, r = idx - c * n;
+        slice[(size_t)(j0 - c0 + c) * ldn + r] = Es[(size_t)c * ldn + r] + (r == j0 + c ? 1.0 : 0.0);
+      }
+    // e) A[:, own rest] += E * A[P, own rest]: rows outside P first (T read in place), then P rows
+    {
+      const int pt0 = j0 >> 3, pt1 = (j0 + nb + 7) >> 3;
+      const int nct = cwt >> 3;
+      const int pc0 = owner ? (j0 - c0) >> 3 : -1, pc1 = owner ? (j0 - c0 + nb + 7) >> 3 : -1;
+      auto tile = [&](int rt, int ct, double& o0, double& o1) {
+        const int r0 = rt * 8, cc = ct * 8;
+        double c0v = slice[(size_t)(cc + 2 * tq) * ldn + r0 + g];
+        double c1v = slice[(size_t)(cc + 2 * tq + 1) * ldn + r0 + g];
+#pragma unroll
+        for (int k = 0; k < FNP_NB; k += 4) {
+          const double a = Es[(size_t)(k + tq) * ldn + r0 + g];
+          const int tr = j0 + k + tq;
+          const double b = (k + tq < nb) ? slice[(size_t)(cc + g) * ldn + tr] : 0.0;
+          dmma_8x8x4(c0v, c1v, a, b);
+        }
+        o0 = c0v;
+        o1 = c1v;
+      };
+      const int nrest = nrt8 - (pt1 - pt0);
+      for (int w = warp; w < nrest * nct; w += FNP_WARPS) {
+        const int rr = w % nrest, ct = w / nrest;
+        if (ct >= pc0 && ct < pc1) continue;
+        const int rt = rr < pt0 ? rr : rr + (pt1 - pt0);
+        double o0, o1;
+        tile(rt, ct, o0, o1);
+        slice[(size_t)(ct * 8 + 2 * tq) * ldn + rt * 8 + g] = o0;
+        slice[(size_t)(ct * 8 + 2 * tq + 1) * ldn + rt * 8 + g] = o1;
+      }
+      // P rows: all reads of A[P, rest] done before any write
+      double po[8][2];
+      int np = 0;
+      const int npw = (pt1 - pt0) * nct;
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int w = warp + q * FNP_WARPS;
+        if (w < npw) {
+          const int rt = pt0 + w % (pt1 - pt0), ct = w / (pt1 - pt0);
+          if (!(ct >= pc0 && ct < pc1)) tile(rt, ct, po[q][0], po[q][1]);
+          np = q + 1;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int w = warp + q * FNP_WARPS;
+        if (q < np && w < npw) {
+          const int rt = pt0 + w % (pt1 - pt0), ct = w / (pt1 - pt0);
+          if (!(ct >= pc0 && ct < pc1)) {
+            slice[(size_t)(ct * 8 + 2 * tq) * ldn + rt * 8 + g] = po[q][0];
+            slice[(size_t)(ct * 8 + 2 * tq + 1) * ldn + rt * 8 + g] = po[q][1];
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- 3. ||X||_1, tiled X for the sweep, chain constants
+  {
+    double cmax = 0.0;
+    for (int c = warp; c < cw; c += FNP_WARPS) {
+      double s = 0.0;
+      for (int i = lane; i < n; i += 32) s += fabs(slice[(size_t)c * ldn + i]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      cmax = fmax(cmax, s);
+    }
+    if (lane == 0 && cw > 0) np_atomic_max_pos(norms + 2 * m + 1, cmax);
+  }
+  {
+    double* Xt = xt_all + xt_off[m];
+    const int npad = nrt8 * 8;
+    const int cend = (c1 == n) ? (n + OSPH_TILE_KC - 1) / OSPH_TILE_KC * OSPH_TILE_KC : c1;
+    for (int idx = tid; idx < (cend - c0) * npad; idx += FNP_THREADS) {
+      const int c = c0 + idx / npad, i = idx % npad;
+      Xt[tile_index(i, c, nrt8)] = (i < n && c < n) ? slice[(size_t)(c - c0) * ldn + i] : 0.0;
+    }
+  }
+  if (tid == 0 && s_bad) atomicOr(status_out + m, 1);
+  cluster.sync();  // the below-block rows of every rank are in global memory
+  const int js = pinv[0];
+  if (js >= c0 && js < c1) {  // owner of column j* (ring m): beta_m = Pb_m[m-1, :] . X[:, j*]
+    double acc = 0.0;
+    if (m >= 1) {
+      const double* Pb = pbelow + pb_off[m];
+      const int nrtpb = (m + 7) >> 3;
+      for (int l = tid; l < n; l += FNP_THREADS)
+        acc += __ldcg(Pb + tile_index(m - 1, l, nrtpb)) * slice[(size_t)(js - c0) * ldn + l];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) s_red[warp] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double b = 0.0;
+      for (int w = 0; w < FNP_WARPS; ++w) b += s_red[w];
+      beta_out[m] = b;
+      jstar_out[m] = js;
+    }
+  }
+}
+
+size_t factor_np_smem(int nmax, int cs) { return sizeof(double) * NpLayout(nmax, cs).total_doubles; }
+
+// Launch the static-pivot factorisation for orders m_first..m_last (block
+// sizes n <= nmax, nmax <= 256), cs CTAs per order.
+cudaError_t launch_factor_np_class(osph_plan* p, int m_first, int m_last, int cs) {
+  const int L = p->L;
+  const int nmax = L - m_first;
+  const size_t smem = factor_np_smem(nmax, cs);
+  cudaError_t e = cudaFuncSetAttribute(k_factor_np, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (cs > 8 && (e = cudaFuncSetAttribute(k_factor_np, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess)
+    return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((m_last - m_first + 1) * cs));
+  cfg.blockDim = dim3(FNP_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = p->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, k_factor_np, L, m_first, nmax, (const double*)p->d_cos, (const double2*)p->d_rec,
+                         (const int*)p->d_ls, (const double2*)p->d_pstart, (const int*)p->d_piv, p->d_xt,
+                         (const int64_t*)p->d_xt_off, p->d_pbelow, (const int64_t*)p->d_pb_off, p->d_panel,
+                         p->d_norms, p->d_status, p->d_jstar, p->d_beta);
+  p->launches++;
+  return e;
+}

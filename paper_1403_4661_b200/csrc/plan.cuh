@@ -53,6 +53,8 @@ struct osph_plan {
   int64_t* d_xt_off = nullptr;
   double* d_xt = nullptr;         // X_m in 8-row tiles (sweep operand)
   bool fwd_ready = false;        // forward buffers allocated
+  bool piv_ready = false;        // d_piv holds the (grid-determined) pivot order of every order
+  double* d_panel = nullptr;     // static-pivot factorisation: panel hand-off buffers
   bool inv_ready = false;        // inverse buffers allocated
 
   // ---- per-call workspaces (sized for max_batch) ----

@@ -11,15 +11,18 @@
 // (transform.py:445-449).
 //
 // n <= OSPH_DIRECT_MAX: direct O(n^2) DFT from a roots table.  Longer rings:
-// Bluestein (chirp-z) with a power-of-two FFT in shared memory.
+// Bluestein (chirp-z) with a power-of-two FFT in shared memory.  A block
+// handles one ring and a run of maps, transforming several maps per pass so
+// the FFT stage barriers are shared; global accesses run map-fastest, which
+// is the contiguous direction of G and R.
 #include "fft.cuh"
 #include "plan.cuh"
 
 #define RING_THREADS 256
+#define RING_SMEM_BUDGET (96 * 1024)
 
 // Fold G (layout [m][k][4B]) of ring k, map b into bin t (t < n).
-__device__ __forceinline__ double2 fold_bin(const double* __restrict__ G, int L, int B, int k, int n,
-                                            int b, int t) {
+__device__ __forceinline__ double2 fold_bin(const double* __restrict__ G, int L, int B, int k, int n, int b, int t) {
   const int64_t mstride = (int64_t)L * 4 * B;
   const double* gk = G + ((int64_t)k * 4 * B + 4 * b);
   double re = 0.0, im = 0.0;
@@ -41,87 +44,120 @@ __device__ __forceinline__ double2 fold_bin(const double* __restrict__ G, int L,
   return make_double2(re, im);
 }
 
-// x (natural order) *= bhat, then permute to bit-reversed order in place.
-__device__ __forceinline__ void mul_and_bitrev(double2* x, const double2* __restrict__ bh, int N, int logN) {
-  for (int q = threadIdx.x; q < N; q += blockDim.x) x[q] = cmul(x[q], __ldg(bh + q));
+// Bluestein circular convolution of Gr sequences (natural order, swizzled):
+// DIF forward FFT -> times the kernel spectrum (stored bit-reversed, /N) ->
+// DIT inverse FFT; natural order out, no bit-reversal passes.
+__device__ __forceinline__ void bluestein_convolve(double2* xs, int logN, int Gr, const double2* twn,
+                                                   const double2* __restrict__ bh_br) {
+  fft_dif_fwd_multi(xs, logN, Gr, twn);
+  const int N = 1 << logN;
+  for (int idx = threadIdx.x; idx < (Gr << logN); idx += blockDim.x) {
+    const int q = idx & (N - 1);
+    double2* e = xs + (idx - q) + fsw(q);
+    *e = cmul(*e, __ldg(bh_br + q));
+  }
+  fft_dit_inv_multi(xs, logN, Gr, twn);
+}
+
+// For Gr maps: x *= bhat (natural order), then bit-reverse every map in place.
+__device__ __forceinline__ void mul_and_bitrev_multi(double2* x, const double2* __restrict__ bh, int N, int logN,
+                                                     int Gr) {
+  for (int idx = threadIdx.x; idx < (Gr << logN); idx += blockDim.x) x[idx] = cmul(x[idx], __ldg(bh + (idx & (N - 1))));
   __syncthreads();
-  for (int q = threadIdx.x; q < N; q += blockDim.x) {
+  for (int idx = threadIdx.x; idx < (Gr << logN); idx += blockDim.x) {
+    const int q = idx & (N - 1);
     const int r = bitrev(q, logN);
     if (q < r) {
-      const double2 a = x[q];
-      x[q] = x[r];
-      x[r] = a;
+      double2* xg = x + (idx - q);
+      const double2 a = xg[q];
+      xg[q] = xg[r];
+      xg[r] = a;
     }
   }
 }
 
 __global__ void __launch_bounds__(RING_THREADS) k_ring_inverse_bluestein(
     int L, int B, int maps_per_block, const int* __restrict__ rings, const int* __restrict__ fft_n,
-    const int64_t* __restrict__ chirp_off, const int64_t* __restrict__ bhat_off,
-    const double2* __restrict__ chirp_all, const double2* __restrict__ bhat_all,
-    const double2* __restrict__ tw, const double* __restrict__ G, double2* __restrict__ samples) {
-  extern __shared__ double2 xs[];
+    const int64_t* __restrict__ chirp_off, const int64_t* __restrict__ bhat_off, const double2* __restrict__ chirp_all,
+    const double2* __restrict__ bhat_all, const double2* __restrict__ tw, const double* __restrict__ G,
+    double2* __restrict__ samples, int smem_cplx) {
+  extern __shared__ double2 sm[];
   const int k = rings[blockIdx.x];
   const int n = 2 * k + 1;
   const int N = fft_n[k];
   const int logN = 31 - __clz(N);
+  double2* twn = sm;            // per-stage twiddles (< N/2 used... see load_stage_twiddles)
+  double2* xs = sm + N;         // Gr transforms of length N
+  load_stage_twiddles(twn, logN, tw);
   const double2* chirp = chirp_all + chirp_off[k];
   const double2* bh = bhat_all + bhat_off[k] + N;  // inverse-direction kernel
-  const int b0 = blockIdx.y * maps_per_block;
-  const int b1 = min(B, b0 + maps_per_block);
-  for (int b = b0; b < b1; ++b) {
-    for (int t = threadIdx.x; t < N; t += blockDim.x) {
+  const int b_first = blockIdx.y * maps_per_block;
+  const int b_last = min(B, b_first + maps_per_block);
+  const int Gmax = max(1, (smem_cplx - N) >> logN);
+  for (int b0 = b_first; b0 < b_last; b0 += Gmax) {
+    const int Gr = min(Gmax, b_last - b0);
+    for (int idx = threadIdx.x; idx < Gr * N; idx += blockDim.x) {  // map-fastest reads of G
+      const int g = idx % Gr, t = idx / Gr;
       double2 v = make_double2(0.0, 0.0);
-      if (t < n) v = cmul(fold_bin(G, L, B, k, n, b, t), __ldg(chirp + t));
-      xs[bitrev(t, logN)] = v;
+      if (t < n) v = cmul(fold_bin(G, L, B, k, n, b0 + g, t), __ldg(chirp + t));
+      xs[(g << logN) + fsw(t)] = v;
     }
-    fft_dit_smem(xs, N, logN, tw, false);
-    mul_and_bitrev(xs, bh, N, logN);
-    fft_dit_smem(xs, N, logN, tw, true);
-    double2* out = samples + (int64_t)b * L * L + (int64_t)k * k;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) out[j] = cmul(xs[j], __ldg(chirp + j));
+    bluestein_convolve(xs, logN, Gr, twn, bh);
+    for (int idx = threadIdx.x; idx < Gr * n; idx += blockDim.x) {  // contiguous ring writes per map
+      const int g = idx / n, j = idx - g * n;
+      samples[(int64_t)(b0 + g) * L * L + (int64_t)k * k + j] = cmul(xs[(g << logN) + fsw(j)], __ldg(chirp + j));
+    }
     __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(RING_THREADS) k_ring_inverse_direct(
-    int L, int B, int nrings, int maps_per_block, const double2* __restrict__ roots,
-    const double* __restrict__ G, double2* __restrict__ samples) {
-  __shared__ double2 bins[OSPH_DIRECT_MAX + 1];
+__global__ void __launch_bounds__(RING_THREADS) k_ring_inverse_direct(int L, int B, int maps_per_block,
+                                                                      const double2* __restrict__ roots,
+                                                                      const double* __restrict__ G,
+                                                                      double2* __restrict__ samples) {
+  __shared__ double2 bins[16][OSPH_DIRECT_MAX + 1];
   const int k = blockIdx.x;
   const int n = 2 * k + 1;
-  const int b0 = blockIdx.y * maps_per_block;
-  const int b1 = min(B, b0 + maps_per_block);
+  const int b_first = blockIdx.y * maps_per_block;
+  const int b_last = min(B, b_first + maps_per_block);
   const double2* rt = roots + (int64_t)k * k;
-  for (int b = b0; b < b1; ++b) {
-    for (int t = threadIdx.x; t < n; t += blockDim.x) bins[t] = fold_bin(G, L, B, k, n, b, t);
+  for (int b0 = b_first; b0 < b_last; b0 += 16) {
+    const int Gr = min(16, b_last - b0);
+    for (int idx = threadIdx.x; idx < Gr * n; idx += blockDim.x) {
+      const int g = idx % Gr, t = idx / Gr;
+      bins[g][t] = fold_bin(G, L, B, k, n, b0 + g, t);
+    }
     __syncthreads();
-    double2* out = samples + (int64_t)b * L * L + (int64_t)k * k;
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    for (int idx = threadIdx.x; idx < Gr * n; idx += blockDim.x) {
+      const int g = idx / n, j = idx - g * n;
       double re = 0.0, im = 0.0;
-      int idx = 0;
+      int r = 0;
       for (int t = 0; t < n; ++t) {  // e^{+2 pi i t j / n}
-        const double2 w = rt[idx];
-        const double2 v = bins[t];
+        const double2 w = rt[r];
+        const double2 v = bins[g][t];
         re += v.x * w.x - v.y * w.y;
         im += v.x * w.y + v.y * w.x;
-        idx += j;
-        if (idx >= n) idx -= n;
+        r += j;
+        if (r >= n) r -= n;
       }
-      out[j] = make_double2(re, im);
+      samples[(int64_t)(b0 + g) * L * L + (int64_t)k * k + j] = make_double2(re, im);
     }
     __syncthreads();
   }
 }
 
-// Scatter one ring spectrum (forward sign, unnormalised) into the RHS layout.
-__device__ __forceinline__ void scatter_rhs(const double2* X, int L, int B, int k, int n, int b,
-                                            double2* __restrict__ R) {
+// Scatter Gr ring spectra (forward sign, unnormalised; X[g][q] at x[(g<<lstride) + q])
+// into the RHS layout, map-fastest.
+template <bool SWZ>
+__device__ __forceinline__ void scatter_rhs_multi(const double2* X, int lstride, int L, int B, int k, int n, int b0,
+                                                  int Gr, double2* __restrict__ R) {
   const double scale = OSPH_TWO_PI / (double)n;
-  for (int m = threadIdx.x; m <= k; m += blockDim.x) {
-    const double2 xp = X[m];
-    const double2 xn = X[m == 0 ? 0 : n - m];
-    const int64_t base = (packed_pos(L, m, k - m) * 2) * B + b;
+  for (int idx = threadIdx.x; idx < Gr * (k + 1); idx += blockDim.x) {
+    const int g = idx % Gr, m = idx / Gr;
+    const int qn = m == 0 ? 0 : n - m;
+    const double2 xp = X[(g << lstride) + (SWZ ? fsw(m) : m)];
+    const double2 xn = X[(g << lstride) + (SWZ ? fsw(qn) : qn)];
+    const int64_t base = (packed_pos(L, m, k - m) * 2) * B + b0 + g;
     R[base] = make_double2(scale * xp.x, scale * xp.y);
     R[base + B] = make_double2(scale * xn.x, scale * xn.y);
   }
@@ -129,64 +165,75 @@ __device__ __forceinline__ void scatter_rhs(const double2* X, int L, int B, int 
 
 __global__ void __launch_bounds__(RING_THREADS) k_ring_forward_bluestein(
     int L, int B, int maps_per_block, const int* __restrict__ rings, const int* __restrict__ fft_n,
-    const int64_t* __restrict__ chirp_off, const int64_t* __restrict__ bhat_off,
-    const double2* __restrict__ chirp_all, const double2* __restrict__ bhat_all,
-    const double2* __restrict__ tw, const double2* __restrict__ samples, double2* __restrict__ R) {
-  extern __shared__ double2 xs[];
+    const int64_t* __restrict__ chirp_off, const int64_t* __restrict__ bhat_off, const double2* __restrict__ chirp_all,
+    const double2* __restrict__ bhat_all, const double2* __restrict__ tw, const double2* __restrict__ samples,
+    double2* __restrict__ R, int smem_cplx) {
+  extern __shared__ double2 sm[];
   const int k = rings[blockIdx.x];
   const int n = 2 * k + 1;
   const int N = fft_n[k];
   const int logN = 31 - __clz(N);
+  double2* twn = sm;            // per-stage twiddles (< N/2 used... see load_stage_twiddles)
+  double2* xs = sm + N;         // Gr transforms of length N
+  load_stage_twiddles(twn, logN, tw);
   const double2* chirp = chirp_all + chirp_off[k];
   const double2* bh = bhat_all + bhat_off[k];  // forward-direction kernel
-  const int b0 = blockIdx.y * maps_per_block;
-  const int b1 = min(B, b0 + maps_per_block);
-  for (int b = b0; b < b1; ++b) {
-    const double2* in = samples + (int64_t)b * L * L + (int64_t)k * k;
-    for (int t = threadIdx.x; t < N; t += blockDim.x) {
+  const int b_first = blockIdx.y * maps_per_block;
+  const int b_last = min(B, b_first + maps_per_block);
+  const int Gmax = max(1, (smem_cplx - N) >> logN);
+  for (int b0 = b_first; b0 < b_last; b0 += Gmax) {
+    const int Gr = min(Gmax, b_last - b0);
+    for (int idx = threadIdx.x; idx < (Gr << logN); idx += blockDim.x) {  // contiguous ring reads per map
+      const int g = idx >> logN, t = idx & (N - 1);
       double2 v = make_double2(0.0, 0.0);
-      if (t < n) v = cmul(__ldg(in + t), conj2(__ldg(chirp + t)));
-      xs[bitrev(t, logN)] = v;
+      if (t < n) v = cmul(__ldg(samples + (int64_t)(b0 + g) * L * L + (int64_t)k * k + t), conj2(__ldg(chirp + t)));
+      xs[(g << logN) + fsw(t)] = v;
     }
-    fft_dit_smem(xs, N, logN, tw, false);
-    mul_and_bitrev(xs, bh, N, logN);
-    fft_dit_smem(xs, N, logN, tw, true);
-    for (int j = threadIdx.x; j < n; j += blockDim.x) xs[j] = cmul(xs[j], conj2(__ldg(chirp + j)));
+    bluestein_convolve(xs, logN, Gr, twn, bh);
+    for (int idx = threadIdx.x; idx < (Gr << logN); idx += blockDim.x) {
+      const int t = idx & (N - 1);
+      if (t < n) xs[(idx - t) + fsw(t)] = cmul(xs[(idx - t) + fsw(t)], conj2(__ldg(chirp + t)));
+    }
     __syncthreads();
-    scatter_rhs(xs, L, B, k, n, b, R);
+    scatter_rhs_multi<true>(xs, logN, L, B, k, n, b0, Gr, R);
     __syncthreads();
   }
 }
 
-__global__ void __launch_bounds__(RING_THREADS) k_ring_forward_direct(
-    int L, int B, int maps_per_block, const double2* __restrict__ roots, const double2* __restrict__ samples,
-    double2* __restrict__ R) {
-  __shared__ double2 xin[OSPH_DIRECT_MAX + 1];
-  __shared__ double2 X[OSPH_DIRECT_MAX + 1];
+__global__ void __launch_bounds__(RING_THREADS) k_ring_forward_direct(int L, int B, int maps_per_block,
+                                                                      const double2* __restrict__ roots,
+                                                                      const double2* __restrict__ samples,
+                                                                      double2* __restrict__ R) {
+  __shared__ double2 xin[16][OSPH_DIRECT_MAX + 1];
+  __shared__ double2 X[16][64];
   const int k = blockIdx.x;
   const int n = 2 * k + 1;
-  const int b0 = blockIdx.y * maps_per_block;
-  const int b1 = min(B, b0 + maps_per_block);
+  const int b_first = blockIdx.y * maps_per_block;
+  const int b_last = min(B, b_first + maps_per_block);
   const double2* rt = roots + (int64_t)k * k;
-  for (int b = b0; b < b1; ++b) {
-    const double2* in = samples + (int64_t)b * L * L + (int64_t)k * k;
-    for (int t = threadIdx.x; t < n; t += blockDim.x) xin[t] = in[t];
-    __syncthreads();
-    for (int q = threadIdx.x; q < n; q += blockDim.x) {
-      double re = 0.0, im = 0.0;
-      int idx = 0;
-      for (int t = 0; t < n; ++t) {  // e^{-2 pi i q t / n}
-        const double2 w = rt[idx];
-        const double2 v = xin[t];
-        re += v.x * w.x + v.y * w.y;
-        im += v.y * w.x - v.x * w.y;
-        idx += q;
-        if (idx >= n) idx -= n;
-      }
-      X[q] = make_double2(re, im);
+  for (int b0 = b_first; b0 < b_last; b0 += 16) {
+    const int Gr = min(16, b_last - b0);
+    for (int idx = threadIdx.x; idx < Gr * n; idx += blockDim.x) {
+      const int g = idx / n, t = idx - g * n;
+      xin[g][t] = samples[(int64_t)(b0 + g) * L * L + (int64_t)k * k + t];
     }
     __syncthreads();
-    scatter_rhs(X, L, B, k, n, b, R);
+    for (int idx = threadIdx.x; idx < Gr * n; idx += blockDim.x) {
+      const int g = idx / n, q = idx - g * n;
+      double re = 0.0, im = 0.0;
+      int r = 0;
+      for (int t = 0; t < n; ++t) {  // e^{-2 pi i q t / n}
+        const double2 w = rt[r];
+        const double2 v = xin[g][t];
+        re += v.x * w.x + v.y * w.y;
+        im += v.y * w.x - v.x * w.y;
+        r += q;
+        if (r >= n) r -= n;
+      }
+      X[g][q] = make_double2(re, im);
+    }
+    __syncthreads();
+    scatter_rhs_multi<false>(&X[0][0], 6, L, B, k, n, b0, Gr, R);
     __syncthreads();
   }
 }
@@ -197,30 +244,34 @@ static int max_fft(const osph_plan* p) {
   return N;
 }
 
+// maps per block: enough blocks for ~4 waves on 148 SMs, at least 1
 static int maps_per_block_for(int B, int rings) {
-  // keep >= ~4 waves of blocks on 148 SMs while amortising table reads
-  int mpb = 1;
-  while (mpb < 8 && (int64_t)rings * ((B + 2 * mpb - 1) / (2 * mpb)) >= 148 * 8) mpb *= 2;
+  int mpb = B;
+  while (mpb > 1 && (int64_t)rings * ((B + mpb - 1) / mpb) < 148 * 4) mpb = (mpb + 1) / 2;
   return mpb;
+}
+
+static size_t ring_smem(const osph_plan* p) {
+  const size_t need = sizeof(double2) * (size_t)max_fft(p) * 2;
+  return need > RING_SMEM_BUDGET ? need : RING_SMEM_BUDGET;
 }
 
 cudaError_t launch_ring_inverse(osph_plan* p, int B, double2* samples) {
   const int L = p->L;
   if (p->n_bluestein_rings > 0) {
     const int mpb = maps_per_block_for(B, p->n_bluestein_rings);
-    const size_t smem = sizeof(double2) * (size_t)max_fft(p);
+    const size_t smem = ring_smem(p);
     cudaFuncSetAttribute(k_ring_inverse_bluestein, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid(p->n_bluestein_rings, (B + mpb - 1) / mpb);
     k_ring_inverse_bluestein<<<grid, RING_THREADS, smem, p->stream>>>(
-        L, B, mpb, p->d_bluestein_rings, p->d_fft_n, p->d_chirp_off, p->d_bhat_off, p->d_chirp, p->d_bhat,
-        p->d_tw, p->d_g, samples);
+        L, B, mpb, p->d_bluestein_rings, p->d_fft_n, p->d_chirp_off, p->d_bhat_off, p->d_chirp, p->d_bhat, p->d_tw,
+        p->d_g, samples, (int)(smem / sizeof(double2)));
     p->launches++;
   }
   if (p->n_direct_rings > 0) {
     const int mpb = maps_per_block_for(B, p->n_direct_rings);
     dim3 grid(p->n_direct_rings, (B + mpb - 1) / mpb);
-    k_ring_inverse_direct<<<grid, 64, 0, p->stream>>>(L, B, p->n_direct_rings, mpb, p->d_roots, p->d_g,
-                                                      samples);
+    k_ring_inverse_direct<<<grid, 128, 0, p->stream>>>(L, B, mpb, p->d_roots, p->d_g, samples);
     p->launches++;
   }
   return cudaGetLastError();
@@ -230,18 +281,18 @@ cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples) {
   const int L = p->L;
   if (p->n_bluestein_rings > 0) {
     const int mpb = maps_per_block_for(B, p->n_bluestein_rings);
-    const size_t smem = sizeof(double2) * (size_t)max_fft(p);
+    const size_t smem = ring_smem(p);
     cudaFuncSetAttribute(k_ring_forward_bluestein, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid(p->n_bluestein_rings, (B + mpb - 1) / mpb);
     k_ring_forward_bluestein<<<grid, RING_THREADS, smem, p->stream>>>(
-        L, B, mpb, p->d_bluestein_rings, p->d_fft_n, p->d_chirp_off, p->d_bhat_off, p->d_chirp, p->d_bhat,
-        p->d_tw, samples, p->d_r);
+        L, B, mpb, p->d_bluestein_rings, p->d_fft_n, p->d_chirp_off, p->d_bhat_off, p->d_chirp, p->d_bhat, p->d_tw,
+        samples, p->d_r, (int)(smem / sizeof(double2)));
     p->launches++;
   }
   if (p->n_direct_rings > 0) {
     const int mpb = maps_per_block_for(B, p->n_direct_rings);
     dim3 grid(p->n_direct_rings, (B + mpb - 1) / mpb);
-    k_ring_forward_direct<<<grid, 64, 0, p->stream>>>(L, B, mpb, p->d_roots, samples, p->d_r);
+    k_ring_forward_direct<<<grid, 128, 0, p->stream>>>(L, B, mpb, p->d_roots, samples, p->d_r);
     p->launches++;
   }
   return cudaGetLastError();

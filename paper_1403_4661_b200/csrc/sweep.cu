@@ -671,38 +671,46 @@ cudaError_t launch_sweep(osph_plan* p, int B, double2* flm) {
   // gather (L * CC/4 <= 8 * 256) and by shared memory
   int g = B >= 3 ? 4 : B;
   while (g > 1 && (size_t)L * g > (size_t)SWEEP_UMAX * SWEEP_THREADS) g /= 2;
-  int T = 1;
-  while (T < 16 && ((B + g - 1) / g) * T * 2 <= 148 * 2 && T * 32 < L) T *= 2;
+  g = std::min(g, std::max(1, env_int("OSPH_SWEEP_G", g)));
   const int KC = SWEEP_KC;
-  int S = 8;
   // a job's tiles must fit one row of threads (side loads) and the per-warp accumulators
   auto tiles_ok = [&](int gg, int TT) {
     const int tpc = ((L + 7) / 8 + TT - 1) / TT;
     return tpc <= 32 && tpc * ((4 * gg + 7) / 8) <= SWEEP_WARPS * SWEEP_IPW;
   };
-  auto fits = [&](int gg, int TT, int kc, int ss) { return sweep_smem_bytes(SweepCfg(L, TT, 4 * gg, kc, ss)) <= cap; };
-  auto mac = [&](int gg, int TT, int kc, int ss) {
-    return gg == 4 ? max_active_clusters<16>(L, TT, kc, ss)
-                   : gg == 2 ? max_active_clusters<8>(L, TT, kc, ss) : max_active_clusters<4>(L, TT, kc, ss);
+  auto fits = [&](int gg, int TT, int ss) { return sweep_smem_bytes(SweepCfg(L, TT, 4 * gg, KC, ss)) <= cap; };
+  auto mac = [&](int gg, int TT, int ss) {
+    return gg == 4 ? max_active_clusters<16>(L, TT, KC, ss)
+                   : gg == 2 ? max_active_clusters<8>(L, TT, KC, ss) : max_active_clusters<4>(L, TT, KC, ss);
   };
-  T = env_int("OSPH_SWEEP_T", T);
-  for (int iter = 0; iter < 16; ++iter) {
-    while (T < 16 && !tiles_ok(g, T)) T *= 2;
-    while (!fits(g, T, KC, S)) {
-      if (S > 3) --S;
-      else if (T < 16) T *= 2;
-      else if (g > 1) g /= 2;
-      else break;
-    }
-    // keep every team resident at once (teams never wait on each other, but
-    // a second wave doubles the sweep's latency-bound wall time)
-    const int teams = (B + g - 1) / g;
-    if (T > 1 && tiles_ok(g, T / 2) && fits(g, T / 2, KC, S) && !getenv("OSPH_SWEEP_T") &&
-        mac(g, T, KC, S) < teams)
-      T /= 2;
-    else
+  // Largest team (cluster) width T whose configuration fits shared memory and
+  // keeps every team resident at once (teams never wait on each other, but a
+  // second wave doubles the latency-bound wall time); deepest ring that fits.
+  int T = 1, S = 3;
+  bool found = false;
+  for (int TT = 16; TT >= 1 && !found; TT /= 2) {
+    if (TT * 32 > 2 * L && TT > 1) continue;  // a team wider than the rows is idle
+    if (!tiles_ok(g, TT)) continue;
+    for (int ss = 8; ss >= 3; --ss) {
+      if (!fits(g, TT, ss)) continue;
+      if (mac(g, TT, ss) >= (B + g - 1) / g) {
+        T = TT;
+        S = ss;
+        found = true;
+      }
       break;
+    }
   }
+  if (!found) {  // several waves of teams: take the narrowest team that fits
+    for (int TT = 1; TT <= 16; TT *= 2)
+      if (tiles_ok(g, TT) && fits(g, TT, 3)) {
+        T = TT;
+        break;
+      }
+    S = 3;
+    while (S < 8 && fits(g, T, S + 1)) ++S;
+  }
+  T = env_int("OSPH_SWEEP_T", T);
   S = env_int("OSPH_SWEEP_S", S);
   if (g == 4) return launch_sweep_cc<16>(p, B, 4, T, KC, S, flm);
   if (g == 2) return launch_sweep_cc<8>(p, B, 2, T, KC, S, flm);

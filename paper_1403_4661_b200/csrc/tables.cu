@@ -156,7 +156,10 @@ __global__ void k_bluestein_tables(const int* __restrict__ rings, const int* __r
     fft_dit_smem(xs, N, logN, tw, false);
     const double inv = 1.0 / (double)N;
     double2* out = bhat + bhat_off[k] + (int64_t)dir * N;
-    for (int u = threadIdx.x; u < N; u += blockDim.x) out[u] = make_double2(xs[u].x * inv, xs[u].y * inv);
+    for (int u = threadIdx.x; u < N; u += blockDim.x) {  // bit-reversed order (see bluestein_convolve)
+      const double2 v = xs[bitrev(u, logN)];
+      out[u] = make_double2(v.x * inv, v.y * inv);
+    }
     __syncthreads();
   }
 }

@@ -183,3 +183,18 @@ def test_torch_device_path(grid_of, rng):
     assert np.abs(dev.cpu().numpy() - host).max() <= 1e-13
     back = osp.forward_sht_batch(dev, g)
     assert np.abs(back.cpu().numpy() - flm).max() <= 1e-10
+
+
+@pytest.mark.parametrize("L,B", [(64, 2), (256, 5)])
+def test_static_pivot_factorisation_matches_first_call(L, B, grid_of, rng):
+    """The first forward on a plan discovers the pivot order; later calls reuse it."""
+    g = grid_of(L)
+    osp.clear_plans()
+    flm = rng.standard_normal((B, L * L)) + 1j * rng.standard_normal((B, L * L))
+    s = osp.inverse_sht_batch(flm, g)
+    first = osp.forward_sht_batch(s, g)
+    second = osp.forward_sht_batch(s, g)
+    third = osp.forward_sht_batch(s, g)
+    assert np.abs(first - flm).max() <= 1e-10
+    assert np.abs(second - first).max() <= 1e-11  # same pivots, blocked vs unblocked rounding
+    assert np.array_equal(second, third)  # deterministic
