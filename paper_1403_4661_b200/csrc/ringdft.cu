@@ -123,9 +123,23 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_inverse_direct(int L, int
   const double2* rt = roots + (int64_t)k * k;
   for (int b0 = b_first; b0 < b_last; b0 += 16) {
     const int Gr = min(16, b_last - b0);
-    for (int idx = threadIdx.x; idx < Gr * n; idx += blockDim.x) {
-      const int g = idx % Gr, t = idx / Gr;
-      bins[g][t] = fold_bin(G, L, B, k, n, b0 + g, t);
+    // fold: short rings gather up to 2L tones per bin, so spread the tones over
+    // the block (map-fastest, coalesced) and accumulate in shared memory
+    for (int idx = threadIdx.x; idx < Gr * n; idx += blockDim.x) bins[idx / n][idx % n] = make_double2(0.0, 0.0);
+    __syncthreads();
+    const int64_t mstride = (int64_t)L * 4 * B;
+    for (int idx = threadIdx.x; idx < Gr * L; idx += blockDim.x) {
+      const int g = idx % Gr, m = idx / Gr;
+      const double4 v = __ldg(reinterpret_cast<const double4*>(G + m * mstride + ((int64_t)k * 4 * B + 4 * (b0 + g))));
+      const int r = m % n;
+      atomicAdd(&bins[g][r].x, v.x);
+      atomicAdd(&bins[g][r].y, v.y);
+      if (m > 0) {
+        const int rn = r == 0 ? 0 : n - r;
+        const double sg = (m & 1) ? -1.0 : 1.0;
+        atomicAdd(&bins[g][rn].x, sg * v.z);
+        atomicAdd(&bins[g][rn].y, sg * v.w);
+      }
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < Gr * n; idx += blockDim.x) {

@@ -667,12 +667,18 @@ static int env_int(const char* name, int dflt) {
 cudaError_t launch_sweep(osph_plan* p, int B, double2* flm) {
   const int L = p->L;
   const size_t cap = 220 * 1024;
+  const int KC = SWEEP_KC;
+  if (p->sweep_cfg_B == B && !getenv("OSPH_SWEEP_T") && !getenv("OSPH_SWEEP_G") && !getenv("OSPH_SWEEP_S")) {
+    const int g = p->sweep_cfg[0], T = p->sweep_cfg[1], S = p->sweep_cfg[2];
+    if (g == 4) return launch_sweep_cc<16>(p, B, 4, T, KC, S, flm);
+    if (g == 2) return launch_sweep_cc<8>(p, B, 2, T, KC, S, flm);
+    return launch_sweep_cc<4>(p, B, 1, T, KC, S, flm);
+  }
   // maps per team: 4 (16 columns) / 2 / 1, limited by the register-held
   // gather (L * CC/4 <= 8 * 256) and by shared memory
   int g = B >= 3 ? 4 : B;
   while (g > 1 && (size_t)L * g > (size_t)SWEEP_UMAX * SWEEP_THREADS) g /= 2;
   g = std::min(g, std::max(1, env_int("OSPH_SWEEP_G", g)));
-  const int KC = SWEEP_KC;
   // a job's tiles must fit one row of threads (side loads) and the per-warp accumulators
   auto tiles_ok = [&](int gg, int TT) {
     const int tpc = ((L + 7) / 8 + TT - 1) / TT;
@@ -686,21 +692,32 @@ cudaError_t launch_sweep(osph_plan* p, int B, double2* flm) {
   // Largest team (cluster) width T whose configuration fits shared memory and
   // keeps every team resident at once (teams never wait on each other, but a
   // second wave doubles the latency-bound wall time); deepest ring that fits.
-  int T = 1, S = 3;
+  // Over maps-per-team g (<= the register limit above) and T, maximise the CTAs
+  // at work subject to residency; ties go to more maps per team (less L2 traffic).
+  int T = 1, S = 3, best_ctas = 0, best_g = g;
   bool found = false;
-  for (int TT = 16; TT >= 1 && !found; TT /= 2) {
-    if (TT * 32 > 2 * L && TT > 1) continue;  // a team wider than the rows is idle
-    if (!tiles_ok(g, TT)) continue;
-    for (int ss = 8; ss >= 3; --ss) {
-      if (!fits(g, TT, ss)) continue;
-      if (mac(g, TT, ss) >= (B + g - 1) / g) {
+  const int gmax = g;
+  for (int gg = gmax; gg >= 1; gg /= 2) {
+    const int teams = (B + gg - 1) / gg;
+    for (int TT = 16; TT >= 1; TT /= 2) {
+      if (TT * 32 > 2 * L && TT > 1) continue;  // a team wider than the rows is idle
+      if (!tiles_ok(gg, TT)) continue;
+      int ss = 8;
+      while (ss >= 3 && !fits(gg, TT, ss)) --ss;
+      if (ss < 3) continue;
+      if (mac(gg, TT, ss) < teams) continue;
+      if (teams * TT > best_ctas) {
+        best_ctas = teams * TT;
+        best_g = gg;
         T = TT;
         S = ss;
         found = true;
       }
-      break;
+      break;  // narrower teams of this g only lose CTAs
     }
+    if (gg == 1) break;
   }
+  if (found) g = best_g;
   if (!found) {  // several waves of teams: take the narrowest team that fits
     for (int TT = 1; TT <= 16; TT *= 2)
       if (tiles_ok(g, TT) && fits(g, TT, 3)) {
@@ -712,6 +729,10 @@ cudaError_t launch_sweep(osph_plan* p, int B, double2* flm) {
   }
   T = env_int("OSPH_SWEEP_T", T);
   S = env_int("OSPH_SWEEP_S", S);
+  p->sweep_cfg_B = B;
+  p->sweep_cfg[0] = g;
+  p->sweep_cfg[1] = T;
+  p->sweep_cfg[2] = S;
   if (g == 4) return launch_sweep_cc<16>(p, B, 4, T, KC, S, flm);
   if (g == 2) return launch_sweep_cc<8>(p, B, 2, T, KC, S, flm);
   return launch_sweep_cc<4>(p, B, 1, T, KC, S, flm);

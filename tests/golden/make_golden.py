@@ -15,6 +15,7 @@ Outputs (committed; nothing at test time reads /root/reference):
       forward_sht(samples) in both methods, roundtrip error, plus legendre tables.
   tests/golden/ref_L256.npz   one map of each BASELINE input recipe at L=256 (inverse
       output + forward output) for the larger parity cases.
+  tests/golden/ref_L512.npz   one real map (BASELINE configs[2] recipe) on the L=512 grid.
   tests/golden/ref_misc.npz   ring_analysis KATs, ill-conditioned order on the
       interleaved L=256 grid, legendre range cases at L=4096.
 """
@@ -120,9 +121,22 @@ def misc():
     np.savez_compressed(OUT / "ref_misc.npz", **out)
 
 
+def l512_real():
+    """One map of BASELINE configs[2] (real maps, sqrt(C_l)) on the reference's L=512 condmin grid."""
+    grid = osp.load_grid(GRIDS / "grid-L512-uniform-condmin.txt")
+    rng = np.random.default_rng(SEED + 3)
+    flm = config_coefficients(512, rng, spectrum="cmb", real=True)
+    s = osp.inverse_sht(osp.HarmonicCoefficients(512, flm.copy()), grid)
+    f = osp.forward_sht(s, grid, method="spectral").values
+    print("L512 real E1", np.abs(f - flm).max())
+    np.savez_compressed(OUT / "ref_L512.npz", thetas=grid.thetas, flm=flm, samples=s.flatten(), fwd=f)
+
+
 if __name__ == "__main__":
     grids()
     for L in (8, 16, 32, 64):
         per_L(L)
     l256_recipes()
     misc()
+    if (GRIDS / "grid-L512-uniform-condmin.txt").exists():
+        l512_real()

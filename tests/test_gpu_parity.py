@@ -198,3 +198,24 @@ def test_static_pivot_factorisation_matches_first_call(L, B, grid_of, rng):
     assert np.abs(first - flm).max() <= 1e-10
     assert np.abs(second - first).max() <= 1e-11  # same pivots, blocked vs unblocked rounding
     assert np.array_equal(second, third)  # deterministic
+
+
+def test_L512_real_recipe(golden, grid_of):
+    """BASELINE configs[2] recipe (real map, sqrt(C_l)) on the reference's L=512 condmin grid."""
+    d = golden("ref_L512.npz")
+    grid = grid_of(512)
+    assert np.array_equal(grid.thetas, d["thetas"])
+    s = osp.inverse_sht_batch(d["flm"][None, :], grid)[0]
+    assert np.abs(s - d["samples"]).max() <= 1e-12 * max(1.0, np.abs(d["samples"]).max())
+    f = osp.forward_sht_batch(d["samples"][None, :], grid)[0]
+    rt = np.abs(d["fwd"] - d["flm"]).max()
+    assert np.abs(f - d["fwd"]).max() <= tol_fwd(rt)
+    assert np.abs(f - d["flm"]).max() <= tol_fwd(rt)
+
+
+@pytest.mark.parametrize("L,B", [(512, 3)])
+def test_L512_batch_roundtrip(L, B, grid_of, rng):
+    g = grid_of(L)
+    flm = rng.standard_normal((B, L * L)) + 1j * rng.standard_normal((B, L * L))
+    f = osp.forward_sht_batch(osp.inverse_sht_batch(flm, g), g)
+    assert np.abs(f - flm).max() <= 1e-10
