@@ -130,7 +130,9 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_inverse_direct(int L, int
     const int64_t mstride = (int64_t)L * 4 * B;
     for (int idx = threadIdx.x; idx < Gr * L; idx += blockDim.x) {
       const int g = idx % Gr, m = idx / Gr;
-      const double4 v = __ldg(reinterpret_cast<const double4*>(G + m * mstride + ((int64_t)k * 4 * B + 4 * (b0 + g))));
+      const double2* src = reinterpret_cast<const double2*>(G + m * mstride + ((int64_t)k * 4 * B + 4 * (b0 + g)));
+      const double2 vp = __ldg(src), vn = __ldg(src + 1);
+      const double4 v = make_double4(vp.x, vp.y, vn.x, vn.y);
       const int r = m % n;
       atomicAdd(&bins[g][r].x, v.x);
       atomicAdd(&bins[g][r].y, v.y);
