@@ -31,6 +31,19 @@ namespace cg = cooperative_groups;
 #define FNP_WARPS 8
 #define FNP_NB 32
 
+#ifdef OSPH_FACTOR_PROF
+#define FNP_MARK(i)                                   \
+  do {                                                \
+    if (threadIdx.x == 0) {                           \
+      const long long _n = clock64();                 \
+      _fa[i] += _n - _ft;                             \
+      _ft = _n;                                       \
+    }                                                 \
+  } while (0)
+#else
+#define FNP_MARK(i)
+#endif
+
 __device__ __forceinline__ void np_atomic_max_pos(unsigned long long* addr, double v) {
   if (!(v >= 0.0) || isinf(v)) v = INFINITY;
   atomicMax(addr, (unsigned long long)__double_as_longlong(v));
@@ -91,7 +104,17 @@ __global__ void __launch_bounds__(FNP_THREADS, 1) k_factor_np(
   double* pg = panel_g + (size_t)slot * 2 * FNP_NB * ldn;
 
   if (tid == 0) s_bad = 0;
+#ifdef OSPH_FACTOR_PROF
+  long long _ft = clock64(), _fa[6] = {0, 0, 0, 0, 0, 0};
+#endif
   for (int j = tid; j < n; j += FNP_THREADS) pinv[__ldg(perm + j)] = j;
+  // Rows n..ldn-1 of the slice and of Es are read by the 8-row tiles and the
+  // k-steps of the last panel (multiplied by zero E entries): they must hold
+  // zeros, not whatever the previous kernel left in shared memory (Es follows
+  // the slice, so the columns of both are one range).  Own padding columns
+  // cw..cwt-1 are zeroed whole.
+  for (int c = warp; c < lay.cwmax + FNP_NB; c += FNP_WARPS)
+    for (int r = (c >= cw && c < lay.cwmax ? 0 : n) + lane; r < ldn; r += 32) slice[(size_t)c * ldn + r] = 0.0;
 
   // ---- 1. generation: own degree columns l = m+c0 .. m+c1-1, rows in pivot order;
   //         rings k < m go to the tiled below-block Pb (sweep operand)
@@ -136,23 +159,23 @@ __global__ void __launch_bounds__(FNP_THREADS, 1) k_factor_np(
     if (lane == 0 && cw > 0) np_atomic_max_pos(norms + 2 * m, cmax);
   }
 
+  FNP_MARK(0);
   // ---- 2. blocked Gauss-Jordan, static pivots
+  const int nct = cwt >> 3;  // own 8-column tiles
   for (int j0 = 0, par = 0; j0 < n; j0 += FNP_NB, par ^= 1) {
     const int nb = min(FNP_NB, n - j0);
     const bool owner = j0 >= c0 && j0 < c1;
     double* pgp = pg + (size_t)par * FNP_NB * ldn;
     if (owner)
-      for (int idx = tid; idx < nb * n; idx += FNP_THREADS) {
-        const int c = idx / n, r = idx - c * n;
-        pgp[(size_t)c * ldn + r] = slice[(size_t)(j0 - c0 + c) * ldn + r];
-      }
+      for (int c = warp; c < nb; c += FNP_WARPS)
+        for (int r = lane; r < n; r += 32) pgp[(size_t)c * ldn + r] = slice[(size_t)(j0 - c0 + c) * ldn + r];
     cluster.sync();
+    FNP_MARK(1);
     // a) panel -> Es (columns >= nb zero)
-    for (int idx = tid; idx < FNP_NB * n; idx += FNP_THREADS) {
-      const int c = idx / n, r = idx - c * n;
-      Es[(size_t)c * ldn + r] = c < nb ? __ldcg(pgp + (size_t)c * ldn + r) : 0.0;
-    }
+    for (int c = warp; c < FNP_NB; c += FNP_WARPS)
+      for (int r = lane; r < n; r += 32) Es[(size_t)c * ldn + r] = c < nb ? __ldcg(pgp + (size_t)c * ldn + r) : 0.0;
     __syncthreads();
+    FNP_MARK(2);
     // b) Dinv = A[P,P]^{-1}: unpivoted Gauss-Jordan in one warp (lane = row)
     if (warp == 0) {
       double d[FNP_NB];
@@ -161,9 +184,11 @@ __global__ void __launch_bounds__(FNP_THREADS, 1) k_factor_np(
 #pragma unroll
       for (int c = 0; c < FNP_NB; ++c) {
         if (c < nb) {
-          if (lane == c)
+          if (lane == c) {
 #pragma unroll
-            for (int cc = 0; cc < FNP_NB; ++cc) rowbuf[cc] = d[cc];
+            for (int cc = 0; cc < FNP_NB; cc += 2)
+              *reinterpret_cast<double2*>(rowbuf + cc) = make_double2(d[cc], d[cc + 1]);
+          }
           __syncwarp();
           const double piv = rowbuf[c];
           if (lane == 0 && (piv == 0.0 || !isfinite(piv))) s_bad = 1;
@@ -174,8 +199,11 @@ __global__ void __launch_bounds__(FNP_THREADS, 1) k_factor_np(
           } else {
             const double f = d[c] * inv;
 #pragma unroll
-            for (int cc = 0; cc < FNP_NB; ++cc)
-              if (cc != c) d[cc] = fma(-f, rowbuf[cc], d[cc]);
+            for (int cc = 0; cc < FNP_NB; cc += 2) {
+              const double2 pr = *reinterpret_cast<const double2*>(rowbuf + cc);
+              if (cc != c) d[cc] = fma(-f, pr.x, d[cc]);
+              if (cc + 1 != c) d[cc + 1] = fma(-f, pr.y, d[cc + 1]);
+            }
             d[c] = -f;
           }
           __syncwarp();
@@ -185,104 +213,118 @@ __global__ void __launch_bounds__(FNP_THREADS, 1) k_factor_np(
       for (int c = 0; c < FNP_NB; ++c) Dinv[lane * FNP_NB + c] = (lane < nb && c < nb) ? d[c] : 0.0;
     }
     __syncthreads();
+    FNP_MARK(3);
     // c) E = -A[:,P] Dinv (rows outside P), E[P] = Dinv - I; in place in Es, one 8-row tile per warp pass
-    {
-      const int pt0 = j0 >> 3, pt1 = (j0 + nb + 7) >> 3;
-      for (int rt = warp; rt < nrt8; rt += FNP_WARPS) {
-        const int r0 = rt * 8;
-        if (rt >= pt0 && rt < pt1) {
-          for (int e = lane; e < 8 * FNP_NB; e += 32) {
-            const int r = e & 7, c = e >> 3;
-            const int row = r0 + r;
-            const int pr = row - j0;
-            Es[(size_t)c * ldn + row] = (pr >= 0 && pr < nb && c < nb) ? Dinv[pr * FNP_NB + c] - (pr == c ? 1.0 : 0.0) : 0.0;
-          }
-          continue;
+    const int pt0 = j0 >> 3, pt1 = (j0 + nb + 7) >> 3;
+    for (int rt = warp; rt < nrt8; rt += FNP_WARPS) {
+      const int r0 = rt * 8;
+      if (rt >= pt0 && rt < pt1) {
+        for (int e = lane; e < 8 * FNP_NB; e += 32) {
+          const int r = e & 7, c = e >> 3;
+          const int pr = r0 + r - j0;
+          Es[(size_t)c * ldn + r0 + r] =
+              (pr >= 0 && pr < nb && c < nb) ? Dinv[pr * FNP_NB + c] - (pr == c ? 1.0 : 0.0) : 0.0;
         }
-        double acc[FNP_NB / 8][2];
+        continue;
+      }
+      double acc[FNP_NB / 8][2];
 #pragma unroll
-        for (int ct = 0; ct < FNP_NB / 8; ++ct) acc[ct][0] = acc[ct][1] = 0.0;
+      for (int ct = 0; ct < FNP_NB / 8; ++ct) acc[ct][0] = acc[ct][1] = 0.0;
 #pragma unroll
-        for (int k = 0; k < FNP_NB; k += 4) {
-          const double a = Es[(size_t)(k + tq) * ldn + r0 + g];
+      for (int k = 0; k < FNP_NB; k += 4) {
+        const double a = Es[(size_t)(k + tq) * ldn + r0 + g];
 #pragma unroll
-          for (int ct = 0; ct < FNP_NB / 8; ++ct)
-            dmma_8x8x4(acc[ct][0], acc[ct][1], a, Dinv[(k + tq) * FNP_NB + ct * 8 + g]);
-        }
-        __syncwarp();
+        for (int ct = 0; ct < FNP_NB / 8; ++ct)
+          dmma_8x8x4(acc[ct][0], acc[ct][1], a, Dinv[(k + tq) * FNP_NB + ct * 8 + g]);
+      }
+      __syncwarp();
 #pragma unroll
-        for (int ct = 0; ct < FNP_NB / 8; ++ct) {
-          Es[(size_t)(ct * 8 + 2 * tq) * ldn + r0 + g] = -acc[ct][0];
-          Es[(size_t)(ct * 8 + 2 * tq + 1) * ldn + r0 + g] = -acc[ct][1];
-        }
+      for (int ct = 0; ct < FNP_NB / 8; ++ct) {
+        Es[(size_t)(ct * 8 + 2 * tq) * ldn + r0 + g] = -acc[ct][0];
+        Es[(size_t)(ct * 8 + 2 * tq + 1) * ldn + r0 + g] = -acc[ct][1];
       }
     }
     __syncthreads();
+    FNP_MARK(4);
     // d) owner: new panel columns = E + I on P
     if (owner)
-      for (int idx = tid; idx < nb * n; idx += FNP_THREADS) {
-        const int c = idx / n, r = idx - c * n;
-        slice[(size_t)(j0 - c0 + c) * ldn + r] = Es[(size_t)c * ldn + r] + (r == j0 + c ? 1.0 : 0.0);
-      }
-    // e) A[:, own rest] += E * A[P, own rest]: rows outside P first (T read in place), then P rows
+      for (int c = warp; c < nb; c += FNP_WARPS)
+        for (int r = lane; r < n; r += 32)
+          slice[(size_t)(j0 - c0 + c) * ldn + r] = Es[(size_t)c * ldn + r] + (r == j0 + c ? 1.0 : 0.0);
+    // e) A[:, own rest] += E * A[P, own rest].  A warp keeps its row tile's E
+    //    fragments in registers and sweeps the column tiles four at a time
+    //    (independent accumulators).  Rows outside P first (they read the P
+    //    rows in place), then the P rows (all reads before any write).
     {
-      const int pt0 = j0 >> 3, pt1 = (j0 + nb + 7) >> 3;
-      const int nct = cwt >> 3;
       const int pc0 = owner ? (j0 - c0) >> 3 : -1, pc1 = owner ? (j0 - c0 + nb + 7) >> 3 : -1;
-      auto tile = [&](int rt, int ct, double& o0, double& o1) {
-        const int r0 = rt * 8, cc = ct * 8;
-        double c0v = slice[(size_t)(cc + 2 * tq) * ldn + r0 + g];
-        double c1v = slice[(size_t)(cc + 2 * tq + 1) * ldn + r0 + g];
+      const int trow = min(j0 + tq, ldn - 1);  // B operand row (k-step 0); E is zero past nb
+      auto row_tile = [&](int rt, bool store_now, double (*keep)[4][2]) {
+        const int r0 = rt * 8;
+        double a[FNP_NB / 4];
 #pragma unroll
-        for (int k = 0; k < FNP_NB; k += 4) {
-          const double a = Es[(size_t)(k + tq) * ldn + r0 + g];
-          const int tr = j0 + k + tq;
-          const double b = (k + tq < nb) ? slice[(size_t)(cc + g) * ldn + tr] : 0.0;
-          dmma_8x8x4(c0v, c1v, a, b);
-        }
-        o0 = c0v;
-        o1 = c1v;
-      };
-      const int nrest = nrt8 - (pt1 - pt0);
-      for (int w = warp; w < nrest * nct; w += FNP_WARPS) {
-        const int rr = w % nrest, ct = w / nrest;
-        if (ct >= pc0 && ct < pc1) continue;
-        const int rt = rr < pt0 ? rr : rr + (pt1 - pt0);
-        double o0, o1;
-        tile(rt, ct, o0, o1);
-        slice[(size_t)(ct * 8 + 2 * tq) * ldn + rt * 8 + g] = o0;
-        slice[(size_t)(ct * 8 + 2 * tq + 1) * ldn + rt * 8 + g] = o1;
-      }
-      // P rows: all reads of A[P, rest] done before any write
-      double po[8][2];
-      int np = 0;
-      const int npw = (pt1 - pt0) * nct;
-      __syncthreads();
+        for (int ks = 0; ks < FNP_NB / 4; ++ks) a[ks] = Es[(size_t)(4 * ks + tq) * ldn + r0 + g];
+        for (int cb = 0; cb < nct; cb += 4) {
+          double acc[4][2];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int w = warp + q * FNP_WARPS;
-        if (w < npw) {
-          const int rt = pt0 + w % (pt1 - pt0), ct = w / (pt1 - pt0);
-          if (!(ct >= pc0 && ct < pc1)) tile(rt, ct, po[q][0], po[q][1]);
-          np = q + 1;
-        }
-      }
-      __syncthreads();
+          for (int u = 0; u < 4; ++u) {
+            const int cc = (cb + u) * 8;
+            const bool ok = cb + u < nct;
+            acc[u][0] = ok ? slice[(size_t)(cc + 2 * tq) * ldn + r0 + g] : 0.0;
+            acc[u][1] = ok ? slice[(size_t)(cc + 2 * tq + 1) * ldn + r0 + g] : 0.0;
+          }
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int w = warp + q * FNP_WARPS;
-        if (q < np && w < npw) {
-          const int rt = pt0 + w % (pt1 - pt0), ct = w / (pt1 - pt0);
-          if (!(ct >= pc0 && ct < pc1)) {
-            slice[(size_t)(ct * 8 + 2 * tq) * ldn + rt * 8 + g] = po[q][0];
-            slice[(size_t)(ct * 8 + 2 * tq + 1) * ldn + rt * 8 + g] = po[q][1];
+          for (int ks = 0; ks < FNP_NB / 4; ++ks) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int cc = min(cb + u, nct - 1) * 8;
+              const double b = slice[(size_t)(cc + g) * ldn + min(trow + 4 * ks, ldn - 1)];
+              dmma_8x8x4(acc[u][0], acc[u][1], a[ks], b);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int ct = cb + u;
+            if (ct >= nct || (ct >= pc0 && ct < pc1)) continue;
+            if (store_now) {
+              slice[(size_t)(ct * 8 + 2 * tq) * ldn + r0 + g] = acc[u][0];
+              slice[(size_t)(ct * 8 + 2 * tq + 1) * ldn + r0 + g] = acc[u][1];
+            } else {
+              keep[cb / 4][u][0] = acc[u][0];
+              keep[cb / 4][u][1] = acc[u][1];
+            }
           }
         }
+      };
+      for (int rt = warp; rt < nrt8; rt += FNP_WARPS)
+        if (!(rt >= pt0 && rt < pt1)) row_tile(rt, true, nullptr);
+      // P rows: nb/8 <= 4 row tiles, one per warp; own columns <= 128 (launcher) -> <= 4 blocks of 4 tiles
+      double keep[4][4][2];
+      const int prt = pt0 + warp;
+      const bool pw = prt < pt1;
+      __syncthreads();
+      if (pw) row_tile(prt, false, keep);
+      __syncthreads();
+      if (pw) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int ct = q * 4 + u;
+            if (ct >= nct || (ct >= pc0 && ct < pc1)) continue;
+            slice[(size_t)(ct * 8 + 2 * tq) * ldn + prt * 8 + g] = keep[q][u][0];
+            slice[(size_t)(ct * 8 + 2 * tq + 1) * ldn + prt * 8 + g] = keep[q][u][1];
+          }
       }
     }
     __syncthreads();
+    FNP_MARK(5);
   }
 
+#ifdef OSPH_FACTOR_PROF
+  if (tid == 0 && blockIdx.x == 0)
+    printf("factor_np m=%d n=%d CS=%d cycles: gen %lld  export+cluster %lld  import %lld  dinv %lld  E %lld  update %lld\n",
+           m, n, CS, _fa[0], _fa[1], _fa[2], _fa[3], _fa[4], _fa[5]);
+#endif
   // ---- 3. ||X||_1, tiled X for the sweep, chain constants
   {
     double cmax = 0.0;
@@ -299,10 +341,9 @@ __global__ void __launch_bounds__(FNP_THREADS, 1) k_factor_np(
     double* Xt = xt_all + xt_off[m];
     const int npad = nrt8 * 8;
     const int cend = (c1 == n) ? (n + OSPH_TILE_KC - 1) / OSPH_TILE_KC * OSPH_TILE_KC : c1;
-    for (int idx = tid; idx < (cend - c0) * npad; idx += FNP_THREADS) {
-      const int c = c0 + idx / npad, i = idx % npad;
-      Xt[tile_index(i, c, nrt8)] = (i < n && c < n) ? slice[(size_t)(c - c0) * ldn + i] : 0.0;
-    }
+    for (int c = c0 + warp; c < cend; c += FNP_WARPS)
+      for (int i = lane; i < npad; i += 32)
+        Xt[tile_index(i, c, nrt8)] = (i < n && c < n) ? slice[(size_t)(c - c0) * ldn + i] : 0.0;
   }
   if (tid == 0 && s_bad) atomicOr(status_out + m, 1);
   cluster.sync();  // the below-block rows of every rank are in global memory

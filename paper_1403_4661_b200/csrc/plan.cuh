@@ -55,6 +55,7 @@ struct osph_plan {
   bool fwd_ready = false;        // forward buffers allocated
   bool piv_ready = false;        // d_piv holds the (grid-determined) pivot order of every order
   double* d_panel = nullptr;     // static-pivot factorisation: panel hand-off buffers
+  double* d_xg = nullptr;        // sweep: x_s of every team, by parity of s (team exchange)
   int sweep_cfg_B = -1;          // cached sweep launch configuration for batch sweep_cfg_B
   int sweep_cfg[3] = {0, 0, 0};  // maps per team, cluster width, ring stages
   bool inv_ready = false;        // inverse buffers allocated

@@ -19,7 +19,7 @@
 // so all bulk work of a step is independent of the chain and a step needs ONE
 // cluster barrier.  Step t (t = L-1 .. 0):
 //   (a) chain -> L_t                                 (shared memory only)
-//   (b) x_t = x'_t + w_t L_t on own rows -> flm, DSMEM broadcast to the team
+//   (b) x_t = x'_t + w_t L_t on own rows -> flm and the team exchange buffer (global)
 //   (c) CORR(t+1): corrections of order t+1 (x_{t+1} complete) on own rings
 //   (d) BULK(t-1): x'_{t-1} on own rows, chain partial a_{t-2} -> DSMEM
 // x'_s is computed one step before it is used; the corrections of order s+1
@@ -90,6 +90,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+// barrier among the 8 consumer warps only (the producer warp never joins it)
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
+
 // -DOSPH_SWEEP_PROF: per-phase cycle counts of CTA 0 (debug builds only)
 #ifdef OSPH_SWEEP_PROF
 #define PROF_DECL            \
@@ -97,22 +109,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   long long _acc[5] = {0, 0, 0, 0, 0};
 #define PROF_MARK(i)                \
   do {                              \
-    __syncthreads();                \
+    consumers_sync();               \
     const long long _n = clock64(); \
     _acc[i] += _n - _pt;            \
     _pt = _n;                       \
   } while (0)
-#define PROF_DUMP()                                                                                  \
-  if (blockIdx.x == 0 && threadIdx.x == 0)                                                           \
-  printf("sweep prof (cycles): chain+axpy %lld  corr %lld  gather %lld  bulk %lld  barrier %lld  "   \
-         "| mbar wait %lld over %lld chunks, compute %lld sync %lld issue %lld\n",                     \
-         _acc[0], _acc[1], _acc[2], _acc[3], _acc[4], prof_wait, prof_chunks, prof_compute, prof_sync, \
-         prof_issue)
+#define PROF_DUMP()                                                                                \
+  if (blockIdx.x == 0 && threadIdx.x == 0)                                                         \
+  printf("sweep prof (cycles): chain+axpy %lld  corr %lld  gather %lld  bulk %lld  barrier %lld\n", \
+         _acc[0], _acc[1], _acc[2], _acc[3], _acc[4])
 #else
 #define PROF_DECL
 #define PROF_MARK(i)
 #define PROF_DUMP()
 #endif
+
+#define SWEEP_THREADS_ALL (SWEEP_THREADS + 32)  // + one producer warp
+
 
 // ---------------------------------------------------------------------------
 // configuration and shared-memory layout
@@ -120,25 +133,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 struct SweepCfg {
   int L, T, CC, KC, S;
   int tpc;  // max 8-row tiles of one job on one CTA
-  int ldx, ldr;
-  size_t xfull, bt, xp, wv, prow, apart, part, late, rch, stage, bar, total;  // offsets in doubles
+  int ldx, ldr, ccp;
+  size_t xrow, gst, xp, wv, prow, apart, late, rch, stage, bar, total;  // offsets in doubles
   __host__ __device__ SweepCfg(int L_, int T_, int CC_, int KC_, int S_) : L(L_), T(T_), CC(CC_), KC(KC_), S(S_) {
     tpc = ((L + 7) / 8 + T - 1) / T;
-    ldx = ((L + 15) / 16) * 16 + 4;
+    ldx = ((L + 31) / 32) * 32;  // rows of the B operands: every chunk of 32 K-rows is in bounds
     ldr = 8 * tpc + 4;
+    // row pitch of the row-major B operands: > CC (column CC stays zero) and
+    // = 4 mod 8 doubles, so the (tq, g) lanes of a DMMA B fragment hit distinct banks
+    ccp = ((CC + 1 + 3) / 8) * 8 + 4;
     size_t o = 0;
-    xfull = o; o += (size_t)2 * (CC + 1) * ldx;  // x_s of the whole team, transposed, by parity (+ zero row)
-    bt = o;    o += (size_t)(CC + 1) * ldx;  // permuted right-hand side (BULK B operand), transposed (+ zero row)
-    xp = o;    o += (size_t)2 * CC * ldr;   // own rows of x'_s, transposed, by parity of s
-    wv = o;    o += (size_t)2 * ldr;        // own rows of w_s, by parity of s
-    prow = o;  o += (size_t)ldr;            // own entries of Pb_s[s-1, :] (chain partial)
-    apart = o; o += (size_t)4 * T * CC;     // chain partials a_s from every rank, slot s % 4
-    part = o;  o += (size_t)SWEEP_WARPS * 64;
-    late = o;  o += (size_t)2 * CC;         // late right-hand-side entries L_s, by parity
-    rch = o;   o += (size_t)2 * CC;         // prefetched R(+-)[s][0], by parity
-    o = (o + 15) & ~(size_t)15;             // 128-byte aligned stages
+    xrow = o;  o += (size_t)ldx * ccp;          // x_{t+1} of the whole team, row-major [l][ccp] (CORR B)
+    gst = o;   o += (size_t)ldx * ccp;          // gathered right-hand side, row-major [j][ccp] (BULK B)
+    xp = o;    o += (size_t)2 * CC * ldr;       // own rows of x'_s, transposed, by parity of s
+    wv = o;    o += (size_t)2 * ldr;            // own rows of w_s, by parity of s
+    prow = o;  o += (size_t)2 * ldr;            // own entries of Pb_s[s-1, :], by parity of s
+    apart = o; o += (size_t)4 * T * CC;         // chain partials a_s from every rank, slot s % 4
+    late = o;  o += (size_t)2 * CC;             // late right-hand-side entries L_s, by parity
+    rch = o;   o += (size_t)2 * CC;             // prefetched R(+-)[s][0], by parity
+    o = (o + 15) & ~(size_t)15;                 // 128-byte aligned stages
     stage = o; o += (size_t)S * tpc * KC * 8;
-    bar = o;   o += (size_t)S;
+    bar = o;   o += (size_t)2 * S;              // full[S], empty[S]
     total = o;
   }
 };
@@ -155,20 +170,21 @@ struct Job {
 };
 
 __device__ __forceinline__ Job make_job(int type, int s, int L, int T, int rank, int KC, const double* xt,
-                                        const int64_t* xt_off, const double* pbt, const int64_t* pb_off) {
+                                        const int64_t* xt_off, const double* pbt, const int64_t* pb_off,
+                                        bool with_offset) {
   Job j;
   j.type = type;
   j.s = s;
   j.K = L - s;
-  const int rows = type == 0 ? j.K : s - 1;   // CORR skips ring s-1 (the chain)
-  const int mrows = type == 0 ? j.K : s;      // rows of the stored matrix
+  const int rows = type == 0 ? j.K : s - 1;  // CORR skips ring s-1 (the chain)
+  const int mrows = type == 0 ? j.K : s;     // rows of the stored matrix
   const int nt = (rows + 7) / 8;
   j.rt0 = (rank * nt) / T;
   j.rt1 = ((rank + 1) * nt) / T;
   j.nch = (j.rt1 > j.rt0 && rows > 0) ? (j.K + KC - 1) / KC : 0;
   j.cstride = (int64_t)((mrows + 7) / 8) * KC * 8;
-  j.A = type == 0 ? xt : pbt;  // base; the offset below is consumed only at issue time
-  j.off = (type == 0 ? xt_off[s] : pb_off[s]) + (int64_t)j.rt0 * KC * 8;
+  j.A = type == 0 ? xt : pbt;
+  j.off = with_offset ? (type == 0 ? xt_off[s] : pb_off[s]) + (int64_t)j.rt0 * KC * 8 : 0;
   return j;
 }
 
@@ -197,21 +213,59 @@ __device__ __forceinline__ bool next_job_id(int L, int& t, int& ph, int& type, i
   return false;
 }
 
-// Producer (thread 0): issues chunk after chunk of the job sequence.
-struct Producer {
-  int t, ph;       // job cursor
-  Job job, nxt;    // current job, next job (decoded ahead)
-  int ch;          // next chunk of the current job
-  bool has, has_nxt;
-  int st;          // stage receiving the next chunk
-};
+// One job's chunk loop for a warp owning NM output tiles (8x8 each), with
+// NCH independent accumulator chains per tile for DMMA latency hiding.
+template <int NM, int CC>
+__device__ __forceinline__ void job_tiles(int nch, int ldb, const double* stages, size_t stage_elems, uint64_t* full,
+                                          uint64_t* empty, int S, int& cst, uint32_t& cphase, const int* aoff,
+                                          const int* boff, const double* Bsrc, int tq, int lane,
+                                          double (&out)[SWEEP_IPW][2]) {
+  constexpr int CH = NM == 1 ? 4 : 2;
+  double acc[NM][CH][2];
+#pragma unroll
+  for (int u = 0; u < NM; ++u)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) acc[u][c][0] = acc[u][c][1] = 0.0;
+  for (int ch = 0; ch < nch; ++ch) {
+    mbar_wait(full + cst, cphase);
+    const double* sA = stages + cst * stage_elems + tq * 8;
+    const double* Bk = Bsrc + (size_t)(ch * SWEEP_KC + tq) * ldb;  // row-major B: [k][column]
+    // columns past K are zero in the tiled operand and finite in Bsrc: no guard
+#pragma unroll
+    for (int ks = 0; ks < SWEEP_KC / 4; ++ks) {
+#pragma unroll
+      for (int u = 0; u < NM; ++u) {
+        const double a = sA[aoff[u] + ks * 32];
+        const double b = Bk[(size_t)ks * 4 * ldb + boff[u]];
+        dmma_8x8x4(acc[u][ks % CH][0], acc[u][ks % CH][1], a, b);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + cst);
+    if (++cst == S) {
+      cst = 0;
+      cphase ^= 1u;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < NM; ++u) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      s0 += acc[u][c][0];
+      s1 += acc[u][c][1];
+    }
+    out[u][0] = s0;
+    out[u][1] = s1;
+  }
+}
 
 template <int CC>
-__global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(
+__global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
     int L, int B, int maps_per_team, int KC, int S, const double* __restrict__ xt, const int64_t* __restrict__ xt_off,
     const int* __restrict__ perm_all, const int* __restrict__ jstar_all, const double* __restrict__ beta_all,
     const double* __restrict__ pbt, const int64_t* __restrict__ pb_off, double2* __restrict__ R,
-    double2* __restrict__ flm) {
+    double2* __restrict__ flm, double* __restrict__ xg_all) {
   cg::cluster_group cluster = cg::this_cluster();
   const int T = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
@@ -222,77 +276,105 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(
   const int g = lane >> 2, tq = lane & 3;
   constexpr int NCT = (CC + 7) / 8;
   constexpr int NB4 = CC / 4;  // map slots of the team
+  const bool producer = warp == SWEEP_WARPS;
 
   extern __shared__ __align__(128) double smem[];
   const SweepCfg cfg(L, T, CC, KC, S);
-  const int ldx = cfg.ldx, ldr = cfg.ldr, tpc = cfg.tpc;
-  double* xfull = smem + cfg.xfull;
-  double* Bt = smem + cfg.bt;
+  const int ldr = cfg.ldr, tpc = cfg.tpc, ccp = cfg.ccp;
+  double* xrow = smem + cfg.xrow;
+  double* gst = smem + cfg.gst;
+  double* xg = xg_all + (size_t)team * 2 * L * CC;  // x_s of the team in global memory, by parity
   double* xp = smem + cfg.xp;
   double* wv = smem + cfg.wv;
   double* prowb = smem + cfg.prow;
   double* apart = smem + cfg.apart;
-  double* part = smem + cfg.part;
   double* late = smem + cfg.late;
   double* rch = smem + cfg.rch;
   double* stages = smem + cfg.stage;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + cfg.bar);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + cfg.bar);
+  uint64_t* empty = full + S;
   const size_t stage_elems = (size_t)tpc * KC * 8;
-#ifdef OSPH_SWEEP_PROF
-  long long prof_wait = 0, prof_chunks = 0, prof_compute = 0, prof_sync = 0, prof_issue = 0;
-#endif
 
-  // ---- producer
-  Producer pr;
-  // The producer keeps the job after the current one decoded ahead of time so
-  // the offset-table loads of make_job never stall a chunk issue.
-  auto find_next = [&](Job& out) -> bool {
-    int type, s;
-    while (next_job_id(L, pr.t, pr.ph, type, s)) {
-      out = make_job(type, s, L, T, rank, SWEEP_KC, xt, xt_off, pbt, pb_off);
-      if (out.nch > 0) return true;
-    }
-    return false;
-  };
-  auto prod_advance = [&]() {
-    pr.job = pr.nxt;
-    pr.has = pr.has_nxt;
-    pr.ch = 0;
-    if (pr.has) pr.has_nxt = find_next(pr.nxt);
-  };
-  auto prod_issue = [&]() {  // thread 0 only: one chunk into stage next % S
-    if (!pr.has) return;
-    const Job& j = pr.job;
-    uint64_t* bar = bars + pr.st;
-    const uint32_t bytes = (uint32_t)((j.rt1 - j.rt0) * KC * 64);
-    mbar_arrive_expect_tx(bar, bytes);
-    bulk_g2s(stages + pr.st * stage_elems, j.A + j.off + pr.ch * j.cstride, bytes, bar);  // one contiguous block
-    if (++pr.st == S) pr.st = 0;
-    if (++pr.ch == j.nch) prod_advance();
-  };
   if (tid == 0) {
-    for (int i = 0; i < S; ++i) mbar_init(bars + i, 1);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, SWEEP_WARPS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    pr.t = L;
-    pr.ph = 1;
-    pr.st = 0;
-    pr.has_nxt = find_next(pr.nxt);
-    prod_advance();
-    for (int i = 0; i < S; ++i) prod_issue();
   }
-  for (int i = tid; i < ldx; i += SWEEP_THREADS) {  // zero rows: B operand of padding columns
-    xfull[(size_t)CC * ldx + i] = 0.0;
-    xfull[(size_t)(2 * CC + 1) * ldx + i] = 0.0;
-    Bt[(size_t)CC * ldx + i] = 0.0;
-  }
+  // B operands start zeroed: padding columns read row CC, and a chunk's columns
+  // past K multiply zero operand tiles, so those entries must be finite
+  for (size_t i = tid; i < cfg.stage; i += SWEEP_THREADS_ALL) smem[i] = 0.0;
   __syncthreads();
 
-  // ---- consumer: one job through the chunk ring
-  int cst = 0;           // stage of the next chunk to consume
-  uint32_t cphase = 0;   // its mbarrier phase parity
-  // Warp w owns output tiles w, w+8, ... (8 rows x 8 columns each) for the
-  // whole job; K is streamed in chunks of SWEEP_KC columns, two independent
-  // accumulator sets per tile (even / odd k-steps) for DMMA latency hiding.
+  // ======================= producer warp: streams every job's A tiles =======================
+  if (producer) {
+    int jt = L, jph = 1;        // decode cursor (jobs with offsets)
+    int ct = L, cph = 1;        // counting cursor (step boundaries)
+    Job cur, nxt;
+    bool has = false, has_nxt = false;
+    int ch = 0, st = 0;
+    long long issued = 0, target = 0;
+    uint32_t ephase_bits = 0;   // per-stage parity of the next empty completion to wait for
+    auto find_next = [&](Job& out) -> bool {
+      int type, s;
+      while (next_job_id(L, jt, jph, type, s)) {
+        out = make_job(type, s, L, T, rank, SWEEP_KC, xt, xt_off, pbt, pb_off, true);
+        if (out.nch > 0) return true;
+      }
+      return false;
+    };
+    auto count_step_chunks = [&](int steps) {  // advance the counting cursor over `steps` steps
+      // prologue = BULK(L-1) only (ct = L, cph = 1); each later step t = CORR(t+1), BULK(t-1)
+      for (int q = 0; q < steps; ++q) {
+        int type, s;
+        const int t_before = ct;
+        while (ct == t_before && next_job_id(L, ct, cph, type, s))
+          target += make_job(type, s, L, T, rank, SWEEP_KC, xt, xt_off, pbt, pb_off, false).nch;
+      }
+    };
+    if (lane == 0) {
+      has = find_next(cur);
+      if (has) has_nxt = find_next(nxt);
+    }
+    auto pump = [&]() {  // issue until `target + S` chunks are out (blocking only on stages freed this step)
+      if (lane != 0) return;
+      while (has && issued < target + S) {
+        if (issued >= S) {  // stage reuse: wait until every consumer warp released it
+          mbar_wait(empty + st, (ephase_bits >> st) & 1u);
+          ephase_bits ^= 1u << st;
+        }
+        uint64_t* bar = full + st;
+        const uint32_t bytes = (uint32_t)((cur.rt1 - cur.rt0) * KC * 64);
+        mbar_arrive_expect_tx(bar, bytes);
+        bulk_g2s(stages + st * stage_elems, cur.A + cur.off + ch * cur.cstride, bytes, bar);
+        ++issued;
+        if (++st == S) st = 0;
+        if (++ch == cur.nch) {
+          cur = nxt;
+          has = has_nxt;
+          ch = 0;
+          if (has) has_nxt = find_next(nxt);
+        }
+      }
+    };
+    count_step_chunks(1);  // prologue: BULK(L-1)
+    pump();
+    __syncwarp();
+    cluster.sync();
+    for (int t = L - 1; t >= 0; --t) {
+      count_step_chunks(1);
+      pump();
+      __syncwarp();
+      cluster.sync();
+    }
+    return;
+  }
+
+  // ======================= consumer warps =======================
+  int cst = 0;          // stage of the next chunk to consume
+  uint32_t cphase = 0;  // its full-barrier parity
+  // Warp w owns output tiles w, w+8, ... (8 rows x 8 columns) of the job.
   auto run_job = [&](const Job& j, const double* Bsrc, int ldb, auto emit) {
     if (j.nch == 0) return;
     const int ntile = j.rt1 - j.rt0;
@@ -307,83 +389,45 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(
       const int rtl = ok ? it % ntile : 0, ct = ok ? it / ntile : 0;
       aoff[u] = rtl * SWEEP_KC * 8 + g;
       const int col = ct * 8 + g;
-      boff[u] = (ok && col < CC ? col : CC) * ldb;  // row CC of Bsrc is a zero row
+      boff[u] = ok && col < CC ? col : CC;  // column CC of Bsrc is a zero column
     }
-    double acc[SWEEP_IPW][2][2];
-#pragma unroll
-    for (int u = 0; u < SWEEP_IPW; ++u) acc[u][0][0] = acc[u][0][1] = acc[u][1][0] = acc[u][1][1] = 0.0;
-    for (int ch = 0; ch < j.nch; ++ch) {
-#ifdef OSPH_SWEEP_PROF
-      const long long _w0 = clock64();
-      mbar_wait(bars + cst, cphase);
-      prof_wait += clock64() - _w0;
-      ++prof_chunks;
-#else
-      mbar_wait(bars + cst, cphase);
-#endif
-      const double* sA = stages + cst * stage_elems + tq * 8;
-      const int kb = ch * SWEEP_KC;
-      const double* Bk = Bsrc + kb + tq;
-      // Columns past K are zero in the tiled operand and finite in Bsrc, so a
-      // ragged last chunk needs no guard.  Branch once per chunk on the warp's
-      // tile count so no predicated-off DMMA slots are issued.
-      auto chunk = [&](auto NM) {
-        constexpr int nm = decltype(NM)::value;
-#pragma unroll
-        for (int ks = 0; ks < SWEEP_KC / 4; ++ks) {
-#pragma unroll
-          for (int u = 0; u < nm; ++u) {
-            const double a = sA[aoff[u] + ks * 32];
-            const double b = Bk[boff[u] + ks * 4];
-            dmma_8x8x4(acc[u][ks & 1][0], acc[u][ks & 1][1], a, b);
+    double res[SWEEP_IPW][2];
+    switch (nmine) {
+      case 1: job_tiles<1, CC>(j.nch, ldb, stages, stage_elems, full, empty, S, cst, cphase, aoff, boff, Bsrc, tq, lane, res); break;
+      case 2: job_tiles<2, CC>(j.nch, ldb, stages, stage_elems, full, empty, S, cst, cphase, aoff, boff, Bsrc, tq, lane, res); break;
+      case 3: job_tiles<3, CC>(j.nch, ldb, stages, stage_elems, full, empty, S, cst, cphase, aoff, boff, Bsrc, tq, lane, res); break;
+      case 4: job_tiles<4, CC>(j.nch, ldb, stages, stage_elems, full, empty, S, cst, cphase, aoff, boff, Bsrc, tq, lane, res); break;
+      default: {  // idle warp: keep the stage/phase bookkeeping and release the stages
+        for (int ch = 0; ch < j.nch; ++ch) {
+          mbar_wait(full + cst, cphase);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty + cst);
+          if (++cst == S) {
+            cst = 0;
+            cphase ^= 1u;
           }
         }
-      };
-      switch (nmine) {
-        case 1: chunk(std::integral_constant<int, 1>{}); break;
-        case 2: chunk(std::integral_constant<int, 2>{}); break;
-        case 3: chunk(std::integral_constant<int, 3>{}); break;
-        case 4: chunk(std::integral_constant<int, 4>{}); break;
-        default: break;
       }
-      if (++cst == S) {
-        cst = 0;
-        cphase ^= 1u;
-      }
-#ifdef OSPH_SWEEP_PROF
-      const long long _c1 = clock64();
-      prof_compute += _c1 - _w0;
-      __syncthreads();  // stage free
-      const long long _c2 = clock64();
-      prof_sync += _c2 - _c1;
-      if (tid == 0) prod_issue();
-      prof_issue += clock64() - _c2;
-#else
-      __syncthreads();  // stage free
-      if (tid == 0) prod_issue();
-#endif
     }
 #pragma unroll
     for (int u = 0; u < SWEEP_IPW; ++u) {
-      const int it = warp + u * SWEEP_WARPS;
       if (u < nmine) {
+        const int it = warp + u * SWEEP_WARPS;
         const int rtl = it % ntile, ct = it / ntile;
         const int c = ct * 8 + 2 * tq;
-        if (c < CC) emit(8 * (j.rt0 + rtl) + g, c, acc[u][0][0] + acc[u][1][0], acc[u][0][1] + acc[u][1][1]);
+        if (c < CC) emit(8 * (j.rt0 + rtl) + g, c, res[u][0], res[u][1]);
       }
     }
   };
 
-  // ---- gathered right-hand side of order s: registers (issued early) -> Bt
+  // ---- gathered right-hand side of order s -> gst (row-major [j][ccp]) by cp.async
   int pidx[SWEEP_UMAX];
-  double2 grp[SWEEP_UMAX], grn[SWEEP_UMAX];
   auto load_perm = [&](int s) {  // data independent: one step ahead
     const int ns = L - s;
     const int* perm = perm_all + packed_pos(L, s, 0);
 #pragma unroll
     for (int u = 0; u < SWEEP_UMAX; ++u) {
-      const int idx = tid + u * SWEEP_THREADS;
-      const int jj = idx / NB4;
+      const int jj = (tid + u * SWEEP_THREADS) / NB4;
       pidx[u] = (jj < ns) ? __ldg(perm + jj) : -1;
     }
   };
@@ -392,31 +436,27 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(
 #pragma unroll
     for (int u = 0; u < SWEEP_UMAX; ++u) {
       const int idx = tid + u * SWEEP_THREADS;
-      const int bl = idx % NB4;
-      grp[u] = grn[u] = make_double2(0.0, 0.0);
+      const int jj = idx / NB4, bl = idx % NB4;
+      if (pidx[u] < 0) continue;
+      double* dst = gst + (size_t)jj * ccp + 4 * bl;
       if (pidx[u] > 0 && bl < gm) {
         const int64_t base = ((ps + pidx[u]) * 2) * B + b0 + bl;
-        grp[u] = __ldcg(R + base);
-        grn[u] = __ldcg(R + base + B);
+        cp_async16(dst, R + base);
+        cp_async16(dst + 2, R + base + B);
+      } else {  // late entry (ring s) is excluded from x'_s; padding map slots are zero
+        dst[0] = dst[1] = dst[2] = dst[3] = 0.0;
       }
     }
   };
-  auto gather_store = [&](int s) {
+  // ---- x_s of the whole team (written to xg by its owners last step) -> xrow
+  auto x_issue = [&](int s) {
     const int ns = L - s;
-    const double sg = (s & 1) ? -1.0 : 1.0;
-#pragma unroll
-    for (int u = 0; u < SWEEP_UMAX; ++u) {
-      const int idx = tid + u * SWEEP_THREADS;
-      const int jj = idx / NB4, bl = idx % NB4;
-      if (jj < ns) {
-        Bt[(size_t)(4 * bl + 0) * ldx + jj] = grp[u].x;
-        Bt[(size_t)(4 * bl + 1) * ldx + jj] = grp[u].y;
-        Bt[(size_t)(4 * bl + 2) * ldx + jj] = sg * grn[u].x;
-        Bt[(size_t)(4 * bl + 3) * ldx + jj] = sg * grn[u].y;
-      }
+    const double* src = xg + (size_t)(s & 1) * L * CC;
+    for (int idx = tid; idx < ns * (CC / 2); idx += SWEEP_THREADS) {
+      const int l = idx / (CC / 2), c = 2 * (idx % (CC / 2));
+      cp_async16(xrow + (size_t)l * ccp + c, src + (size_t)l * CC + c);
     }
   };
-
   auto load_rch = [&](int s) {  // R(+-)[s][0] of every map -> rch[s & 1]
     if (tid < NB4) {
       double2 rp = make_double2(0.0, 0.0), rn = rp;
@@ -433,9 +473,10 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(
     }
   };
 
-  // BULK(s): x'_s on own rows, w_s, chain partial a_{s-1}
+  // BULK(s): x'_s on own rows, w_s, chain partial a_{s-1}.  The gathered
+  // right-hand side is unsigned; the (-1)^s of the -m columns is applied here.
   auto bulk = [&](int s) {
-    const Job j = make_job(0, s, L, T, rank, KC, xt, xt_off, pbt, pb_off);
+    const Job j = make_job(0, s, L, T, rank, SWEEP_KC, xt, xt_off, pbt, pb_off, false);
     const int ns = j.K;
     const int r0 = 8 * j.rt0, r1 = min(ns, 8 * j.rt1);
     // data-independent side loads, consumed after the GEMM
@@ -447,17 +488,19 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(
       if (s >= 1) pl = __ldg(pbt + pb_off[s] + tile_index(s - 1, l, (s + 7) >> 3));
     }
     double* xps = xp + (size_t)(s & 1) * CC * ldr;
-    run_job(j, Bt, ldx, [&](int l, int c, double v0, double v1) {
+    const double ss = (s & 1) ? -1.0 : 1.0;
+    run_job(j, gst, ccp, [&](int l, int c, double v0, double v1) {
       if (l < ns) {
-        xps[(size_t)c * ldr + (l - r0)] = v0;
-        xps[(size_t)(c + 1) * ldr + (l - r0)] = v1;
+        const double sg = (c & 2) ? ss : 1.0;
+        xps[(size_t)c * ldr + (l - r0)] = sg * v0;
+        xps[(size_t)(c + 1) * ldr + (l - r0)] = sg * v1;
       }
     });
     if (tid < r1 - r0) {
       wv[(size_t)(s & 1) * ldr + tid] = wl;
       prowb[tid] = pl;
     }
-    __syncthreads();
+    consumers_sync();
     if (s >= 1) {
       for (int c = warp; c < CC; c += SWEEP_WARPS) {
         double acc = 0.0;
@@ -472,8 +515,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(
   // ---- prologue: x'_{L-1}, a_{L-2}, R[L-1][0]
   load_perm(L - 1);
   gather_issue(L - 1);
-  gather_store(L - 1);
-  __syncthreads();
+  cp_async_commit();
+  cp_async_wait_all();
+  consumers_sync();
   bulk(L - 1);
   load_rch(L - 1);
   if (L >= 2) load_perm(L - 2);
@@ -485,12 +529,17 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(
     const int nt = L - t;
     const double st = (t & 1) ? -1.0 : 1.0;
     const double bt = beta_next;
+    const bool corr = t >= 1 && t + 1 <= L - 1;
     if (t >= 1) beta_next = __ldg(beta_all + t);  // consumed one step later
-    // right-hand side of order t-1 is final now: start its gather
+    // x_{t+1} (complete since the last cluster barrier) for CORR(t+1): group 1
+    if (corr) x_issue(t + 1);
+    cp_async_commit();
+    // right-hand side of order t-1 is final now: its gather is group 2
     if (t >= 1) gather_issue(t - 1);
+    cp_async_commit();
     if (t == 0) load_rch(0);  // order-2 corrections to ring 0 land one step earlier
-    __syncthreads();
-    // ---- (a) chain: late entries L_t of every map
+    // ---- (a) chain: late entries L_t of every map (threads tid < gm own map tid;
+    // rch and late were written by the same threads)
     if (tid < NB4 && tid < gm) {
       const int b = tid;
       double gp_r = 0.0, gp_i = 0.0, gm_r = 0.0, gm_i = 0.0;  // G+_{t+1}(theta_t), G-_{t+1}(theta_t)
@@ -521,24 +570,21 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(
         lt[3] = st * (rr[3] - gp_i);
       }
     }
-    __syncthreads();
-    // ---- (b) x_t = x'_t + w_t L_t on own rows -> flm and every rank's xfull
+    consumers_sync();
+    // ---- (b) x_t = x'_t + w_t L_t on own rows -> flm and the team exchange xg
     {
       const int nrt = (nt + 7) / 8;
       const int r0 = 8 * ((rank * nrt) / T), r1 = min(nt, 8 * (((rank + 1) * nrt) / T));
       const double* xps = xp + (size_t)(t & 1) * CC * ldr;
       const double* wvs = wv + (size_t)(t & 1) * ldr;
       const double* lt = late + (size_t)(t & 1) * CC;
-      double* xf = xfull + (size_t)(t & 1) * (CC + 1) * ldx;
+      double* xo = xg + (size_t)(t & 1) * L * CC;
       for (int idx = tid; idx < (r1 - r0) * (CC / 2); idx += SWEEP_THREADS) {
         const int l = r0 + idx / (CC / 2), c = 2 * (idx % (CC / 2));
         const double wl = wvs[l - r0];
         const double v0 = xps[(size_t)c * ldr + (l - r0)] + wl * lt[c];
         const double v1 = xps[(size_t)(c + 1) * ldr + (l - r0)] + wl * lt[c + 1];
-        for (int q = 0; q < T; ++q) {
-          *cluster.map_shared_rank(xf + (size_t)c * ldx + l, q) = v0;
-          *cluster.map_shared_rank(xf + (size_t)(c + 1) * ldx + l, q) = v1;
-        }
+        __stcg(reinterpret_cast<double2*>(xo + (size_t)l * CC + c), make_double2(v0, v1));
         const int bl = c >> 2;
         if (bl < gm) {
           const int64_t ell = t + l;
@@ -550,11 +596,13 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(
     }
     PROF_MARK(0);
     // ---- (c) CORR(t+1): corrections of order s = t+1 on own rings k < t
-    if (t >= 1 && t + 1 <= L - 1) {
+    if (corr) {
       const int s = t + 1;
       const double ss = (s & 1) ? -1.0 : 1.0;
-      const Job j = make_job(1, s, L, T, rank, KC, xt, xt_off, pbt, pb_off);
-      run_job(j, xfull + (size_t)(s & 1) * (CC + 1) * ldx, ldx, [&](int k, int c, double v0, double v1) {
+      cp_async_wait_group1();
+      consumers_sync();
+      const Job j = make_job(1, s, L, T, rank, SWEEP_KC, xt, xt_off, pbt, pb_off, false);
+      run_job(j, xrow, ccp, [&](int k, int c, double v0, double v1) {
         const int bl = c >> 2;
         if (k >= s - 1 || bl >= gm) return;  // ring s-1 is the chain
         const bool plus = (c & 2) == 0;
@@ -582,9 +630,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS, 1) k_sweep(
     PROF_MARK(1);
     // ---- (d) BULK(t-1): x'_{t-1}, a_{t-2}; prefetch R[t-1][0] and the next permutation
     if (t >= 1) {
-      gather_store(t - 1);
+      cp_async_wait_all();
       if (t >= 2) load_perm(t - 2);
-      __syncthreads();
+      consumers_sync();
       PROF_MARK(2);
       bulk(t - 1);
       if (t >= 2) load_rch(t - 1);
@@ -611,7 +659,7 @@ static cudaError_t launch_sweep_cc(osph_plan* p, int B, int g, int T, int KC, in
     return e;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)(teams * T));
-  lc.blockDim = dim3(SWEEP_THREADS);
+  lc.blockDim = dim3(SWEEP_THREADS_ALL);
   lc.dynamicSmemBytes = smem;
   lc.stream = p->stream;
   cudaLaunchAttribute attr[1];
@@ -629,7 +677,7 @@ static cudaError_t launch_sweep_cc(osph_plan* p, int B, int g, int T, int KC, in
   }
   e = cudaLaunchKernelEx(&lc, kern, L, B, g, KC, S, (const double*)p->d_xt, (const int64_t*)p->d_xt_off,
                          (const int*)p->d_piv, (const int*)p->d_jstar, (const double*)p->d_beta,
-                         (const double*)p->d_pbelow, (const int64_t*)p->d_pb_off, p->d_r, flm);
+                         (const double*)p->d_pbelow, (const int64_t*)p->d_pb_off, p->d_r, flm, p->d_xg);
   p->launches++;
   return e;
 }
@@ -642,7 +690,7 @@ static int max_active_clusters(int L, int T, int KC, int S) {
   if (T > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)T);
-  lc.blockDim = dim3(SWEEP_THREADS);
+  lc.blockDim = dim3(SWEEP_THREADS_ALL);
   lc.dynamicSmemBytes = smem;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -702,7 +750,7 @@ cudaError_t launch_sweep(osph_plan* p, int B, double2* flm) {
     for (int TT = 16; TT >= 1; TT /= 2) {
       if (TT * 32 > 2 * L && TT > 1) continue;  // a team wider than the rows is idle
       if (!tiles_ok(gg, TT)) continue;
-      int ss = 8;
+      int ss = 16;
       while (ss >= 3 && !fits(gg, TT, ss)) --ss;
       if (ss < 3) continue;
       if (mac(gg, TT, ss) < teams) continue;
@@ -725,7 +773,7 @@ cudaError_t launch_sweep(osph_plan* p, int B, double2* flm) {
         break;
       }
     S = 3;
-    while (S < 8 && fits(g, T, S + 1)) ++S;
+    while (S < 16 && fits(g, T, S + 1)) ++S;
   }
   T = env_int("OSPH_SWEEP_T", T);
   S = env_int("OSPH_SWEEP_S", S);
