@@ -53,6 +53,10 @@ namespace cg = cooperative_groups;
 #define SWEEP_IPW 4     // max accumulator tiles per warp
 #define SWEEP_UMAX 8    // max gathered right-hand-side entries per thread
 #define SWEEP_KC 32     // K columns per streamed chunk
+#define SWEEP_SMAX 6    // ring stages: deeper rings measured slower (L=256: S=9 +13%)
+#ifndef SWEEP_MINB
+#define SWEEP_MINB 1    // resident CTAs per SM the register budget is sized for
+#endif
 
 // ---------------------------------------------------------------------------
 // mbarrier / bulk-copy PTX
@@ -93,6 +97,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
@@ -104,9 +111,10 @@ __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 256
 
 // -DOSPH_SWEEP_PROF: per-phase cycle counts of CTA 0 (debug builds only)
 #ifdef OSPH_SWEEP_PROF
+#define PROF_N 9
 #define PROF_DECL            \
   long long _pt = clock64(); \
-  long long _acc[5] = {0, 0, 0, 0, 0};
+  long long _acc[PROF_N] = {};
 #define PROF_MARK(i)                \
   do {                              \
     consumers_sync();               \
@@ -114,10 +122,11 @@ __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, 256
     _acc[i] += _n - _pt;            \
     _pt = _n;                       \
   } while (0)
-#define PROF_DUMP()                                                                                \
-  if (blockIdx.x == 0 && threadIdx.x == 0)                                                         \
-  printf("sweep prof (cycles): chain+axpy %lld  corr %lld  gather %lld  bulk %lld  barrier %lld\n", \
-         _acc[0], _acc[1], _acc[2], _acc[3], _acc[4])
+#define PROF_DUMP()                                                                                           \
+  if (blockIdx.x == 0 && threadIdx.x == 0)                                                                    \
+  printf("sweep prof (cycles): issue %lld chain %lld axpy %lld corr-wait %lld corr %lld bulk-wait %lld "      \
+         "bulk-gemm %lld bulk-rest %lld barrier %lld\n",                                                      \
+         _acc[0], _acc[1], _acc[2], _acc[3], _acc[4], _acc[5], _acc[6], _acc[7], _acc[8])
 #else
 #define PROF_DECL
 #define PROF_MARK(i)
@@ -261,7 +270,7 @@ __device__ __forceinline__ void job_tiles(int nch, int ldb, const double* stages
 }
 
 template <int CC>
-__global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
+__global__ void __launch_bounds__(SWEEP_THREADS_ALL, SWEEP_MINB) k_sweep(
     int L, int B, int maps_per_team, int KC, int S, const double* __restrict__ xt, const int64_t* __restrict__ xt_off,
     const int* __restrict__ perm_all, const int* __restrict__ jstar_all, const double* __restrict__ beta_all,
     const double* __restrict__ pbt, const int64_t* __restrict__ pb_off, double2* __restrict__ R,
@@ -372,6 +381,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
   }
 
   // ======================= consumer warps =======================
+  PROF_DECL
   int cst = 0;          // stage of the next chunk to consume
   uint32_t cphase = 0;  // its full-barrier parity
   // Warp w owns output tiles w, w+8, ... (8 rows x 8 columns) of the job.
@@ -457,14 +467,10 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
       cp_async16(xrow + (size_t)l * ccp + c, src + (size_t)l * CC + c);
     }
   };
-  auto load_rch = [&](int s) {  // R(+-)[s][0] of every map -> rch[s & 1]
-    if (tid < NB4) {
-      double2 rp = make_double2(0.0, 0.0), rn = rp;
-      if (tid < gm) {
-        const int64_t base = (packed_pos(L, s, 0) * 2) * B + b0 + tid;
-        rp = __ldcg(R + base);
-        rn = __ldcg(R + base + B);
-      }
+  auto load_rch = [&](int s) {  // R(+-)[s][0] of every map -> rch[s & 1] (synchronous)
+    if (tid < gm) {
+      const int64_t base = (packed_pos(L, s, 0) * 2) * B + b0 + tid;
+      const double2 rp = __ldcg(R + base), rn = __ldcg(R + base + B);
       double* d = rch + (size_t)(s & 1) * CC + 4 * tid;
       d[0] = rp.x;
       d[1] = rp.y;
@@ -472,21 +478,42 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
       d[3] = rn.y;
     }
   };
+  auto rch_issue = [&](int s) {  // the same by cp.async (slots gm..NB4-1 stay zero)
+    if (tid < gm) {
+      const int64_t base = (packed_pos(L, s, 0) * 2) * B + b0 + tid;
+      double* d = rch + (size_t)(s & 1) * CC + 4 * tid;
+      cp_async16(d, R + base);
+      cp_async16(d + 2, R + base + B);
+    }
+  };
+  // data-independent operands of BULK(s) -> smem: w_s = X_s[own rows, j*_s] and
+  // Pb_s[s-1, own rows]; the scalars (offsets, j*) are loaded one step earlier
+  int64_t sx_off = 0, sp_off = 0;
+  int sjs = 0;
+  auto side_scalars = [&](int s) {
+    if (s >= 0) {
+      sx_off = __ldg(xt_off + s);
+      sp_off = __ldg(pb_off + s);
+      sjs = __ldg(jstar_all + s);
+    }
+  };
+  auto side_issue = [&](int s) {
+    const int ns = L - s, nrt = (ns + 7) / 8;
+    const int r0 = 8 * ((rank * nrt) / T), r1 = min(ns, 8 * (((rank + 1) * nrt) / T));
+    if (tid < r1 - r0) {
+      const int l = r0 + tid;
+      cp_async8(wv + (size_t)(s & 1) * ldr + tid, xt + sx_off + tile_index(l, sjs, nrt));
+      if (s >= 1) cp_async8(prowb + tid, pbt + sp_off + tile_index(s - 1, l, (s + 7) >> 3));
+    }
+  };
 
-  // BULK(s): x'_s on own rows, w_s, chain partial a_{s-1}.  The gathered
-  // right-hand side is unsigned; the (-1)^s of the -m columns is applied here.
+  // BULK(s): x'_s on own rows, chain partial a_{s-1} (w_s and the Pb row are in
+  // smem already).  The gathered right-hand side is unsigned; the (-1)^s of the
+  // -m columns is applied here.
   auto bulk = [&](int s) {
     const Job j = make_job(0, s, L, T, rank, SWEEP_KC, xt, xt_off, pbt, pb_off, false);
     const int ns = j.K;
     const int r0 = 8 * j.rt0, r1 = min(ns, 8 * j.rt1);
-    // data-independent side loads, consumed after the GEMM
-    double wl = 0.0, pl = 0.0;
-    if (tid < r1 - r0) {
-      const int l = r0 + tid;
-      const double* X = xt + xt_off[s];
-      wl = __ldg(X + tile_index(l, __ldg(jstar_all + s), (ns + 7) >> 3));
-      if (s >= 1) pl = __ldg(pbt + pb_off[s] + tile_index(s - 1, l, (s + 7) >> 3));
-    }
     double* xps = xp + (size_t)(s & 1) * CC * ldr;
     const double ss = (s & 1) ? -1.0 : 1.0;
     run_job(j, gst, ccp, [&](int l, int c, double v0, double v1) {
@@ -496,11 +523,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
         xps[(size_t)(c + 1) * ldr + (l - r0)] = sg * v1;
       }
     });
-    if (tid < r1 - r0) {
-      wv[(size_t)(s & 1) * ldr + tid] = wl;
-      prowb[tid] = pl;
-    }
     consumers_sync();
+    PROF_MARK(6);
     if (s >= 1) {
       for (int c = warp; c < CC; c += SWEEP_WARPS) {
         double acc = 0.0;
@@ -514,16 +538,18 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
 
   // ---- prologue: x'_{L-1}, a_{L-2}, R[L-1][0]
   load_perm(L - 1);
+  side_scalars(L - 1);
   gather_issue(L - 1);
+  side_issue(L - 1);
   cp_async_commit();
   cp_async_wait_all();
   consumers_sync();
   bulk(L - 1);
   load_rch(L - 1);
   if (L >= 2) load_perm(L - 2);
+  side_scalars(L - 2);
   cluster.sync();
 
-  PROF_DECL
   double beta_next = L >= 2 ? __ldg(beta_all + L - 1) : 0.0;  // beta_{t+1} of the coming step
   for (int t = L - 1; t >= 0; --t) {
     const int nt = L - t;
@@ -534,10 +560,17 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
     // x_{t+1} (complete since the last cluster barrier) for CORR(t+1): group 1
     if (corr) x_issue(t + 1);
     cp_async_commit();
-    // right-hand side of order t-1 is final now: its gather is group 2
-    if (t >= 1) gather_issue(t - 1);
+    // group 2: the right-hand side of order t-1 (final now: every correction but
+    // the chain's has landed), its late entry R[t-1][0] and BULK(t-1)'s side operands
+    if (t >= 1) {
+      gather_issue(t - 1);
+      side_issue(t - 1);
+      if (t >= 2) rch_issue(t - 1);  // R[0][0] takes order-2 corrections at step 1
+    }
     cp_async_commit();
-    if (t == 0) load_rch(0);  // order-2 corrections to ring 0 land one step earlier
+    if (t >= 2) side_scalars(t - 2);
+    if (t == 0) load_rch(0);
+    PROF_MARK(0);
     // ---- (a) chain: late entries L_t of every map (threads tid < gm own map tid;
     // rch and late were written by the same threads)
     if (tid < NB4 && tid < gm) {
@@ -571,6 +604,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
       }
     }
     consumers_sync();
+    PROF_MARK(1);
     // ---- (b) x_t = x'_t + w_t L_t on own rows -> flm and the team exchange xg
     {
       const int nrt = (nt + 7) / 8;
@@ -594,13 +628,14 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
         }
       }
     }
-    PROF_MARK(0);
+    PROF_MARK(2);
     // ---- (c) CORR(t+1): corrections of order s = t+1 on own rings k < t
     if (corr) {
       const int s = t + 1;
       const double ss = (s & 1) ? -1.0 : 1.0;
       cp_async_wait_group1();
       consumers_sync();
+      PROF_MARK(3);
       const Job j = make_job(1, s, L, T, rank, SWEEP_KC, xt, xt_off, pbt, pb_off, false);
       run_job(j, xrow, ccp, [&](int k, int c, double v0, double v1) {
         const int bl = c >> 2;
@@ -627,19 +662,18 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
         atomicAdd(&rp->y, -gi);
       });
     }
-    PROF_MARK(1);
-    // ---- (d) BULK(t-1): x'_{t-1}, a_{t-2}; prefetch R[t-1][0] and the next permutation
+    PROF_MARK(4);
+    // ---- (d) BULK(t-1): x'_{t-1}, a_{t-2}; the next permutation
     if (t >= 1) {
       cp_async_wait_all();
       if (t >= 2) load_perm(t - 2);
       consumers_sync();
-      PROF_MARK(2);
+      PROF_MARK(5);
       bulk(t - 1);
-      if (t >= 2) load_rch(t - 1);
     }
-    PROF_MARK(3);
+    PROF_MARK(7);
     cluster.sync();
-    PROF_MARK(4);
+    PROF_MARK(8);
   }
   PROF_DUMP();
 }
@@ -750,7 +784,7 @@ cudaError_t launch_sweep(osph_plan* p, int B, double2* flm) {
     for (int TT = 16; TT >= 1; TT /= 2) {
       if (TT * 32 > 2 * L && TT > 1) continue;  // a team wider than the rows is idle
       if (!tiles_ok(gg, TT)) continue;
-      int ss = 16;
+      int ss = SWEEP_SMAX;
       while (ss >= 3 && !fits(gg, TT, ss)) --ss;
       if (ss < 3) continue;
       if (mac(gg, TT, ss) < teams) continue;
@@ -773,7 +807,7 @@ cudaError_t launch_sweep(osph_plan* p, int B, double2* flm) {
         break;
       }
     S = 3;
-    while (S < 16 && fits(g, T, S + 1)) ++S;
+    while (S < SWEEP_SMAX && fits(g, T, S + 1)) ++S;
   }
   T = env_int("OSPH_SWEEP_T", T);
   S = env_int("OSPH_SWEEP_S", S);
