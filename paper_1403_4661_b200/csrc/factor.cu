@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(FAC_THREADS, 1) k_factor_gj(
     const int64_t* __restrict__ pb_off, double* __restrict__ ainv, double* __restrict__ pbelow,
     int* __restrict__ perm_all, unsigned long long* __restrict__ norms, int* __restrict__ status_out,
     int* __restrict__ jstar_out, double* __restrict__ beta_out, double* __restrict__ xt_all,
-    const int64_t* __restrict__ xt_off) {
+    const int64_t* __restrict__ xt_off, double* __restrict__ u_out) {
   cg::cluster_group cluster = cg::this_cluster();
   const int CS = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
@@ -337,6 +337,22 @@ __global__ void __launch_bounds__(FAC_THREADS, 1) k_factor_gj(
         Xt[tile_index(i, col, nrt)] = (i < n && col < n) ? __ldcg(A + (int64_t)col * n + i) : 0.0;
   }
 
+  // u_m[j] = Pb_m[ring m-1, :] . X[:, j] for own columns: the sweep's chain
+  // partial a_{m-1} = Pb_m[m-1, :] . x'_m is u_m . (P rhs_m)
+  {
+    double* u = u_out + packed_pos(L, m, 0);
+    const int nrtpb = (m + 7) >> 3;
+    for (int col = cown0 + warp; col < cown1; col += FAC_THREADS / 32) {
+      double s = 0.0;
+      if (m >= 1)
+        for (int i = lane; i < n; i += 32)
+          s += __ldcg(Pb + tile_index(m - 1, i, nrtpb)) * __ldcg(A + (int64_t)col * n + i);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) u[col] = s;
+    }
+  }
+
   // ---- 4. sweep chain constants (rank 0): j* = column of X fed by ring m
   // (perm[j*] = 0) and beta_m = Pb_m[ring m-1, :] . X[:, j*], the coupling of
   // order m's late right-hand-side entry into ring m-1 of order m-1.
@@ -407,7 +423,7 @@ static cudaError_t launch_class(osph_plan* p, int m_first, int m_last, int cs) {
   e = cudaLaunchKernelEx(&cfg, kern, L, m_first, (const double*)p->d_cos, (const double2*)p->d_rec,
                          (const int*)p->d_ls, (const double2*)p->d_pstart, (const int64_t*)p->d_ainv_off,
                          (const int64_t*)p->d_pb_off, p->d_ainv, p->d_pbelow, p->d_piv, p->d_norms,
-                         p->d_status, p->d_jstar, p->d_beta, p->d_xt, (const int64_t*)p->d_xt_off);
+                         p->d_status, p->d_jstar, p->d_beta, p->d_xt, (const int64_t*)p->d_xt_off, p->d_u);
   p->launches++;
   return e;
 }

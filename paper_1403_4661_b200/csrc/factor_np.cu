@@ -72,7 +72,8 @@ __global__ void __launch_bounds__(FNP_THREADS, 1) k_factor_np(
     const int* __restrict__ ls_tab, const double2* __restrict__ pstart, const int* __restrict__ perm_all,
     double* __restrict__ xt_all, const int64_t* __restrict__ xt_off, double* __restrict__ pbelow,
     const int64_t* __restrict__ pb_off, double* __restrict__ panel_g, unsigned long long* __restrict__ norms,
-    int* __restrict__ status_out, int* __restrict__ jstar_out, double* __restrict__ beta_out) {
+    int* __restrict__ status_out, int* __restrict__ jstar_out, double* __restrict__ beta_out,
+    double* __restrict__ u_out) {
   cg::cluster_group cluster = cg::this_cluster();
   const int CS = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
@@ -347,6 +348,21 @@ __global__ void __launch_bounds__(FNP_THREADS, 1) k_factor_np(
   }
   if (tid == 0 && s_bad) atomicOr(status_out + m, 1);
   cluster.sync();  // the below-block rows of every rank are in global memory
+  // u_m[j] = Pb_m[ring m-1, :] . X[:, j] for own columns: the sweep's chain
+  // partial a_{m-1} = Pb_m[m-1, :] . x'_m is u_m . (P rhs_m)
+  {
+    double* u = u_out + packed_pos(L, m, 0);
+    const double* Pb = pbelow + pb_off[m];
+    const int nrtpb = (m + 7) >> 3;
+    for (int c = warp; c < cw; c += FNP_WARPS) {
+      double s = 0.0;
+      if (m >= 1)
+        for (int l = lane; l < n; l += 32) s += __ldcg(Pb + tile_index(m - 1, l, nrtpb)) * slice[(size_t)c * ldn + l];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) u[c0 + c] = s;
+    }
+  }
   const int js = pinv[0];
   if (js >= c0 && js < c1) {  // owner of column j* (ring m): beta_m = Pb_m[m-1, :] . X[:, j*]
     double acc = 0.0;
@@ -396,7 +412,7 @@ cudaError_t launch_factor_np_class(osph_plan* p, int m_first, int m_last, int cs
   e = cudaLaunchKernelEx(&cfg, k_factor_np, L, m_first, nmax, (const double*)p->d_cos, (const double2*)p->d_rec,
                          (const int*)p->d_ls, (const double2*)p->d_pstart, (const int*)p->d_piv, p->d_xt,
                          (const int64_t*)p->d_xt_off, p->d_pbelow, (const int64_t*)p->d_pb_off, p->d_panel,
-                         p->d_norms, p->d_status, p->d_jstar, p->d_beta);
+                         p->d_norms, p->d_status, p->d_jstar, p->d_beta, p->d_u);
   p->launches++;
   return e;
 }
