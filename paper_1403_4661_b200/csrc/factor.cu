@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(FAC_THREADS, 1) k_factor_gj(
     const int64_t* __restrict__ pb_off, double* __restrict__ ainv, double* __restrict__ pbelow,
     int* __restrict__ perm_all, unsigned long long* __restrict__ norms, int* __restrict__ status_out,
     int* __restrict__ jstar_out, double* __restrict__ beta_out, double* __restrict__ xt_all,
-    const int64_t* __restrict__ xt_off, double* __restrict__ u_out) {
+    const int64_t* __restrict__ xt_off, double* __restrict__ u_out, double* __restrict__ w_out) {
   cg::cluster_group cluster = cg::this_cluster();
   const int CS = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
@@ -332,15 +332,19 @@ __global__ void __launch_bounds__(FAC_THREADS, 1) k_factor_gj(
     const int nrt = npad >> 3;
     // the owner of the last columns also zero-fills the padding columns of the last chunk
     const int cend = (cown1 == n) ? (n + OSPH_TILE_KC - 1) / OSPH_TILE_KC * OSPH_TILE_KC : cown1;
-    for (int col = cown0; col < cend; ++col)
+    // column col of X (pivot order) is column perm[col] of X P^T (natural ring
+    // order, the sweep's operand); the late ring's column (perm = 0) is zero
+    for (int col = cown0; col < cend; ++col) {
+      const int cn = col < n ? __ldcg(perm + col) : col;
       for (int i = tid; i < npad; i += FAC_THREADS)
-        Xt[tile_index(i, col, nrt)] = (i < n && col < n) ? __ldcg(A + (int64_t)col * n + i) : 0.0;
+        Xt[tile_index(i, cn, nrt)] = (i < n && col < n && cn != 0) ? __ldcg(A + (int64_t)col * n + i) : 0.0;
+    }
   }
 
-  // u_m[j] = Pb_m[ring m-1, :] . X[:, j] for own columns: the sweep's chain
-  // partial a_{m-1} = Pb_m[m-1, :] . x'_m is u_m . (P rhs_m)
+  // u_m[j] = Pb_m[ring m-1, :] . X[:, j] for own columns, stored in natural ring
+  // order: the sweep's chain partial a_{m-1} = Pb_m[m-1, :] . x'_m is u_m . rhs_m
   {
-    double* u = u_out + packed_pos(L, m, 0);
+    double* u = u_out + (size_t)m * L;
     const int nrtpb = (m + 7) >> 3;
     for (int col = cown0 + warp; col < cown1; col += FAC_THREADS / 32) {
       double s = 0.0;
@@ -349,7 +353,10 @@ __global__ void __launch_bounds__(FAC_THREADS, 1) k_factor_gj(
           s += __ldcg(Pb + tile_index(m - 1, i, nrtpb)) * __ldcg(A + (int64_t)col * n + i);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) u[col] = s;
+      if (lane == 0) {
+        const int cn = __ldcg(perm + col);  // natural ring order; the late ring's weight is zero
+        u[cn] = cn != 0 ? s : 0.0;
+      }
     }
   }
 
@@ -378,6 +385,7 @@ __global__ void __launch_bounds__(FAC_THREADS, 1) k_factor_gj(
       beta_out[m] = b;
       jstar_out[m] = js;
     }
+    for (int l = tid; l < n; l += FAC_THREADS) w_out[(size_t)m * L + l] = __ldcg(A + (int64_t)js * n + l);
   }
 }
 
@@ -423,7 +431,7 @@ static cudaError_t launch_class(osph_plan* p, int m_first, int m_last, int cs) {
   e = cudaLaunchKernelEx(&cfg, kern, L, m_first, (const double*)p->d_cos, (const double2*)p->d_rec,
                          (const int*)p->d_ls, (const double2*)p->d_pstart, (const int64_t*)p->d_ainv_off,
                          (const int64_t*)p->d_pb_off, p->d_ainv, p->d_pbelow, p->d_piv, p->d_norms,
-                         p->d_status, p->d_jstar, p->d_beta, p->d_xt, (const int64_t*)p->d_xt_off, p->d_u);
+                         p->d_status, p->d_jstar, p->d_beta, p->d_xt, (const int64_t*)p->d_xt_off, p->d_u, p->d_w);
   p->launches++;
   return e;
 }

@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(FNP_THREADS, 1) k_factor_np(
     double* __restrict__ xt_all, const int64_t* __restrict__ xt_off, double* __restrict__ pbelow,
     const int64_t* __restrict__ pb_off, double* __restrict__ panel_g, unsigned long long* __restrict__ norms,
     int* __restrict__ status_out, int* __restrict__ jstar_out, double* __restrict__ beta_out,
-    double* __restrict__ u_out) {
+    double* __restrict__ u_out, double* __restrict__ w_out) {
   cg::cluster_group cluster = cg::this_cluster();
   const int CS = (int)cluster.num_blocks();
   const int rank = (int)cluster.block_rank();
@@ -342,16 +342,23 @@ __global__ void __launch_bounds__(FNP_THREADS, 1) k_factor_np(
     double* Xt = xt_all + xt_off[m];
     const int npad = nrt8 * 8;
     const int cend = (c1 == n) ? (n + OSPH_TILE_KC - 1) / OSPH_TILE_KC * OSPH_TILE_KC : c1;
-    for (int c = c0 + warp; c < cend; c += FNP_WARPS)
+    // column c of X (pivot order) is column perm[c] of X P^T (natural ring
+    // order, the sweep's operand); the late ring's column (perm = 0) is zero
+    for (int c = c0 + warp; c < cend; c += FNP_WARPS) {
+      const int cn = c < n ? __ldg(perm + c) : c;
       for (int i = lane; i < npad; i += 32)
-        Xt[tile_index(i, c, nrt8)] = (i < n && c < n) ? slice[(size_t)(c - c0) * ldn + i] : 0.0;
+        Xt[tile_index(i, cn, nrt8)] = (i < n && c < n && cn != 0) ? slice[(size_t)(c - c0) * ldn + i] : 0.0;
+    }
+    const int jl = pinv[0];  // w_m = X[:, j*], the late ring's column
+    if (jl >= c0 && jl < c1)
+      for (int i = tid; i < n; i += FNP_THREADS) w_out[(size_t)m * L + i] = slice[(size_t)(jl - c0) * ldn + i];
   }
   if (tid == 0 && s_bad) atomicOr(status_out + m, 1);
   cluster.sync();  // the below-block rows of every rank are in global memory
-  // u_m[j] = Pb_m[ring m-1, :] . X[:, j] for own columns: the sweep's chain
-  // partial a_{m-1} = Pb_m[m-1, :] . x'_m is u_m . (P rhs_m)
+  // u_m[j] = Pb_m[ring m-1, :] . X[:, j] for own columns, stored in natural ring
+  // order: the sweep's chain partial a_{m-1} = Pb_m[m-1, :] . x'_m is u_m . rhs_m
   {
-    double* u = u_out + packed_pos(L, m, 0);
+    double* u = u_out + (size_t)m * L;
     const double* Pb = pbelow + pb_off[m];
     const int nrtpb = (m + 7) >> 3;
     for (int c = warp; c < cw; c += FNP_WARPS) {
@@ -360,7 +367,10 @@ __global__ void __launch_bounds__(FNP_THREADS, 1) k_factor_np(
         for (int l = lane; l < n; l += 32) s += __ldcg(Pb + tile_index(m - 1, l, nrtpb)) * slice[(size_t)c * ldn + l];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) u[c0 + c] = s;
+      if (lane == 0) {
+        const int cn = __ldg(perm + c0 + c);  // natural ring order; the late ring's weight is zero
+        u[cn] = cn != 0 ? s : 0.0;
+      }
     }
   }
   const int js = pinv[0];
@@ -412,7 +422,7 @@ cudaError_t launch_factor_np_class(osph_plan* p, int m_first, int m_last, int cs
   e = cudaLaunchKernelEx(&cfg, k_factor_np, L, m_first, nmax, (const double*)p->d_cos, (const double2*)p->d_rec,
                          (const int*)p->d_ls, (const double2*)p->d_pstart, (const int*)p->d_piv, p->d_xt,
                          (const int64_t*)p->d_xt_off, p->d_pbelow, (const int64_t*)p->d_pb_off, p->d_panel,
-                         p->d_norms, p->d_status, p->d_jstar, p->d_beta, p->d_u);
+                         p->d_norms, p->d_status, p->d_jstar, p->d_beta, p->d_u, p->d_w);
   p->launches++;
   return e;
 }

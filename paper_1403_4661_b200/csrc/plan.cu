@@ -51,7 +51,7 @@ static void plan_free(osph_plan* p) {
   void* ptrs[] = {p->d_cos, p->d_sin, p->d_rec, p->d_ls, p->d_pstart, p->d_ring_order, p->d_fft_n,
                   p->d_chirp_off, p->d_bhat_off, p->d_chirp, p->d_bhat, p->d_tw, p->d_roots,
                   p->d_bluestein_rings, p->d_ainv_off, p->d_pb_off, p->d_ainv, p->d_pbelow, p->d_piv,
-                  p->d_norms, p->d_kappa, p->d_status, p->d_jstar, p->d_beta, p->d_u, p->d_xt_off, p->d_xt, p->d_panel, p->d_xg,
+                  p->d_norms, p->d_kappa, p->d_status, p->d_jstar, p->d_beta, p->d_u, p->d_w, p->d_xt_off, p->d_xt, p->d_panel, p->d_xg,
                   p->d_fpack, p->d_g, p->d_r,
                   p->d_in, p->d_out};
   for (void* q : ptrs)
@@ -251,7 +251,11 @@ static int ensure_forward(osph_plan* p) {
     CUDA_TRY(dalloc(&p->d_panel, nmax * 2 * 32 * (((nmax + 15) / 16) * 16 + 4)));
   }
   CUDA_TRY(dalloc(&p->d_beta, (size_t)L));
-  CUDA_TRY(dalloc(&p->d_u, (size_t)L * (L + 1) / 2));
+  // [L][L] + 2: the sweep's bulk copies round their sizes up to 16 bytes
+  CUDA_TRY(dalloc(&p->d_u, (size_t)L * L + 2));
+  CUDA_TRY(dalloc(&p->d_w, (size_t)L * L + 2));
+  CUDA_TRY(cudaMemsetAsync(p->d_u, 0, sizeof(double) * ((size_t)L * L + 2), st));
+  CUDA_TRY(cudaMemsetAsync(p->d_w, 0, sizeof(double) * ((size_t)L * L + 2), st));
   // teams * (4 maps-per-team) columns <= 4 (B + 3); two parities of L rows
   CUDA_TRY(dalloc(&p->d_xg, (size_t)8 * L * (B + 3)));
   CUDA_TRY(dalloc(&p->d_r, (size_t)L * (L + 1) * B));

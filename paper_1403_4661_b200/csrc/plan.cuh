@@ -49,7 +49,8 @@ struct osph_plan {
   int* d_status = nullptr;       // [L] 0 ok, 1 zero/non-finite pivot
   int* d_jstar = nullptr;        // [L] column of X_m fed by ring m (perm[j*] = 0)
   double* d_beta = nullptr;      // [L] beta_m = Pb_m[m-1, :] . X_m[:, j*]
-  double* d_u = nullptr;         // [packed] u_m = Pb_m[m-1, :] X_m (chain partial a_{m-1} = u_m . rhs_m)
+  double* d_u = nullptr;         // [L][L] u_m = Pb_m[m-1, :] X_m P^T (chain partial a_{m-1} = u_m . rhs_m)
+  double* d_w = nullptr;         // [L][L] w_m = X_m[:, j*] (late-entry column)
   std::vector<int64_t> h_xt_off;  // [L+1] offset of order m's 8-row-tiled inverse
   int64_t* d_xt_off = nullptr;
   double* d_xt = nullptr;         // X_m in 8-row tiles (sweep operand)

@@ -41,6 +41,8 @@
 // independent, so a batch fills the GPU with teams and a single map gets one
 // wide team.
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -61,6 +63,7 @@ namespace cg = cooperative_groups;
 #define SWEEP_SMAX 6    // ring stages per group
 #define SWEEP_BAR_C 1   // named barriers of the two groups
 #define SWEEP_BAR_B 2
+#define SWEEP_BOXR 64   // rows per TMA box of the right-hand side
 
 // ---------------------------------------------------------------------------
 // mbarrier / bulk-copy PTX
@@ -125,6 +128,16 @@ __device__ __forceinline__ int mod_small(int a, int n) {
   if (r >= n) r -= n;
   return r;
 }
+// TMA tile load of a 3-D box (right-hand-side rows) into shared memory
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+// generic-proxy accesses before async-proxy (bulk copy) accesses of the same memory
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;\n" ::: "memory"); }
 // named barrier of one warp group (the other groups and the producers never join it)
 __device__ __forceinline__ void group_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
@@ -158,28 +171,27 @@ __device__ __forceinline__ void group_sync(int id, int nthreads) {
 struct SweepCfg {
   int L, T, CC, KC, S;
   int tpc;  // max 8-row tiles of one job on one CTA
-  int ldx, ldr, ccp;
-  size_t xrow, gst, xp, wv, ubuf, apart, late, rch, permb, stage, bar, total;  // offsets in doubles
+  int ldx, ldr;
+  size_t gst, xrow, xp, wv, ubuf, apart, late, rch, stage, bar, total;  // offsets in doubles
   __host__ __device__ SweepCfg(int L_, int T_, int CC_, int KC_, int S_) : L(L_), T(T_), CC(CC_), KC(KC_), S(S_) {
     tpc = ((L + 7) / 8 + T - 1) / T;
-    ldx = ((L + 31) / 32) * 32;  // rows of the B operands: every chunk of 32 K-rows is in bounds
+    // rows of the B operands: whole TMA boxes and whole 32-row K chunks stay in bounds
+    ldx = ((L + SWEEP_BOXR - 1) / SWEEP_BOXR) * SWEEP_BOXR;
     ldr = 8 * tpc + 4;
-    // row pitch of the row-major B operands: > CC (column CC stays zero) and
-    // = 4 mod 8 doubles, so the (tq, g) lanes of a DMMA B fragment hit distinct banks
-    ccp = ((CC + 1 + 3) / 8) * 8 + 4;
+    auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };  // 128-byte alignment
     size_t o = 0;
-    xrow = o;  o += (size_t)ldx * ccp;          // x_{t+1} of the whole team, row-major [l][ccp] (CORR B)
-    gst = o;   o += (size_t)ldx * ccp;          // gathered right-hand side, row-major [j][ccp] (BULK B)
-    xp = o;    o += (size_t)2 * CC * ldr;       // own rows of x'_s, transposed, by parity of s
-    wv = o;    o += (size_t)2 * ldr;            // own rows of w_s, by parity of s
-    ubuf = o;  o += (size_t)ldx;                // u_s = Pb_s[s-1, :] X_s (chain partial weights)
-    apart = o; o += (size_t)4 * CC;             // chain partials a_s, slot s % 4
-    late = o;  o += (size_t)2 * CC;             // late right-hand-side entries L_s, by parity
-    rch = o;   o += (size_t)2 * CC;             // prefetched R(+-)[s][0], by parity
-    permb = o; o += (size_t)ldx;                // pivot order of order s (ints), by parity
-    o = (o + 15) & ~(size_t)15;                 // 128-byte aligned stages
+    // B operands, row-major [row][CC] exactly as the bulk copies deliver them:
+    // a DMMA B fragment (rows k+tq, columns g) then covers 32 consecutive doubles
+    gst = o;   o = al(o + (size_t)ldx * CC);    // right-hand side of order s, natural ring order (BULK B)
+    xrow = o;  o = al(o + (size_t)ldx * CC);    // x_{t+1} of the whole team (CORR B)
+    ubuf = o;  o = al(o + (size_t)ldx);         // u_s (chain partial weights), natural ring order
+    xp = o;    o = al(o + (size_t)2 * CC * ldr);  // own rows of x'_s, transposed, by parity of s
+    wv = o;    o = al(o + (size_t)2 * ldr);     // own rows of w_s, by parity of s
+    apart = o; o = al(o + (size_t)4 * SWEEP_WB * CC);  // chain partials a_s per BULK warp, slot s % 4
+    late = o;  o = al(o + (size_t)2 * CC);      // late right-hand-side entries L_s, by parity
+    rch = o;   o = al(o + (size_t)2 * CC);      // prefetched R(+-)[s][0], by parity
     stage = o; o += (size_t)2 * S * tpc * KC * 8;  // ring B (BULK) then ring C (CORR)
-    bar = o;   o += (size_t)4 * S;              // fullB[S], emptyB[S], fullC[S], emptyC[S]
+    bar = o;   o += (size_t)4 * S + 2;          // fullB[S], emptyB[S], fullC[S], emptyC[S], inB, inC
     total = o;
   }
 };
@@ -225,7 +237,7 @@ struct Ring {
 
 // One job's chunk loop for a warp owning NM output tiles (8x8 each), with
 // CH independent accumulator chains per tile for DMMA latency hiding.
-template <int NM>
+template <int NM, int CC>
 __device__ __forceinline__ void job_tiles(int nch, int ldb, const Ring& rg, int& cst, uint32_t& cphase,
                                           const int* aoff, const int* boff, const double* Bsrc, int tq, int lane,
                                           double (&out)[SWEEP_IPW][2]) {
@@ -245,7 +257,8 @@ __device__ __forceinline__ void job_tiles(int nch, int ldb, const Ring& rg, int&
 #pragma unroll
       for (int u = 0; u < NM; ++u) {
         const double a = sA[aoff[u] + ks * 32];
-        const double b = Bk[(size_t)ks * 4 * ldb + boff[u]];
+        // CC = 4: the columns 4..7 of the 8-wide tile are zero
+        const double b = (CC >= 8 || boff[u] < CC) ? Bk[(size_t)ks * 4 * ldb + boff[u]] : 0.0;
         dmma_8x8x4(acc[u][ks % CH][0], acc[u][ks % CH][1], a, b);
       }
     }
@@ -289,14 +302,14 @@ __device__ __forceinline__ void run_job(const Job& j, const Ring& rg, int& cst, 
     const int rtl = ok ? it - ct * ntile : 0;
     aoff[u] = rtl * SWEEP_KC * 8 + g;
     const int col = ct * 8 + g;
-    boff[u] = ok && col < CC ? col : CC;  // column CC of Bsrc is a zero column
+    boff[u] = col;
   }
   double res[SWEEP_IPW][2];
   switch (nmine) {
-    case 1: job_tiles<1>(j.nch, ldb, rg, cst, cphase, aoff, boff, Bsrc, tq, lane, res); break;
-    case 2: job_tiles<2>(j.nch, ldb, rg, cst, cphase, aoff, boff, Bsrc, tq, lane, res); break;
-    case 3: job_tiles<3>(j.nch, ldb, rg, cst, cphase, aoff, boff, Bsrc, tq, lane, res); break;
-    case 4: job_tiles<4>(j.nch, ldb, rg, cst, cphase, aoff, boff, Bsrc, tq, lane, res); break;
+    case 1: job_tiles<1, CC>(j.nch, ldb, rg, cst, cphase, aoff, boff, Bsrc, tq, lane, res); break;
+    case 2: job_tiles<2, CC>(j.nch, ldb, rg, cst, cphase, aoff, boff, Bsrc, tq, lane, res); break;
+    case 3: job_tiles<3, CC>(j.nch, ldb, rg, cst, cphase, aoff, boff, Bsrc, tq, lane, res); break;
+    case 4: job_tiles<4, CC>(j.nch, ldb, rg, cst, cphase, aoff, boff, Bsrc, tq, lane, res); break;
     default: {  // idle warp: keep the stage/phase bookkeeping and release the stages
       for (int ch = 0; ch < j.nch; ++ch) {
         mbar_wait(rg.full + cst, cphase);
@@ -375,35 +388,35 @@ __device__ __forceinline__ void produce(const Ring& rg, int nsteps, int lane,
 
 template <int CC>
 __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
-    int L, int B, int maps_per_team, int KC, int S, const double* __restrict__ xt, const int64_t* __restrict__ xt_off,
-    const int* __restrict__ perm_all, const int* __restrict__ jstar_all, const double* __restrict__ beta_all,
-    const double* __restrict__ pbt, const int64_t* __restrict__ pb_off, double2* __restrict__ R,
-    double2* __restrict__ flm, double* __restrict__ xg_all, const double* __restrict__ u_all) {
-  cg::cluster_group cluster = cg::this_cluster();
-  const int T = (int)cluster.num_blocks();
-  const int rank = (int)cluster.block_rank();
+    int L, int B, int maps_per_team, int KC, int S, const __grid_constant__ CUtensorMap tmR,
+    const double* __restrict__ xt, const int64_t* __restrict__ xt_off, const double* __restrict__ beta_all,
+    const double* __restrict__ pbt, const int64_t* __restrict__ pb_off, const double* __restrict__ u_all,
+    const double* __restrict__ w_all, double2* __restrict__ R, double2* __restrict__ flm,
+    double* __restrict__ xg_all) {
+  const int T = (int)cg::this_cluster().num_blocks();
+  const int rank = (int)cg::this_cluster().block_rank();
   const int lgT = __ffs(T) - 1;  // T is a power of two (launch_sweep)
   const int team = (int)(blockIdx.x >> lgT);
   const int b0 = team * maps_per_team;
   const int gm = min(maps_per_team, B - b0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tq = lane & 3;
-  constexpr int NB4 = CC / 4;  // map slots of the team
 
   extern __shared__ __align__(128) double smem[];
   const SweepCfg cfg(L, T, CC, KC, S);
-  const int ldr = cfg.ldr, tpc = cfg.tpc, ccp = cfg.ccp;
-  double* xrow = smem + cfg.xrow;
+  const int ldr = cfg.ldr, tpc = cfg.tpc;
   double* gst = smem + cfg.gst;
+  double* xrow = smem + cfg.xrow;
+  double* ubuf = smem + cfg.ubuf;
   double* xg = xg_all + (size_t)team * 2 * L * CC;  // x_s of the team in global memory, by parity
   double* xp = smem + cfg.xp;
   double* wv = smem + cfg.wv;
-  double* ubuf = smem + cfg.ubuf;
   double* apart = smem + cfg.apart;
   double* late = smem + cfg.late;
   double* rch = smem + cfg.rch;
-  int* permb = reinterpret_cast<int*>(smem + cfg.permb);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + cfg.bar);
+  uint64_t* inB = bars + 4 * S;  // B operands of BULK landed
+  uint64_t* inC = inB + 1;       // x_{t+1} for CORR landed
   const size_t stage_elems = (size_t)tpc * KC * 8;
   const Ring ringB{smem + cfg.stage, bars, bars + S, stage_elems, S};
   const Ring ringC{smem + cfg.stage + (size_t)S * stage_elems, bars + 2 * S, bars + 3 * S, stage_elems, S};
@@ -415,11 +428,14 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
       mbar_init(ringC.full + i, 1);
       mbar_init(ringC.empty + i, SWEEP_WC);
     }
+    mbar_init(inB, 1);
+    mbar_init(inC, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  // B operands start zeroed: padding columns read column CC, and a chunk's
-  // rows past K multiply zero operand tiles, so those entries must be finite
+  // B operands start zeroed: a chunk's rows past K multiply zero operand tiles,
+  // so those entries must be finite
   for (size_t i = tid; i < cfg.stage; i += SWEEP_THREADS_ALL) smem[i] = 0.0;
+  fence_proxy_async();
   __syncthreads();
 
   // Steps: q = 0 is the prologue, q = L - t is step t.
@@ -459,7 +475,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
     (void)gn;
     PROF_DECL
     int cst = 0;
-    uint32_t cphase = 0;
+    uint32_t cphase = 0, inphase = 0;
     auto load_rch = [&](int s) {  // R(+-)[s][0] of every map -> rch[s & 1] (synchronous)
       if (gt < gm) {
         const int64_t base = (packed_pos(L, s, 0) * 2) * B + b0 + gt;
@@ -488,16 +504,15 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
       const double bt = beta_next;
       const bool corr = t >= 1 && t + 1 <= L - 1;
       if (t >= 1) beta_next = __ldg(beta_all + t);  // consumed one step later
-      // x_{t+1} (complete since the last cluster barrier) for CORR(t+1), and the
-      // late entry R[t-1][0] of the next step (final now; R[0][0] takes order-2
-      // corrections at step 1 and is read synchronously at step 0)
-      if (corr) {
-        const double* src = xg + (size_t)((t + 1) & 1) * L * CC;
-        for (int idx = gt; idx < (nt - 1) * (CC / 2); idx += SWEEP_NC) {
-          const int l = idx / (CC / 2), c = 2 * (idx % (CC / 2));
-          cp_async16(xrow + (size_t)l * ccp + c, src + (size_t)l * CC + c);
-        }
+      // x_{t+1} (complete since the last cluster barrier) for CORR(t+1): one bulk copy
+      if (corr && gt == 0) {
+        fence_proxy_async();
+        const uint32_t bytes = (uint32_t)((nt - 1) * CC * 8);
+        mbar_arrive_expect_tx(inC, bytes);
+        bulk_g2s(xrow, xg + (size_t)((t + 1) & 1) * L * CC, bytes, inC);
       }
+      // the late entry R[t-1][0] of the next step (final now; R[0][0] takes
+      // order-2 corrections at step 1 and is read synchronously at step 0)
       if (t >= 2) rch_issue(t - 1);
       cp_async_commit();
       if (t == 0) load_rch(0);
@@ -509,7 +524,12 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
         double gp_r = 0.0, gp_i = 0.0, gm_r = 0.0, gm_i = 0.0;  // G+_{t+1}(theta_t), G-_{t+1}(theta_t)
         if (t < L - 1) {
           const double s1 = ((t + 1) & 1) ? -1.0 : 1.0;
-          const double* a = apart + (size_t)(t & 3) * CC + 4 * b;
+          double a[4] = {0.0, 0.0, 0.0, 0.0};
+          const double* ap = apart + (size_t)(t & 3) * SWEEP_WB * CC + 4 * b;
+#pragma unroll
+          for (int w = 0; w < SWEEP_WB; ++w)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] += ap[w * CC + u];
           const double* ln = late + (size_t)((t + 1) & 1) * CC + 4 * b;
           gp_r = a[0] + bt * ln[0];
           gp_i = a[1] + bt * ln[1];
@@ -556,15 +576,15 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
         }
       }
       PROF_MARK(2);
-      cp_async_wait_all();
       // ---- (c) CORR(t+1): corrections of order s = t+1 on own rings k < t
       if (corr) {
         const int s = t + 1;
         const double ss = (s & 1) ? -1.0 : 1.0;
-        group_sync(SWEEP_BAR_C, SWEEP_NC);
+        mbar_wait(inC, inphase);
+        inphase ^= 1u;
         PROF_MARK(3);
         const Job j = make_job(1, s, L, lgT, rank, SWEEP_KC, xt, xt_off, pbt, pb_off, false);
-        run_job<CC>(j, ringC, cst, cphase, gw, SWEEP_WC, xrow, ccp, g, tq, lane, [&](int k, int c, double v0, double v1) {
+        run_job<CC>(j, ringC, cst, cphase, gw, SWEEP_WC, xrow, CC, g, tq, lane, [&](int k, int c, double v0, double v1) {
           const int bl = c >> 2;
           if (k >= s - 1 || bl >= gm) return;  // ring s-1 is the chain
           const bool plus = (c & 2) == 0;
@@ -590,6 +610,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
         });
       }
       PROF_MARK(4);
+      cp_async_wait_all();
+      // this step's x_t stores and reductions are read by bulk copies next step
+      fence_proxy_async();
       cluster_sync_all();
       PROF_MARK(5);
     }
@@ -605,107 +628,99 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
     (void)gn;
     PROF_DECL
     int cst = 0;
-    uint32_t cphase = 0;
-    // pivot order of order s -> permb[s & 1] (one step ahead, by cp.async)
-    auto perm_issue = [&](int s) {
-      const int ns = L - s;
-      const int* perm = perm_all + packed_pos(L, s, 0);
-      int* d = permb + (size_t)(s & 1) * cfg.ldx;
-      for (int i = gt; i < ns; i += SWEEP_NB) cp_async4(d + i, perm + i);
+    uint32_t cphase = 0, inphase = 0;
+    // Columns of gst are [+-][map][re, im] (the TMA box order); every other
+    // buffer uses [map][+-][re, im].  Column pair c, c+1 of gst -> canonical pair.
+    auto canon_col = [](int c) {
+      const int sl = c >= CC / 2 ? 1 : 0;
+      return 4 * ((c - sl * (CC / 2)) >> 1) + 2 * sl;
     };
-    // gathered right-hand side of order s -> gst (row-major [j][ccp]), unsigned
-    auto gather_issue = [&](int s) {
-      const int ns = L - s;
-      const int64_t ps = packed_pos(L, s, 0);
-      const int* pm = permb + (size_t)(s & 1) * cfg.ldx;
-      for (int idx = gt; idx < ns * NB4; idx += SWEEP_NB) {
-        const int jj = idx / NB4, bl = idx % NB4;
-        const int pj = pm[jj];
-        double* dst = gst + (size_t)jj * ccp + 4 * bl;
-        if (pj > 0 && bl < gm) {
-          const int64_t base = ((ps + pj) * 2) * B + b0 + bl;
-          cp_async16(dst, R + base);
-          cp_async16(dst + 2, R + base + B);
-        } else {  // late entry (ring s) is excluded from x'_s; padding map slots are zero
-          dst[0] = dst[1] = dst[2] = dst[3] = 0.0;
-        }
-      }
-    };
-    // data-independent operands of BULK(s) -> smem: w_s = X_s[own rows, j*_s] and
-    // u_s; the scalars (offset, j*) are loaded one step earlier
-    int64_t sx_off = 0;
-    int sjs = 0;
-    auto side_scalars = [&](int s) {
-      if (s >= 0) {
-        sx_off = __ldg(xt_off + s);
-        sjs = __ldg(jstar_all + s);
-      }
-    };
-    auto side_issue = [&](int s) {
+    // B operands of BULK(s), one thread, bulk copies: the right-hand side rows
+    // pos(s, 0..ns-1) of the team's maps (TMA boxes of the [pos][+-][map] R),
+    // w_s on own rows and u_s
+    auto operands_issue = [&](int s) {
+      if (gt != 0) return;
+      fence_proxy_async();
       const int ns = L - s, nrt = (ns + 7) / 8;
       const int r0 = 8 * ((rank * nrt) >> lgT), r1 = min(ns, 8 * (((rank + 1) * nrt) >> lgT));
-      for (int i = gt; i < r1 - r0; i += SWEEP_NB)
-        cp_async8(wv + (size_t)(s & 1) * ldr + i, xt + sx_off + tile_index(r0 + i, sjs, nrt));
-      if (s >= 1) {
-        const double* us = u_all + packed_pos(L, s, 0);
-        for (int i = gt; i < ns; i += SWEEP_NB) cp_async8(ubuf + i, us + i);
-      }
+      const int nbox = (ns + SWEEP_BOXR - 1) / SWEEP_BOXR;
+      const uint32_t wb = (uint32_t)(((max(r1 - r0, 0) + 1) & ~1) * 8);
+      const uint32_t ub = (uint32_t)(((ns + 1) & ~1) * 8);
+      mbar_arrive_expect_tx(inB, (uint32_t)(nbox * SWEEP_BOXR * CC * 8) + wb + ub);
+      const int pos0 = (int)packed_pos(L, s, 0);
+      for (int q = 0; q < nbox; ++q)
+        tma_load_3d(gst + (size_t)q * SWEEP_BOXR * CC, &tmR, 2 * b0, 0, pos0 + q * SWEEP_BOXR, inB);
+      if (wb) bulk_g2s(wv + (size_t)(s & 1) * ldr, w_all + (size_t)s * L + r0, wb, inB);
+      bulk_g2s(ubuf, u_all + (size_t)s * L, ub, inB);
     };
     // BULK(s): x'_s on own rows (the (-1)^s of the -m columns applied here),
-    // and the chain partial a_{s-1} = u_s . (P rhs_s) of the whole team: every
-    // CTA holds the full gathered right-hand side, so no exchange is needed
+    // and the chain partial a_{s-1} = u_s . rhs_s of the whole team: every CTA
+    // holds the full right-hand side, so no exchange is needed
     auto bulk = [&](int s) {
       const Job j = make_job(0, s, L, lgT, rank, SWEEP_KC, xt, xt_off, pbt, pb_off, false);
       const int ns = j.K;
       const int r0 = 8 * j.rt0;
       double* xps = xp + (size_t)(s & 1) * CC * ldr;
       const double ss = (s & 1) ? -1.0 : 1.0;
-      run_job<CC>(j, ringB, cst, cphase, gw, SWEEP_WB, gst, ccp, g, tq, lane, [&](int l, int c, double v0, double v1) {
+      run_job<CC>(j, ringB, cst, cphase, gw, SWEEP_WB, gst, CC, g, tq, lane, [&](int l, int c, double v0, double v1) {
         if (l < ns) {
-          const double sg = (c & 2) ? ss : 1.0;
-          xps[(size_t)c * ldr + (l - r0)] = sg * v0;
-          xps[(size_t)(c + 1) * ldr + (l - r0)] = sg * v1;
+          const int cc = canon_col(c);
+          const double sg = (cc & 2) ? ss : 1.0;
+          xps[(size_t)cc * ldr + (l - r0)] = sg * v0;
+          xps[(size_t)(cc + 1) * ldr + (l - r0)] = sg * v1;
         }
       });
       PROF_MARK(3);
-      if (s >= 1) {
-        for (int c = gw; c < CC; c += SWEEP_WB) {
-          double acc = 0.0;
-          for (int l = lane; l < ns; l += 32) acc += ubuf[l] * gst[(size_t)l * ccp + c];
+      if (s >= 1) {  // u_s . rhs_s on the tensor cores: row 0 of an 8 x K A operand
+        constexpr int NCT = (CC + 7) / 8;
+        double acc[NCT][2][2];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-          if (lane == 0) apart[((s - 1) & 3) * CC + c] = (c & 2) ? ss * acc : acc;
+        for (int ct = 0; ct < NCT; ++ct) acc[ct][0][0] = acc[ct][0][1] = acc[ct][1][0] = acc[ct][1][1] = 0.0;
+        const int nks = (ns + 3) >> 2;
+        for (int kk = gw; kk < nks; kk += 2 * SWEEP_WB) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (kk + h * SWEEP_WB >= nks) break;  // warp-uniform
+            const int k = 4 * (kk + h * SWEEP_WB) + tq;  // rows ns..4*nks-1: u is zero there
+            const double a = g == 0 ? ubuf[k] : 0.0;
+#pragma unroll
+            for (int ct = 0; ct < NCT; ++ct) {
+              const int col = ct * 8 + g;
+              const double b = (CC >= 8 || col < CC) ? gst[(size_t)k * CC + col] : 0.0;
+              dmma_8x8x4(acc[ct][h][0], acc[ct][h][1], a, b);
+            }
+          }
+        }
+        if (g == 0) {
+          double* ap = apart + ((s - 1) & 3) * SWEEP_WB * CC + gw * CC;
+#pragma unroll
+          for (int ct = 0; ct < NCT; ++ct) {
+            const int c = ct * 8 + 2 * tq;
+            if (c < CC) {
+              const int cc = canon_col(c);
+              const double sg = (cc & 2) ? ss : 1.0;
+              ap[cc] = sg * (acc[ct][0][0] + acc[ct][1][0]);
+              ap[cc + 1] = sg * (acc[ct][0][1] + acc[ct][1][1]);
+            }
+          }
         }
       }
     };
 
     // ---- prologue: x'_{L-1}, a_{L-2}
-    perm_issue(L - 1);
-    side_scalars(L - 1);
-    cp_async_commit();
-    cp_async_wait_all();
-    group_sync(SWEEP_BAR_B, SWEEP_NB);
-    gather_issue(L - 1);
-    side_issue(L - 1);
-    if (L >= 2) perm_issue(L - 2);
-    cp_async_commit();
-    cp_async_wait_all();
-    group_sync(SWEEP_BAR_B, SWEEP_NB);
+    operands_issue(L - 1);
+    mbar_wait(inB, inphase);
+    inphase ^= 1u;
     bulk(L - 1);
-    side_scalars(L - 2);
     cluster_sync_all();
     for (int t = L - 1; t >= 0; --t) {
       if (t >= 1) {
         // the right-hand side of order t-1 is final now: every correction but
         // the chain's has landed
-        gather_issue(t - 1);
-        side_issue(t - 1);
-        if (t >= 2) perm_issue(t - 2);
-        cp_async_commit();
-        if (t >= 2) side_scalars(t - 2);
+        operands_issue(t - 1);
         PROF_MARK(0);
-        cp_async_wait_all();
-        group_sync(SWEEP_BAR_B, SWEEP_NB);
+        mbar_wait(inB, inphase);
+        inphase ^= 1u;
         PROF_MARK(1);
         bulk(t - 1);
       }
@@ -747,9 +762,27 @@ static cudaError_t launch_sweep_cc(osph_plan* p, int B, int g, int T, int KC, in
     fprintf(stderr, "[osph] sweep L=%d B=%d maps/team=%d teams=%d T=%d KC=%d S=%d smem=%zu maxActiveClusters=%d\n", L,
             B, g, teams, T, KC, S, smem, nclusters);
   }
-  e = cudaLaunchKernelEx(&lc, kern, L, B, g, KC, S, (const double*)p->d_xt, (const int64_t*)p->d_xt_off,
-                         (const int*)p->d_piv, (const int*)p->d_jstar, (const double*)p->d_beta,
-                         (const double*)p->d_pbelow, (const int64_t*)p->d_pb_off, p->d_r, flm, p->d_xg, (const double*)p->d_u);
+  // R as a 3-D tensor [pos][+-][2 B doubles]: one box = SWEEP_BOXR positions x
+  // both signs x the team's maps, delivered row-major [row][CC] (maps past B zero-filled)
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if ((e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q)) != cudaSuccess)
+      return e;
+    if (!encode) return cudaErrorSymbolNotFound;
+  }
+  CUtensorMap tm;
+  const cuuint64_t dims[3] = {(cuuint64_t)2 * B, 2, (cuuint64_t)L * (L + 1) / 2};
+  const cuuint64_t strides[2] = {(cuuint64_t)2 * B * sizeof(double), (cuuint64_t)4 * B * sizeof(double)};
+  const cuuint32_t box[3] = {(cuuint32_t)(2 * g), 2, SWEEP_BOXR};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)p->d_r, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  e = cudaLaunchKernelEx(&lc, kern, L, B, g, KC, S, tm, (const double*)p->d_xt, (const int64_t*)p->d_xt_off,
+                         (const double*)p->d_beta, (const double*)p->d_pbelow, (const int64_t*)p->d_pb_off,
+                         (const double*)p->d_u, (const double*)p->d_w, p->d_r, flm, p->d_xg);
   p->launches++;
   return e;
 }
