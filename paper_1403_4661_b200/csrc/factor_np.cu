@@ -7,10 +7,10 @@
 // O(L^2) tables -- the reference likewise caches O(L^2) tables per band
 // limit, transform.py:268-301).  Every later call regenerates A_m in that row
 // order and inverts it by blocked Gauss-Jordan WITHOUT a pivot search -- the
-// identical elimination sequence, so the same rounding behaviour -- which
-// turns each panel step into a 32x32 diagonal-block inverse (one warp) plus
-// two GEMMs on the fp64 tensor cores:
-//     Dinv = A[P,P]^{-1},  E = -A[:,P] Dinv (E[P] = Dinv - I),  A[:, rest] += E A[P, rest].
+// identical elimination sequence -- which turns each panel step into an
+// unblocked elimination of the n x 32 panel (one row per thread, in
+// registers, one barrier per pivot) plus one GEMM on the fp64 tensor cores:
+//     [E + I on P] = GJ(A[:, P]),  A[:, rest] += E A[P, rest].
 // The O(L^3) work (generation + inversion) is still done per call.
 //
 // One thread-block cluster per order; CTA r owns a contiguous slice of the
@@ -22,6 +22,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
+#include <utility>
 
 #include "plan.cuh"
 
@@ -44,6 +46,11 @@ namespace cg = cooperative_groups;
 #define FNP_MARK(i)
 #endif
 
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+
 __device__ __forceinline__ void np_atomic_max_pos(unsigned long long* addr, double v) {
   if (!(v >= 0.0) || isinf(v)) v = INFINITY;
   atomicMax(addr, (unsigned long long)__double_as_longlong(v));
@@ -51,7 +58,7 @@ __device__ __forceinline__ void np_atomic_max_pos(unsigned long long* addr, doub
 
 struct NpLayout {
   int ldn, cwmax;
-  size_t slice, es, dinv, rowbuf, pinv_bytes_off, total_doubles;
+  size_t slice, es, rowbuf, pinv_bytes_off, total_doubles;
   __host__ __device__ NpLayout(int nmax, int CS) {
     ldn = ((nmax + 15) / 16) * 16 + 4;
     const int units = (nmax + FNP_NB - 1) / FNP_NB;
@@ -59,8 +66,7 @@ struct NpLayout {
     size_t o = 0;
     slice = o;  o += (size_t)cwmax * ldn;
     es = o;     o += (size_t)FNP_NB * ldn;
-    dinv = o;   o += (size_t)FNP_NB * FNP_NB;
-    rowbuf = o; o += FNP_NB;
+    rowbuf = o; o += 2 * FNP_NB;
     pinv_bytes_off = o;  // ints follow
     o += (size_t)(nmax + 1) / 2 + 1;
     total_doubles = o;
@@ -89,8 +95,7 @@ __global__ void __launch_bounds__(FNP_THREADS, 1) k_factor_np(
   const int ldn = lay.ldn;
   double* slice = smem + lay.slice;    // own columns, column-major, ld = ldn
   double* Es = smem + lay.es;          // panel / E, column-major [NB][ldn]
-  double* Dinv = smem + lay.dinv;      // [NB][NB] row-major
-  double* rowbuf = smem + lay.rowbuf;  // pivot row broadcast for the diagonal inverse
+  double* rowbuf = smem + lay.rowbuf;  // scaled pivot row broadcast, double-buffered
   int* pinv = reinterpret_cast<int*>(smem + lay.pinv_bytes_off);
   __shared__ int s_bad;
   __shared__ double s_red[FNP_WARPS];
@@ -163,161 +168,151 @@ __global__ void __launch_bounds__(FNP_THREADS, 1) k_factor_np(
   FNP_MARK(0);
   // ---- 2. blocked Gauss-Jordan, static pivots
   const int nct = cwt >> 3;  // own 8-column tiles
+  auto export_panel = [&](int jp, double* dst) {  // own columns jp .. jp+nb-1 -> global
+    const int nbp = min(FNP_NB, n - jp);
+    for (int c = warp; c < nbp; c += FNP_WARPS)
+      for (int r = lane; r < n; r += 32) dst[(size_t)c * ldn + r] = slice[(size_t)(jp - c0 + c) * ldn + r];
+  };
   for (int j0 = 0, par = 0; j0 < n; j0 += FNP_NB, par ^= 1) {
     const int nb = min(FNP_NB, n - j0);
     const bool owner = j0 >= c0 && j0 < c1;
     double* pgp = pg + (size_t)par * FNP_NB * ldn;
-    if (owner)
-      for (int c = warp; c < nb; c += FNP_WARPS)
-        for (int r = lane; r < n; r += 32) pgp[(size_t)c * ldn + r] = slice[(size_t)(j0 - c0 + c) * ldn + r];
-    cluster.sync();
+    if (owner) export_panel(j0, pgp);
+    cluster_arrive();
+    cluster_wait();
     FNP_MARK(1);
-    // a) panel -> Es (columns >= nb zero)
-    for (int c = warp; c < FNP_NB; c += FNP_WARPS)
-      for (int r = lane; r < n; r += 32) Es[(size_t)c * ldn + r] = c < nb ? __ldcg(pgp + (size_t)c * ldn + r) : 0.0;
-    __syncthreads();
-    FNP_MARK(2);
-    // b) Dinv = A[P,P]^{-1}: unpivoted Gauss-Jordan in one warp (lane = row)
-    if (warp == 0) {
-      double d[FNP_NB];
+    // a) panel -> registers, thread = row (columns >= nb zero)
+    double d[FNP_NB];
+    const bool hasrow = tid < n;
 #pragma unroll
-      for (int c = 0; c < FNP_NB; ++c) d[c] = (lane < nb && c < nb) ? Es[(size_t)c * ldn + j0 + lane] : 0.0;
+    for (int c = 0; c < FNP_NB; ++c)
+      d[c] = (hasrow && c < nb) ? __ldcg(pgp + (size_t)c * ldn + tid) : 0.0;
+    FNP_MARK(2);
+    // b) unblocked Gauss-Jordan on the n x nb panel (the same elimination the
+    //    full in-place inversion applies to these columns), one row per thread
+    //    in registers.  The row is kept ROTATED so that the current pivot column
+    //    is always d[0]: step p maps d[c] <- column (p + c) mod 32, so the loop
+    //    body has static register indices and stays rolled (the code runs 32
+    //    times per panel from the instruction cache).  Pivot row r = j0 + p is
+    //    published unscaled with its reciprocal (double-buffered: one barrier
+    //    per pivot); every other row subtracts g = f / piv times it, and the
+    //    pivot column's entry becomes -g.  The result is the new panel E + I on P.
+    // published record: [pivot row columns p+1 .. p+31 (rotated), 1 / pivot]
+    auto publish = [&](double* pn) {
+#pragma unroll
+      for (int c = 0; c < FNP_NB - 2; c += 2) *reinterpret_cast<double2*>(pn + c) = make_double2(d[c + 1], d[c + 2]);
+      if (d[0] == 0.0 || !isfinite(d[0])) s_bad = 1;
+      *reinterpret_cast<double2*>(pn + FNP_NB - 2) = make_double2(d[FNP_NB - 1], 1.0 / d[0]);
+    };
+    double rsc = 1.0;  // scale of this row (1/piv once it has been the pivot)
+    if (hasrow && tid == j0) publish(rowbuf);
+    for (int p = 0; p < nb; ++p) {
+      __syncthreads();
+      const double* pr = rowbuf + (p & 1) * FNP_NB;
+      double v[FNP_NB];
+#pragma unroll
+      for (int c = 0; c < FNP_NB; c += 2) {
+        const double2 t2 = *reinterpret_cast<const double2*>(pr + c);
+        v[c] = t2.x;
+        v[c + 1] = t2.y;
+      }
+      const double inv = v[FNP_NB - 1];
+      if (hasrow) {
+        // lazy pivot scaling: the pivot row only rotates (gg = 0, its new
+        // column is 1) and remembers its scale 1/piv, applied after the panel
+        // -- no divergent branch in the step
+        const bool ispiv = tid == j0 + p;
+        const double gg = ispiv ? 0.0 : d[0] * inv;
+        rsc = ispiv ? inv : rsc;
+#pragma unroll
+        for (int c = 0; c < FNP_NB - 1; ++c) d[c] = fma(-gg, v[c], d[c + 1]);
+        d[FNP_NB - 1] = ispiv ? 1.0 : -gg;
+        if (p + 1 < nb && tid == j0 + p + 1) publish(rowbuf + ((p + 1) & 1) * FNP_NB);  // next pivot: d[0]
+      }
+    }
+    FNP_MARK(3);
+    // c) E -> Es (E = new panel - I on P); d) owner: new panel columns.
+    //    After nb steps d[c] holds column (c + nb) mod 32.
+    if (hasrow) {
 #pragma unroll
       for (int c = 0; c < FNP_NB; ++c) {
-        if (c < nb) {
-          if (lane == c) {
-#pragma unroll
-            for (int cc = 0; cc < FNP_NB; cc += 2)
-              *reinterpret_cast<double2*>(rowbuf + cc) = make_double2(d[cc], d[cc + 1]);
-          }
-          __syncwarp();
-          const double piv = rowbuf[c];
-          if (lane == 0 && (piv == 0.0 || !isfinite(piv))) s_bad = 1;
-          const double inv = 1.0 / piv;
-          if (lane == c) {
-#pragma unroll
-            for (int cc = 0; cc < FNP_NB; ++cc) d[cc] = (cc == c) ? inv : d[cc] * inv;
-          } else {
-            const double f = d[c] * inv;
-#pragma unroll
-            for (int cc = 0; cc < FNP_NB; cc += 2) {
-              const double2 pr = *reinterpret_cast<const double2*>(rowbuf + cc);
-              if (cc != c) d[cc] = fma(-f, pr.x, d[cc]);
-              if (cc + 1 != c) d[cc + 1] = fma(-f, pr.y, d[cc + 1]);
-            }
-            d[c] = -f;
-          }
-          __syncwarp();
-        }
+        const int col = (c + nb) & (FNP_NB - 1);
+        const double x = d[c] * rsc;
+        Es[(size_t)col * ldn + tid] = x - (tid == j0 + col ? 1.0 : 0.0);
+        if (owner && col < nb) slice[(size_t)(j0 - c0 + col) * ldn + tid] = x;
       }
-#pragma unroll
-      for (int c = 0; c < FNP_NB; ++c) Dinv[lane * FNP_NB + c] = (lane < nb && c < nb) ? d[c] : 0.0;
     }
-    __syncthreads();
-    FNP_MARK(3);
-    // c) E = -A[:,P] Dinv (rows outside P), E[P] = Dinv - I; in place in Es, one 8-row tile per warp pass
     const int pt0 = j0 >> 3, pt1 = (j0 + nb + 7) >> 3;
-    for (int rt = warp; rt < nrt8; rt += FNP_WARPS) {
-      const int r0 = rt * 8;
-      if (rt >= pt0 && rt < pt1) {
-        for (int e = lane; e < 8 * FNP_NB; e += 32) {
-          const int r = e & 7, c = e >> 3;
-          const int pr = r0 + r - j0;
-          Es[(size_t)c * ldn + r0 + r] =
-              (pr >= 0 && pr < nb && c < nb) ? Dinv[pr * FNP_NB + c] - (pr == c ? 1.0 : 0.0) : 0.0;
-        }
-        continue;
-      }
-      double acc[FNP_NB / 8][2];
-#pragma unroll
-      for (int ct = 0; ct < FNP_NB / 8; ++ct) acc[ct][0] = acc[ct][1] = 0.0;
-#pragma unroll
-      for (int k = 0; k < FNP_NB; k += 4) {
-        const double a = Es[(size_t)(k + tq) * ldn + r0 + g];
-#pragma unroll
-        for (int ct = 0; ct < FNP_NB / 8; ++ct)
-          dmma_8x8x4(acc[ct][0], acc[ct][1], a, Dinv[(k + tq) * FNP_NB + ct * 8 + g]);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int ct = 0; ct < FNP_NB / 8; ++ct) {
-        Es[(size_t)(ct * 8 + 2 * tq) * ldn + r0 + g] = -acc[ct][0];
-        Es[(size_t)(ct * 8 + 2 * tq + 1) * ldn + r0 + g] = -acc[ct][1];
-      }
-    }
     __syncthreads();
     FNP_MARK(4);
-    // d) owner: new panel columns = E + I on P
-    if (owner)
-      for (int c = warp; c < nb; c += FNP_WARPS)
-        for (int r = lane; r < n; r += 32)
-          slice[(size_t)(j0 - c0 + c) * ldn + r] = Es[(size_t)c * ldn + r] + (r == j0 + c ? 1.0 : 0.0);
     // e) A[:, own rest] += E * A[P, own rest].  A warp keeps its row tile's E
     //    fragments in registers and sweeps the column tiles four at a time
     //    (independent accumulators).  Rows outside P first (they read the P
-    //    rows in place), then the P rows (all reads before any write).
-    {
-      const int pc0 = owner ? (j0 - c0) >> 3 : -1, pc1 = owner ? (j0 - c0 + nb + 7) >> 3 : -1;
-      const int trow = min(j0 + tq, ldn - 1);  // B operand row (k-step 0); E is zero past nb
-      auto row_tile = [&](int rt, bool store_now, double (*keep)[4][2]) {
-        const int r0 = rt * 8;
-        double a[FNP_NB / 4];
+    //    rows in place), then the P rows (all reads before any write).  Column
+    //    tiles [lo, hi) minus the current panel's and minus [x0, x1).
+    const int pc0 = owner ? (j0 - c0) >> 3 : -1, pc1 = owner ? (j0 - c0 + nb + 7) >> 3 : -1;
+    const int trow = min(j0 + tq, ldn - 1);  // B operand row (k-step 0); E is zero past nb
+    auto row_tile = [&](int rt, bool store_now, double (*keep)[4][2], int lo, int hi, int x0, int x1) {
+      const int r0 = rt * 8;
+      double a[FNP_NB / 4];
 #pragma unroll
-        for (int ks = 0; ks < FNP_NB / 4; ++ks) a[ks] = Es[(size_t)(4 * ks + tq) * ldn + r0 + g];
-        for (int cb = 0; cb < nct; cb += 4) {
-          double acc[4][2];
+      for (int ks = 0; ks < FNP_NB / 4; ++ks) a[ks] = Es[(size_t)(4 * ks + tq) * ldn + r0 + g];
+      for (int cb = lo; cb < hi; cb += 4) {
+        double acc[4][2];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int cc = (cb + u) * 8;
-            const bool ok = cb + u < nct;
-            acc[u][0] = ok ? slice[(size_t)(cc + 2 * tq) * ldn + r0 + g] : 0.0;
-            acc[u][1] = ok ? slice[(size_t)(cc + 2 * tq + 1) * ldn + r0 + g] : 0.0;
-          }
+        for (int u = 0; u < 4; ++u) {
+          const int cc = (cb + u) * 8;
+          const bool ok = cb + u < hi;
+          acc[u][0] = ok ? slice[(size_t)(cc + 2 * tq) * ldn + r0 + g] : 0.0;
+          acc[u][1] = ok ? slice[(size_t)(cc + 2 * tq + 1) * ldn + r0 + g] : 0.0;
+        }
 #pragma unroll
-          for (int ks = 0; ks < FNP_NB / 4; ++ks) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int cc = min(cb + u, nct - 1) * 8;
-              const double b = slice[(size_t)(cc + g) * ldn + min(trow + 4 * ks, ldn - 1)];
-              dmma_8x8x4(acc[u][0], acc[u][1], a[ks], b);
-            }
-          }
+        for (int ks = 0; ks < FNP_NB / 4; ++ks) {
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int ct = cb + u;
-            if (ct >= nct || (ct >= pc0 && ct < pc1)) continue;
-            if (store_now) {
-              slice[(size_t)(ct * 8 + 2 * tq) * ldn + r0 + g] = acc[u][0];
-              slice[(size_t)(ct * 8 + 2 * tq + 1) * ldn + r0 + g] = acc[u][1];
-            } else {
-              keep[cb / 4][u][0] = acc[u][0];
-              keep[cb / 4][u][1] = acc[u][1];
-            }
+            const int cc = min(cb + u, hi - 1) * 8;
+            const double b = slice[(size_t)(cc + g) * ldn + min(trow + 4 * ks, ldn - 1)];
+            dmma_8x8x4(acc[u][0], acc[u][1], a[ks], b);
           }
         }
-      };
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int ct = cb + u;
+          if (ct >= hi || (ct >= pc0 && ct < pc1) || (ct >= x0 && ct < x1)) continue;
+          if (store_now) {
+            slice[(size_t)(ct * 8 + 2 * tq) * ldn + r0 + g] = acc[u][0];
+            slice[(size_t)(ct * 8 + 2 * tq + 1) * ldn + r0 + g] = acc[u][1];
+          } else {
+            keep[(cb - lo) / 4][u][0] = acc[u][0];
+            keep[(cb - lo) / 4][u][1] = acc[u][1];
+          }
+        }
+      }
+    };
+    auto update_cols = [&](int lo, int hi, int x0, int x1) {
       for (int rt = warp; rt < nrt8; rt += FNP_WARPS)
-        if (!(rt >= pt0 && rt < pt1)) row_tile(rt, true, nullptr);
-      // P rows: nb/8 <= 4 row tiles, one per warp; own columns <= 128 (launcher) -> <= 4 blocks of 4 tiles
+        if (!(rt >= pt0 && rt < pt1)) row_tile(rt, true, nullptr, lo, hi, x0, x1);
+      // P rows: nb/8 <= 4 row tiles, one per warp; <= 16 column tiles -> <= 4 blocks of 4
       double keep[4][4][2];
       const int prt = pt0 + warp;
       const bool pw = prt < pt1;
       __syncthreads();
-      if (pw) row_tile(prt, false, keep);
+      if (pw) row_tile(prt, false, keep, lo, hi, x0, x1);
       __syncthreads();
       if (pw) {
 #pragma unroll
         for (int q = 0; q < 4; ++q)
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int ct = q * 4 + u;
-            if (ct >= nct || (ct >= pc0 && ct < pc1)) continue;
+            const int ct = lo + q * 4 + u;
+            if (ct >= hi || (ct >= pc0 && ct < pc1) || (ct >= x0 && ct < x1)) continue;
             slice[(size_t)(ct * 8 + 2 * tq) * ldn + prt * 8 + g] = keep[q][u][0];
             slice[(size_t)(ct * 8 + 2 * tq + 1) * ldn + prt * 8 + g] = keep[q][u][1];
           }
       }
-    }
-    __syncthreads();
+      __syncthreads();
+    };
+    update_cols(0, nct, 0, 0);
     FNP_MARK(5);
   }
 
