@@ -58,6 +58,14 @@ static void plan_free(osph_plan* p) {
     if (q) cudaFree(q);
   for (cudaEvent_t& e : p->ev)
     if (e) cudaEventDestroy(e);
+  for (int c = 0; c < osph_plan::kIoChunks; ++c) {
+    if (p->ev_in[c]) cudaEventDestroy(p->ev_in[c]);
+    if (p->ev_done[c]) cudaEventDestroy(p->ev_done[c]);
+  }
+  if (p->ev_start) cudaEventDestroy(p->ev_start);
+  if (p->ev_out) cudaEventDestroy(p->ev_out);
+  if (p->s_in) cudaStreamDestroy(p->s_in);
+  if (p->s_out) cudaStreamDestroy(p->s_out);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   delete p;
 }
@@ -121,6 +129,14 @@ extern "C" int osph_plan_create(int L, const double* thetas, int max_batch, int 
   PLAN_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
   p->own_stream = true;
   for (cudaEvent_t& e : p->ev) PLAN_TRY(cudaEventCreate(&e));
+  PLAN_TRY(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
+  PLAN_TRY(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
+  for (int c = 0; c < osph_plan::kIoChunks; ++c) {
+    PLAN_TRY(cudaEventCreateWithFlags(&p->ev_in[c], cudaEventDisableTiming));
+    PLAN_TRY(cudaEventCreateWithFlags(&p->ev_done[c], cudaEventDisableTiming));
+  }
+  PLAN_TRY(cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming));
+  PLAN_TRY(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
   cudaStream_t st = p->stream;
 
   std::vector<double> c(L), s(L);
@@ -288,6 +304,10 @@ static int check_call(osph_plan* p, int B, const void* a, void* b, int kind) {
   return OSPH_OK;
 }
 
+// Host buffers: the batch is cut into up to kIoChunks map chunks; chunk c's
+// H2D copy (s_in), compute (plan stream) and D2H copy (s_out) are chained by
+// events, so copies of neighbouring chunks overlap the compute in both
+// directions.  Device buffers: one pass on the plan stream.
 extern "C" int osph_inverse(osph_plan* p, int B, const void* flm, void* samples, int kind) {
   g_last_error.clear();
   int rc = check_call(p, B, flm, samples, kind);
@@ -296,25 +316,43 @@ extern "C" int osph_inverse(osph_plan* p, int B, const void* flm, void* samples,
   if ((rc = ensure_inverse(p))) return rc;
   const bool host = !(kind & OSPH_DEVICE);
   if (host && (rc = ensure_io(p))) return rc;
-  const size_t bytes = sizeof(double2) * (size_t)B * p->L * p->L;
+  const size_t per_map = (size_t)p->L * p->L;
   cudaStream_t st = p->stream;
   p->launches = 0;
-  const double2* in = (const double2*)flm;
-  double2* out = (double2*)samples;
-  if (host) {
-    CUDA_TRY(cudaMemcpyAsync(p->d_in, flm, bytes, cudaMemcpyHostToDevice, st));
-    in = p->d_in;
-    out = p->d_out;
+  if (!host) {
+    CUDA_TRY(cudaEventRecord(p->ev[0], st));
+    CUDA_TRY(launch_pack(p, B, (const double2*)flm));
+    CUDA_TRY(cudaEventRecord(p->ev[1], st));
+    CUDA_TRY(launch_synth(p, B));
+    CUDA_TRY(cudaEventRecord(p->ev[2], st));
+    CUDA_TRY(launch_ring_inverse(p, B, (double2*)samples));
+    CUDA_TRY(cudaEventRecord(p->ev[3], st));
+  } else {
+    const int nch = std::min(B, osph_plan::kIoChunks);
+    CUDA_TRY(cudaEventRecord(p->ev_start, st));  // earlier work on the plan stream (staging buffers)
+    CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
+    CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->ev_start, 0));
+    for (int c = 0; c < nch; ++c) {
+      const int b0 = (int)((int64_t)B * c / nch), b1 = (int)((int64_t)B * (c + 1) / nch), bc = b1 - b0;
+      const size_t off = (size_t)b0 * per_map, bytes = sizeof(double2) * (size_t)bc * per_map;
+      CUDA_TRY(cudaMemcpyAsync(p->d_in + off, (const double2*)flm + off, bytes, cudaMemcpyHostToDevice, p->s_in));
+      CUDA_TRY(cudaEventRecord(p->ev_in[c], p->s_in));
+      CUDA_TRY(cudaStreamWaitEvent(st, p->ev_in[c], 0));
+      if (c == 0) CUDA_TRY(cudaEventRecord(p->ev[0], st));
+      CUDA_TRY(launch_pack(p, bc, p->d_in + off));
+      if (c == 0) CUDA_TRY(cudaEventRecord(p->ev[1], st));
+      CUDA_TRY(launch_synth(p, bc));
+      if (c == 0) CUDA_TRY(cudaEventRecord(p->ev[2], st));
+      CUDA_TRY(launch_ring_inverse(p, bc, p->d_out + off));
+      CUDA_TRY(cudaEventRecord(p->ev_done[c], st));
+      CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->ev_done[c], 0));
+      CUDA_TRY(cudaMemcpyAsync((double2*)samples + off, p->d_out + off, bytes, cudaMemcpyDeviceToHost, p->s_out));
+    }
+    CUDA_TRY(cudaEventRecord(p->ev[3], st));
+    CUDA_TRY(cudaEventRecord(p->ev_out, p->s_out));
+    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_out, 0));  // the plan stream covers the whole call
   }
-  CUDA_TRY(cudaEventRecord(p->ev[0], st));
-  CUDA_TRY(launch_pack(p, B, in));
-  CUDA_TRY(cudaEventRecord(p->ev[1], st));
-  CUDA_TRY(launch_synth(p, B));
-  CUDA_TRY(cudaEventRecord(p->ev[2], st));
-  CUDA_TRY(launch_ring_inverse(p, B, out));
-  CUDA_TRY(cudaEventRecord(p->ev[3], st));
   p->have_inv = true;
-  if (host) CUDA_TRY(cudaMemcpyAsync(samples, p->d_out, bytes, cudaMemcpyDeviceToHost, st));
   if (!(kind & OSPH_ASYNC)) CUDA_TRY(cudaStreamSynchronize(st));
   return OSPH_OK;
 }
@@ -336,22 +374,43 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
   const size_t bytes = sizeof(double2) * (size_t)B * L * L;
   cudaStream_t st = p->stream;
   p->launches = 0;
-  const double2* in = (const double2*)samples;
-  double2* out = (double2*)flm;
-  if (host) {
-    CUDA_TRY(cudaMemcpyAsync(p->d_in, samples, bytes, cudaMemcpyHostToDevice, st));
-    in = p->d_in;
-    out = p->d_out;
+  double2* out = host ? p->d_out : (double2*)flm;
+  if (!host) {
+    CUDA_TRY(cudaEventRecord(p->ev[4], st));
+    CUDA_TRY(launch_ring_forward(p, B, (const double2*)samples));
+    CUDA_TRY(cudaEventRecord(p->ev[5], st));
+    CUDA_TRY(cudaEventRecord(p->ev[6], st));
+    CUDA_TRY(launch_factor(p));
+    CUDA_TRY(cudaEventRecord(p->ev[7], st));
+  } else {
+    // the factorisation needs no data: it runs while the samples are copied in,
+    // and each chunk's ring DFTs start as soon as the chunk has landed
+    const int nch = std::min(B, osph_plan::kIoChunks);
+    CUDA_TRY(cudaEventRecord(p->ev_start, st));
+    CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
+    CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->ev_start, 0));
+    for (int c = 0; c < nch; ++c) {
+      const int b0 = (int)((int64_t)B * c / nch), b1 = (int)((int64_t)B * (c + 1) / nch);
+      const size_t off = (size_t)b0 * L * L, cb = sizeof(double2) * (size_t)(b1 - b0) * L * L;
+      CUDA_TRY(cudaMemcpyAsync(p->d_in + off, (const double2*)samples + off, cb, cudaMemcpyHostToDevice, p->s_in));
+      CUDA_TRY(cudaEventRecord(p->ev_in[c], p->s_in));
+    }
+    CUDA_TRY(cudaEventRecord(p->ev[6], st));
+    CUDA_TRY(launch_factor(p));
+    CUDA_TRY(cudaEventRecord(p->ev[7], st));
+    for (int c = 0; c < nch; ++c) {
+      const int b0 = (int)((int64_t)B * c / nch), b1 = (int)((int64_t)B * (c + 1) / nch);
+      CUDA_TRY(cudaStreamWaitEvent(st, p->ev_in[c], 0));
+      if (c == 0) CUDA_TRY(cudaEventRecord(p->ev[4], st));
+      CUDA_TRY(launch_ring_forward(p, B, p->d_in, b0, b1 - b0));
+    }
+    CUDA_TRY(cudaEventRecord(p->ev[5], st));
   }
-  CUDA_TRY(cudaEventRecord(p->ev[4], st));
-  CUDA_TRY(launch_ring_forward(p, B, in));
-  CUDA_TRY(cudaEventRecord(p->ev[5], st));
-  CUDA_TRY(launch_factor(p));
-  CUDA_TRY(cudaEventRecord(p->ev[6], st));
   if (getenv("OSPH_SWEEP_POISON"))  // debug: stale reads of the team exchange show up as NaN
     CUDA_TRY(cudaMemsetAsync(p->d_xg, 0xff, sizeof(double) * (size_t)8 * p->L * (p->max_batch + 3), p->stream));
+  CUDA_TRY(cudaEventRecord(p->ev[8], st));
   CUDA_TRY(launch_sweep(p, B, out));
-  CUDA_TRY(cudaEventRecord(p->ev[7], st));
+  CUDA_TRY(cudaEventRecord(p->ev[9], st));
   p->have_fwd = true;
   if (host) CUDA_TRY(cudaMemcpyAsync(flm, p->d_out, bytes, cudaMemcpyDeviceToHost, st));
   if (kind & OSPH_ASYNC) return OSPH_OK;
@@ -359,8 +418,8 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
   if (stats) {
     float t01 = 0, t12 = 0, t23 = 0;
     cudaEventElapsedTime(&t01, p->ev[4], p->ev[5]);
-    cudaEventElapsedTime(&t12, p->ev[5], p->ev[6]);
-    cudaEventElapsedTime(&t23, p->ev[6], p->ev[7]);
+    cudaEventElapsedTime(&t12, p->ev[6], p->ev[7]);
+    cudaEventElapsedTime(&t23, p->ev[8], p->ev[9]);
     stats->factor_seconds = t12 * 1e-3;
     stats->sweep_seconds = t23 * 1e-3;
     stats->solve_seconds = (t12 + t23) * 1e-3;
@@ -425,16 +484,14 @@ extern "C" int osph_last_stage_times(const osph_plan* p, double* seconds) {
     osph_set_error("NULL argument");
     return OSPH_ERR_ARG;
   }
-  for (int d = 0; d < 2; ++d) {
-    const bool have = d == 0 ? p->have_inv : p->have_fwd;
-    for (int i = 0; i < 3; ++i) {
-      float ms = 0.f;
-      if (have) {
-        CUDA_TRY(cudaEventSynchronize(p->ev[4 * d + 3]));
-        CUDA_TRY(cudaEventElapsedTime(&ms, p->ev[4 * d + i], p->ev[4 * d + i + 1]));
-      }
-      seconds[3 * d + i] = ms * 1e-3;
+  static const int pairs[6][2] = {{0, 1}, {1, 2}, {2, 3}, {4, 5}, {6, 7}, {8, 9}};
+  for (int i = 0; i < 6; ++i) {
+    float ms = 0.f;
+    if (i < 3 ? p->have_inv : p->have_fwd) {
+      CUDA_TRY(cudaEventSynchronize(p->ev[pairs[i][1]]));
+      CUDA_TRY(cudaEventElapsedTime(&ms, p->ev[pairs[i][0]], p->ev[pairs[i][1]]));
     }
+    seconds[i] = ms * 1e-3;
   }
   return OSPH_OK;
 }

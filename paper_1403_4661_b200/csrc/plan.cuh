@@ -69,7 +69,12 @@ struct osph_plan {
   double2* d_in = nullptr;    // device staging of host inputs  [B][L^2]
   double2* d_out = nullptr;   // device staging of host outputs [B][L^2]
 
-  cudaEvent_t ev[8] = {};  // [0..3] last inverse stages, [4..7] last forward stages
+  // stage events: inverse 0 pack 1 synth 2 ring 3; forward ring 4-5, factor 6-7, sweep 8-9
+  cudaEvent_t ev[10] = {};
+  // host-buffer calls: copies on their own streams, overlapped with compute chunk by chunk
+  static constexpr int kIoChunks = 4;
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_in[kIoChunks] = {}, ev_done[kIoChunks] = {}, ev_start = nullptr, ev_out = nullptr;
   bool have_inv = false, have_fwd = false;
 };
 
@@ -79,7 +84,8 @@ void osph_set_error(const std::string& msg);
 // ---- launchers (each returns cudaError_t of the launch) ----
 cudaError_t launch_tables(osph_plan* p);                                   // tables.cu
 cudaError_t launch_ring_inverse(osph_plan* p, int B, double2* samples);    // ringdft.cu
-cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples);  // ringdft.cu
+// maps [bofs, bofs + nb) of a batch of B (nb < 0: all B)
+cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples, int bofs = 0, int nb = -1);  // ringdft.cu
 cudaError_t launch_pack(osph_plan* p, int B, const double2* flm);          // synth.cu
 cudaError_t launch_synth(osph_plan* p, int B);                             // synth.cu
 cudaError_t launch_factor(osph_plan* p);                                   // factor.cu

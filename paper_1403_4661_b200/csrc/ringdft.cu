@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_forward_bluestein(
     int L, int B, int maps_per_block, const int* __restrict__ rings, const int* __restrict__ fft_n,
     const int64_t* __restrict__ chirp_off, const int64_t* __restrict__ bhat_off, const double2* __restrict__ chirp_all,
     const double2* __restrict__ bhat_all, const double2* __restrict__ tw, const double2* __restrict__ samples,
-    double2* __restrict__ R, int smem_cplx) {
+    double2* __restrict__ R, int smem_cplx, int bofs, int bend) {
   extern __shared__ double2 sm[];
   const int k = rings[blockIdx.x];
   const int n = 2 * k + 1;
@@ -194,8 +194,9 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_forward_bluestein(
   load_stage_twiddles(twn, logN, tw);
   const double2* chirp = chirp_all + chirp_off[k];
   const double2* bh = bhat_all + bhat_off[k];  // forward-direction kernel
-  const int b_first = blockIdx.y * maps_per_block;
-  const int b_last = min(B, b_first + maps_per_block);
+  // maps [bofs, bend) of a batch of B (R keeps the batch stride B)
+  const int b_first = bofs + blockIdx.y * maps_per_block;
+  const int b_last = min(bend, b_first + maps_per_block);
   const int Gmax = max(1, (smem_cplx - N) >> logN);
   for (int b0 = b_first; b0 < b_last; b0 += Gmax) {
     const int Gr = min(Gmax, b_last - b0);
@@ -219,13 +220,13 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_forward_bluestein(
 __global__ void __launch_bounds__(RING_THREADS) k_ring_forward_direct(int L, int B, int maps_per_block,
                                                                       const double2* __restrict__ roots,
                                                                       const double2* __restrict__ samples,
-                                                                      double2* __restrict__ R) {
+                                                                      double2* __restrict__ R, int bofs, int bend) {
   __shared__ double2 xin[16][OSPH_DIRECT_MAX + 1];
   __shared__ double2 X[16][64];
   const int k = blockIdx.x;
   const int n = 2 * k + 1;
-  const int b_first = blockIdx.y * maps_per_block;
-  const int b_last = min(B, b_first + maps_per_block);
+  const int b_first = bofs + blockIdx.y * maps_per_block;
+  const int b_last = min(bend, b_first + maps_per_block);
   const double2* rt = roots + (int64_t)k * k;
   for (int b0 = b_first; b0 < b_last; b0 += 16) {
     const int Gr = min(16, b_last - b0);
@@ -293,22 +294,23 @@ cudaError_t launch_ring_inverse(osph_plan* p, int B, double2* samples) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples) {
+cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples, int bofs, int nb) {
   const int L = p->L;
+  if (nb < 0) nb = B;
   if (p->n_bluestein_rings > 0) {
-    const int mpb = maps_per_block_for(B, p->n_bluestein_rings);
+    const int mpb = maps_per_block_for(nb, p->n_bluestein_rings);
     const size_t smem = ring_smem(p);
     cudaFuncSetAttribute(k_ring_forward_bluestein, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 grid(p->n_bluestein_rings, (B + mpb - 1) / mpb);
+    dim3 grid(p->n_bluestein_rings, (nb + mpb - 1) / mpb);
     k_ring_forward_bluestein<<<grid, RING_THREADS, smem, p->stream>>>(
         L, B, mpb, p->d_bluestein_rings, p->d_fft_n, p->d_chirp_off, p->d_bhat_off, p->d_chirp, p->d_bhat, p->d_tw,
-        samples, p->d_r, (int)(smem / sizeof(double2)));
+        samples, p->d_r, (int)(smem / sizeof(double2)), bofs, bofs + nb);
     p->launches++;
   }
   if (p->n_direct_rings > 0) {
-    const int mpb = maps_per_block_for(B, p->n_direct_rings);
-    dim3 grid(p->n_direct_rings, (B + mpb - 1) / mpb);
-    k_ring_forward_direct<<<grid, 128, 0, p->stream>>>(L, B, mpb, p->d_roots, samples, p->d_r);
+    const int mpb = maps_per_block_for(nb, p->n_direct_rings);
+    dim3 grid(p->n_direct_rings, (nb + mpb - 1) / mpb);
+    k_ring_forward_direct<<<grid, 128, 0, p->stream>>>(L, B, mpb, p->d_roots, samples, p->d_r, bofs, bofs + nb);
     p->launches++;
   }
   return cudaGetLastError();
