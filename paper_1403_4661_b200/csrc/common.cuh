@@ -24,6 +24,15 @@ __host__ __device__ __forceinline__ int64_t packed_pos(int L, int m, int i) {
   return (int64_t)m * L - ((int64_t)m * (m - 1)) / 2 + i;
 }
 
+// Forward right-hand side / ring spectra R, TEAM-MAJOR: the maps are grouped in
+// teams of G = 2^lgG (the sweep's maps per team) and a team's slab
+// [pos][+-][map] is contiguous, so a team reads the right-hand side of order m
+// (positions pos(m, 0..n-1)) as one block and teams working on the same order
+// touch different L2 lines (no atomic hot-spotting across teams).
+__host__ __device__ __forceinline__ int64_t r_index(int64_t pos, int slot, int b, int lgG, int64_t npos) {
+  return ((((int64_t)(b >> lgG) * npos + pos) * 2 + slot) << lgG) + (b & ((1 << lgG) - 1));
+}
+
 // Chunk-major 8-row tiling of the sweep operands (X_m and the below-block
 // Pb_m): columns are grouped in chunks of OSPH_TILE_KC, rows in tiles of 8;
 // element (r, k) of a matrix with nrt row tiles lives at

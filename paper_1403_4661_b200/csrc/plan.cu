@@ -51,7 +51,7 @@ static void plan_free(osph_plan* p) {
   void* ptrs[] = {p->d_cos, p->d_sin, p->d_rec, p->d_ls, p->d_pstart, p->d_ring_order, p->d_fft_n,
                   p->d_chirp_off, p->d_bhat_off, p->d_chirp, p->d_bhat, p->d_tw, p->d_roots,
                   p->d_bluestein_rings, p->d_ainv_off, p->d_pb_off, p->d_ainv, p->d_pbelow, p->d_piv,
-                  p->d_norms, p->d_kappa, p->d_status, p->d_jstar, p->d_beta, p->d_u, p->d_w, p->d_xt_off, p->d_xt, p->d_panel, p->d_xg,
+                  p->d_norms, p->d_kappa, p->d_status, p->d_jstar, p->d_beta, p->d_u, p->d_w, p->d_xt_off, p->d_xt, p->d_panel,
                   p->d_fpack, p->d_g, p->d_r,
                   p->d_in, p->d_out};
   for (void* q : ptrs)
@@ -272,9 +272,9 @@ static int ensure_forward(osph_plan* p) {
   CUDA_TRY(dalloc(&p->d_w, (size_t)L * L + 2));
   CUDA_TRY(cudaMemsetAsync(p->d_u, 0, sizeof(double) * ((size_t)L * L + 2), st));
   CUDA_TRY(cudaMemsetAsync(p->d_w, 0, sizeof(double) * ((size_t)L * L + 2), st));
-  // teams * (4 maps-per-team) columns <= 4 (B + 3); two parities of L rows
-  CUDA_TRY(dalloc(&p->d_xg, (size_t)8 * L * (B + 3)));
-  CUDA_TRY(dalloc(&p->d_r, (size_t)L * (L + 1) * B));
+  // teams of up to 4 maps: the last team's padding maps stay zero
+  CUDA_TRY(dalloc(&p->d_r, (size_t)L * (L + 1) * (B + 3)));
+  CUDA_TRY(cudaMemsetAsync(p->d_r, 0, sizeof(double2) * (size_t)L * (L + 1) * (B + 3), st));
   CUDA_TRY(cudaStreamSynchronize(st));
   p->fwd_ready = true;
   return OSPH_OK;
@@ -406,8 +406,6 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
     }
     CUDA_TRY(cudaEventRecord(p->ev[5], st));
   }
-  if (getenv("OSPH_SWEEP_POISON"))  // debug: stale reads of the team exchange show up as NaN
-    CUDA_TRY(cudaMemsetAsync(p->d_xg, 0xff, sizeof(double) * (size_t)8 * p->L * (p->max_batch + 3), p->stream));
   CUDA_TRY(cudaEventRecord(p->ev[8], st));
   CUDA_TRY(launch_sweep(p, B, out));
   CUDA_TRY(cudaEventRecord(p->ev[9], st));

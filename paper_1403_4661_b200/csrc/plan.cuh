@@ -57,7 +57,6 @@ struct osph_plan {
   bool fwd_ready = false;        // forward buffers allocated
   bool piv_ready = false;        // d_piv holds the (grid-determined) pivot order of every order
   double* d_panel = nullptr;     // static-pivot factorisation: panel hand-off buffers
-  double* d_xg = nullptr;        // sweep: x_s of every team, by parity of s (team exchange)
   int sweep_cfg_B = -1;          // cached sweep launch configuration for batch sweep_cfg_B
   int sweep_cfg[3] = {0, 0, 0};  // maps per team, cluster width, ring stages
   bool inv_ready = false;        // inverse buffers allocated
@@ -65,7 +64,7 @@ struct osph_plan {
   // ---- per-call workspaces (sized for max_batch) ----
   double* d_fpack = nullptr;  // inverse: packed coefficients [pos(m,l)][4B]
   double* d_g = nullptr;      // inverse: G [m][k][4B]
-  double2* d_r = nullptr;     // forward: order-major ring spectra [pos(m,k-m)][2][B]
+  double2* d_r = nullptr;     // forward: ring spectra, team-major [team][pos(m,k-m)][2][G] (common.cuh r_index)
   double2* d_in = nullptr;    // device staging of host inputs  [B][L^2]
   double2* d_out = nullptr;   // device staging of host outputs [B][L^2]
 
@@ -90,4 +89,5 @@ cudaError_t launch_pack(osph_plan* p, int B, const double2* flm);          // sy
 cudaError_t launch_synth(osph_plan* p, int B);                             // synth.cu
 cudaError_t launch_factor(osph_plan* p);                                   // factor.cu
 cudaError_t launch_sweep(osph_plan* p, int B, double2* flm);               // sweep.cu
+int sweep_maps_per_team(osph_plan* p, int B);  // sweep.cu: launch configuration (cached per B), 1/2/4
 cudaError_t launch_ring_pair(int n, int m, const double2* v, double2* out, cudaStream_t st);  // ringdft.cu

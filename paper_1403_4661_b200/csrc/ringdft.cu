@@ -165,17 +165,18 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_inverse_direct(int L, int
 // Scatter Gr ring spectra (forward sign, unnormalised; X[g][q] at x[(g<<lstride) + q])
 // into the RHS layout, map-fastest.
 template <bool SWZ>
-__device__ __forceinline__ void scatter_rhs_multi(const double2* X, int lstride, int L, int B, int k, int n, int b0,
+__device__ __forceinline__ void scatter_rhs_multi(const double2* X, int lstride, int L, int lgG, int k, int n, int b0,
                                                   int Gr, double2* __restrict__ R) {
+  const int64_t npos = (int64_t)L * (L + 1) / 2;
   const double scale = OSPH_TWO_PI / (double)n;
   for (int idx = threadIdx.x; idx < Gr * (k + 1); idx += blockDim.x) {
     const int g = idx % Gr, m = idx / Gr;
     const int qn = m == 0 ? 0 : n - m;
     const double2 xp = X[(g << lstride) + (SWZ ? fsw(m) : m)];
     const double2 xn = X[(g << lstride) + (SWZ ? fsw(qn) : qn)];
-    const int64_t base = (packed_pos(L, m, k - m) * 2) * B + b0 + g;
+    const int64_t base = r_index(packed_pos(L, m, k - m), 0, b0 + g, lgG, npos);
     R[base] = make_double2(scale * xp.x, scale * xp.y);
-    R[base + B] = make_double2(scale * xn.x, scale * xn.y);
+    R[base + (1 << lgG)] = make_double2(scale * xn.x, scale * xn.y);
   }
 }
 
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_forward_bluestein(
     int L, int B, int maps_per_block, const int* __restrict__ rings, const int* __restrict__ fft_n,
     const int64_t* __restrict__ chirp_off, const int64_t* __restrict__ bhat_off, const double2* __restrict__ chirp_all,
     const double2* __restrict__ bhat_all, const double2* __restrict__ tw, const double2* __restrict__ samples,
-    double2* __restrict__ R, int smem_cplx, int bofs, int bend) {
+    double2* __restrict__ R, int smem_cplx, int bofs, int bend, int lgG) {
   extern __shared__ double2 sm[];
   const int k = rings[blockIdx.x];
   const int n = 2 * k + 1;
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_forward_bluestein(
       if (t < n) xs[(idx - t) + fsw(t)] = cmul(xs[(idx - t) + fsw(t)], conj2(__ldg(chirp + t)));
     }
     __syncthreads();
-    scatter_rhs_multi<true>(xs, logN, L, B, k, n, b0, Gr, R);
+    scatter_rhs_multi<true>(xs, logN, L, lgG, k, n, b0, Gr, R);
     __syncthreads();
   }
 }
@@ -220,7 +221,8 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_forward_bluestein(
 __global__ void __launch_bounds__(RING_THREADS) k_ring_forward_direct(int L, int B, int maps_per_block,
                                                                       const double2* __restrict__ roots,
                                                                       const double2* __restrict__ samples,
-                                                                      double2* __restrict__ R, int bofs, int bend) {
+                                                                      double2* __restrict__ R, int bofs, int bend,
+                                                                      int lgG) {
   __shared__ double2 xin[16][OSPH_DIRECT_MAX + 1];
   __shared__ double2 X[16][64];
   const int k = blockIdx.x;
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_forward_direct(int L, int
       X[g][q] = make_double2(re, im);
     }
     __syncthreads();
-    scatter_rhs_multi<false>(&X[0][0], 6, L, B, k, n, b0, Gr, R);
+    scatter_rhs_multi<false>(&X[0][0], 6, L, lgG, k, n, b0, Gr, R);
     __syncthreads();
   }
 }
@@ -297,6 +299,7 @@ cudaError_t launch_ring_inverse(osph_plan* p, int B, double2* samples) {
 cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples, int bofs, int nb) {
   const int L = p->L;
   if (nb < 0) nb = B;
+  const int lgG = __builtin_ctz(sweep_maps_per_team(p, B));  // team-major R (common.cuh)
   if (p->n_bluestein_rings > 0) {
     const int mpb = maps_per_block_for(nb, p->n_bluestein_rings);
     const size_t smem = ring_smem(p);
@@ -304,13 +307,13 @@ cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples, int
     dim3 grid(p->n_bluestein_rings, (nb + mpb - 1) / mpb);
     k_ring_forward_bluestein<<<grid, RING_THREADS, smem, p->stream>>>(
         L, B, mpb, p->d_bluestein_rings, p->d_fft_n, p->d_chirp_off, p->d_bhat_off, p->d_chirp, p->d_bhat, p->d_tw,
-        samples, p->d_r, (int)(smem / sizeof(double2)), bofs, bofs + nb);
+        samples, p->d_r, (int)(smem / sizeof(double2)), bofs, bofs + nb, lgG);
     p->launches++;
   }
   if (p->n_direct_rings > 0) {
     const int mpb = maps_per_block_for(nb, p->n_direct_rings);
     dim3 grid(p->n_direct_rings, (nb + mpb - 1) / mpb);
-    k_ring_forward_direct<<<grid, 128, 0, p->stream>>>(L, B, mpb, p->d_roots, samples, p->d_r, bofs, bofs + nb);
+    k_ring_forward_direct<<<grid, 128, 0, p->stream>>>(L, B, mpb, p->d_roots, samples, p->d_r, bofs, bofs + nb, lgG);
     p->launches++;
   }
   return cudaGetLastError();

@@ -41,8 +41,6 @@
 // independent, so a batch fills the GPU with teams and a single map gets one
 // wide team.
 #include <cooperative_groups.h>
-#include <cuda.h>
-#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -57,13 +55,13 @@ namespace cg = cooperative_groups;
 #define SWEEP_WB 4      // BULK warps
 #define SWEEP_NC (SWEEP_WC * 32)
 #define SWEEP_NB (SWEEP_WB * 32)
-#define SWEEP_THREADS_ALL (SWEEP_NC + SWEEP_NB + 64)  // + one producer warp per group
+#define SWEEP_THREADS_ALL (SWEEP_NC + SWEEP_NB + 96)  // + one producer warp per group + the output warp
 #define SWEEP_IPW 4     // max accumulator tiles per warp
 #define SWEEP_KC 32     // K columns per streamed chunk
 #define SWEEP_SMAX 6    // ring stages per group
 #define SWEEP_BAR_C 1   // named barriers of the two groups
 #define SWEEP_BAR_B 2
-#define SWEEP_BOXR 64   // rows per TMA box of the right-hand side
+#define SWEEP_PF_MIN 2  // orders >= this get their right-hand side prefetched a step early
 
 // ---------------------------------------------------------------------------
 // mbarrier / bulk-copy PTX
@@ -117,8 +115,45 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 // full cluster barrier (release/acquire: orders the step's global, shared and
 // DSMEM writes before every CTA's next step)
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+#ifdef OSPH_SWEEP_PROF
+__device__ long long g_prof_arrive[16];  // per warp of CTA 0: cycles spent inside the release arrive
+#endif
+// Step barrier.  MODE 0: release arrival (MEMBAR.GPU + ERRBAR: waits for every
+// outstanding write of the warp); 1: CTA-scope fence + relaxed arrival (the
+// warp's writes are only read inside its own CTA); 2: relaxed arrival (no
+// writes to order, or ordered by an earlier explicit fence).  Always an
+// acquire wait.
+template <int MODE>
+__device__ __forceinline__ void step_barrier() {
+#ifdef OSPH_SWEEP_PROF
+  const long long ta = clock64();
+#endif
+  if (MODE == 0) asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  if (MODE == 1) asm volatile("fence.acq_rel.cta;\nbarrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+  if (MODE == 2) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+#ifdef OSPH_SWEEP_PROF
+  const long long tb = clock64();
+  if (blockIdx.x == 0 && (threadIdx.x & 31) == 0) g_prof_arrive[threadIdx.x >> 5] += tb - ta;
+#endif
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() { step_barrier<0>(); }
+// Alias target of a correction of order s on ring k: R[pos(tm, k - tm)][slot]
+// (transform.py:459-463 in the order-major layout; r == 0 puts both tones in bin 0)
+__device__ __forceinline__ int mod_small(int a, int n);
+__device__ __forceinline__ void corr_target(int s, int k, bool plus, int& tm, int& slot) {
+  const int nk = 2 * k + 1;
+  const int r = mod_small(s, nk);
+  if (r == 0) {
+    tm = 0;
+    slot = 0;
+  } else if (r <= k) {
+    tm = r;
+    slot = plus ? 0 : 1;
+  } else {
+    tm = nk - r;
+    slot = plus ? 1 : 0;
+  }
 }
 // a mod n for 0 <= a < 2^22, 0 < n < 2^22 without an integer division
 __device__ __forceinline__ int mod_small(int a, int n) {
@@ -128,13 +163,17 @@ __device__ __forceinline__ int mod_small(int a, int n) {
   if (r >= n) r -= n;
   return r;
 }
-// TMA tile load of a 3-D box (right-hand-side rows) into shared memory
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-      "[%5];\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// shared::cluster address of `p` (a local shared-memory pointer) in CTA `rank`
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
 }
 // generic-proxy accesses before async-proxy (bulk copy) accesses of the same memory
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;\n" ::: "memory"); }
@@ -156,8 +195,8 @@ __device__ __forceinline__ void group_sync(int id, int nthreads) {
     _pt = _n;                       \
   } while (0)
 #define PROF_DUMP(name)                                                                                     \
-  if (blockIdx.x == 0 && gt == 0)                                                                           \
-  printf("sweep prof %s (cycles): %lld %lld %lld %lld %lld %lld\n", name, _acc[0], _acc[1], _acc[2], _acc[3], \
+  if (blockIdx.x < 4 && gt == 0)                                                                            \
+  printf("sweep prof %s cta %d (cycles): %lld %lld %lld %lld %lld %lld\n", name, (int)blockIdx.x, _acc[0], _acc[1], _acc[2], _acc[3], \
          _acc[4], _acc[5])
 #else
 #define PROF_DECL
@@ -172,26 +211,27 @@ struct SweepCfg {
   int L, T, CC, KC, S;
   int tpc;  // max 8-row tiles of one job on one CTA
   int ldx, ldr;
-  size_t gst, xrow, xp, wv, ubuf, apart, late, rch, stage, bar, total;  // offsets in doubles
+  size_t gst, xrow, xst, xp, wv, ubuf, fix, apart, late, rch, stage, bar, total;  // offsets in doubles
   __host__ __device__ SweepCfg(int L_, int T_, int CC_, int KC_, int S_) : L(L_), T(T_), CC(CC_), KC(KC_), S(S_) {
     tpc = ((L + 7) / 8 + T - 1) / T;
-    // rows of the B operands: whole TMA boxes and whole 32-row K chunks stay in bounds
-    ldx = ((L + SWEEP_BOXR - 1) / SWEEP_BOXR) * SWEEP_BOXR;
+    ldx = ((L + 31) / 32) * 32;  // rows of the B operands: whole 32-row K chunks stay in bounds
     ldr = 8 * tpc + 4;
     auto al = [](size_t v) { return (v + 15) & ~(size_t)15; };  // 128-byte alignment
     size_t o = 0;
     // B operands, row-major [row][CC] exactly as the bulk copies deliver them:
     // a DMMA B fragment (rows k+tq, columns g) then covers 32 consecutive doubles
-    gst = o;   o = al(o + (size_t)ldx * CC);    // right-hand side of order s, natural ring order (BULK B)
-    xrow = o;  o = al(o + (size_t)ldx * CC);    // x_{t+1} of the whole team (CORR B)
-    ubuf = o;  o = al(o + (size_t)ldx);         // u_s (chain partial weights), natural ring order
+    gst = o;   o = al(o + (size_t)2 * ldx * CC);  // right-hand side of order s by parity, natural ring order (BULK B)
+    xrow = o;  o = al(o + (size_t)2 * ldx * CC);  // x_s of the whole team by parity (CORR B), pushed over DSMEM
+    xst = o;   o = al(o + (size_t)2 * 8 * tpc * CC);  // own rows of x_s by parity, staged for the output warp
+    ubuf = o;  o = al(o + (size_t)2 * ldx);     // u_s (chain partial weights) by parity, natural ring order
+    fix = o;   o = al(o + (size_t)2 * CC);      // row-1 correction of order s by parity (DSMEM from CORR(s+3))
     xp = o;    o = al(o + (size_t)2 * CC * ldr);  // own rows of x'_s, transposed, by parity of s
-    wv = o;    o = al(o + (size_t)2 * ldr);     // own rows of w_s, by parity of s
+    wv = o;    o = al(o + (size_t)4 * ldr);     // own rows of w_s, by s mod 4 (prefetched two steps ahead)
     apart = o; o = al(o + (size_t)4 * SWEEP_WB * CC);  // chain partials a_s per BULK warp, slot s % 4
     late = o;  o = al(o + (size_t)2 * CC);      // late right-hand-side entries L_s, by parity
     rch = o;   o = al(o + (size_t)2 * CC);      // prefetched R(+-)[s][0], by parity
     stage = o; o += (size_t)2 * S * tpc * KC * 8;  // ring B (BULK) then ring C (CORR)
-    bar = o;   o += (size_t)4 * S + 2;          // fullB[S], emptyB[S], fullC[S], emptyC[S], inB, inC
+    bar = o;   o += (size_t)4 * S + 2;          // fullB[S], emptyB[S], fullC[S], emptyC[S], inB[2]
     total = o;
   }
 };
@@ -340,15 +380,17 @@ __device__ __forceinline__ void run_job(const Job& j, const Ring& rg, int& cst, 
 // chunks of this step plus S more are out -- every stage it waits for is
 // released within the current step, so the per-step cluster barrier cannot
 // deadlock with a blocked producer.
-template <typename StepJob>
-__device__ __forceinline__ void produce(const Ring& rg, int nsteps, int lane,
-                                        StepJob step_job) {
+template <typename StepJob, typename StepHook>
+__device__ __forceinline__ void produce(const Ring& rg, int nsteps, int lane, StepJob step_job, StepHook hook) {
   Job cur;
   int q_dec = 0;  // next step whose job is decoded
   bool has = false;
   int ch = 0, st = 0;
   long long issued = 0, target = 0;
   uint32_t ephase_bits = 0;  // per-stage parity of the next empty completion to wait for
+#ifdef OSPH_SWEEP_PROF
+  long long arr_acc = 0, t_top = clock64();
+#endif
   auto next = [&]() {
     has = false;
     while (q_dec < nsteps) {
@@ -362,6 +404,7 @@ __device__ __forceinline__ void produce(const Ring& rg, int nsteps, int lane,
   if (lane == 0) next();
   for (int q = 0; q < nsteps; ++q) {
     if (lane == 0) {
+      hook(q);  // per-step work of the producer thread (after the step's barrier)
       const Job jq = step_job(q, false);
       if (jq.type >= 0) target += jq.nch;
       while (has && issued < target + rg.S) {
@@ -381,23 +424,34 @@ __device__ __forceinline__ void produce(const Ring& rg, int nsteps, int lane,
         }
       }
     }
+#ifdef OSPH_SWEEP_PROF
+    if (lane == 0) arr_acc += clock64() - t_top;
+#endif
     __syncwarp();
-    cluster_sync_all();
+    step_barrier<2>();  // bulk copies are tracked by mbarriers, not by this barrier
+#ifdef OSPH_SWEEP_PROF
+    t_top = clock64();
+#endif
   }
+#ifdef OSPH_SWEEP_PROF
+  if (blockIdx.x == 0 && lane == 0) printf("sweep prof producer %s: work before arrive %lld cycles\n", rg.S == -1 ? "" : (threadIdx.x >> 5) == SWEEP_WC + SWEEP_WB ? "B" : "C", arr_acc);
+#endif
 }
 
 template <int CC>
 __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
-    int L, int B, int maps_per_team, int KC, int S, const __grid_constant__ CUtensorMap tmR,
+    int L, int B, int maps_per_team, int KC, int S,
     const double* __restrict__ xt, const int64_t* __restrict__ xt_off, const double* __restrict__ beta_all,
     const double* __restrict__ pbt, const int64_t* __restrict__ pb_off, const double* __restrict__ u_all,
-    const double* __restrict__ w_all, double2* __restrict__ R, double2* __restrict__ flm,
-    double* __restrict__ xg_all) {
+    const double* __restrict__ w_all, double2* __restrict__ R, double2* __restrict__ flm) {
   const int T = (int)cg::this_cluster().num_blocks();
   const int rank = (int)cg::this_cluster().block_rank();
   const int lgT = __ffs(T) - 1;  // T is a power of two (launch_sweep)
   const int team = (int)(blockIdx.x >> lgT);
   const int b0 = team * maps_per_team;
+  const int G = maps_per_team;  // a power of two
+  // this team's slab of the team-major right-hand side [pos][+-][G] (common.cuh)
+  double2* const Rt = R + (int64_t)team * ((int64_t)L * (L + 1) / 2) * 2 * G;
   const int gm = min(maps_per_team, B - b0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tq = lane & 3;
@@ -407,16 +461,17 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
   const int ldr = cfg.ldr, tpc = cfg.tpc;
   double* gst = smem + cfg.gst;
   double* xrow = smem + cfg.xrow;
+  double* xst = smem + cfg.xst;
   double* ubuf = smem + cfg.ubuf;
-  double* xg = xg_all + (size_t)team * 2 * L * CC;  // x_s of the team in global memory, by parity
   double* xp = smem + cfg.xp;
   double* wv = smem + cfg.wv;
   double* apart = smem + cfg.apart;
   double* late = smem + cfg.late;
   double* rch = smem + cfg.rch;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + cfg.bar);
-  uint64_t* inB = bars + 4 * S;  // B operands of BULK landed
-  uint64_t* inC = inB + 1;       // x_{t+1} for CORR landed
+  uint64_t* inB = bars + 4 * S;  // B operands of BULK landed, by parity of the order
+  double* fix = smem + cfg.fix;
+
   const size_t stage_elems = (size_t)tpc * KC * 8;
   const Ring ringB{smem + cfg.stage, bars, bars + S, stage_elems, S};
   const Ring ringC{smem + cfg.stage + (size_t)S * stage_elems, bars + 2 * S, bars + 3 * S, stage_elems, S};
@@ -429,7 +484,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
       mbar_init(ringC.empty + i, SWEEP_WC);
     }
     mbar_init(inB, 1);
-    mbar_init(inC, 1);
+    mbar_init(inB + 1, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   // B operands start zeroed: a chunk's rows past K multiply zero operand tiles,
@@ -441,6 +496,25 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
   // Steps: q = 0 is the prologue, q = L - t is step t.
   const int nsteps = L + 1;
 
+  // B operands of BULK(s) -> buffers of parity s (one thread, bulk copies):
+  // the right-hand side rows pos(s, 0..ns-1) of the team's maps (TMA boxes of
+  // the [pos][+-][map] R), w_s on own rows and u_s.  Orders >= SWEEP_PF_MIN
+  // are fetched one step early (their last correction but row 1's has landed;
+  // row 1's arrives through `fix`), so BULK does not wait on the copy.
+  auto operands_issue = [&](int s) {
+    fence_proxy_async();
+    const int ns = L - s, nrt = (ns + 7) / 8;
+    const int r0 = 8 * ((rank * nrt) >> lgT), r1 = min(ns, 8 * (((rank + 1) * nrt) >> lgT));
+    const uint32_t wb = (uint32_t)(((max(r1 - r0, 0) + 1) & ~1) * 8);
+    const uint32_t ub = (uint32_t)(((ns + 1) & ~1) * 8);
+    const uint32_t rb = (uint32_t)(ns * CC * 8);  // rows pos(s, 0..ns-1) of the team slab: [+-][map][re, im]
+    uint64_t* bar = inB + (s & 1);
+    mbar_arrive_expect_tx(bar, rb + wb + ub);
+    bulk_g2s(gst + (size_t)(s & 1) * cfg.ldx * CC, Rt + packed_pos(L, s, 0) * 2 * G, rb, bar);
+    if (wb) bulk_g2s(wv + (size_t)(s & 3) * ldr, w_all + (size_t)s * L + r0, wb, bar);
+    bulk_g2s(ubuf + (size_t)(s & 1) * cfg.ldx, u_all + (size_t)s * L, ub, bar);
+  };
+
   // ======================= producers =======================
   if (warp == SWEEP_WC + SWEEP_WB) {  // ring B: BULK(L-1) in the prologue, BULK(t-1) at step t
     produce(ringB, nsteps, lane, [&](int q, bool off) {
@@ -451,6 +525,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
         return j;
       }
       return make_job(0, s, L, lgT, rank, SWEEP_KC, xt, xt_off, pbt, pb_off, off);
+    }, [&](int q) {  // prefetch BULK's operands of order t-2 at step t (L-2 in the prologue)
+      const int s2 = q == 0 ? L - 2 : L - q - 2;
+      if (s2 >= 0) operands_issue(s2);
     });
     return;
   }
@@ -463,7 +540,53 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
         return j;
       }
       return make_job(1, t + 1, L, lgT, rank, SWEEP_KC, xt, xt_off, pbt, pb_off, off);
-    });
+    }, [](int) {});
+    return;
+  }
+
+  if (warp == SWEEP_WC + SWEEP_WB + 2) {
+    // ======================= output warp =======================
+    // Writes x_s (own rows, staged by the chain/CORR warps one step earlier) to
+    // flm.  Its HBM stores are not read inside the kernel, so it arrives at the
+    // step barrier relaxed (a release would wait for them).
+    auto write_out = [&](int s) {
+      const int ns = L - s, nrt = (ns + 7) / 8;
+      const int r0 = 8 * ((rank * nrt) >> lgT), r1 = min(ns, 8 * (((rank + 1) * nrt) >> lgT));
+      const double* xs = xst + (size_t)(s & 1) * 8 * tpc * CC;
+      for (int idx = lane; idx < (r1 - r0) * (CC / 2); idx += 32) {
+        const int l = r0 + idx / (CC / 2), c = 2 * (idx % (CC / 2));
+        const int bl = c >> 2;
+        if (bl >= gm) continue;
+        const double2 v = *reinterpret_cast<const double2*>(xs + (size_t)(l - r0) * CC + c);
+        const int64_t ell = s + l;
+        double2* f = flm + (int64_t)(b0 + bl) * L * L + ell * ell + ell;
+        if ((c & 2) == 0) __stcs(f + s, v);
+        else if (s > 0) __stcs(f - s, v);
+      }
+    };
+#ifdef OSPH_SWEEP_PROF
+    long long o_acc = 0, o_top = clock64();
+#endif
+    for (int q = 0; q < nsteps; ++q) {
+      const int t = L - q;  // step t (q = 0: prologue)
+      if (q >= 2) write_out(t + 1);  // x_{t+1}
+#ifdef OSPH_SWEEP_PROF
+      if (lane == 0) o_acc += clock64() - o_top;
+#endif
+      __syncwarp();
+      step_barrier<2>();
+#ifdef OSPH_SWEEP_PROF
+      o_top = clock64();
+#endif
+    }
+#ifdef OSPH_SWEEP_PROF
+    if (blockIdx.x == 0 && lane == 0) printf("sweep prof output warp: work before arrive %lld cycles\n", o_acc);
+    if (blockIdx.x == 0 && lane == 0) {
+      __nanosleep(100000);
+      for (int w = 0; w < 11; ++w) printf("sweep prof arrive warp %d: %lld\n", w, g_prof_arrive[w]);
+    }
+#endif
+    write_out(0);
     return;
   }
 
@@ -475,11 +598,11 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
     (void)gn;
     PROF_DECL
     int cst = 0;
-    uint32_t cphase = 0, inphase = 0;
+    uint32_t cphase = 0;
     auto load_rch = [&](int s) {  // R(+-)[s][0] of every map -> rch[s & 1] (synchronous)
       if (gt < gm) {
-        const int64_t base = (packed_pos(L, s, 0) * 2) * B + b0 + gt;
-        const double2 rp = __ldcg(R + base), rn = __ldcg(R + base + B);
+        const int64_t base = (packed_pos(L, s, 0) * 2) * G + gt;
+        const double2 rp = __ldcg(Rt + base), rn = __ldcg(Rt + base + G);
         double* d = rch + (size_t)(s & 1) * CC + 4 * gt;
         d[0] = rp.x;
         d[1] = rp.y;
@@ -489,10 +612,10 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
     };
     auto rch_issue = [&](int s) {  // the same by cp.async (slots gm..NB4-1 stay zero)
       if (gt < gm) {
-        const int64_t base = (packed_pos(L, s, 0) * 2) * B + b0 + gt;
+        const int64_t base = (packed_pos(L, s, 0) * 2) * G + gt;
         double* d = rch + (size_t)(s & 1) * CC + 4 * gt;
-        cp_async16(d, R + base);
-        cp_async16(d + 2, R + base + B);
+        cp_async16(d, Rt + base);
+        cp_async16(d + 2, Rt + base + G);
       }
     };
     load_rch(L - 1);
@@ -504,13 +627,6 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
       const double bt = beta_next;
       const bool corr = t >= 1 && t + 1 <= L - 1;
       if (t >= 1) beta_next = __ldg(beta_all + t);  // consumed one step later
-      // x_{t+1} (complete since the last cluster barrier) for CORR(t+1): one bulk copy
-      if (corr && gt == 0) {
-        fence_proxy_async();
-        const uint32_t bytes = (uint32_t)((nt - 1) * CC * 8);
-        mbar_arrive_expect_tx(inC, bytes);
-        bulk_g2s(xrow, xg + (size_t)((t + 1) & 1) * L * CC, bytes, inC);
-      }
       // the late entry R[t-1][0] of the next step (final now; R[0][0] takes
       // order-2 corrections at step 1 and is read synchronously at step 0)
       if (t >= 2) rch_issue(t - 1);
@@ -552,26 +668,27 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
       }
       group_sync(SWEEP_BAR_C, SWEEP_NC);
       PROF_MARK(1);
-      // ---- (b) x_t = x'_t + w_t L_t on own rows -> flm and the team exchange xg
+      // ---- (b) x_t = x'_t + w_t L_t on own rows -> every CTA's xrow (DSMEM) and
+      // the local staging for the output warp (flm)
       {
         const int nrt = (nt + 7) / 8;
         const int r0 = 8 * ((rank * nrt) >> lgT), r1 = min(nt, 8 * (((rank + 1) * nrt) >> lgT));
         const double* xps = xp + (size_t)(t & 1) * CC * ldr;
-        const double* wvs = wv + (size_t)(t & 1) * ldr;
+        const double* wvs = wv + (size_t)(t & 3) * ldr;
         const double* lt = late + (size_t)(t & 1) * CC;
-        double* xo = xg + (size_t)(t & 1) * L * CC;
+        double* xo = xrow + (size_t)(t & 1) * cfg.ldx * CC;
+        double* xs = xst + (size_t)(t & 1) * 8 * tpc * CC;
+        // x_t is needed by CORR(t) at step t-1 (1 <= t-1, t <= L-1)
+        const bool push = t >= 2 && t <= L - 1;
         for (int idx = gt; idx < (r1 - r0) * (CC / 2); idx += SWEEP_NC) {
           const int l = r0 + idx / (CC / 2), c = 2 * (idx % (CC / 2));
           const double wl = wvs[l - r0];
-          const double v0 = xps[(size_t)c * ldr + (l - r0)] + wl * lt[c];
-          const double v1 = xps[(size_t)(c + 1) * ldr + (l - r0)] + wl * lt[c + 1];
-          __stcg(reinterpret_cast<double2*>(xo + (size_t)l * CC + c), make_double2(v0, v1));
-          const int bl = c >> 2;
-          if (bl < gm) {
-            const int64_t ell = t + l;
-            double2* f = flm + (int64_t)(b0 + bl) * L * L + ell * ell + ell;
-            if ((c & 2) == 0) f[t] = make_double2(v0, v1);
-            else if (t > 0) f[-t] = make_double2(v0, v1);
+          const double2 v = make_double2(xps[(size_t)c * ldr + (l - r0)] + wl * lt[c],
+                                         xps[(size_t)(c + 1) * ldr + (l - r0)] + wl * lt[c + 1]);
+          *reinterpret_cast<double2*>(xs + (size_t)(l - r0) * CC + c) = v;
+          if (push) {
+            double2* dst = reinterpret_cast<double2*>(xo + (size_t)l * CC + c);
+            for (int q = 0; q < T; ++q) *cg::this_cluster().map_shared_rank(dst, q) = v;
           }
         }
       }
@@ -580,40 +697,43 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
       if (corr) {
         const int s = t + 1;
         const double ss = (s & 1) ? -1.0 : 1.0;
-        mbar_wait(inC, inphase);
-        inphase ^= 1u;
         PROF_MARK(3);
         const Job j = make_job(1, s, L, lgT, rank, SWEEP_KC, xt, xt_off, pbt, pb_off, false);
-        run_job<CC>(j, ringC, cst, cphase, gw, SWEEP_WC, xrow, CC, g, tq, lane, [&](int k, int c, double v0, double v1) {
+        run_job<CC>(j, ringC, cst, cphase, gw, SWEEP_WC, xrow + (size_t)(s & 1) * cfg.ldx * CC, CC, g, tq, lane,
+                    [&](int k, int c, double v0, double v1) {
           const int bl = c >> 2;
           if (k >= s - 1 || bl >= gm) return;  // ring s-1 is the chain
           const bool plus = (c & 2) == 0;
           const double gr = plus ? v0 : ss * v0, gi = plus ? v1 : ss * v1;
-          const int nk = 2 * k + 1;
-          const int r = mod_small(s, nk);
-          int tm, slot;
-          if (r == 0) {
-            tm = 0;
-            slot = 0;
-          } else if (r <= k) {
-            tm = r;
-            slot = plus ? 0 : 1;
-          } else {
-            tm = nk - r;
-            slot = plus ? 1 : 0;
+          if (k == s - 2 && s - 3 >= SWEEP_PF_MIN) {
+            // row 1 of order s-3 (ring s-2): its right-hand side was prefetched
+            // before this correction, so the correction goes to every CTA's
+            // fix-up slot (DSMEM) instead of R
+            int tm, slot;
+            corr_target(s, k, plus, tm, slot);
+            const int col = slot * (CC / 2) + 2 * bl;  // gst column order [+-][map][re, im]
+            double* fx = fix + ((s - 3) & 1) * CC + col;
+            for (int q = 0; q < T; ++q) {
+              double* rf = cg::this_cluster().map_shared_rank(fx, q);
+              rf[0] = -gr;
+              rf[1] = -gi;
+            }
+            return;
           }
-          // fire-and-forget reductions (RED.ADD.F64): no load latency on the step's
-          // critical path; at most two tones (r == 0) hit one bin per step
-          double2* rp = R + (packed_pos(L, tm, k - tm) * 2 + slot) * B + b0 + bl;
+          int tm, slot;
+          corr_target(s, k, plus, tm, slot);
+          // fire-and-forget reductions (RED.ADD.F64)
+          double2* rp = Rt + (packed_pos(L, tm, k - tm) * 2 + slot) * G + bl;
           atomicAdd(&rp->x, -gr);
           atomicAdd(&rp->y, -gi);
         });
       }
       PROF_MARK(4);
       cp_async_wait_all();
-      // this step's x_t stores and reductions are read by bulk copies next step
+      // release: this step's reductions (read by bulk copies: proxy fence too),
+      // the DSMEM pushes of x_t and the fix-ups
       fence_proxy_async();
-      cluster_sync_all();
+      step_barrier<0>();
       PROF_MARK(5);
     }
     PROF_DUMP("chain/corr");
@@ -628,30 +748,17 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
     (void)gn;
     PROF_DECL
     int cst = 0;
-    uint32_t cphase = 0, inphase = 0;
+    uint32_t cphase = 0;
     // Columns of gst are [+-][map][re, im] (the TMA box order); every other
     // buffer uses [map][+-][re, im].  Column pair c, c+1 of gst -> canonical pair.
     auto canon_col = [](int c) {
       const int sl = c >= CC / 2 ? 1 : 0;
       return 4 * ((c - sl * (CC / 2)) >> 1) + 2 * sl;
     };
-    // B operands of BULK(s), one thread, bulk copies: the right-hand side rows
-    // pos(s, 0..ns-1) of the team's maps (TMA boxes of the [pos][+-][map] R),
-    // w_s on own rows and u_s
-    auto operands_issue = [&](int s) {
-      if (gt != 0) return;
-      fence_proxy_async();
-      const int ns = L - s, nrt = (ns + 7) / 8;
-      const int r0 = 8 * ((rank * nrt) >> lgT), r1 = min(ns, 8 * (((rank + 1) * nrt) >> lgT));
-      const int nbox = (ns + SWEEP_BOXR - 1) / SWEEP_BOXR;
-      const uint32_t wb = (uint32_t)(((max(r1 - r0, 0) + 1) & ~1) * 8);
-      const uint32_t ub = (uint32_t)(((ns + 1) & ~1) * 8);
-      mbar_arrive_expect_tx(inB, (uint32_t)(nbox * SWEEP_BOXR * CC * 8) + wb + ub);
-      const int pos0 = (int)packed_pos(L, s, 0);
-      for (int q = 0; q < nbox; ++q)
-        tma_load_3d(gst + (size_t)q * SWEEP_BOXR * CC, &tmR, 2 * b0, 0, pos0 + q * SWEEP_BOXR, inB);
-      if (wb) bulk_g2s(wv + (size_t)(s & 1) * ldr, w_all + (size_t)s * L + r0, wb, inB);
-      bulk_g2s(ubuf, u_all + (size_t)s * L, ub, inB);
+    uint32_t inph = 0;  // phase bit per parity buffer
+    auto operands_wait = [&](int s) {
+      mbar_wait(inB + (s & 1), (inph >> (s & 1)) & 1u);
+      inph ^= 1u << (s & 1);
     };
     // BULK(s): x'_s on own rows (the (-1)^s of the -m columns applied here),
     // and the chain partial a_{s-1} = u_s . rhs_s of the whole team: every CTA
@@ -660,9 +767,11 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
       const Job j = make_job(0, s, L, lgT, rank, SWEEP_KC, xt, xt_off, pbt, pb_off, false);
       const int ns = j.K;
       const int r0 = 8 * j.rt0;
+      const double* gs = gst + (size_t)(s & 1) * cfg.ldx * CC;
+      const double* ub = ubuf + (size_t)(s & 1) * cfg.ldx;
       double* xps = xp + (size_t)(s & 1) * CC * ldr;
       const double ss = (s & 1) ? -1.0 : 1.0;
-      run_job<CC>(j, ringB, cst, cphase, gw, SWEEP_WB, gst, CC, g, tq, lane, [&](int l, int c, double v0, double v1) {
+      run_job<CC>(j, ringB, cst, cphase, gw, SWEEP_WB, gs, CC, g, tq, lane, [&](int l, int c, double v0, double v1) {
         if (l < ns) {
           const int cc = canon_col(c);
           const double sg = (cc & 2) ? ss : 1.0;
@@ -682,11 +791,11 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
           for (int h = 0; h < 2; ++h) {
             if (kk + h * SWEEP_WB >= nks) break;  // warp-uniform
             const int k = 4 * (kk + h * SWEEP_WB) + tq;  // rows ns..4*nks-1: u is zero there
-            const double a = g == 0 ? ubuf[k] : 0.0;
+            const double a = g == 0 ? ub[k] : 0.0;
 #pragma unroll
             for (int ct = 0; ct < NCT; ++ct) {
               const int col = ct * 8 + g;
-              const double b = (CC >= 8 || col < CC) ? gst[(size_t)k * CC + col] : 0.0;
+              const double b = (CC >= 8 || col < CC) ? gs[(size_t)k * CC + col] : 0.0;
               dmma_8x8x4(acc[ct][h][0], acc[ct][h][1], a, b);
             }
           }
@@ -707,25 +816,30 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
       }
     };
 
-    // ---- prologue: x'_{L-1}, a_{L-2}
-    operands_issue(L - 1);
-    mbar_wait(inB, inphase);
-    inphase ^= 1u;
+    // ---- prologue: x'_{L-1}, a_{L-2} (the producer prefetches order L-2)
+    if (gt == 0) operands_issue(L - 1);
+    operands_wait(L - 1);
     bulk(L - 1);
-    cluster_sync_all();
+    step_barrier<1>();  // x'_s, a_s: read by this CTA's chain/CORR warps only
     for (int t = L - 1; t >= 0; --t) {
       if (t >= 1) {
-        // the right-hand side of order t-1 is final now: every correction but
-        // the chain's has landed
-        operands_issue(t - 1);
-        PROF_MARK(0);
-        mbar_wait(inB, inphase);
-        inphase ^= 1u;
+        const int s = t - 1;
+        operands_wait(s);  // issued at step t+1 (or in the prologue)
+        if (s >= SWEEP_PF_MIN) {
+          // the one correction the early copy missed: CORR(s+3) on ring s+1,
+          // pushed into `fix` during the last step (none if CORR(s+3) does not exist)
+          if (gt < CC) gst[((size_t)(s & 1) * cfg.ldx + 1) * CC + gt] += fix[(s & 1) * CC + gt];
+        } else {
+          // small orders: aliases are dense, fetch again now that R is final
+          if (gt == 0) operands_issue(s);
+          operands_wait(s);
+        }
+        group_sync(SWEEP_BAR_B, SWEEP_NB);
         PROF_MARK(1);
-        bulk(t - 1);
+        bulk(s);
       }
       PROF_MARK(4);
-      cluster_sync_all();
+      step_barrier<1>();
       PROF_MARK(5);
     }
     PROF_DUMP("bulk");
@@ -762,27 +876,9 @@ static cudaError_t launch_sweep_cc(osph_plan* p, int B, int g, int T, int KC, in
     fprintf(stderr, "[osph] sweep L=%d B=%d maps/team=%d teams=%d T=%d KC=%d S=%d smem=%zu maxActiveClusters=%d\n", L,
             B, g, teams, T, KC, S, smem, nclusters);
   }
-  // R as a 3-D tensor [pos][+-][2 B doubles]: one box = SWEEP_BOXR positions x
-  // both signs x the team's maps, delivered row-major [row][CC] (maps past B zero-filled)
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
-    cudaDriverEntryPointQueryResult q;
-    if ((e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q)) != cudaSuccess)
-      return e;
-    if (!encode) return cudaErrorSymbolNotFound;
-  }
-  CUtensorMap tm;
-  const cuuint64_t dims[3] = {(cuuint64_t)2 * B, 2, (cuuint64_t)L * (L + 1) / 2};
-  const cuuint64_t strides[2] = {(cuuint64_t)2 * B * sizeof(double), (cuuint64_t)4 * B * sizeof(double)};
-  const cuuint32_t box[3] = {(cuuint32_t)(2 * g), 2, SWEEP_BOXR};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)p->d_r, dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return cudaErrorInvalidValue;
-  e = cudaLaunchKernelEx(&lc, kern, L, B, g, KC, S, tm, (const double*)p->d_xt, (const int64_t*)p->d_xt_off,
+  e = cudaLaunchKernelEx(&lc, kern, L, B, g, KC, S, (const double*)p->d_xt, (const int64_t*)p->d_xt_off,
                          (const double*)p->d_beta, (const double*)p->d_pbelow, (const int64_t*)p->d_pb_off,
-                         (const double*)p->d_u, (const double*)p->d_w, p->d_r, flm, p->d_xg);
+                         (const double*)p->d_u, (const double*)p->d_w, p->d_r, flm);
   p->launches++;
   return e;
 }
@@ -817,16 +913,14 @@ static int env_int(const char* name, int dflt) {
   return v ? atoi(v) : dflt;
 }
 
-cudaError_t launch_sweep(osph_plan* p, int B, double2* flm) {
+// Launch configuration for batch B (cached): maps per team g (1, 2, 4), team
+// width T (power of two), ring stages S.  Returns g, which also fixes the
+// team-major layout of R written by the forward ring DFTs.
+int sweep_maps_per_team(osph_plan* p, int B) {
   const int L = p->L;
   const size_t cap = 220 * 1024;
   const int KC = SWEEP_KC;
-  if (p->sweep_cfg_B == B && !getenv("OSPH_SWEEP_T") && !getenv("OSPH_SWEEP_G") && !getenv("OSPH_SWEEP_S")) {
-    const int g = p->sweep_cfg[0], T = p->sweep_cfg[1], S = p->sweep_cfg[2];
-    if (g == 4) return launch_sweep_cc<16>(p, B, 4, T, KC, S, flm);
-    if (g == 2) return launch_sweep_cc<8>(p, B, 2, T, KC, S, flm);
-    return launch_sweep_cc<4>(p, B, 1, T, KC, S, flm);
-  }
+  if (p->sweep_cfg_B == B) return p->sweep_cfg[0];
   // maps per team: 4 (16 columns) / 2 / 1, limited by shared memory
   int g = B >= 3 ? 4 : B;
   g = std::min(g, std::max(1, env_int("OSPH_SWEEP_G", g)));
@@ -885,7 +979,12 @@ cudaError_t launch_sweep(osph_plan* p, int B, double2* flm) {
   p->sweep_cfg[0] = g;
   p->sweep_cfg[1] = T;
   p->sweep_cfg[2] = S;
-  if (g == 4) return launch_sweep_cc<16>(p, B, 4, T, KC, S, flm);
-  if (g == 2) return launch_sweep_cc<8>(p, B, 2, T, KC, S, flm);
-  return launch_sweep_cc<4>(p, B, 1, T, KC, S, flm);
+  return g;
+}
+
+cudaError_t launch_sweep(osph_plan* p, int B, double2* flm) {
+  const int g = sweep_maps_per_team(p, B), T = p->sweep_cfg[1], S = p->sweep_cfg[2];
+  if (g == 4) return launch_sweep_cc<16>(p, B, 4, T, SWEEP_KC, S, flm);
+  if (g == 2) return launch_sweep_cc<8>(p, B, 2, T, SWEEP_KC, S, flm);
+  return launch_sweep_cc<4>(p, B, 1, T, SWEEP_KC, S, flm);
 }
