@@ -14,6 +14,8 @@
 //   * k_synth_dmma (C >= 16): 64x64 output tiles on fp64 tensor cores
 //     (mma.sync m8n8k4 -> SASS DMMA.8x8x4); P tiles generated into shared
 //     memory by two warps while the others stage F.
+#include <cstdlib>
+
 #include "plan.cuh"
 
 // flm [B][L^2] complex -> F [pos(m, l-m)][4B] doubles:
@@ -102,24 +104,38 @@ __global__ void __launch_bounds__(SYN_FMA_THREADS) k_synth_fma(
 }
 
 // ---------------------------------------------------------------------------
-// DMMA path: C >= 16.  Block tile 64 rings x 64 columns, K chunks of 16 degrees.
+// DMMA path: C >= 16.  Block tile 64 rings x TN columns (TN = 64/128/256: the
+// Legendre block generated for a tile is reused by TN columns), K chunks of 16
+// degrees, double
+// buffered: two warps run the ring recurrences of the next chunk and every
+// thread streams its share of the next F chunk with cp.async while the chunk
+// in hand is multiplied on the tensor cores.
 
 #define SYN_TM 64
-#define SYN_TN 64
 #define SYN_TK 16
 #define SYN_THREADS 256
-#define SYN_PAD 8
+#define SYN_PAD 4  // row pitch = 4 mod 16 doubles: conflict-free DMMA fragment loads
 
-__global__ void __launch_bounds__(SYN_THREADS, 2) k_synth_dmma(
+__device__ __forceinline__ void syn_cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+
+template <int TN>
+__global__ void __launch_bounds__(SYN_THREADS, TN > 128 ? 1 : 2) k_synth_dmma(
     int L, int C, const double* __restrict__ costh, const double2* __restrict__ rec,
     const int* __restrict__ ls_tab, const double2* __restrict__ pstart, const int* __restrict__ ring_order,
     const double* __restrict__ F, double* __restrict__ G) {
-  __shared__ __align__(16) double Ps[2][SYN_TK][SYN_TM + SYN_PAD];
-  __shared__ __align__(16) double Fs[2][SYN_TK][SYN_TN + SYN_PAD];
+  constexpr int NT = TN / 16;  // 8-column tiles per warp (warp tile 16 rows x TN/2 columns)
+  extern __shared__ __align__(16) double syn_smem[];
+  double(*Ps)[SYN_TK][SYN_TM + SYN_PAD] = reinterpret_cast<double(*)[SYN_TK][SYN_TM + SYN_PAD]>(syn_smem);
+  double(*Fs)[SYN_TK][TN + SYN_PAD] =
+      reinterpret_cast<double(*)[SYN_TK][TN + SYN_PAD]>(syn_smem + 2 * SYN_TK * (SYN_TM + SYN_PAD));
   __shared__ int s_lmin[2];
   const int m = blockIdx.z;
   const int row0 = blockIdx.y * SYN_TM;
-  const int col0 = blockIdx.x * SYN_TN;
+  const int col0 = blockIdx.x * TN;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tq = lane & 3;
@@ -149,16 +165,26 @@ __global__ void __launch_bounds__(SYN_THREADS, 2) k_synth_dmma(
   const double* Fm = F + packed_pos(L, m, 0) * (int64_t)C;
   const double2* recm = rec + packed_pos(L, m, 0);
 
-  // warp tile: 16 rows x 32 cols -> 2 x 4 m8n8 tiles
   const int wr = (warp & 3) * 16;
-  const int wc = (warp >> 2) * 32;
-  double acc[2][4][2];
+  const int wc = (warp >> 2) * (TN / 2);
+  double acc[2][NT][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   auto produce = [&](int buf, int ks) {
+    // F chunk: 16 degrees x TN columns, 16-byte async copies (zero outside)
+    for (int i = tid; i < SYN_TK * TN / 2; i += SYN_THREADS) {
+      const int j = i / (TN / 2);
+      const int c2 = (i % (TN / 2)) * 2;
+      const int l = ks + j;
+      const int c = col0 + c2;
+      double* dst = &Fs[buf][j][c2];
+      if (l < L && c < C) syn_cp_async16(dst, Fm + (int64_t)(l - m) * C + c);  // C is a multiple of 4
+      else *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
     if (tid < SYN_TM) {
       for (int j = 0; j < SYN_TK; ++j) {
         const int l = ks + j;
@@ -172,40 +198,28 @@ __global__ void __launch_bounds__(SYN_THREADS, 2) k_synth_dmma(
         }
         Ps[buf][j][tid] = v;
       }
-    } else {
-      for (int i = tid - SYN_TM; i < SYN_TK * SYN_TN / 2; i += SYN_THREADS - SYN_TM) {
-        const int j = i / (SYN_TN / 2);
-        const int c2 = (i % (SYN_TN / 2)) * 2;
-        const int l = ks + j;
-        const int c = col0 + c2;
-        double2 v = make_double2(0.0, 0.0);
-        if (l < L) {
-          const double* src = Fm + (int64_t)(l - m) * C + c;
-          if (c + 1 < C) v = __ldg(reinterpret_cast<const double2*>(src));
-          else if (c < C) v.x = __ldg(src);
-        }
-        *reinterpret_cast<double2*>(&Fs[buf][j][c2]) = v;
-      }
     }
   };
 
   int buf = 0;
   if (kfirst < L) produce(0, kfirst);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
   for (int ks = kfirst; ks < L; ks += SYN_TK) {
     if (ks + SYN_TK < L) produce(buf ^ 1, ks + SYN_TK);
 #pragma unroll
     for (int kk = 0; kk < SYN_TK; kk += 4) {
-      double a[2], b[4];
+      double a[2];
 #pragma unroll
       for (int i = 0; i < 2; ++i) a[i] = Ps[buf][kk + tq][wr + i * 8 + g];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Fs[buf][kk + tq][wc + j * 8 + g];
+      for (int j = 0; j < NT; ++j) {
+        const double b = Fs[buf][kk + tq][wc + j * 8 + g];
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int i = 0; i < 2; ++i) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b);
+      }
     }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
     buf ^= 1;
   }
@@ -217,12 +231,23 @@ __global__ void __launch_bounds__(SYN_THREADS, 2) k_synth_dmma(
     const int k = ring_order[r];
     double* grow = G + ((int64_t)m * L + k) * C;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NT; ++j) {
       const int c = col0 + wc + j * 8 + 2 * tq;
-      if (c + 1 < C) *reinterpret_cast<double2*>(grow + c) = make_double2(acc[i][j][0], acc[i][j][1]);
-      else if (c < C) grow[c] = acc[i][j][0];
+      if (c < C) *reinterpret_cast<double2*>(grow + c) = make_double2(acc[i][j][0], acc[i][j][1]);
     }
   }
+}
+
+template <int TN>
+static cudaError_t launch_synth_tn(osph_plan* p, int C) {
+  const int L = p->L;
+  const size_t smem = sizeof(double) * 2 * SYN_TK * ((SYN_TM + SYN_PAD) + (TN + SYN_PAD));
+  cudaError_t e = cudaFuncSetAttribute(k_synth_dmma<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((C + TN - 1) / TN, (L + SYN_TM - 1) / SYN_TM, L);
+  k_synth_dmma<TN><<<grid, SYN_THREADS, smem, p->stream>>>(L, C, p->d_cos, p->d_rec, p->d_ls, p->d_pstart,
+                                                           p->d_ring_order, p->d_fpack, p->d_g);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_synth(osph_plan* p, int B) {
@@ -237,9 +262,11 @@ cudaError_t launch_synth(osph_plan* p, int B) {
       k_synth_fma<8><<<grid, SYN_FMA_THREADS, 0, p->stream>>>(L, p->d_cos, p->d_rec, p->d_ls, p->d_pstart,
                                                             p->d_ring_order, p->d_fpack, p->d_g);
   } else {
-    dim3 grid((C + SYN_TN - 1) / SYN_TN, (L + SYN_TM - 1) / SYN_TM, L);
-    k_synth_dmma<<<grid, SYN_THREADS, 0, p->stream>>>(L, C, p->d_cos, p->d_rec, p->d_ls, p->d_pstart,
-                                                     p->d_ring_order, p->d_fpack, p->d_g);
+    // widest column tile that the batch fills at least half of
+    static const int tn_env = getenv("OSPH_SYNTH_TN") ? atoi(getenv("OSPH_SYNTH_TN")) : 0;
+    const int tn = tn_env ? tn_env : (C > 64 ? 128 : 64);  // measured: 128 beats 256 (1 block/SM) at C = 256
+    cudaError_t e = tn == 256 ? launch_synth_tn<256>(p, C) : tn == 128 ? launch_synth_tn<128>(p, C) : launch_synth_tn<64>(p, C);
+    if (e != cudaSuccess) return e;
   }
   p->launches++;
   return cudaGetLastError();
