@@ -98,6 +98,13 @@ int osph_forward(osph_plan* plan, int B, const void* samples, void* flm, int ptr
  * |m| > (n-1)/2 (AliasingError) and even n with OSPH_ERR_ARG. */
 int osph_ring_analysis(const double* ring, int n, int m, double* out, int device);
 
+/* legendre_table(m, grid.thetas, L) (legendre.py:110-143) on the device for
+ * all L plan rings: out[(l - m) * ld + k] = Y_lm(theta_k, 0) for l = m..L-1,
+ * k < L (degree-major; ld >= L).  Values below 2^-500 are returned as 0.
+ * ptr_kind must include OSPH_DEVICE (OSPH_ASYNC: enqueue on the plan stream).
+ * Used by the grid optimiser (optimize_order, sampling.py:217-278). */
+int osph_legendre_block(osph_plan* plan, int m, double* out, int64_t ld, int ptr_kind);
+
 /* Device time of the stages of the last inverse and the last forward call, in
  * seconds: seconds[0..2] = inverse {pack, Legendre synthesis, ring inverse DFTs},
  * seconds[3..5] = forward {ring forward DFTs, per-order factorisation, sweep}

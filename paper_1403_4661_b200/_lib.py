@@ -44,6 +44,7 @@ SIGNATURES = {
     "osph_inverse": (_I, [_P, _I, _P, _P, _I]),
     "osph_forward": (_I, [_P, _I, _P, _P, _I, _I, ctypes.POINTER(OsphStats)]),
     "osph_ring_analysis": (_I, [_P, _I, _I, _P, _I]),
+    "osph_legendre_block": (_I, [_P, _I, _P, ctypes.c_int64, _I]),
     "osph_last_launch_count": (_I, [_P]),
     "osph_last_stage_times": (_I, [_P, _P]),
     "osph_last_error": (ctypes.c_char_p, []),

@@ -43,7 +43,7 @@
 
 namespace cg = cooperative_groups;
 
-cudaError_t launch_factor_np_class(osph_plan* p, int m_first, int m_last, int cs);  // factor_np.cu
+cudaError_t launch_factor_np_class(osph_plan* p, int m_first, int m_last, int cs, cudaStream_t st);  // factor_np.cu
 
 #define FAC_THREADS 256
 #define FAC_TC 8      // column tile width of the rank-NB update
@@ -405,7 +405,7 @@ struct FacClass {
 };
 
 template <int RPT, int NB>
-static cudaError_t launch_class(osph_plan* p, int m_first, int m_last, int cs) {
+static cudaError_t launch_class(osph_plan* p, int m_first, int m_last, int cs, cudaStream_t st) {
   const int L = p->L;
   const int n = L - m_first;
   const size_t smem = sizeof(double) * ((size_t)NB * n + (size_t)NB * FAC_SUPER);
@@ -420,7 +420,7 @@ static cudaError_t launch_class(osph_plan* p, int m_first, int m_last, int cs) {
   cfg.gridDim = dim3((unsigned)((m_last - m_first + 1) * cs));
   cfg.blockDim = dim3(FAC_THREADS);
   cfg.dynamicSmemBytes = smem;
-  cfg.stream = p->stream;
+  cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cs;
@@ -438,34 +438,48 @@ static cudaError_t launch_class(osph_plan* p, int m_first, int m_last, int cs) {
 
 // Orders are grouped by block size n = L - m; each group gets a kernel
 // instantiation whose register tile fits n and a cluster size that scales
-// the rank-NB update with n^2.
-cudaError_t launch_factor(osph_plan* p) {
+// the rank-NB update with n^2.  The largest class runs on `st`; the smaller
+// classes run on `st2` so they fill the SMs the large class's tail leaves idle
+// (the classes write disjoint orders).  Both streams are joined back into `st`.
+cudaError_t launch_factor(osph_plan* p, cudaStream_t st, cudaStream_t st2) {
   const int L = p->L;
   cudaError_t e;
-  if ((e = cudaMemsetAsync(p->d_norms, 0, sizeof(unsigned long long) * 2 * L, p->stream)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(p->d_status, 0, sizeof(int) * L, p->stream)) != cudaSuccess) return e;
+  if (!st) st = p->stream;
+  if ((e = cudaMemsetAsync(p->d_norms, 0, sizeof(unsigned long long) * 2 * L, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(p->d_status, 0, sizeof(int) * L, st)) != cudaSuccess) return e;
+  if (st2) {
+    if ((e = cudaEventRecord(p->ev_fac[0], st)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(st2, p->ev_fac[0], 0)) != cudaSuccess) return e;
+  }
   // classes by n (inclusive upper bounds), processed largest first
   struct Cls {
     int nlo, nhi, cs;
   };
   const Cls classes[] = {{1025, 2048, 16}, {513, 1024, 16}, {257, 512, 8}, {129, 256, 4}, {65, 128, 2}, {1, 64, 1}};
   const bool static_piv = p->piv_ready && !getenv("OSPH_FACTOR_PIVOTED");
+  bool first = true;
   for (const Cls& c : classes) {
     const int nhi = std::min(c.nhi, L);
     if (nhi < c.nlo) continue;
     const int m_first = L - nhi, m_last = L - c.nlo;
+    cudaStream_t s = (first || !st2) ? st : st2;
+    first = false;
     if (static_piv && nhi <= 256) {  // pivot order known: shared-memory static-pivot kernel
-      e = launch_factor_np_class(p, m_first, m_last, nhi > 128 ? 4 : 1);
+      e = launch_factor_np_class(p, m_first, m_last, nhi > 128 ? 4 : 1, s);
       if (e != cudaSuccess) return e;
       continue;
     }
-    if (nhi > 1024) e = launch_class<8, 8>(p, m_first, m_last, c.cs);
-    else if (nhi > 512) e = launch_class<4, 16>(p, m_first, m_last, c.cs);
-    else if (nhi > 256) e = launch_class<2, 32>(p, m_first, m_last, c.cs);
-    else e = launch_class<1, 32>(p, m_first, m_last, c.cs);
+    if (nhi > 1024) e = launch_class<8, 8>(p, m_first, m_last, c.cs, s);
+    else if (nhi > 512) e = launch_class<4, 16>(p, m_first, m_last, c.cs, s);
+    else if (nhi > 256) e = launch_class<2, 32>(p, m_first, m_last, c.cs, s);
+    else e = launch_class<1, 32>(p, m_first, m_last, c.cs, s);
     if (e != cudaSuccess) return e;
   }
-  k_kappa<<<(L + 127) / 128, 128, 0, p->stream>>>(L, p->d_norms, p->d_kappa);
+  if (st2) {
+    if ((e = cudaEventRecord(p->ev_fac[1], st2)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(st, p->ev_fac[1], 0)) != cudaSuccess) return e;
+  }
+  k_kappa<<<(L + 127) / 128, 128, 0, st>>>(L, p->d_norms, p->d_kappa);
   p->launches++;
   p->piv_ready = true;  // the pivot order depends on the grid only
   return cudaGetLastError();

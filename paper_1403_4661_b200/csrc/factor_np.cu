@@ -107,7 +107,9 @@ __global__ void __launch_bounds__(FNP_THREADS, 1) k_factor_np(
   const int cw = max(0, c1 - c0);
   const int cwt = (cw + 7) & ~7;  // own columns rounded to 8-column tiles
   const int nrt8 = (n + 7) >> 3;
-  double* pg = panel_g + (size_t)slot * 2 * FNP_NB * ldn;
+  // hand-off slot per order (classes may run concurrently on different streams)
+  const int nall = min(L, 256), ldn_all = ((nall + 15) / 16) * 16 + 4;
+  double* pg = panel_g + (size_t)(m - (L - nall)) * 2 * FNP_NB * ldn_all;
 
   if (tid == 0) s_bad = 0;
 #ifdef OSPH_FACTOR_PROF
@@ -394,7 +396,7 @@ size_t factor_np_smem(int nmax, int cs) { return sizeof(double) * NpLayout(nmax,
 
 // Launch the static-pivot factorisation for orders m_first..m_last (block
 // sizes n <= nmax, nmax <= 256), cs CTAs per order.
-cudaError_t launch_factor_np_class(osph_plan* p, int m_first, int m_last, int cs) {
+cudaError_t launch_factor_np_class(osph_plan* p, int m_first, int m_last, int cs, cudaStream_t st) {
   const int L = p->L;
   const int nmax = L - m_first;
   const size_t smem = factor_np_smem(nmax, cs);
@@ -406,7 +408,7 @@ cudaError_t launch_factor_np_class(osph_plan* p, int m_first, int m_last, int cs
   cfg.gridDim = dim3((unsigned)((m_last - m_first + 1) * cs));
   cfg.blockDim = dim3(FNP_THREADS);
   cfg.dynamicSmemBytes = smem;
-  cfg.stream = p->stream;
+  cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cs;

@@ -66,6 +66,9 @@ static void plan_free(osph_plan* p) {
   if (p->ev_out) cudaEventDestroy(p->ev_out);
   if (p->s_in) cudaStreamDestroy(p->s_in);
   if (p->s_out) cudaStreamDestroy(p->s_out);
+  if (p->s_fac) cudaStreamDestroy(p->s_fac);
+  for (cudaEvent_t& e : p->ev_fac)
+    if (e) cudaEventDestroy(e);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   delete p;
 }
@@ -131,6 +134,8 @@ extern "C" int osph_plan_create(int L, const double* thetas, int max_batch, int 
   for (cudaEvent_t& e : p->ev) PLAN_TRY(cudaEventCreate(&e));
   PLAN_TRY(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
   PLAN_TRY(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
+  PLAN_TRY(cudaStreamCreateWithFlags(&p->s_fac, cudaStreamNonBlocking));
+  for (cudaEvent_t& e : p->ev_fac) PLAN_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (int c = 0; c < osph_plan::kIoChunks; ++c) {
     PLAN_TRY(cudaEventCreateWithFlags(&p->ev_in[c], cudaEventDisableTiming));
     PLAN_TRY(cudaEventCreateWithFlags(&p->ev_done[c], cudaEventDisableTiming));
@@ -376,12 +381,16 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
   p->launches = 0;
   double2* out = host ? p->d_out : (double2*)flm;
   if (!host) {
+    // the factorisation needs no data: it runs on a side stream beside the ring DFTs
+    CUDA_TRY(cudaEventRecord(p->ev_start, st));
+    CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
+    CUDA_TRY(cudaEventRecord(p->ev[6], p->s_in));
+    CUDA_TRY(launch_factor(p, p->s_in, p->s_fac));
+    CUDA_TRY(cudaEventRecord(p->ev[7], p->s_in));
     CUDA_TRY(cudaEventRecord(p->ev[4], st));
     CUDA_TRY(launch_ring_forward(p, B, (const double2*)samples));
     CUDA_TRY(cudaEventRecord(p->ev[5], st));
-    CUDA_TRY(cudaEventRecord(p->ev[6], st));
-    CUDA_TRY(launch_factor(p));
-    CUDA_TRY(cudaEventRecord(p->ev[7], st));
+    CUDA_TRY(cudaStreamWaitEvent(st, p->ev[7], 0));
   } else {
     // the factorisation needs no data: it runs while the samples are copied in,
     // and each chunk's ring DFTs start as soon as the chunk has landed
@@ -396,7 +405,7 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
       CUDA_TRY(cudaEventRecord(p->ev_in[c], p->s_in));
     }
     CUDA_TRY(cudaEventRecord(p->ev[6], st));
-    CUDA_TRY(launch_factor(p));
+    CUDA_TRY(launch_factor(p, st, p->s_fac));
     CUDA_TRY(cudaEventRecord(p->ev[7], st));
     for (int c = 0; c < nch; ++c) {
       const int b0 = (int)((int64_t)B * c / nch), b1 = (int)((int64_t)B * (c + 1) / nch);
@@ -445,6 +454,26 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
       }
     }
   }
+  return OSPH_OK;
+}
+
+extern "C" int osph_legendre_block(osph_plan* p, int m, double* out, int64_t ld, int kind) {
+  g_last_error.clear();
+  if (!p || !out) {
+    osph_set_error("NULL plan or output pointer");
+    return OSPH_ERR_ARG;
+  }
+  if (m < 0 || m >= p->L) {
+    osph_set_error("order " + std::to_string(m) + " invalid for band limit " + std::to_string(p->L));
+    return OSPH_ERR_ARG;
+  }
+  if (ld < p->L || !(kind & OSPH_DEVICE) || (kind & ~(OSPH_DEVICE | OSPH_ASYNC))) {
+    osph_set_error("osph_legendre_block needs a device pointer and ld >= L");
+    return OSPH_ERR_ARG;
+  }
+  CUDA_TRY(cudaSetDevice(p->device));
+  CUDA_TRY(launch_legendre_block(p, m, out, ld));
+  if (!(kind & OSPH_ASYNC)) CUDA_TRY(cudaStreamSynchronize(p->stream));
   return OSPH_OK;
 }
 

@@ -72,7 +72,8 @@ struct osph_plan {
   cudaEvent_t ev[10] = {};
   // host-buffer calls: copies on their own streams, overlapped with compute chunk by chunk
   static constexpr int kIoChunks = 4;
-  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaStream_t s_in = nullptr, s_out = nullptr, s_fac = nullptr;
+  cudaEvent_t ev_fac[2] = {};
   cudaEvent_t ev_in[kIoChunks] = {}, ev_done[kIoChunks] = {}, ev_start = nullptr, ev_out = nullptr;
   bool have_inv = false, have_fwd = false;
 };
@@ -81,13 +82,15 @@ struct osph_plan {
 void osph_set_error(const std::string& msg);
 
 // ---- launchers (each returns cudaError_t of the launch) ----
-cudaError_t launch_tables(osph_plan* p);                                   // tables.cu
+cudaError_t launch_tables(osph_plan* p);
+cudaError_t launch_legendre_block(osph_plan* p, int m, double* out, int64_t ld);  // tables.cu                                   // tables.cu
 cudaError_t launch_ring_inverse(osph_plan* p, int B, double2* samples);    // ringdft.cu
 // maps [bofs, bofs + nb) of a batch of B (nb < 0: all B)
 cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples, int bofs = 0, int nb = -1);  // ringdft.cu
 cudaError_t launch_pack(osph_plan* p, int B, const double2* flm);          // synth.cu
 cudaError_t launch_synth(osph_plan* p, int B);                             // synth.cu
-cudaError_t launch_factor(osph_plan* p);                                   // factor.cu
+// factor classes on st (largest) and st2 (the rest; nullptr = all on st), joined into st
+cudaError_t launch_factor(osph_plan* p, cudaStream_t st = nullptr, cudaStream_t st2 = nullptr);  // factor.cu
 cudaError_t launch_sweep(osph_plan* p, int B, double2* flm);               // sweep.cu
 int sweep_maps_per_team(osph_plan* p, int B);  // sweep.cu: launch configuration (cached per B), 1/2/4
 cudaError_t launch_ring_pair(int n, int m, const double2* v, double2* out, cudaStream_t st);  // ringdft.cu

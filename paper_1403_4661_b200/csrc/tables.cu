@@ -100,6 +100,41 @@ __global__ void k_start_table(int L, const double* __restrict__ costh, const dou
   pstart[t] = make_double2(prev, curr);
 }
 
+// legendre_table(m, thetas, L) (legendre.py:110-143) for every plan ring k:
+// out[(l - m) * ld + k] = Y_lm(theta_k, 0), l = m..L-1 (degree-major, so the
+// stores of a warp are coalesced).  Degrees below the start degree ls are
+// < 2^-500 (the reference's rescaled values there are below every term they
+// are summed with) and are written as 0; from ls on, the plain recurrence in
+// the same fma form as the hot kernels.
+__global__ void k_legendre_block(int L, int m, const double* __restrict__ costh, const double2* __restrict__ rec,
+                                 const int* __restrict__ ls_tab, const double2* __restrict__ pstart,
+                                 double* __restrict__ out, int64_t ld) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= L) return;
+  const int64_t t = (int64_t)m * L + k;
+  const int ls = ls_tab[t];
+  for (int l = m; l < min(ls, L); ++l) out[(int64_t)(l - m) * ld + k] = 0.0;
+  if (ls >= L) return;
+  const double2 pr = pstart[t];
+  const double x = costh[k];
+  const double2* rm = rec + packed_pos(L, m, 0);
+  double p0 = pr.x, p1 = pr.y;
+  out[(int64_t)(ls - m) * ld + k] = p1;
+  for (int l = ls; l < L - 1; ++l) {
+    const double2 ar = rm[l - m];
+    const double nxt = fma(x, p1, -ar.x * p0) * ar.y;
+    p0 = p1;
+    p1 = nxt;
+    out[(int64_t)(l + 1 - m) * ld + k] = p1;
+  }
+}
+
+cudaError_t launch_legendre_block(osph_plan* p, int m, double* out, int64_t ld) {
+  k_legendre_block<<<(p->L + 127) / 128, 128, 0, p->stream>>>(p->L, m, p->d_cos, p->d_rec, p->d_ls, p->d_pstart,
+                                                              out, ld);
+  return cudaGetLastError();
+}
+
 __global__ void k_twiddles(double2* __restrict__ tw) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= OSPH_TW_SIZE / 2) return;
