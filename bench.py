@@ -43,6 +43,7 @@ CONFIGS = {
     1: dict(L=64, B=1, spectrum="white", real=False, grid="grid-L64-uniform-condmin.txt"),
     2: dict(L=256, B=64, spectrum="cmb", real=False, grid="grid-L256-uniform-condmin.txt"),
     3: dict(L=512, B=256, spectrum="cmb", real=True, grid="grid-L512-uniform-condmin.txt"),
+    4: dict(L=2048, B=1, spectrum="white", real=False, grid="grid-L2048-uniform-condmin.txt"),
 }
 
 
@@ -221,6 +222,7 @@ def workload_config(cfg, args):
                         f"inverse then forward per step",
             "L": cfg["L"], "maps_per_gpu": cfg["B"], "global_batch": cfg["B"] * args.gpus,
             "grid": cfg["grid"], "parallelism": f"maps sharded over {args.gpus} GPU(s)",
+            "real_maps": "two real maps per complex transform (OSPH_REAL)" if cfg["real"] else None,
             "l2": "flushed (256 MiB write) before every timed step"}
 
 
@@ -247,7 +249,8 @@ def run_ours(args, cfg):
     plan.set_stream(osp.transform.torch_stream_handle(stream))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    kind = 1 | 2  # OSPH_DEVICE | OSPH_ASYNC
+    real = bool(cfg["real"])
+    kind = 1 | 2 | (4 if real else 0)  # OSPH_DEVICE | OSPH_ASYNC (| OSPH_REAL: two real maps per complex transform)
 
     def step():
         plan.inverse_raw(B, flm.data_ptr(), samples.data_ptr(), kind)
@@ -296,15 +299,15 @@ def run_ours(args, cfg):
     s_pin = torch.empty_like(flm_pin).pin_memory()
     b_pin = torch.empty_like(flm_pin).pin_memory()
     fn, sn, bn = flm_pin.numpy(), s_pin.numpy(), b_pin.numpy()
-    osp.inverse_sht_batch(fn, grid, out=sn, device=local)
-    osp.forward_sht_batch(sn, grid, out=bn, check=False, device=local)
+    osp.inverse_sht_batch(fn, grid, out=sn, device=local, real=real)
+    osp.forward_sht_batch(sn, grid, out=bn, check=False, device=local, real=real)
     e2e_t = []
     for _ in range(max(1, min(args.steps, 5))):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        osp.inverse_sht_batch(fn, grid, out=sn, device=local)
-        osp.forward_sht_batch(sn, grid, out=bn, check=True, device=local)
+        osp.inverse_sht_batch(fn, grid, out=sn, device=local, real=real)
+        osp.forward_sht_batch(sn, grid, out=bn, check=True, device=local, real=real)
         e2e_t.append(time.perf_counter() - t0)
     e2e_err = float(np.abs(bn - fn).max())
     if world > 1:
@@ -316,7 +319,7 @@ def run_ours(args, cfg):
     e2e_value = world * B / e2e_mean
 
     if rank == 0:
-        fl = flops(L, B)
+        fl = flops(L, (B + 1) // 2 if real else B)  # real maps: algorithmic work of the paired transforms
         st_i = stage_i / args.steps
         st_f = stage_f / args.steps
         stages = {"pack": st_i[0], "synth": st_i[1], "ring_inverse": st_i[2],

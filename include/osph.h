@@ -55,6 +55,11 @@ extern "C" {
 #define OSPH_HOST 0   /* host pointers: the library copies in and out (pinned memory is fastest) */
 #define OSPH_DEVICE 1 /* device pointers on the plan's device */
 #define OSPH_ASYNC 2  /* with OSPH_DEVICE: enqueue on the plan stream and return immediately */
+#define OSPH_REAL 4   /* real-valued maps: flm conjugate-symmetric (f_{l,-m} = (-1)^m conj f_lm) /
+                         samples real (imaginary parts ignored); layouts unchanged (complex128),
+                         output samples have zero imaginary parts.  Pairs of maps run as one
+                         complex transform (half the work); results equal the complex path's
+                         to rounding. */
 
 typedef struct osph_plan osph_plan;
 

@@ -234,6 +234,48 @@ def rings_from_tones(g_plus, g_minus, L: int) -> np.ndarray:
     return out
 
 
+def inverse_rings(flm: np.ndarray, thetas: np.ndarray, rings) -> dict:
+    """inverse_sht restricted to the listed rings: {k: samples of ring k}.
+
+    The same steps as inverse_sht (transform.py:347-357): _g_accumulate on the
+    rings' co-latitudes only, then _fold_bins and the per-ring ifft for those
+    rings -- O(L^2) per ring, so large-L rings can be checked one by one.
+    """
+    thetas = np.asarray(thetas, dtype=np.float64)
+    L = thetas.size
+    flm = np.asarray(flm, dtype=np.complex128)
+    offsets, a_curr, a_next, seed_fac = packed_tables(L)
+    fcols = np.empty((L * (L + 1) // 2, 4))
+    for m in range(L):
+        ells = np.arange(m, L)
+        fp = flm[ells * ells + ells + m]
+        fn = flm[ells * ells + ells - m]
+        sl = slice(offsets[m], offsets[m + 1])
+        fcols[sl, 0], fcols[sl, 1], fcols[sl, 2], fcols[sl, 3] = fp.real, fp.imag, fn.real, fn.imag
+    rings = [int(k) for k in rings]
+    th = thetas[rings]
+    out = np.empty((len(rings), L, 4))
+    _clib().oracle_g_accumulate(
+        _p(np.ascontiguousarray(np.cos(th))), _p(np.ascontiguousarray(np.sin(th))), len(rings), _p(fcols),
+        _p(seed_fac), _p(a_curr), _p(a_next), _p(offsets), L, _p(out),
+    )
+    out *= TWO_PI
+    signs = np.ones(L)
+    signs[1::2] = -1.0
+    res = {}
+    for i, k in enumerate(rings):
+        n = 2 * k + 1
+        gp = out[i, :, 0] + 1j * out[i, :, 1]
+        gn = (out[i, :, 2] + 1j * out[i, :, 3]) * signs
+        bins = np.zeros(n, dtype=np.complex128)
+        for m in range(L):  # _fold_bins order (transform.py:204-218)
+            bins[m % n] += gp[m]
+            if m > 0:
+                bins[(-m) % n] += gn[m]
+        res[k] = (n / TWO_PI) * np.fft.ifft(bins)
+    return res
+
+
 def inverse_sht(flm: np.ndarray, thetas: np.ndarray) -> np.ndarray:
     """Flat complex128[L^2] coefficients -> flat ring-major samples (transform.py:347-357)."""
     thetas = np.asarray(thetas, dtype=np.float64)

@@ -17,7 +17,7 @@ _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libosph.so"
 
 OSPH_OK, OSPH_ERR_ARG, OSPH_ERR_ILLCOND, OSPH_ERR_CUDA, OSPH_ERR_NCCL = 0, 1, 2, 3, 4
-OSPH_HOST, OSPH_DEVICE, OSPH_ASYNC = 0, 1, 2
+OSPH_HOST, OSPH_DEVICE, OSPH_ASYNC, OSPH_REAL = 0, 1, 2, 4
 ABI_VERSION = 1
 
 

@@ -16,7 +16,9 @@
 // Ring DFTs with n <= OSPH_DIRECT_MAX use a direct O(n^2) DFT; longer rings
 // use Bluestein with a power-of-two FFT of size >= 2n-1 held in shared memory.
 #define OSPH_DIRECT_MAX 63
-#define OSPH_FFT_MAX 8192  // largest in-smem FFT (complex double: 128 KB)
+#define OSPH_FFT_MAX 8192  // largest one-CTA FFT (complex double: 128 KB); 16384 runs on 2-CTA clusters
+#define OSPH_SW_SMEM 2048     // per-stage FFT twiddles kept in shared memory (spans < 1024)
+#define OSPH_SW_GLOBAL 16384  // global per-stage twiddle table: spans up to 4096 (N <= 16384)
 
 // Position of (order m, ring/degree offset i) in order-major packed storage:
 // sum_{m'<m} (L - m') + i   (same packing as transform.py:268-291 offsets).

@@ -458,9 +458,15 @@ cudaError_t launch_factor(osph_plan* p, cudaStream_t st, cudaStream_t st2) {
   const Cls classes[] = {{1025, 2048, 16}, {513, 1024, 16}, {257, 512, 8}, {129, 256, 4}, {65, 128, 2}, {1, 64, 1}};
   const bool static_piv = p->piv_ready && !getenv("OSPH_FACTOR_PIVOTED");
   bool first = true;
+  if (static_piv && L > 256 && !getenv("OSPH_FACTOR_NO_BF")) {
+    // every order with n > 256 in one breadth-first blocked pass (factor_bf.cu)
+    if ((e = launch_factor_bf(p, 0, L - 257, st)) != cudaSuccess) return e;
+    first = false;
+  }
   for (const Cls& c : classes) {
     const int nhi = std::min(c.nhi, L);
     if (nhi < c.nlo) continue;
+    if (!first && static_piv && nhi > 256 && !getenv("OSPH_FACTOR_NO_BF")) continue;  // done by the BF pass
     const int m_first = L - nhi, m_last = L - c.nlo;
     cudaStream_t s = (first || !st2) ? st : st2;
     first = false;

@@ -1,0 +1,398 @@
+// factor_bf.cu -- batched, breadth-first blocked Gauss-Jordan inversion of the
+// large per-order blocks (n = L - m > 256) with the grid-determined pivot order.
+//
+// Same result as factor.cu / factor_np.cu (explicit X = (P A_m)^{-1}, A_m =
+// 2pi Y_lm(theta_k), k >= m, l >= m; transform.py:416-429, blocks.py:88-116),
+// organised for throughput instead of per-order latency.  With the pivot
+// order known (recorded by the partial-pivoting kernel on the plan's first
+// call; it depends only on the grid), row i of the working matrix is ring
+// m + perm[i] and Gauss-Jordan needs no interchanges, so a panel step on the
+// column block J = [j0, j0 + nb) is purely block-algebraic:
+//     D = A[J, J]^{-1}                 (nb x nb, one CTA per order)
+//     E = -A[:, J] D,  E[J] = D - I    (n x nb, parallel over row tiles)
+//     A[:, K] += E A[J, K]   (K != J)  (rank-nb update, DMMA tiles)
+//     A[:, J]  = E + I_J
+// and every order with n > j0 takes the step in the same three launches.
+// The update (2 n^2 nb flops per order and step, nb = 64) is the bulk of the
+// work: 64 x 64 output tiles on the fp64 tensor cores (mma.sync m8n8k4 ->
+// DMMA.8x8x4), operands staged in shared memory.  After the last step the
+// epilogue emits the sweep operands exactly as factor_np.cu does (X in
+// chunk-major 8-row tiles with natural-order columns, w_m, u_m, j*, beta_m)
+// plus ||X||_1 for the condition estimate.
+#include <algorithm>
+#include <vector>
+
+#include "plan.cuh"
+
+#define BF_NB 64       // panel width
+#define BF_T 64        // output tile (rows and columns)
+#define BF_THREADS 256
+#define BF_LDS (BF_NB + 4)  // padded smem row stride (doubles)
+
+__device__ __forceinline__ void bf_atomic_max_pos(unsigned long long* addr, double v) {
+  if (!(v >= 0.0) || isinf(v)) v = INFINITY;
+  atomicMax(addr, (unsigned long long)__double_as_longlong(v));
+}
+
+// Work item lookup: order index within the launch from a prefix table of
+// per-order item counts (binary search; pre[0] = 0, pre[cnt] = total).
+__device__ __forceinline__ int bf_find(const int* __restrict__ pre, int cnt, int item) {
+  int lo = 0, hi = cnt;  // pre[lo] <= item < pre[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(pre + mid) <= item) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// ---- 1. the blocks: 2pi Y_lm(theta_{m + perm[i]}) at row i (column-major,
+// column = degree l - m); rings k < m go to the tiled below-block Pb_m.
+__global__ void __launch_bounds__(BF_THREADS) k_bf_generate(int L, int m_first, const double* __restrict__ costh,
+                                                            const double2* __restrict__ rec,
+                                                            const int* __restrict__ ls_tab,
+                                                            const double2* __restrict__ pstart,
+                                                            const int* __restrict__ perm_all,
+                                                            const int64_t* __restrict__ ainv_off,
+                                                            const int64_t* __restrict__ pb_off,
+                                                            double* __restrict__ ainv, double* __restrict__ pbelow) {
+  const int m = m_first + blockIdx.y;
+  const int n = L - m;
+  const int t = blockIdx.x * BF_THREADS + threadIdx.x;
+  if (t >= L) return;
+  int k, row = -1;
+  if (t < n) {
+    row = t;
+    k = m + __ldg(perm_all + packed_pos(L, m, t));
+  } else {
+    k = t - n;  // ring below the block
+  }
+  double* A = ainv + __ldg(ainv_off + m);
+  double* Pb = pbelow + __ldg(pb_off + m);
+  const int64_t ts = (int64_t)m * L + k;
+  const int ls = __ldg(ls_tab + ts);
+  const double2 pp = __ldg(pstart + ts);
+  double p0 = pp.x, p1 = pp.y;
+  const double x = __ldg(costh + k);
+  const double2* recm = rec + packed_pos(L, m, 0);
+  const int nrtpb = (m + 7) >> 3;
+  for (int l = m; l < L; ++l) {
+    double v = 0.0;
+    if (l >= ls) {
+      v = OSPH_TWO_PI * p1;
+      const double2 ar = __ldg(recm + (l - m));
+      const double nxt = fma(x, p1, -ar.x * p0) * ar.y;
+      p0 = p1;
+      p1 = nxt;
+    }
+    if (row >= 0) A[(int64_t)(l - m) * n + row] = v;
+    else Pb[tile_index(k, l - m, nrtpb)] = v;
+  }
+}
+
+// ||A||_1 (or ||X||_1 after the sweep of panels): one warp per column.
+__global__ void __launch_bounds__(BF_THREADS) k_bf_colnorm(int L, int m_first, const int64_t* __restrict__ ainv_off,
+                                                           const double* __restrict__ ainv,
+                                                           unsigned long long* __restrict__ norms, int which) {
+  const int m = m_first + blockIdx.y;
+  const int n = L - m;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* A = ainv + __ldg(ainv_off + m);
+  double cmax = 0.0;
+  for (int c = blockIdx.x * (BF_THREADS / 32) + warp; c < n; c += gridDim.x * (BF_THREADS / 32)) {
+    double s = 0.0;
+    for (int i = lane; i < n; i += 32) s += fabs(__ldcg(A + (int64_t)c * n + i));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    cmax = fmax(cmax, s);
+  }
+  if (lane == 0 && cmax > 0.0) bf_atomic_max_pos(norms + 2 * m + which, cmax);
+}
+
+// ---- 2a. D = A[J, J]^{-1} (in-place Gauss-Jordan, no interchanges) and the
+// row block R = A[J, :] (the update's B operand, snapshotted before the update).
+__global__ void __launch_bounds__(BF_THREADS) k_bf_diag(int L, int m_first, int j0, const int64_t* __restrict__ ainv_off,
+                                                        const double* __restrict__ ainv, double* __restrict__ dbuf,
+                                                        double* __restrict__ rbuf, const int64_t* __restrict__ bf_off,
+                                                        int* __restrict__ status) {
+  __shared__ double D[BF_NB][BF_NB + 1];
+  const int m = m_first + blockIdx.x;
+  const int n = L - m;
+  const int nb = min(BF_NB, n - j0);
+  const double* A = ainv + __ldg(ainv_off + m);
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < BF_NB * BF_NB; idx += BF_THREADS) {
+    const int r = idx & (BF_NB - 1), c = idx >> 6;
+    D[r][c] = (r < nb && c < nb) ? __ldcg(A + (int64_t)(j0 + c) * n + j0 + r) : (r == c ? 1.0 : 0.0);
+  }
+  // R = A[J, :], layout [col][NB]
+  double* R = rbuf + __ldg(bf_off + m);
+  for (int idx = tid; idx < n * BF_NB; idx += BF_THREADS) {
+    const int r = idx & (BF_NB - 1), c = idx >> 6;
+    R[idx] = r < nb ? __ldcg(A + (int64_t)c * n + j0 + r) : 0.0;
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int p = 0; p < nb; ++p) {
+    const double piv = D[p][p];
+    const double inv = 1.0 / piv;
+    if (tid == 0 && (piv == 0.0 || !isfinite(piv))) bad = true;
+    double nv[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int idx = tid + q * BF_THREADS;
+      const int r = idx & (BF_NB - 1), c = idx >> 6;
+      double v = D[r][c];
+      if (r == p) v = (c == p) ? inv : v * inv;
+      else v = (c == p) ? -v * inv : fma(-D[r][p] * inv, D[p][c], v);
+      nv[q] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int idx = tid + q * BF_THREADS;
+      D[idx & (BF_NB - 1)][idx >> 6] = nv[q];
+    }
+    __syncthreads();
+  }
+  if (bad) atomicOr(status + m, 1);
+  double* Dg = dbuf + (size_t)blockIdx.x * BF_NB * BF_NB;
+  for (int idx = tid; idx < BF_NB * BF_NB; idx += BF_THREADS) Dg[idx] = D[idx & (BF_NB - 1)][idx >> 6];
+}
+
+// ---- 2b. E = -A[I, J] D (E[J] = D - I) per 64-row tile; A[I, J] = E + I_J.
+__global__ void __launch_bounds__(BF_THREADS) k_bf_panel(int L, int m_first, int j0, const int* __restrict__ pre,
+                                                         int cnt, const int64_t* __restrict__ ainv_off,
+                                                         double* __restrict__ ainv, const double* __restrict__ dbuf,
+                                                         double* __restrict__ ebuf, const int64_t* __restrict__ bf_off) {
+  extern __shared__ double bf_sm[];
+  double(*As)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm);
+  double(*Ds)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm + BF_T * BF_LDS);
+  const int oi = bf_find(pre, cnt, blockIdx.x);
+  const int m = m_first + oi;
+  const int n = L - m;
+  const int nb = min(BF_NB, n - j0);
+  const int i0 = (blockIdx.x - __ldg(pre + oi)) * BF_T;
+  double* A = ainv + __ldg(ainv_off + m);
+  const double* Dg = dbuf + (size_t)oi * BF_NB * BF_NB;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < BF_T * BF_NB; idx += BF_THREADS) {
+    const int r = idx & (BF_T - 1), c = idx >> 6;
+    As[r][c] = (i0 + r < n && c < nb) ? __ldcg(A + (int64_t)(j0 + c) * n + i0 + r) : 0.0;
+    Ds[r][c] = __ldcg(Dg + idx);  // [c][r] order in memory: D[r][c] at c*NB + r
+  }
+  __syncthreads();
+  double* E = ebuf + __ldg(bf_off + m);  // [col][n]
+  // thread -> row r (64), 16 column groups of 4
+  const int r = tid & (BF_T - 1), cg4 = tid >> 6;  // 4 groups x 16 columns
+  const int gi = i0 + r;
+  const bool inJ = gi >= j0 && gi < j0 + nb;
+  for (int c = cg4 * 16; c < cg4 * 16 + 16; ++c) {
+    if (c >= nb || gi >= n) continue;
+    double v;
+    if (inJ) {
+      v = Ds[gi - j0][c] - ((gi - j0 == c) ? 1.0 : 0.0);
+    } else {
+      double s = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < BF_NB; ++k) s = fma(As[r][k], Ds[k][c], s);
+      v = -s;
+    }
+    E[(int64_t)c * n + gi] = v;
+    A[(int64_t)(j0 + c) * n + gi] = v + ((inJ && gi - j0 == c) ? 1.0 : 0.0);
+  }
+}
+
+// ---- 2c. A[I, K] += E[I, :] R[:, K] for every 64 x 64 tile outside column block J.
+__global__ void __launch_bounds__(BF_THREADS, 2) k_bf_update(int L, int m_first, int j0, const int* __restrict__ pre,
+                                                             int cnt, const int64_t* __restrict__ ainv_off,
+                                                             double* __restrict__ ainv, const double* __restrict__ ebuf,
+                                                             const double* __restrict__ rbuf,
+                                                             const int64_t* __restrict__ bf_off) {
+  extern __shared__ double bf_sm[];
+  double(*Es)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm);              // [row][k]
+  double(*Rs)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm + BF_T * BF_LDS);  // [k][col]
+  const int oi = bf_find(pre, cnt, blockIdx.x);
+  const int m = m_first + oi;
+  const int n = L - m;
+  const int nb = min(BF_NB, n - j0);
+  const int nt = (n + BF_T - 1) / BF_T;
+  const int local = blockIdx.x - __ldg(pre + oi);
+  const int rt = local % nt;
+  int ct = local / nt;
+  if (ct >= j0 / BF_T) ++ct;  // skip the panel's column tile
+  const int i0 = rt * BF_T, c0 = ct * BF_T;
+  double* A = ainv + __ldg(ainv_off + m);
+  const double* E = ebuf + __ldg(bf_off + m);
+  const double* R = rbuf + __ldg(bf_off + m);
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < BF_T * BF_NB; idx += BF_THREADS) {
+    const int a = idx & 63, b = idx >> 6;
+    Es[a][b] = (i0 + a < n && b < nb) ? __ldcg(E + (int64_t)b * n + i0 + a) : 0.0;  // row a, k b
+    Rs[a][b] = (c0 + b < n) ? __ldcg(R + (int64_t)(c0 + b) * BF_NB + a) : 0.0;     // k a, col b
+  }
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = (warp & 1) * 32, wc = (warp >> 1) * 16;  // warp tile 32 rows x 16 cols
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int row = i0 + wr + 8 * i + g, col = c0 + wc + 8 * j + 2 * t;
+      acc[i][j][0] = (row < n && col < n) ? __ldcg(A + (int64_t)col * n + row) : 0.0;
+      acc[i][j][1] = (row < n && col + 1 < n) ? __ldcg(A + (int64_t)(col + 1) * n + row) : 0.0;
+    }
+  __syncthreads();
+#pragma unroll 4
+  for (int k0 = 0; k0 < BF_NB; k0 += 4) {
+    double a[4], b[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = Es[wr + 8 * i + g][k0 + t];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) b[j] = Rs[k0 + t][wc + 8 * j + g];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int row = i0 + wr + 8 * i + g, col = c0 + wc + 8 * j + 2 * t;
+      if (row < n && col < n) A[(int64_t)col * n + row] = acc[i][j][0];
+      if (row < n && col + 1 < n) A[(int64_t)(col + 1) * n + row] = acc[i][j][1];
+    }
+}
+
+// ---- 3. sweep operands from X (column c = pivot position, ring perm[c]):
+// chunk-major tiles with natural-order columns (the late ring's column zero),
+// u_m[perm[c]] = Pb_m[m-1, :] X[:, c], and for c = j* (perm = 0): w_m, beta_m, j*.
+__global__ void __launch_bounds__(BF_THREADS) k_bf_epilogue(int L, int m_first, const int64_t* __restrict__ ainv_off,
+                                                            const double* __restrict__ ainv,
+                                                            const int* __restrict__ perm_all,
+                                                            const int64_t* __restrict__ xt_off,
+                                                            double* __restrict__ xt_all,
+                                                            const int64_t* __restrict__ pb_off,
+                                                            const double* __restrict__ pbelow, double* __restrict__ u_out,
+                                                            double* __restrict__ w_out, double* __restrict__ beta_out,
+                                                            int* __restrict__ jstar_out) {
+  const int m = m_first + blockIdx.y;
+  const int n = L - m;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* A = ainv + __ldg(ainv_off + m);
+  const int* perm = perm_all + packed_pos(L, m, 0);
+  double* Xt = xt_all + __ldg(xt_off + m);
+  const double* Pb = pbelow + __ldg(pb_off + m);
+  const int nrt = (n + 7) >> 3, nrtpb = (m + 7) >> 3;
+  for (int c = blockIdx.x * (BF_THREADS / 32) + warp; c < n; c += gridDim.x * (BF_THREADS / 32)) {
+    const int cn = __ldg(perm + c);
+    const double* col = A + (int64_t)c * n;
+    double s = 0.0;
+    for (int i = lane; i < n; i += 32) {
+      const double v = __ldcg(col + i);
+      Xt[tile_index(i, cn, nrt)] = cn != 0 ? v : 0.0;
+      if (m >= 1) s = fma(__ldcg(Pb + tile_index(m - 1, i, nrtpb)), v, s);
+      if (cn == 0) w_out[(size_t)m * L + i] = v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      u_out[(size_t)m * L + cn] = cn != 0 ? s : 0.0;
+      if (cn == 0) {
+        beta_out[m] = s;
+        jstar_out[m] = c;
+      }
+    }
+  }
+}
+
+// Host driver: orders m_first..m_last (all with n > 256), static pivots.
+cudaError_t launch_factor_bf(osph_plan* p, int m_first, int m_last, cudaStream_t st) {
+  const int L = p->L;
+  const int cnt_all = m_last - m_first + 1;
+  const int nmax = L - m_first;
+  cudaError_t e;
+  if (p->bf_m_first != m_first || p->bf_m_last != m_last) {
+    // per-step prefix tables of panel (row-tile) and update (tile) work items
+    const int nsteps = (nmax + BF_NB - 1) / BF_NB;
+    std::vector<int> tab;
+    p->h_bf_step.assign(nsteps, {});
+    for (int sidx = 0; sidx < nsteps; ++sidx) {
+      const int j0 = sidx * BF_NB;
+      int cnt = 0;
+      for (int m = m_first; m <= m_last; ++m)
+        if (L - m > j0) cnt = m - m_first + 1;
+      auto& d = p->h_bf_step[sidx];
+      d.cnt = cnt;
+      d.pre_panel = (int)tab.size();
+      int acc = 0;
+      for (int o = 0; o <= cnt; ++o) {
+        tab.push_back(acc);
+        if (o < cnt) acc += (L - (m_first + o) + BF_T - 1) / BF_T;
+      }
+      d.n_panel = acc;
+      d.pre_upd = (int)tab.size();
+      acc = 0;
+      for (int o = 0; o <= cnt; ++o) {
+        tab.push_back(acc);
+        if (o < cnt) {
+          const int nt = (L - (m_first + o) + BF_T - 1) / BF_T;
+          acc += nt * (nt - 1);
+        }
+      }
+      d.n_upd = acc;
+    }
+    cudaFree(p->d_bf_tab);
+    p->d_bf_tab = nullptr;
+    if ((e = cudaMalloc(&p->d_bf_tab, sizeof(int) * tab.size())) != cudaSuccess) return e;
+    if ((e = cudaMemcpy(p->d_bf_tab, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return e;
+    // E and R panels: NB x n doubles per order; D: NB^2 per order
+    std::vector<int64_t> off(L + 1, 0);
+    for (int m = 0; m < L; ++m) off[m + 1] = off[m] + ((m >= m_first && m <= m_last) ? (int64_t)BF_NB * (L - m) : 0);
+    cudaFree(p->d_bf_off);
+    cudaFree(p->d_bf_e);
+    cudaFree(p->d_bf_r);
+    cudaFree(p->d_bf_d);
+    p->d_bf_off = nullptr;
+    p->d_bf_e = p->d_bf_r = p->d_bf_d = nullptr;
+    if ((e = cudaMalloc(&p->d_bf_off, sizeof(int64_t) * (L + 1))) != cudaSuccess) return e;
+    if ((e = cudaMemcpy(p->d_bf_off, off.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return e;
+    if ((e = cudaMalloc(&p->d_bf_e, sizeof(double) * off[L])) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&p->d_bf_r, sizeof(double) * off[L])) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&p->d_bf_d, sizeof(double) * BF_NB * BF_NB * cnt_all)) != cudaSuccess) return e;
+    p->bf_m_first = m_first;
+    p->bf_m_last = m_last;
+  }
+  const size_t sm2 = sizeof(double) * 2 * BF_T * BF_LDS;
+  if ((e = cudaFuncSetAttribute(k_bf_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute(k_bf_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)
+    return e;
+  k_bf_generate<<<dim3((L + BF_THREADS - 1) / BF_THREADS, cnt_all), BF_THREADS, 0, st>>>(
+      L, m_first, p->d_cos, p->d_rec, p->d_ls, p->d_pstart, p->d_piv, p->d_ainv_off, p->d_pb_off, p->d_ainv,
+      p->d_pbelow);
+  k_bf_colnorm<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, p->d_ainv_off, p->d_ainv, p->d_norms, 0);
+  p->launches += 2;
+  for (size_t sidx = 0; sidx < p->h_bf_step.size(); ++sidx) {
+    const auto& d = p->h_bf_step[sidx];
+    const int j0 = (int)sidx * BF_NB;
+    k_bf_diag<<<d.cnt, BF_THREADS, 0, st>>>(L, m_first, j0, p->d_ainv_off, p->d_ainv, p->d_bf_d, p->d_bf_r,
+                                            p->d_bf_off, p->d_status);
+    k_bf_panel<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, p->d_bf_tab + d.pre_panel, d.cnt, p->d_ainv_off,
+                                                 p->d_ainv, p->d_bf_d, p->d_bf_e, p->d_bf_off);
+    if (d.n_upd > 0)
+      k_bf_update<<<d.n_upd, BF_THREADS, sm2, st>>>(L, m_first, j0, p->d_bf_tab + d.pre_upd, d.cnt, p->d_ainv_off,
+                                                  p->d_ainv, p->d_bf_e, p->d_bf_r, p->d_bf_off);
+    p->launches += 3;
+  }
+  k_bf_colnorm<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, p->d_ainv_off, p->d_ainv, p->d_norms, 1);
+  k_bf_epilogue<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, p->d_ainv_off, p->d_ainv, p->d_piv,
+                                                         p->d_xt_off, p->d_xt, p->d_pb_off, p->d_pbelow, p->d_u,
+                                                         p->d_w, p->d_beta, p->d_jstar);
+  p->launches += 2;
+  return cudaGetLastError();
+}

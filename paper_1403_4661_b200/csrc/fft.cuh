@@ -123,8 +123,24 @@ __device__ __forceinline__ void load_twiddles(double2* twn, int logN, const doub
 
 __device__ __forceinline__ int fsw(int e) { return e ^ ((e >> 2) & 7); }
 
+// Per-stage twiddles (layout: see load_stage_twiddles).  The entries of the
+// short spans (h < 1024, the first OSPH_SW_SMEM) are copied to shared memory;
+// the few long-span stages read the plan's global table (L1/L2 resident), so
+// an 8192-point transform fits one CTA next to its data.
+struct StageTw {
+  const double2* s;
+  const double2* __restrict__ g;
+  __device__ __forceinline__ double2 operator()(int i) const { return i < OSPH_SW_SMEM ? s[i] : __ldg(g + i); }
+};
+
+// smem copy of the first min(N, OSPH_SW_SMEM) entries of the global stage table
+__device__ __forceinline__ void load_stage_twiddles_smem(double2* sw, int logN, const double2* __restrict__ gsw) {
+  const int cnt = min(1 << logN, OSPH_SW_SMEM);
+  for (int j = threadIdx.x; j < cnt; j += blockDim.x) sw[j] = __ldg(gsw + j);
+}
+
 // forward-sign DIF, G transforms of length N (x[g*N + fsw(t)])
-static __device__ void fft_dif_fwd_multi(double2* x, int logN, int G, const double2* twn) {
+static __device__ void fft_dif_fwd_multi(double2* x, int logN, int G, const StageTw twn) {
   const int N = 1 << logN;
   const int lq = logN - 2;
   int lh = logN - 2;  // span of the first radix-4 stage: N/4
@@ -136,7 +152,7 @@ static __device__ void fft_dif_fwd_multi(double2* x, int logN, int G, const doub
       const int jj = j & ((1 << lq) - 1);
       const int pos = jj & (h - 1);
       const int i0 = ((jj - pos) << 2) + pos, i1 = i0 + h, i2 = i1 + h, i3 = i2 + h;
-      const double2 w4 = twn[2 * (h - 1) + h + pos], w2 = twn[2 * (h - 1) + pos];
+      const double2 w4 = twn(2 * (h - 1) + h + pos), w2 = twn(2 * (h - 1) + pos);
       const double2 x0 = xg[fsw(i0)], x1 = xg[fsw(i1)], x2 = xg[fsw(i2)], x3 = xg[fsw(i3)];
       const double2 t0 = cadd(x0, x2), t1 = cadd(x1, x3);
       double2 t2 = cmul(csub(x0, x2), w4);
@@ -163,7 +179,7 @@ static __device__ void fft_dif_fwd_multi(double2* x, int logN, int G, const doub
 }
 
 // inverse-sign DIT, input bit-reversed, output natural (unnormalised)
-static __device__ void fft_dit_inv_multi(double2* x, int logN, int G, const double2* twn) {
+static __device__ void fft_dit_inv_multi(double2* x, int logN, int G, const StageTw twn) {
   const int N = 1 << logN;
   __syncthreads();
   int lh = 0;
@@ -187,7 +203,7 @@ static __device__ void fft_dit_inv_multi(double2* x, int logN, int G, const doub
       const int jj = j & ((1 << lq) - 1);
       const int pos = jj & (h - 1);
       const int i0 = ((jj - pos) << 2) + pos, i1 = i0 + h, i2 = i1 + h, i3 = i2 + h;
-      const double2 w1 = conj2(twn[2 * (h - 1) + pos]), w2 = conj2(twn[2 * (h - 1) + h + pos]);
+      const double2 w1 = conj2(twn(2 * (h - 1) + pos)), w2 = conj2(twn(2 * (h - 1) + h + pos));
       const double2 a0 = xg[fsw(i0)], a1 = cmul(w1, xg[fsw(i1)]), a2 = xg[fsw(i2)], a3 = cmul(w1, xg[fsw(i3)]);
       const double2 b0 = cadd(a0, a1), b1 = csub(a0, a1), b2 = cadd(a2, a3), b3 = csub(a2, a3);
       const double2 c2 = cmul(w2, b2);
@@ -202,16 +218,8 @@ static __device__ void fft_dit_inv_multi(double2* x, int logN, int G, const doub
   }
 }
 
-// Per-stage twiddle tables for fft_dif_fwd_multi / fft_dit_inv_multi: for the
+// Per-stage twiddle table for fft_dif_fwd_multi / fft_dit_inv_multi: for the
 // radix-4 stage of span h = 2^lh, W_2h^pos at sw[2(h-1) + pos] and W_4h^pos at
-// sw[2(h-1) + h + pos] (pos < h), so a warp reads consecutive entries.
-// Size 2(N/4 ... ) < N entries.
-__device__ __forceinline__ void load_stage_twiddles(double2* sw, int logN, const double2* __restrict__ tw) {
-  for (int lh = 0; lh <= logN - 2; ++lh) {
-    const int h = 1 << lh;
-    for (int pos = threadIdx.x; pos < h; pos += blockDim.x) {
-      sw[2 * (h - 1) + pos] = __ldg(tw + (pos << (14 - lh - 1)));
-      sw[2 * (h - 1) + h + pos] = __ldg(tw + (pos << (14 - lh - 2)));
-    }
-  }
-}
+// sw[2(h-1) + h + pos] (pos < h), so a warp reads consecutive entries.  The
+// entries do not depend on N (a transform of size N uses the first N - 2);
+// built once per plan into global memory (OSPH_SW_GLOBAL entries).

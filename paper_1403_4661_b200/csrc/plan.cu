@@ -53,7 +53,8 @@ static void plan_free(osph_plan* p) {
                   p->d_bluestein_rings, p->d_ainv_off, p->d_pb_off, p->d_ainv, p->d_pbelow, p->d_piv,
                   p->d_norms, p->d_kappa, p->d_status, p->d_jstar, p->d_beta, p->d_u, p->d_w, p->d_xt_off, p->d_xt, p->d_panel,
                   p->d_fpack, p->d_g, p->d_r,
-                  p->d_in, p->d_out};
+                  p->d_in, p->d_out, p->d_sw, p->d_xbuf, p->d_bf_tab, p->d_bf_off, p->d_bf_e, p->d_bf_r,
+                  p->d_bf_d};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (cudaEvent_t& e : p->ev)
@@ -67,6 +68,8 @@ static void plan_free(osph_plan* p) {
   if (p->s_in) cudaStreamDestroy(p->s_in);
   if (p->s_out) cudaStreamDestroy(p->s_out);
   if (p->s_fac) cudaStreamDestroy(p->s_fac);
+  cudaFree(p->d_z1);
+  cudaFree(p->d_z2);
   for (cudaEvent_t& e : p->ev_fac)
     if (e) cudaEventDestroy(e);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
@@ -170,12 +173,12 @@ extern "C" int osph_plan_create(int L, const double* thetas, int max_batch, int 
   PLAN_TRY(dalloc(&p->d_bhat, (size_t)p->h_bhat_off[L]));
   PLAN_TRY(dalloc(&p->d_tw, 8192));
   PLAN_TRY(dalloc(&p->d_roots, (size_t)(OSPH_DIRECT_MAX + 1) * (OSPH_DIRECT_MAX + 1) / 4 + 64));
+  PLAN_TRY(dalloc(&p->d_sw, OSPH_SW_GLOBAL));
   for (int k = 0; k < L; ++k) {
-    if (p->h_fft_n[k] > OSPH_FFT_MAX) {
-      osph_set_error("ring DFT length exceeds the in-shared-memory FFT (L > 2048 not supported yet)");
-      return fail(OSPH_ERR_ARG);
-    }
+    if (p->h_fft_n[k] > 2 * OSPH_FFT_MAX) p->dft_ok = false;
+    if (p->h_fft_n[k] > OSPH_FFT_MAX) p->n_big_rings++;
   }
+  if (!p->dft_ok) p->n_bluestein_rings = p->n_big_rings = 0;  // Legendre tables only (osph_legendre_block)
   PLAN_TRY(launch_tables(p));
   PLAN_TRY(cudaStreamSynchronize(st));
   *out = p;
@@ -272,6 +275,7 @@ static int ensure_forward(osph_plan* p) {
     CUDA_TRY(dalloc(&p->d_panel, nmax * 2 * 32 * (((nmax + 15) / 16) * 16 + 4)));
   }
   CUDA_TRY(dalloc(&p->d_beta, (size_t)L));
+  CUDA_TRY(dalloc(&p->d_xbuf, (size_t)2 * L * B));
   // [L][L] + 2: the sweep's bulk copies round their sizes up to 16 bytes
   CUDA_TRY(dalloc(&p->d_u, (size_t)L * L + 2));
   CUDA_TRY(dalloc(&p->d_w, (size_t)L * L + 2));
@@ -290,6 +294,10 @@ static int check_call(osph_plan* p, int B, const void* a, void* b, int kind) {
     osph_set_error("plan is NULL");
     return OSPH_ERR_ARG;
   }
+  if (!p->dft_ok) {
+    osph_set_error("ring DFT length exceeds the in-shared-memory FFT (transforms need L <= 2048 in this build)");
+    return OSPH_ERR_ARG;
+  }
   if (B < 1 || B > p->max_batch) {
     osph_set_error("batch " + std::to_string(B) + " outside [1, max_batch=" + std::to_string(p->max_batch) + "]");
     return OSPH_ERR_ARG;
@@ -298,7 +306,7 @@ static int check_call(osph_plan* p, int B, const void* a, void* b, int kind) {
     osph_set_error("NULL data pointer");
     return OSPH_ERR_ARG;
   }
-  if (kind & ~(OSPH_DEVICE | OSPH_ASYNC)) {
+  if (kind & ~(OSPH_DEVICE | OSPH_ASYNC | OSPH_REAL)) {
     osph_set_error("unknown ptr_kind flags");
     return OSPH_ERR_ARG;
   }
@@ -313,6 +321,140 @@ static int check_call(osph_plan* p, int B, const void* a, void* b, int kind) {
 // H2D copy (s_in), compute (plan stream) and D2H copy (s_out) are chained by
 // events, so copies of neighbouring chunks overlap the compute in both
 // directions.  Device buffers: one pass on the plan stream.
+// ---------------------------------------------------------------------------
+// Real maps (OSPH_REAL).  The transforms are complex-linear, so two real maps
+// a, b run as ONE complex map z = a + i b: the inverse of f_a + i f_b is
+// a + i b (both syntheses are real), and the forward of a + i b is
+// F(a) + i F(b) with F(a)_{l,-m} = (-1)^m conj F(a)_{lm}, so
+//   F(a)_lm = (z_lm + c) / 2,  F(b)_lm = (z_lm - c) / (2i),  c = (-1)^m conj z_{l,-m}.
+// Half the maps go through the transform; pairing/unpairing are one HBM pass each.
+
+__global__ void k_pair_flm(int B, int64_t n, const double2* __restrict__ f, double2* __restrict__ z) {
+  const int p = blockIdx.y;
+  const double2* fa = f + (size_t)(2 * p) * n;
+  const double2* fb = (2 * p + 1 < B) ? f + (size_t)(2 * p + 1) * n : nullptr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 a = fa[i];
+    const double2 b = fb ? fb[i] : make_double2(0.0, 0.0);
+    z[(size_t)p * n + i] = make_double2(a.x - b.y, a.y + b.x);
+  }
+}
+
+__global__ void k_unpair_samples(int B, int64_t n, const double2* __restrict__ z, double2* __restrict__ s) {
+  const int p = blockIdx.y;
+  double2* sa = s + (size_t)(2 * p) * n;
+  double2* sb = (2 * p + 1 < B) ? s + (size_t)(2 * p + 1) * n : nullptr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = z[(size_t)p * n + i];
+    sa[i] = make_double2(v.x, 0.0);
+    if (sb) sb[i] = make_double2(v.y, 0.0);
+  }
+}
+
+__global__ void k_pair_samples(int B, int64_t n, const double2* __restrict__ s, double2* __restrict__ z) {
+  const int p = blockIdx.y;
+  const double2* sa = s + (size_t)(2 * p) * n;
+  const double2* sb = (2 * p + 1 < B) ? s + (size_t)(2 * p + 1) * n : nullptr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    z[(size_t)p * n + i] = make_double2(sa[i].x, sb ? sb[i].x : 0.0);
+}
+
+// flm index i = l^2 + l + m; its mirror l^2 + l - m = 2(l^2 + l) - i.
+__global__ void k_unpair_flm(int B, int L, const double2* __restrict__ z, double2* __restrict__ f) {
+  const int p = blockIdx.y;
+  const int64_t n = (int64_t)L * L;
+  const double2* zp = z + (size_t)p * n;
+  double2* fa = f + (size_t)(2 * p) * n;
+  double2* fb = (2 * p + 1 < B) ? f + (size_t)(2 * p + 1) * n : nullptr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = (int64_t)sqrt((double)i);
+    const int64_t ll = (l * l > i) ? l - 1 : ((l + 1) * (l + 1) <= i ? l + 1 : l);
+    const int64_t c0 = ll * ll + ll;
+    const int64_t m = i - c0;
+    const double sg = (m & 1) ? -1.0 : 1.0;
+    const double2 a = zp[i], b = zp[2 * c0 - i];
+    const double2 c = make_double2(sg * b.x, -sg * b.y);  // (-1)^m conj z_{l,-m}
+    fa[i] = make_double2(0.5 * (a.x + c.x), 0.5 * (a.y + c.y));
+    if (fb) fb[i] = make_double2(0.5 * (a.y - c.y), -0.5 * (a.x - c.x));  // (a - c) / 2i
+  }
+}
+
+static int ensure_real(osph_plan* p) {
+  if (p->d_z1) return OSPH_OK;
+  const size_t n = (size_t)((p->max_batch + 1) / 2) * p->L * p->L;
+  CUDA_TRY(dalloc(&p->d_z1, n));
+  CUDA_TRY(dalloc(&p->d_z2, n));
+  return OSPH_OK;
+}
+
+static dim3 pair_grid(int pairs, int64_t n) {
+  return dim3((unsigned)std::min<int64_t>((n + 255) / 256, 1184), (unsigned)pairs);
+}
+
+static int inverse_real(osph_plan* p, int B, const void* flm, void* samples, bool host) {
+  int rc;
+  if ((rc = ensure_real(p))) return rc;
+  const int L = p->L, Bp = (B + 1) / 2;
+  const int64_t n = (int64_t)L * L;
+  const size_t bytes = sizeof(double2) * (size_t)B * n;
+  cudaStream_t st = p->stream;
+  const double2* src = (const double2*)flm;
+  double2* dst = (double2*)samples;
+  if (host) {
+    CUDA_TRY(cudaMemcpyAsync(p->d_in, flm, bytes, cudaMemcpyHostToDevice, st));
+    src = p->d_in;
+    dst = p->d_out;
+  }
+  k_pair_flm<<<pair_grid(Bp, n), 256, 0, st>>>(B, n, src, p->d_z1);
+  CUDA_TRY(cudaEventRecord(p->ev[0], st));
+  CUDA_TRY(launch_pack(p, Bp, p->d_z1));
+  CUDA_TRY(cudaEventRecord(p->ev[1], st));
+  CUDA_TRY(launch_synth(p, Bp));
+  CUDA_TRY(cudaEventRecord(p->ev[2], st));
+  CUDA_TRY(launch_ring_inverse(p, Bp, p->d_z2));
+  CUDA_TRY(cudaEventRecord(p->ev[3], st));
+  k_unpair_samples<<<pair_grid(Bp, n), 256, 0, st>>>(B, n, p->d_z2, dst);
+  CUDA_TRY(cudaGetLastError());
+  p->launches += 2;
+  if (host) CUDA_TRY(cudaMemcpyAsync(samples, p->d_out, bytes, cudaMemcpyDeviceToHost, st));
+  return OSPH_OK;
+}
+
+static int forward_real(osph_plan* p, int B, const void* samples, void* flm, bool host) {
+  int rc;
+  if ((rc = ensure_real(p))) return rc;
+  const int L = p->L, Bp = (B + 1) / 2;
+  const int64_t n = (int64_t)L * L;
+  const size_t bytes = sizeof(double2) * (size_t)B * n;
+  cudaStream_t st = p->stream;
+  const double2* src = (const double2*)samples;
+  double2* dst = (double2*)flm;
+  // the factorisation needs no data: side streams, beside the copy, pairing and ring DFTs
+  CUDA_TRY(cudaEventRecord(p->ev_start, st));
+  CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
+  CUDA_TRY(cudaEventRecord(p->ev[6], p->s_in));
+  CUDA_TRY(launch_factor(p, p->s_in, p->s_fac));
+  CUDA_TRY(cudaEventRecord(p->ev[7], p->s_in));
+  if (host) {
+    CUDA_TRY(cudaMemcpyAsync(p->d_in, samples, bytes, cudaMemcpyHostToDevice, st));
+    src = p->d_in;
+    dst = p->d_out;
+  }
+  k_pair_samples<<<pair_grid(Bp, n), 256, 0, st>>>(B, n, src, p->d_z1);
+  CUDA_TRY(cudaEventRecord(p->ev[4], st));
+  CUDA_TRY(launch_ring_forward(p, Bp, p->d_z1));
+  CUDA_TRY(cudaEventRecord(p->ev[5], st));
+  CUDA_TRY(cudaStreamWaitEvent(st, p->ev[7], 0));
+  CUDA_TRY(cudaEventRecord(p->ev[8], st));
+  CUDA_TRY(launch_sweep(p, Bp, p->d_z2));
+  CUDA_TRY(cudaEventRecord(p->ev[9], st));
+  k_unpair_flm<<<pair_grid(Bp, n), 256, 0, st>>>(B, L, p->d_z2, dst);
+  CUDA_TRY(cudaGetLastError());
+  p->launches += 2;
+  if (host) CUDA_TRY(cudaMemcpyAsync(flm, p->d_out, bytes, cudaMemcpyDeviceToHost, st));
+  return OSPH_OK;
+}
+
 extern "C" int osph_inverse(osph_plan* p, int B, const void* flm, void* samples, int kind) {
   g_last_error.clear();
   int rc = check_call(p, B, flm, samples, kind);
@@ -324,7 +466,9 @@ extern "C" int osph_inverse(osph_plan* p, int B, const void* flm, void* samples,
   const size_t per_map = (size_t)p->L * p->L;
   cudaStream_t st = p->stream;
   p->launches = 0;
-  if (!host) {
+  if (kind & OSPH_REAL) {
+    if ((rc = inverse_real(p, B, flm, samples, host))) return rc;
+  } else if (!host) {
     CUDA_TRY(cudaEventRecord(p->ev[0], st));
     CUDA_TRY(launch_pack(p, B, (const double2*)flm));
     CUDA_TRY(cudaEventRecord(p->ev[1], st));
@@ -380,7 +524,9 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
   cudaStream_t st = p->stream;
   p->launches = 0;
   double2* out = host ? p->d_out : (double2*)flm;
-  if (!host) {
+  if (kind & OSPH_REAL) {
+    if ((rc = forward_real(p, B, samples, flm, host))) return rc;
+  } else if (!host) {
     // the factorisation needs no data: it runs on a side stream beside the ring DFTs
     CUDA_TRY(cudaEventRecord(p->ev_start, st));
     CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
@@ -415,11 +561,13 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
     }
     CUDA_TRY(cudaEventRecord(p->ev[5], st));
   }
-  CUDA_TRY(cudaEventRecord(p->ev[8], st));
-  CUDA_TRY(launch_sweep(p, B, out));
-  CUDA_TRY(cudaEventRecord(p->ev[9], st));
+  if (!(kind & OSPH_REAL)) {
+    CUDA_TRY(cudaEventRecord(p->ev[8], st));
+    CUDA_TRY(launch_sweep(p, B, out));
+    CUDA_TRY(cudaEventRecord(p->ev[9], st));
+    if (host) CUDA_TRY(cudaMemcpyAsync(flm, p->d_out, bytes, cudaMemcpyDeviceToHost, st));
+  }
   p->have_fwd = true;
-  if (host) CUDA_TRY(cudaMemcpyAsync(flm, p->d_out, bytes, cudaMemcpyDeviceToHost, st));
   if (kind & OSPH_ASYNC) return OSPH_OK;
   CUDA_TRY(cudaStreamSynchronize(st));
   if (stats) {

@@ -35,6 +35,9 @@ struct osph_plan {
   int n_bluestein_rings = 0;
   int* d_bluestein_rings = nullptr;  // ring ids that use Bluestein, largest first
   int n_direct_rings = 0;
+  int n_big_rings = 0;  // rings with a 16384-point Bluestein FFT (2-CTA clusters; first in d_bluestein_rings)
+  double2* d_sw = nullptr;  // [OSPH_SW_GLOBAL] per-stage FFT twiddles (fft.cuh)
+  bool dft_ok = true;  // every ring's Bluestein FFT fits one CTA (else: tables-only plan)
 
   // ---- forward factor storage (per call, data independent) ----
   std::vector<int64_t> h_ainv_off;  // [L+1] offset of order m's n x n inverse
@@ -59,7 +62,20 @@ struct osph_plan {
   double* d_panel = nullptr;     // static-pivot factorisation: panel hand-off buffers
   int sweep_cfg_B = -1;          // cached sweep launch configuration for batch sweep_cfg_B
   int sweep_cfg[3] = {0, 0, 0};  // maps per team, cluster width, ring stages
+  bool sweep_large = false;      // L > 1024: two kernels per order (sweep_large.cu), plain R layout
+  double2* d_xbuf = nullptr;     // sweep_large: x_s of every map [B][+-][L]
   bool inv_ready = false;        // inverse buffers allocated
+  // breadth-first factorisation of the orders with n > 256 (factor_bf.cu)
+  struct BfStep {
+    int cnt = 0, pre_panel = 0, n_panel = 0, pre_upd = 0, n_upd = 0;
+  };
+  int bf_m_first = -1, bf_m_last = -1;
+  std::vector<BfStep> h_bf_step;
+  int* d_bf_tab = nullptr;       // per-step prefix tables of work items
+  int64_t* d_bf_off = nullptr;   // [L+1] offsets of the E / R panels (NB x n per order)
+  double* d_bf_e = nullptr;
+  double* d_bf_r = nullptr;
+  double* d_bf_d = nullptr;      // NB x NB diagonal-block inverses
 
   // ---- per-call workspaces (sized for max_batch) ----
   double* d_fpack = nullptr;  // inverse: packed coefficients [pos(m,l)][4B]
@@ -67,6 +83,8 @@ struct osph_plan {
   double2* d_r = nullptr;     // forward: ring spectra, team-major [team][pos(m,k-m)][2][G] (common.cuh r_index)
   double2* d_in = nullptr;    // device staging of host inputs  [B][L^2]
   double2* d_out = nullptr;   // device staging of host outputs [B][L^2]
+  double2* d_z1 = nullptr;    // real maps (OSPH_REAL): paired complex maps [ceil(B/2)][L^2]
+  double2* d_z2 = nullptr;
 
   // stage events: inverse 0 pack 1 synth 2 ring 3; forward ring 4-5, factor 6-7, sweep 8-9
   cudaEvent_t ev[10] = {};
@@ -92,5 +110,7 @@ cudaError_t launch_synth(osph_plan* p, int B);                             // sy
 // factor classes on st (largest) and st2 (the rest; nullptr = all on st), joined into st
 cudaError_t launch_factor(osph_plan* p, cudaStream_t st = nullptr, cudaStream_t st2 = nullptr);  // factor.cu
 cudaError_t launch_sweep(osph_plan* p, int B, double2* flm);               // sweep.cu
-int sweep_maps_per_team(osph_plan* p, int B);  // sweep.cu: launch configuration (cached per B), 1/2/4
+int sweep_maps_per_team(osph_plan* p, int B);
+cudaError_t launch_sweep_large(osph_plan* p, int B, double2* flm);  // sweep_large.cu
+cudaError_t launch_factor_bf(osph_plan* p, int m_first, int m_last, cudaStream_t st);  // factor_bf.cu  // sweep.cu: launch configuration (cached per B), 1/2/4
 cudaError_t launch_ring_pair(int n, int m, const double2* v, double2* out, cudaStream_t st);  // ringdft.cu

@@ -15,8 +15,12 @@
 // handles one ring and a run of maps, transforming several maps per pass so
 // the FFT stage barriers are shared; global accesses run map-fastest, which
 // is the contiguous direction of G and R.
+#include <cooperative_groups.h>
+
 #include "fft.cuh"
 #include "plan.cuh"
+
+namespace cg = cooperative_groups;
 
 #define RING_THREADS 256
 #define RING_SMEM_BUDGET (96 * 1024)
@@ -47,7 +51,7 @@ __device__ __forceinline__ double2 fold_bin(const double* __restrict__ G, int L,
 // Bluestein circular convolution of Gr sequences (natural order, swizzled):
 // DIF forward FFT -> times the kernel spectrum (stored bit-reversed, /N) ->
 // DIT inverse FFT; natural order out, no bit-reversal passes.
-__device__ __forceinline__ void bluestein_convolve(double2* xs, int logN, int Gr, const double2* twn,
+__device__ __forceinline__ void bluestein_convolve(double2* xs, int logN, int Gr, const StageTw twn,
                                                    const double2* __restrict__ bh_br) {
   fft_dif_fwd_multi(xs, logN, Gr, twn);
   const int N = 1 << logN;
@@ -79,21 +83,21 @@ __device__ __forceinline__ void mul_and_bitrev_multi(double2* x, const double2* 
 __global__ void __launch_bounds__(RING_THREADS) k_ring_inverse_bluestein(
     int L, int B, int maps_per_block, const int* __restrict__ rings, const int* __restrict__ fft_n,
     const int64_t* __restrict__ chirp_off, const int64_t* __restrict__ bhat_off, const double2* __restrict__ chirp_all,
-    const double2* __restrict__ bhat_all, const double2* __restrict__ tw, const double* __restrict__ G,
+    const double2* __restrict__ bhat_all, const double2* __restrict__ gsw, const double* __restrict__ G,
     double2* __restrict__ samples, int smem_cplx) {
   extern __shared__ double2 sm[];
   const int k = rings[blockIdx.x];
   const int n = 2 * k + 1;
   const int N = fft_n[k];
   const int logN = 31 - __clz(N);
-  double2* twn = sm;            // per-stage twiddles (< N/2 used... see load_stage_twiddles)
-  double2* xs = sm + N;         // Gr transforms of length N
-  load_stage_twiddles(twn, logN, tw);
+  double2* xs = sm + OSPH_SW_SMEM;  // Gr transforms of length N after the short-span twiddles
+  load_stage_twiddles_smem(sm, logN, gsw);
+  const StageTw twn{sm, gsw};
   const double2* chirp = chirp_all + chirp_off[k];
   const double2* bh = bhat_all + bhat_off[k] + N;  // inverse-direction kernel
   const int b_first = blockIdx.y * maps_per_block;
   const int b_last = min(B, b_first + maps_per_block);
-  const int Gmax = max(1, (smem_cplx - N) >> logN);
+  const int Gmax = max(1, (smem_cplx - OSPH_SW_SMEM) >> logN);
   for (int b0 = b_first; b0 < b_last; b0 += Gmax) {
     const int Gr = min(Gmax, b_last - b0);
     for (int idx = threadIdx.x; idx < Gr * N; idx += blockDim.x) {  // map-fastest reads of G
@@ -183,22 +187,22 @@ __device__ __forceinline__ void scatter_rhs_multi(const double2* X, int lstride,
 __global__ void __launch_bounds__(RING_THREADS) k_ring_forward_bluestein(
     int L, int B, int maps_per_block, const int* __restrict__ rings, const int* __restrict__ fft_n,
     const int64_t* __restrict__ chirp_off, const int64_t* __restrict__ bhat_off, const double2* __restrict__ chirp_all,
-    const double2* __restrict__ bhat_all, const double2* __restrict__ tw, const double2* __restrict__ samples,
+    const double2* __restrict__ bhat_all, const double2* __restrict__ gsw, const double2* __restrict__ samples,
     double2* __restrict__ R, int smem_cplx, int bofs, int bend, int lgG) {
   extern __shared__ double2 sm[];
   const int k = rings[blockIdx.x];
   const int n = 2 * k + 1;
   const int N = fft_n[k];
   const int logN = 31 - __clz(N);
-  double2* twn = sm;            // per-stage twiddles (< N/2 used... see load_stage_twiddles)
-  double2* xs = sm + N;         // Gr transforms of length N
-  load_stage_twiddles(twn, logN, tw);
+  double2* xs = sm + OSPH_SW_SMEM;  // Gr transforms of length N after the short-span twiddles
+  load_stage_twiddles_smem(sm, logN, gsw);
+  const StageTw twn{sm, gsw};
   const double2* chirp = chirp_all + chirp_off[k];
   const double2* bh = bhat_all + bhat_off[k];  // forward-direction kernel
   // maps [bofs, bend) of a batch of B (R keeps the batch stride B)
   const int b_first = bofs + blockIdx.y * maps_per_block;
   const int b_last = min(bend, b_first + maps_per_block);
-  const int Gmax = max(1, (smem_cplx - N) >> logN);
+  const int Gmax = max(1, (smem_cplx - OSPH_SW_SMEM) >> logN);
   for (int b0 = b_first; b0 < b_last; b0 += Gmax) {
     const int Gr = min(Gmax, b_last - b0);
     for (int idx = threadIdx.x; idx < (Gr << logN); idx += blockDim.x) {  // contiguous ring reads per map
@@ -257,9 +261,137 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_forward_direct(int L, int
   }
 }
 
-static int max_fft(const osph_plan* p) {
+
+static int maps_per_block_for(int B, int rings);
+
+// ---------------------------------------------------------------------------
+// Rings whose Bluestein FFT is N = 2M = 16384 points (n = 2k+1 > 4096, L > 2048):
+// one 2-CTA cluster per ring, each CTA holding M points.  Because n <= M the
+// upper half of the chirped input is zero, so the first (span-M) stage of the
+// decimation-in-frequency transform is local: CTA 0 keeps a_t, CTA 1 takes
+// a_t W_N^t; each then runs an M-point DIF, multiplies by its half of the
+// bit-reversed kernel spectrum and runs an M-point DIT -- exactly the first
+// log2(N) - 1 stages of the N-point inverse.  Only outputs t < n <= M are
+// needed, so the last (span-M) stage reduces to y_t = u_t + conj(W_N^t) v_t:
+// CTA 1 applies the twiddle, CTA 0 adds CTA 1's half through distributed
+// shared memory.  tw[t] = W_16384^t (the plan's twiddle table).
+#define BIG_M 8192
+#define BIG_LOGM 13
+
+__device__ __forceinline__ void big_first_stage(double2* xs, int rank, int n, const double2* __restrict__ tw) {
+  if (rank == 1)
+    for (int t = threadIdx.x; t < n; t += blockDim.x) xs[fsw(t)] = cmul(xs[fsw(t)], __ldg(tw + t));
+}
+
+__device__ __forceinline__ void big_last_stage_prep(double2* xs, int rank, int n, const double2* __restrict__ tw) {
+  if (rank == 1)
+    for (int t = threadIdx.x; t < n; t += blockDim.x) xs[fsw(t)] = cmul(xs[fsw(t)], conj2(__ldg(tw + t)));
+}
+
+__global__ void __launch_bounds__(RING_THREADS) k_ring_inverse_bluestein2(
+    int L, int B, int maps_per_block, const int* __restrict__ rings, const int64_t* __restrict__ chirp_off,
+    const int64_t* __restrict__ bhat_off, const double2* __restrict__ chirp_all, const double2* __restrict__ bhat_all,
+    const double2* __restrict__ tw, const double2* __restrict__ gsw, const double* __restrict__ G,
+    double2* __restrict__ samples) {
+  extern __shared__ double2 sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int k = rings[blockIdx.x >> 1];
+  const int n = 2 * k + 1;
+  double2* xs = sm + OSPH_SW_SMEM;
+  load_stage_twiddles_smem(sm, BIG_LOGM, gsw);
+  const StageTw twn{sm, gsw};
+  const double2* xr = cl.map_shared_rank(xs, 1);
+  const double2* chirp = chirp_all + chirp_off[k];
+  const double2* bh = bhat_all + bhat_off[k] + 2 * BIG_M + rank * BIG_M;  // inverse-direction kernel, own half
+  const int b_first = blockIdx.y * maps_per_block;
+  const int b_last = min(B, b_first + maps_per_block);
+  for (int b = b_first; b < b_last; ++b) {
+    for (int t = threadIdx.x; t < BIG_M; t += blockDim.x) {
+      double2 v = make_double2(0.0, 0.0);
+      if (t < n) v = cmul(fold_bin(G, L, B, k, n, b, t), __ldg(chirp + t));
+      xs[fsw(t)] = v;
+    }
+    __syncthreads();
+    big_first_stage(xs, rank, n, tw);
+    bluestein_convolve(xs, BIG_LOGM, 1, twn, bh);
+    big_last_stage_prep(xs, rank, n, tw);
+    cl.sync();
+    if (rank == 0)
+      for (int j = threadIdx.x; j < n; j += blockDim.x)
+        samples[(int64_t)b * L * L + (int64_t)k * k + j] = cmul(cadd(xs[fsw(j)], xr[fsw(j)]), __ldg(chirp + j));
+    cl.sync();  // CTA 1's half stays valid until CTA 0 has read it
+  }
+}
+
+__global__ void __launch_bounds__(RING_THREADS) k_ring_forward_bluestein2(
+    int L, int B, int maps_per_block, const int* __restrict__ rings, const int64_t* __restrict__ chirp_off,
+    const int64_t* __restrict__ bhat_off, const double2* __restrict__ chirp_all, const double2* __restrict__ bhat_all,
+    const double2* __restrict__ tw, const double2* __restrict__ gsw, const double2* __restrict__ samples,
+    double2* __restrict__ R, int bofs, int bend, int lgG) {
+  extern __shared__ double2 sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int k = rings[blockIdx.x >> 1];
+  const int n = 2 * k + 1;
+  double2* xs = sm + OSPH_SW_SMEM;
+  load_stage_twiddles_smem(sm, BIG_LOGM, gsw);
+  const StageTw twn{sm, gsw};
+  const double2* xr = cl.map_shared_rank(xs, 1);
+  const double2* chirp = chirp_all + chirp_off[k];
+  const double2* bh = bhat_all + bhat_off[k] + rank * BIG_M;  // forward-direction kernel, own half
+  const int b_first = bofs + blockIdx.y * maps_per_block;
+  const int b_last = min(bend, b_first + maps_per_block);
+  for (int b = b_first; b < b_last; ++b) {
+    for (int t = threadIdx.x; t < BIG_M; t += blockDim.x) {
+      double2 v = make_double2(0.0, 0.0);
+      if (t < n) v = cmul(__ldg(samples + (int64_t)b * L * L + (int64_t)k * k + t), conj2(__ldg(chirp + t)));
+      xs[fsw(t)] = v;
+    }
+    __syncthreads();
+    big_first_stage(xs, rank, n, tw);
+    bluestein_convolve(xs, BIG_LOGM, 1, twn, bh);
+    big_last_stage_prep(xs, rank, n, tw);
+    cl.sync();
+    if (rank == 0)
+      for (int t = threadIdx.x; t < n; t += blockDim.x)
+        xs[fsw(t)] = cmul(cadd(xs[fsw(t)], xr[fsw(t)]), conj2(__ldg(chirp + t)));
+    cl.sync();  // CTA 1 may overwrite its half only after CTA 0 has read it
+    if (rank == 0) {
+      scatter_rhs_multi<true>(xs, BIG_LOGM, L, lgG, k, n, b, 1, R);
+      __syncthreads();
+    }
+  }
+}
+
+static size_t big_smem() { return sizeof(double2) * (size_t)(OSPH_SW_SMEM + BIG_M); }
+
+static cudaError_t launch_big(const void* kern, osph_plan* p, int nb, void** args) {
+  const size_t smem = big_smem();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int mpb = maps_per_block_for(nb, p->n_big_rings);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)(2 * p->n_big_rings), (unsigned)((nb + mpb - 1) / mpb));
+  lc.blockDim = dim3(RING_THREADS);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = p->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  *(int*)args[2] = mpb;
+  e = cudaLaunchKernelExC(&lc, kern, args);
+  p->launches++;
+  return e;
+}
+
+static int max_fft(const osph_plan* p) {  // largest single-CTA Bluestein FFT
   int N = 0;
-  for (int v : p->h_fft_n) N = v > N ? v : N;
+  for (int v : p->h_fft_n) N = (v > N && v <= OSPH_FFT_MAX) ? v : N;
   return N;
 }
 
@@ -271,20 +403,29 @@ static int maps_per_block_for(int B, int rings) {
 }
 
 static size_t ring_smem(const osph_plan* p) {
-  const size_t need = sizeof(double2) * (size_t)max_fft(p) * 2;
+  const size_t need = sizeof(double2) * ((size_t)max_fft(p) + OSPH_SW_SMEM);
   return need > RING_SMEM_BUDGET ? need : RING_SMEM_BUDGET;
 }
 
 cudaError_t launch_ring_inverse(osph_plan* p, int B, double2* samples) {
   const int L = p->L;
-  if (p->n_bluestein_rings > 0) {
-    const int mpb = maps_per_block_for(B, p->n_bluestein_rings);
+  if (p->n_big_rings > 0) {  // the largest rings come first in d_bluestein_rings
+    int Li = L, Bi = B, mpb = 0;
+    const int* rings = p->d_bluestein_rings;
+    void* args[] = {&Li, &Bi, &mpb, &rings, &p->d_chirp_off, &p->d_bhat_off, &p->d_chirp, &p->d_bhat,
+                    &p->d_tw, &p->d_sw, &p->d_g, &samples};
+    cudaError_t e = launch_big((const void*)k_ring_inverse_bluestein2, p, B, args);
+    if (e != cudaSuccess) return e;
+  }
+  const int nsmall = p->n_bluestein_rings - p->n_big_rings;
+  if (nsmall > 0) {
+    const int mpb = maps_per_block_for(B, nsmall);
     const size_t smem = ring_smem(p);
     cudaFuncSetAttribute(k_ring_inverse_bluestein, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 grid(p->n_bluestein_rings, (B + mpb - 1) / mpb);
+    dim3 grid(nsmall, (B + mpb - 1) / mpb);
     k_ring_inverse_bluestein<<<grid, RING_THREADS, smem, p->stream>>>(
-        L, B, mpb, p->d_bluestein_rings, p->d_fft_n, p->d_chirp_off, p->d_bhat_off, p->d_chirp, p->d_bhat, p->d_tw,
-        p->d_g, samples, (int)(smem / sizeof(double2)));
+        L, B, mpb, p->d_bluestein_rings + p->n_big_rings, p->d_fft_n, p->d_chirp_off, p->d_bhat_off, p->d_chirp,
+        p->d_bhat, p->d_sw, p->d_g, samples, (int)(smem / sizeof(double2)));
     p->launches++;
   }
   if (p->n_direct_rings > 0) {
@@ -299,15 +440,24 @@ cudaError_t launch_ring_inverse(osph_plan* p, int B, double2* samples) {
 cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples, int bofs, int nb) {
   const int L = p->L;
   if (nb < 0) nb = B;
-  const int lgG = __builtin_ctz(sweep_maps_per_team(p, B));  // team-major R (common.cuh)
-  if (p->n_bluestein_rings > 0) {
-    const int mpb = maps_per_block_for(nb, p->n_bluestein_rings);
+  int lgG = __builtin_ctz(sweep_maps_per_team(p, B));  // team-major R (common.cuh)
+  if (p->n_big_rings > 0) {
+    int Li = L, Bi = B, mpb = 0, b0 = bofs, b1 = bofs + nb;
+    const int* rings = p->d_bluestein_rings;
+    void* args[] = {&Li, &Bi, &mpb, &rings, &p->d_chirp_off, &p->d_bhat_off, &p->d_chirp, &p->d_bhat,
+                    &p->d_tw, &p->d_sw, &samples, &p->d_r, &b0, &b1, &lgG};
+    cudaError_t e = launch_big((const void*)k_ring_forward_bluestein2, p, nb, args);
+    if (e != cudaSuccess) return e;
+  }
+  const int nsmall = p->n_bluestein_rings - p->n_big_rings;
+  if (nsmall > 0) {
+    const int mpb = maps_per_block_for(nb, nsmall);
     const size_t smem = ring_smem(p);
     cudaFuncSetAttribute(k_ring_forward_bluestein, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 grid(p->n_bluestein_rings, (nb + mpb - 1) / mpb);
+    dim3 grid(nsmall, (nb + mpb - 1) / mpb);
     k_ring_forward_bluestein<<<grid, RING_THREADS, smem, p->stream>>>(
-        L, B, mpb, p->d_bluestein_rings, p->d_fft_n, p->d_chirp_off, p->d_bhat_off, p->d_chirp, p->d_bhat, p->d_tw,
-        samples, p->d_r, (int)(smem / sizeof(double2)), bofs, bofs + nb, lgG);
+        L, B, mpb, p->d_bluestein_rings + p->n_big_rings, p->d_fft_n, p->d_chirp_off, p->d_bhat_off, p->d_chirp,
+        p->d_bhat, p->d_sw, samples, p->d_r, (int)(smem / sizeof(double2)), bofs, bofs + nb, lgG);
     p->launches++;
   }
   if (p->n_direct_rings > 0) {

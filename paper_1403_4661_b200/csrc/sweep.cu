@@ -921,6 +921,13 @@ int sweep_maps_per_team(osph_plan* p, int B) {
   const size_t cap = 220 * 1024;
   const int KC = SWEEP_KC;
   if (p->sweep_cfg_B == B) return p->sweep_cfg[0];
+  if (L > 1024 || getenv("OSPH_SWEEP_LARGE")) {  // the right-hand sides no longer fit the persistent kernel's smem
+    p->sweep_large = true;
+    p->sweep_cfg_B = B;
+    p->sweep_cfg[0] = 1;
+    p->sweep_cfg[1] = p->sweep_cfg[2] = 0;
+    return 1;
+  }
   // maps per team: 4 (16 columns) / 2 / 1, limited by shared memory
   int g = B >= 3 ? 4 : B;
   g = std::min(g, std::max(1, env_int("OSPH_SWEEP_G", g)));
@@ -963,14 +970,26 @@ int sweep_maps_per_team(osph_plan* p, int B) {
     if (gg == 1) break;
   }
   if (found) g = best_g;
-  if (!found) {  // several waves of teams: take the narrowest team that fits
-    for (int TT = 1; TT <= 16; TT *= 2)
-      if (tiles_ok(g, TT) && fits(g, TT, 3)) {
-        T = TT;
-        break;
+  if (!found) {
+    // several waves of teams: over (g, T) that fit, maximise the maps in flight
+    // (resident teams x maps per team); ties go to the narrower team
+    int best_flight = 0;
+    for (int gg = gmax; gg >= 1; gg /= 2) {
+      for (int TT = 1; TT <= 16; TT *= 2) {
+        if (TT * 32 > 2 * L && TT > 1) break;
+        if (!tiles_ok(gg, TT) || !fits(gg, TT, 3)) continue;
+        int ss = 3;
+        while (ss < SWEEP_SMAX && fits(gg, TT, ss + 1)) ++ss;
+        const int flight = std::min((B + gg - 1) / gg, mac(gg, TT, ss)) * gg;
+        if (flight > best_flight) {
+          best_flight = flight;
+          g = gg;
+          T = TT;
+          S = ss;
+        }
       }
-    S = 3;
-    while (S < SWEEP_SMAX && fits(g, T, S + 1)) ++S;
+      if (gg == 1) break;
+    }
   }
   T = env_int("OSPH_SWEEP_T", T);
   while (T & (T - 1)) T &= T - 1;  // the kernel needs a power-of-two team width
@@ -984,6 +1003,7 @@ int sweep_maps_per_team(osph_plan* p, int B) {
 
 cudaError_t launch_sweep(osph_plan* p, int B, double2* flm) {
   const int g = sweep_maps_per_team(p, B), T = p->sweep_cfg[1], S = p->sweep_cfg[2];
+  if (p->sweep_large) return launch_sweep_large(p, B, flm);
   if (g == 4) return launch_sweep_cc<16>(p, B, 4, T, SWEEP_KC, S, flm);
   if (g == 2) return launch_sweep_cc<8>(p, B, 2, T, SWEEP_KC, S, flm);
   return launch_sweep_cc<4>(p, B, 1, T, SWEEP_KC, S, flm);

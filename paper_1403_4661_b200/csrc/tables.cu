@@ -135,6 +135,18 @@ cudaError_t launch_legendre_block(osph_plan* p, int m, double* out, int64_t ld) 
   return cudaGetLastError();
 }
 
+__global__ void k_stage_twiddles(double2* __restrict__ sw) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= OSPH_SW_GLOBAL / 2) return;  // i = (h - 1) + pos over h = 1, 2, 4, ..., 4096
+  const int lh = 31 - __clz(i + 1);
+  const int h = 1 << lh, pos = i + 1 - h;
+  double s, c;
+  sincospi(-2.0 * (double)pos / (double)(2 * h), &s, &c);
+  sw[2 * (h - 1) + pos] = make_double2(c, s);
+  sincospi(-2.0 * (double)pos / (double)(4 * h), &s, &c);
+  sw[2 * (h - 1) + h + pos] = make_double2(c, s);
+}
+
 __global__ void k_twiddles(double2* __restrict__ tw) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= OSPH_TW_SIZE / 2) return;
@@ -157,15 +169,21 @@ __global__ void k_small_roots(int nrings, double2* __restrict__ roots) {
 
 // Bluestein tables for one ring per block: chirp[t] = e^{i pi t^2/n} and, for
 // both directions, bhat = FFT_N(conjugate chirp kernel) / N.
-__global__ void k_bluestein_tables(const int* __restrict__ rings, const int* __restrict__ fft_n,
+// One block per ring (grid-stride over nrings).  scratch == nullptr: the
+// N-point work array lives in shared memory; otherwise in global memory at
+// scratch + blockIdx.x * N (the 16384-point kernels of L > 2048, one-time setup).
+__global__ void k_bluestein_tables(int nrings, const int* __restrict__ rings, const int* __restrict__ fft_n,
                                    const int64_t* __restrict__ chirp_off,
                                    const int64_t* __restrict__ bhat_off, const double2* __restrict__ tw,
-                                   double2* __restrict__ chirp, double2* __restrict__ bhat) {
-  extern __shared__ double2 xs[];
-  const int k = rings[blockIdx.x];
+                                   double2* __restrict__ chirp, double2* __restrict__ bhat,
+                                   double2* __restrict__ scratch) {
+  extern __shared__ double2 xs_sm[];
+  for (int ri = blockIdx.x; ri < nrings; ri += gridDim.x) {
+  const int k = rings[ri];
   const int n = 2 * k + 1;
   const int N = fft_n[k];
   const int logN = 31 - __clz(N);
+  double2* xs = scratch ? scratch + (size_t)blockIdx.x * N : xs_sm;
   double2* ch = chirp + chirp_off[k];
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
     const int64_t r = ((int64_t)t * t) % (2 * (int64_t)n);
@@ -197,6 +215,7 @@ __global__ void k_bluestein_tables(const int* __restrict__ rings, const int* __r
     }
     __syncthreads();
   }
+  }
 }
 
 static int next_pow2(int v) {
@@ -223,16 +242,28 @@ cudaError_t launch_tables(osph_plan* p) {
     cudaFreeAsync(seed_mant, st);
   }
   k_twiddles<<<(OSPH_TW_SIZE / 2 + 255) / 256, 256, 0, st>>>(p->d_tw);
-  const int nsmall = std::min(L, (OSPH_DIRECT_MAX - 1) / 2 + 1);
-  k_small_roots<<<nsmall, 64, 0, st>>>(nsmall, p->d_roots);
-  if (p->n_bluestein_rings > 0) {
+  const int ndirect = std::min(L, (OSPH_DIRECT_MAX - 1) / 2 + 1);
+  k_small_roots<<<ndirect, 64, 0, st>>>(ndirect, p->d_roots);
+  k_stage_twiddles<<<OSPH_SW_GLOBAL / 2 / 256, 256, 0, st>>>(p->d_sw);
+  const int nsmall = p->n_bluestein_rings - p->n_big_rings;
+  if (nsmall > 0) {
     int maxN = 0;
-    for (int k = 0; k < L; ++k) maxN = std::max(maxN, p->h_fft_n[k]);
+    for (int k = 0; k < L; ++k)
+      if (p->h_fft_n[k] <= OSPH_FFT_MAX) maxN = std::max(maxN, p->h_fft_n[k]);
     const size_t smem = sizeof(double2) * (size_t)maxN;
     cudaFuncSetAttribute(k_bluestein_tables, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_bluestein_tables<<<p->n_bluestein_rings, 256, smem, st>>>(p->d_bluestein_rings, p->d_fft_n,
-                                                                 p->d_chirp_off, p->d_bhat_off, p->d_tw,
-                                                                 p->d_chirp, p->d_bhat);
+    k_bluestein_tables<<<nsmall, 256, smem, st>>>(nsmall, p->d_bluestein_rings + p->n_big_rings, p->d_fft_n,
+                                                  p->d_chirp_off, p->d_bhat_off, p->d_tw, p->d_chirp, p->d_bhat,
+                                                  nullptr);
+  }
+  if (p->n_big_rings > 0) {  // 16384-point kernel spectra: work arrays in global memory
+    const int nb = std::min(p->n_big_rings, 296);
+    double2* scratch = nullptr;
+    if ((e = cudaMallocAsync(&scratch, sizeof(double2) * (size_t)nb * 2 * OSPH_FFT_MAX, st)) != cudaSuccess)
+      return e;
+    k_bluestein_tables<<<nb, 256, 0, st>>>(p->n_big_rings, p->d_bluestein_rings, p->d_fft_n, p->d_chirp_off,
+                                           p->d_bhat_off, p->d_tw, p->d_chirp, p->d_bhat, scratch);
+    cudaFreeAsync(scratch, st);
   }
   return cudaGetLastError();
 }

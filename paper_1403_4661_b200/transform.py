@@ -211,7 +211,7 @@ def _is_torch_cuda(x) -> bool:
     return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
 
 
-def _run(direction: str, data, grid, out=None, check: bool = True, device: int = 0):
+def _run(direction: str, data, grid, out=None, check: bool = True, device: int = 0, real: bool = False):
     """Shared driver: numpy (host) or CUDA torch tensor (device) batches of shape (B, L^2)."""
     L = grid.band_limit if hasattr(grid, "band_limit") else len(grid)
     if _is_torch_cuda(data):
@@ -227,12 +227,13 @@ def _run(direction: str, data, grid, out=None, check: bool = True, device: int =
         dev = x.device.index or 0
         y = out if out is not None else torch.empty_like(x)
         plan = get_plan(grid, B, dev)
+        kind = _lib.OSPH_DEVICE | (_lib.OSPH_REAL if real else 0)
         with plan.lock:
             plan.set_stream(torch_stream_handle(torch.cuda.current_stream(x.device)))
             if direction == "inverse":
-                plan.inverse_raw(B, x.data_ptr(), y.data_ptr(), _lib.OSPH_DEVICE)
+                plan.inverse_raw(B, x.data_ptr(), y.data_ptr(), kind)
                 return y, None
-            st = plan.forward_raw(B, x.data_ptr(), y.data_ptr(), _lib.OSPH_DEVICE, check)
+            st = plan.forward_raw(B, x.data_ptr(), y.data_ptr(), kind, check)
             return y, st
     x = np.ascontiguousarray(np.asarray(data, dtype=np.complex128))
     if x.ndim == 1:
@@ -242,24 +243,34 @@ def _run(direction: str, data, grid, out=None, check: bool = True, device: int =
     B = x.shape[0]
     y = out if out is not None else np.empty_like(x)
     plan = get_plan(grid, B, device)
+    kind = _lib.OSPH_HOST | (_lib.OSPH_REAL if real else 0)
     with plan.lock:
         plan.set_stream(None)
         if direction == "inverse":
-            plan.inverse_raw(B, x.ctypes.data, y.ctypes.data, _lib.OSPH_HOST)
+            plan.inverse_raw(B, x.ctypes.data, y.ctypes.data, kind)
             return y, None
-        st = plan.forward_raw(B, x.ctypes.data, y.ctypes.data, _lib.OSPH_HOST, check)
+        st = plan.forward_raw(B, x.ctypes.data, y.ctypes.data, kind, check)
         return y, st
 
 
-def inverse_sht_batch(flm, grid, out=None, device: int = 0):
-    """B maps at once: flm (B, L^2) in l^2+l+m order -> samples (B, L^2), ring-major."""
-    return _run("inverse", flm, grid, out=out, device=device)[0]
+def inverse_sht_batch(flm, grid, out=None, device: int = 0, *, real: bool = False):
+    """B maps at once: flm (B, L^2) in l^2+l+m order -> samples (B, L^2), ring-major.
+
+    ``real=True`` declares real-valued maps (f_{l,-m} = (-1)^m conj f_lm): pairs of
+    maps run as one complex transform and the samples come back with zero
+    imaginary parts (OSPH_REAL).
+    """
+    return _run("inverse", flm, grid, out=out, device=device, real=real)[0]
 
 
 def forward_sht_batch(samples, grid, *, check: bool = True, stats: TransformStats | None = None, out=None,
-                      device: int = 0):
-    """B maps at once: samples (B, L^2) -> coefficients (B, L^2)."""
-    y, st = _run("forward", samples, grid, out=out, check=check, device=device)
+                      device: int = 0, real: bool = False):
+    """B maps at once: samples (B, L^2) -> coefficients (B, L^2).
+
+    ``real=True`` declares real-valued samples (imaginary parts are ignored);
+    the coefficients come back complete (both signs of m), as the complex path's.
+    """
+    y, st = _run("forward", samples, grid, out=out, check=check, device=device, real=real)
     if stats is not None and st is not None:
         stats.solve_seconds = st.solve_seconds
         stats.orders = st.orders

@@ -219,3 +219,111 @@ def test_L512_batch_roundtrip(L, B, grid_of, rng):
     flm = rng.standard_normal((B, L * L)) + 1j * rng.standard_normal((B, L * L))
     f = osp.forward_sht_batch(osp.inverse_sht_batch(flm, g), g)
     assert np.abs(f - flm).max() <= 1e-10
+
+
+# ---------------------------------------------------------------------------
+# real maps (OSPH_REAL): two real maps per complex transform
+
+
+def _real_flm(L, B, seed):
+    from oracle import optisph_oracle as O
+
+    rng = np.random.default_rng(seed)
+    return np.stack([O.config_coefficients(L, rng, spectrum="cmb", real=True) for _ in range(B)])
+
+
+@pytest.mark.parametrize("L,B", [(64, 3), (256, 4)])
+def test_real_maps_match_complex_path(L, B, grid_of):
+    g = grid_of(L)
+    flm = _real_flm(L, B, 11)
+    s_c = osp.inverse_sht_batch(flm, g)
+    s_r = osp.inverse_sht_batch(flm, g, real=True)
+    assert np.all(s_r.imag == 0.0)
+    assert np.abs(s_r - s_c).max() <= 1e-12
+    f_c = osp.forward_sht_batch(s_c, g)
+    f_r = osp.forward_sht_batch(s_c, g, real=True)
+    assert np.abs(f_r - f_c).max() <= 1e-11
+    assert np.abs(f_r - flm).max() <= 1e-11
+
+
+def test_real_maps_device_path(grid_of):
+    import torch
+
+    g = grid_of(64)
+    flm = _real_flm(64, 5, 12)
+    x = torch.from_numpy(flm).cuda()
+    s = osp.inverse_sht_batch(x, g, real=True)
+    f = osp.forward_sht_batch(s, g, real=True)
+    torch.cuda.synchronize()
+    assert np.abs(f.cpu().numpy() - flm).max() <= 1e-11
+
+
+def test_L512_real_recipe_real_path(golden, grid_of):
+    """BASELINE configs[2] recipe through the real-map path (reference fixtures)."""
+    d = golden("ref_L512.npz")
+    grid = grid_of(512)
+    s = osp.inverse_sht_batch(d["flm"][None, :], grid, real=True)[0]
+    assert np.abs(s - d["samples"]).max() <= 1e-12 * max(1.0, np.abs(d["samples"]).max())
+    f = osp.forward_sht_batch(d["samples"][None, :], grid, real=True)[0]
+    rt = np.abs(d["fwd"] - d["flm"]).max()
+    assert np.abs(f - d["fwd"]).max() <= tol_fwd(rt)
+
+
+def test_L512_batched_real_maps(grid_of):
+    """Config 3 shape class (many real maps at L=512: waves of sweep teams)."""
+    g = grid_of(512)
+    flm = _real_flm(512, 40, 13)
+    s = osp.inverse_sht_batch(flm, g, real=True)
+    f = osp.forward_sht_batch(s, g, real=True)
+    assert np.abs(f - flm).max() <= 1e-11
+
+
+# ---------------------------------------------------------------------------
+# on-device Legendre rows and the GPU grid optimiser
+
+
+@pytest.mark.parametrize("L,m", [(64, 0), (64, 17), (256, 3), (256, 200)])
+def test_legendre_block_matches_oracle(L, m):
+    import ctypes
+
+    import torch
+
+    from oracle import optisph_oracle as O
+    from paper_1403_4661_b200 import _lib, sampling
+
+    th = sampling.equiangular_candidates(L)
+    plan = osp.transform.Plan(th, 1, 0)
+    buf = torch.empty((L - m, L), dtype=torch.float64, device="cuda")
+    _lib.raise_for(plan._lib.osph_legendre_block(plan.handle, m, ctypes.c_void_p(buf.data_ptr()), L,
+                                                 _lib.OSPH_DEVICE))
+    got = buf.T.cpu().numpy()
+    ref = O.legendre_table(m, th, L)
+    scale = np.abs(ref).max()
+    assert np.abs(got - ref).max() <= 1e-12 * scale  # fma vs plain recurrence rounding
+
+
+@pytest.mark.parametrize("L", [64, 256])
+def test_gpu_grid_optimiser_reproduces_reference(L, grid_of):
+    from paper_1403_4661_b200 import gridopt
+
+    g = gridopt.optimize_order(L)
+    assert np.array_equal(g.permutation, grid_of(L).permutation)
+
+
+# ---------------------------------------------------------------------------
+# large band limits: 8192-point (one CTA) and 16384-point (2-CTA cluster) Bluestein rings
+
+
+@pytest.mark.parametrize("L,rings", [(2048, [0, 31, 32, 100, 1023, 1024, 2047]),
+                                     (4096, [0, 40, 2047, 2048, 3000, 4095])])
+def test_large_L_inverse_rings_match_oracle(L, rings, grid_of):
+    from oracle import optisph_oracle as O
+
+    grid = grid_of(2048) if L == 2048 else osp.interleaved_grid(L)  # synthesis needs no conditioning
+    rng = np.random.default_rng(L)
+    flm = rng.standard_normal(L * L) + 1j * rng.standard_normal(L * L)
+    s = osp.inverse_sht_batch(flm[None, :], grid)[0]
+    ref = O.inverse_rings(flm, grid.thetas, rings)
+    for k in rings:
+        got = s[k * k:(k + 1) ** 2]
+        assert np.abs(got - ref[k]).max() <= 1e-11 * max(1.0, np.abs(ref[k]).max()), k

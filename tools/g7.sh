@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -q -m gpu -x -k "large_L or legendre or gridopt or real" > gpurun_out/pytest_gpu_a.txt 2>&1; tail -5 gpurun_out/pytest_gpu_a.txt
+timeout 900 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.txt 2>&1; tail -5 gpurun_out/pytest_gpu.txt
+timeout 600 python bench.py --config 4 --steps 3 --warmup 3 --no-cpu > gpurun_out/bench4.json 2> gpurun_out/bench4.err; tail -1 gpurun_out/bench4.json; tail -3 gpurun_out/bench4.err
