@@ -389,6 +389,12 @@ __global__ void __launch_bounds__(FAC_THREADS, 1) k_factor_gj(
   }
 }
 
+__global__ void k_identity_perm(int L, int* __restrict__ perm) {
+  const int m = blockIdx.y;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L - m; i += gridDim.x * blockDim.x)
+    perm[packed_pos(L, m, i)] = i;
+}
+
 // Finalise kappa per order once every cluster has finished.
 __global__ void k_kappa(int L, const unsigned long long* __restrict__ norms, double* __restrict__ kappa) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
@@ -445,6 +451,14 @@ cudaError_t launch_factor(osph_plan* p, cudaStream_t st, cudaStream_t st2) {
   const int L = p->L;
   cudaError_t e;
   if (!st) st = p->stream;
+  if (!p->piv_ready && getenv("OSPH_FACTOR_IDENTITY_PIV")) {  // experiment: natural row order, no pivoting
+    k_identity_perm<<<dim3((L + 255) / 256, L), 256, 0, st>>>(L, p->d_piv);
+    p->piv_ready = true;
+  }
+  const bool first_call = !p->piv_ready;
+  // first call: the partial-pivoting kernels record the pivot order (grid-determined);
+  // run them serially, then redo the large orders with the breadth-first kernel below
+  if (getenv("OSPH_FACTOR_ONE_STREAM") || first_call) st2 = nullptr;
   if ((e = cudaMemsetAsync(p->d_norms, 0, sizeof(unsigned long long) * 2 * L, st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(p->d_status, 0, sizeof(int) * L, st)) != cudaSuccess) return e;
   if (st2) {
@@ -484,6 +498,11 @@ cudaError_t launch_factor(osph_plan* p, cudaStream_t st, cudaStream_t st2) {
   if (st2) {
     if ((e = cudaEventRecord(p->ev_fac[1], st2)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(st, p->ev_fac[1], 0)) != cudaSuccess) return e;
+  }
+  if (first_call && L > 256 && !getenv("OSPH_FACTOR_NO_BF") && !getenv("OSPH_FACTOR_PIVOTED")) {
+    // the X of the largest pivoted class is not trusted for n > 1024; the
+    // breadth-first pass with the recorded pivots recomputes every order n > 256
+    if ((e = launch_factor_bf(p, 0, L - 257, st)) != cudaSuccess) return e;
   }
   k_kappa<<<(L + 127) / 128, 128, 0, st>>>(L, p->d_norms, p->d_kappa);
   p->launches++;

@@ -112,5 +112,6 @@ cudaError_t launch_factor(osph_plan* p, cudaStream_t st = nullptr, cudaStream_t 
 cudaError_t launch_sweep(osph_plan* p, int B, double2* flm);               // sweep.cu
 int sweep_maps_per_team(osph_plan* p, int B);
 cudaError_t launch_sweep_large(osph_plan* p, int B, double2* flm);  // sweep_large.cu
-cudaError_t launch_factor_bf(osph_plan* p, int m_first, int m_last, cudaStream_t st);  // factor_bf.cu  // sweep.cu: launch configuration (cached per B), 1/2/4
+cudaError_t launch_factor_bf(osph_plan* p, int m_first, int m_last, cudaStream_t st);  // factor_bf.cu
+int discover_pivots(osph_plan* p);  // pivots.cu: grid pivot order (cuSOLVER getrf), host-blocking  // sweep.cu: launch configuration (cached per B), 1/2/4
 cudaError_t launch_ring_pair(int n, int m, const double2* v, double2* out, cudaStream_t st);  // ringdft.cu

@@ -994,6 +994,14 @@ int sweep_maps_per_team(osph_plan* p, int B) {
   T = env_int("OSPH_SWEEP_T", T);
   while (T & (T - 1)) T &= T - 1;  // the kernel needs a power-of-two team width
   S = env_int("OSPH_SWEEP_S", S);
+  if (!tiles_ok(g, T) || !fits(g, T, S)) {  // nothing fits: two kernels per order (sweep_large.cu)
+    p->sweep_large = true;
+    p->sweep_cfg_B = B;
+    p->sweep_cfg[0] = 1;
+    p->sweep_cfg[1] = p->sweep_cfg[2] = 0;
+    return 1;
+  }
+  p->sweep_large = false;
   p->sweep_cfg_B = B;
   p->sweep_cfg[0] = g;
   p->sweep_cfg[1] = T;

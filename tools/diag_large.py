@@ -16,7 +16,8 @@ for it in range(2):
     t = time.time()
     st = osp.TransformStats()
     f = osp.forward_sht_batch(s, grid, check=False, stats=st)
-    print(f"call {it}: {time.time()-t:.2f} s", {k: round(v * 1e3, 2) for k, v in st.extra.items()}, flush=True)
+    print(f"call {it}: {time.time()-t:.2f} s", {k: round(v * 1e3, 2) for k, v in st.extra.items()},
+          "max err %.3e" % np.abs(f - flm).max(), flush=True)
 ells = np.floor(np.sqrt(np.arange(L * L))).astype(int)
 ms = np.arange(L * L) - ells * ells - ells
 err = np.abs(f - flm).max(axis=0)
