@@ -34,6 +34,17 @@ __device__ __forceinline__ void bf_atomic_max_pos(unsigned long long* addr, doub
   atomicMax(addr, (unsigned long long)__double_as_longlong(v));
 }
 
+__device__ __forceinline__ uint32_t bf_smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bf_cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(bf_smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void bf_cp_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// E panels keep an even column stride so 16-byte async copies stay aligned.
+__host__ __device__ __forceinline__ int bf_lde(int n) { return (n + 1) & ~1; }
+
 // Work item lookup: order index within the launch from a prefix table of
 // per-order item counts (binary search; pre[0] = 0, pre[cnt] = total).
 __device__ __forceinline__ int bf_find(const int* __restrict__ pre, int cnt, int item) {
@@ -166,11 +177,14 @@ __global__ void __launch_bounds__(BF_THREADS) k_bf_panel(int L, int m_first, int
                                                          double* __restrict__ ainv, const double* __restrict__ dbuf,
                                                          double* __restrict__ ebuf, const int64_t* __restrict__ bf_off) {
   extern __shared__ double bf_sm[];
-  double(*As)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm);
-  double(*Ds)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm + BF_T * BF_LDS);
-  const int oi = bf_find(pre, cnt, blockIdx.x);
+  double(*At)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm);                 // [k][row]
+  double(*Ds)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm + BF_NB * BF_LDS);  // [k][c]
+  __shared__ int s_oi;
+  if (threadIdx.x == 0) s_oi = bf_find(pre, cnt, blockIdx.x);
+  __syncthreads();
+  const int oi = s_oi;
   const int m = m_first + oi;
-  const int n = L - m;
+  const int n = L - m, lde = bf_lde(n);
   const int nb = min(BF_NB, n - j0);
   const int i0 = (blockIdx.x - __ldg(pre + oi)) * BF_T;
   double* A = ainv + __ldg(ainv_off + m);
@@ -178,43 +192,54 @@ __global__ void __launch_bounds__(BF_THREADS) k_bf_panel(int L, int m_first, int
   const int tid = threadIdx.x;
   for (int idx = tid; idx < BF_T * BF_NB; idx += BF_THREADS) {
     const int r = idx & (BF_T - 1), c = idx >> 6;
-    As[r][c] = (i0 + r < n && c < nb) ? __ldcg(A + (int64_t)(j0 + c) * n + i0 + r) : 0.0;
-    Ds[r][c] = __ldcg(Dg + idx);  // [c][r] order in memory: D[r][c] at c*NB + r
+    At[c][r] = (i0 + r < n && c < nb) ? __ldcg(A + (int64_t)(j0 + c) * n + i0 + r) : 0.0;
+    Ds[c][r] = __ldcg(Dg + idx);  // D[r][c] is stored at c * NB + r
   }
   __syncthreads();
-  double* E = ebuf + __ldg(bf_off + m);  // [col][n]
-  // thread -> row r (64), 16 column groups of 4
-  const int r = tid & (BF_T - 1), cg4 = tid >> 6;  // 4 groups x 16 columns
+  double* E = ebuf + __ldg(bf_off + m);  // [col][lde]
+  const int r = tid & (BF_T - 1), cg4 = tid >> 6;  // row r, columns cg4*16 .. +16
   const int gi = i0 + r;
   const bool inJ = gi >= j0 && gi < j0 + nb;
-  for (int c = cg4 * 16; c < cg4 * 16 + 16; ++c) {
-    if (c >= nb || gi >= n) continue;
-    double v;
-    if (inJ) {
-      v = Ds[gi - j0][c] - ((gi - j0 == c) ? 1.0 : 0.0);
-    } else {
-      double s = 0.0;
-#pragma unroll 8
-      for (int k = 0; k < BF_NB; ++k) s = fma(As[r][k], Ds[k][c], s);
-      v = -s;
+  double acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+  if (!inJ) {
+#pragma unroll 4
+    for (int k = 0; k < BF_NB; ++k) {
+      const double a = At[k][r];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc[q] = fma(a, Ds[cg4 * 16 + q][k], acc[q]);
     }
-    E[(int64_t)c * n + gi] = v;
-    A[(int64_t)(j0 + c) * n + gi] = v + ((inJ && gi - j0 == c) ? 1.0 : 0.0);
+  }
+  if (gi < n) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int c = cg4 * 16 + q;
+      if (c >= nb) continue;
+      const double v = inJ ? Ds[c][gi - j0] - ((gi - j0 == c) ? 1.0 : 0.0) : -acc[q];
+      E[(int64_t)c * lde + gi] = v;
+      A[(int64_t)(j0 + c) * n + gi] = v + ((inJ && gi - j0 == c) ? 1.0 : 0.0);
+    }
   }
 }
 
 // ---- 2c. A[I, K] += E[I, :] R[:, K] for every 64 x 64 tile outside column block J.
-__global__ void __launch_bounds__(BF_THREADS, 2) k_bf_update(int L, int m_first, int j0, const int* __restrict__ pre,
+// E and R are staged by 16-byte async copies (k-major / column-major in smem,
+// matching their global layouts) while the C fragments load from global.
+__global__ void __launch_bounds__(BF_THREADS, 3) k_bf_update(int L, int m_first, int j0, const int* __restrict__ pre,
                                                              int cnt, const int64_t* __restrict__ ainv_off,
                                                              double* __restrict__ ainv, const double* __restrict__ ebuf,
                                                              const double* __restrict__ rbuf,
                                                              const int64_t* __restrict__ bf_off) {
-  extern __shared__ double bf_sm[];
-  double(*Es)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm);              // [row][k]
-  double(*Rs)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm + BF_T * BF_LDS);  // [k][col]
-  const int oi = bf_find(pre, cnt, blockIdx.x);
+  extern __shared__ __align__(16) double bf_sm[];
+  double(*Et)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm);                 // [k][row]
+  double(*Rt)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm + BF_NB * BF_LDS);  // [col][k]
+  __shared__ int s_oi;
+  if (threadIdx.x == 0) s_oi = bf_find(pre, cnt, blockIdx.x);
+  __syncthreads();
+  const int oi = s_oi;
   const int m = m_first + oi;
-  const int n = L - m;
+  const int n = L - m, lde = bf_lde(n);
   const int nb = min(BF_NB, n - j0);
   const int nt = (n + BF_T - 1) / BF_T;
   const int local = blockIdx.x - __ldg(pre + oi);
@@ -226,10 +251,20 @@ __global__ void __launch_bounds__(BF_THREADS, 2) k_bf_update(int L, int m_first,
   const double* E = ebuf + __ldg(bf_off + m);
   const double* R = rbuf + __ldg(bf_off + m);
   const int tid = threadIdx.x;
-  for (int idx = tid; idx < BF_T * BF_NB; idx += BF_THREADS) {
-    const int a = idx & 63, b = idx >> 6;
-    Es[a][b] = (i0 + a < n && b < nb) ? __ldcg(E + (int64_t)b * n + i0 + a) : 0.0;  // row a, k b
-    Rs[a][b] = (c0 + b < n) ? __ldcg(R + (int64_t)(c0 + b) * BF_NB + a) : 0.0;     // k a, col b
+  // async staging: 64 x 64 doubles each = 2048 16-byte chunks, 8 per thread per operand
+  for (int idx = tid; idx < BF_T * BF_NB / 2; idx += BF_THREADS) {
+    const int k = idx >> 5, r2 = (idx & 31) * 2;  // E: column k, rows r2, r2+1
+    if (k < nb && i0 + r2 + 1 < lde) bf_cp16(&Et[k][r2], E + (int64_t)k * lde + i0 + r2);
+    else {
+      Et[k][r2] = 0.0;
+      Et[k][r2 + 1] = 0.0;
+    }
+    const int c = idx >> 5, k2 = (idx & 31) * 2;  // R: column c0 + c, k2, k2+1
+    if (c0 + c < n) bf_cp16(&Rt[c][k2], R + (int64_t)(c0 + c) * BF_NB + k2);
+    else {
+      Rt[c][k2] = 0.0;
+      Rt[c][k2 + 1] = 0.0;
+    }
   }
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -243,14 +278,16 @@ __global__ void __launch_bounds__(BF_THREADS, 2) k_bf_update(int L, int m_first,
       acc[i][j][0] = (row < n && col < n) ? __ldcg(A + (int64_t)col * n + row) : 0.0;
       acc[i][j][1] = (row < n && col + 1 < n) ? __ldcg(A + (int64_t)(col + 1) * n + row) : 0.0;
     }
+  bf_cp_wait_all();
   __syncthreads();
+  // rows of E beyond n (padding) are zero in E only if i0 + r < n: mask them here
 #pragma unroll 4
   for (int k0 = 0; k0 < BF_NB; k0 += 4) {
     double a[4], b[2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = Es[wr + 8 * i + g][k0 + t];
+    for (int i = 0; i < 4; ++i) a[i] = Et[k0 + t][wr + 8 * i + g];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) b[j] = Rs[k0 + t][wc + 8 * j + g];
+    for (int j = 0; j < 2; ++j) b[j] = Rt[wc + 8 * j + g][k0 + t];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -351,7 +388,7 @@ cudaError_t launch_factor_bf(osph_plan* p, int m_first, int m_last, cudaStream_t
       return e;
     // E and R panels: NB x n doubles per order; D: NB^2 per order
     std::vector<int64_t> off(L + 1, 0);
-    for (int m = 0; m < L; ++m) off[m + 1] = off[m] + ((m >= m_first && m <= m_last) ? (int64_t)BF_NB * (L - m) : 0);
+    for (int m = 0; m < L; ++m) off[m + 1] = off[m] + ((m >= m_first && m <= m_last) ? (int64_t)BF_NB * bf_lde(L - m) : 0);
     cudaFree(p->d_bf_off);
     cudaFree(p->d_bf_e);
     cudaFree(p->d_bf_r);
@@ -367,7 +404,7 @@ cudaError_t launch_factor_bf(osph_plan* p, int m_first, int m_last, cudaStream_t
     p->bf_m_first = m_first;
     p->bf_m_last = m_last;
   }
-  const size_t sm2 = sizeof(double) * 2 * BF_T * BF_LDS;
+  const size_t sm2 = sizeof(double) * 2 * BF_T * BF_LDS + 16;
   if ((e = cudaFuncSetAttribute(k_bf_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)
     return e;
   if ((e = cudaFuncSetAttribute(k_bf_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)

@@ -13,6 +13,8 @@
 // launch gap (~2-3 us) is small against it; nothing is pipelined across
 // orders.  One warp per matrix row (8 rows per block), lanes striding K,
 // maps in passes of SL_MAPS with all their columns accumulated at once.
+#include <cstdlib>
+
 #include "plan.cuh"
 
 #define SL_THREADS 256
@@ -140,17 +142,211 @@ __global__ void __launch_bounds__(SL_THREADS) k_sweep_corr(int L, int s, int B, 
   }
 }
 
+
+// Tile-coalesced variants: one block per 8-row tile, warps split the 32-column
+// chunks, lane = column: a lane reads its column's 8 rows as one contiguous
+// 64-byte run, so a warp consumes a whole 2 KB tile block per step.
+template <int MB>
+__global__ void __launch_bounds__(SL_THREADS) k_sweep_solve_t(int L, int s, int B, const double* __restrict__ xt,
+                                                              const int64_t* __restrict__ xt_off,
+                                                              const double* __restrict__ w_all,
+                                                              const double2* __restrict__ R,
+                                                              double2* __restrict__ xbuf, double2* __restrict__ flm) {
+  __shared__ double red[SL_THREADS / 32][8][4 * MB];
+  const int n = L - s, nrt = (n + 7) >> 3;
+  const int rt = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* X = xt + __ldg(xt_off + s);
+  const int64_t npos = (int64_t)L * (L + 1) / 2, p0 = packed_pos(L, s, 0);
+  const int nch = (n + 31) >> 5;
+  for (int b0 = blockIdx.y * MB; b0 < B; b0 += gridDim.y * MB) {
+    double acc[8][4 * MB];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int q = 0; q < 4 * MB; ++q) acc[r][q] = 0.0;
+    for (int c = warp; c < nch; c += SL_THREADS / 32) {
+      const int j = c * 32 + lane;
+      if (j < n) {
+        const double2* xp = reinterpret_cast<const double2*>(X + ((int64_t)c * nrt + rt) * 256 + lane * 8);
+        double xr[8];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const double2 v = __ldg(xp + h);
+          xr[2 * h] = v.x;
+          xr[2 * h + 1] = v.y;
+        }
+#pragma unroll
+        for (int q = 0; q < MB; ++q) {
+          if (b0 + q < B) {
+            const double2* rp = R + ((int64_t)(b0 + q) * npos + p0 + j) * 2;
+            const double2 gp = __ldg(rp), gn = __ldg(rp + 1);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              acc[r][4 * q + 0] = fma(xr[r], gp.x, acc[r][4 * q + 0]);
+              acc[r][4 * q + 1] = fma(xr[r], gp.y, acc[r][4 * q + 1]);
+              acc[r][4 * q + 2] = fma(xr[r], gn.x, acc[r][4 * q + 2]);
+              acc[r][4 * q + 3] = fma(xr[r], gn.y, acc[r][4 * q + 3]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int q = 0; q < 4 * MB; ++q) {
+        const double v = warp_sum(acc[r][q]);
+        if (lane == 0) red[warp][r][q] = v;
+      }
+    __syncthreads();
+    if (threadIdx.x < 8 * MB) {
+      const int r = threadIdx.x & 7, q = threadIdx.x >> 3;
+      const int row = rt * 8 + r;
+      if (row < n && b0 + q < B) {
+        double v[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int w = 0; w < SL_THREADS / 32; ++w)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] += red[w][r][4 * q + u];
+        const double w = __ldg(w_all + (int64_t)s * L + row);  // X[:, j*]: the late ring's column
+        const double2* rp = R + ((int64_t)(b0 + q) * npos + p0) * 2;
+        const double2 gp = rp[0], gn = rp[1];
+        const double sg = (s & 1) ? -1.0 : 1.0;
+        const double2 xp = make_double2(fma(w, gp.x, v[0]), fma(w, gp.y, v[1]));
+        const double2 xn = make_double2(sg * fma(w, gn.x, v[2]), sg * fma(w, gn.y, v[3]));
+        xbuf[((int64_t)(b0 + q) * 2 + 0) * L + row] = xp;
+        xbuf[((int64_t)(b0 + q) * 2 + 1) * L + row] = xn;
+        const int64_t ell = s + row;
+        double2* f = flm + (int64_t)(b0 + q) * L * L + ell * ell + ell;
+        f[s] = xp;
+        if (s > 0) f[-s] = xn;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int MB>
+__global__ void __launch_bounds__(SL_THREADS) k_sweep_corr_t(int L, int s, int B, const double* __restrict__ pbt,
+                                                             const int64_t* __restrict__ pb_off,
+                                                             const double2* __restrict__ xbuf,
+                                                             double2* __restrict__ R) {
+  __shared__ double red[SL_THREADS / 32][8][4 * MB];
+  const int n = L - s, nrtpb = (s + 7) >> 3;
+  const int rt = blockIdx.x;  // rings 8 rt .. 8 rt + 7 (< s)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* Pb = pbt + __ldg(pb_off + s);
+  const int64_t npos = (int64_t)L * (L + 1) / 2;
+  const int nch = (n + 31) >> 5;
+  for (int b0 = blockIdx.y * MB; b0 < B; b0 += gridDim.y * MB) {
+    double acc[8][4 * MB];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int q = 0; q < 4 * MB; ++q) acc[r][q] = 0.0;
+    for (int c = warp; c < nch; c += SL_THREADS / 32) {
+      const int l = c * 32 + lane;
+      if (l < n) {
+        const double2* pp = reinterpret_cast<const double2*>(Pb + ((int64_t)c * nrtpb + rt) * 256 + lane * 8);
+        double pr[8];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const double2 v = __ldg(pp + h);
+          pr[2 * h] = v.x;
+          pr[2 * h + 1] = v.y;
+        }
+#pragma unroll
+        for (int q = 0; q < MB; ++q) {
+          if (b0 + q < B) {
+            const double2 xp = __ldg(xbuf + ((int64_t)(b0 + q) * 2 + 0) * L + l);
+            const double2 xn = __ldg(xbuf + ((int64_t)(b0 + q) * 2 + 1) * L + l);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              acc[r][4 * q + 0] = fma(pr[r], xp.x, acc[r][4 * q + 0]);
+              acc[r][4 * q + 1] = fma(pr[r], xp.y, acc[r][4 * q + 1]);
+              acc[r][4 * q + 2] = fma(pr[r], xn.x, acc[r][4 * q + 2]);
+              acc[r][4 * q + 3] = fma(pr[r], xn.y, acc[r][4 * q + 3]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int q = 0; q < 4 * MB; ++q) {
+        const double v = warp_sum(acc[r][q]);
+        if (lane == 0) red[warp][r][q] = v;
+      }
+    __syncthreads();
+    if (threadIdx.x < 8 * MB) {
+      const int r = threadIdx.x & 7, q = threadIdx.x >> 3;
+      const int k = rt * 8 + r;
+      if (k < s && b0 + q < B) {
+        double v[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int w = 0; w < SL_THREADS / 32; ++w)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] += red[w][r][4 * q + u];
+        const double sg = (s & 1) ? -1.0 : 1.0;
+        const int nk = 2 * k + 1, rr = s % nk;
+        int tm, slot_p, slot_n;
+        if (rr == 0) {
+          tm = 0;
+          slot_p = slot_n = 0;
+        } else if (rr <= k) {
+          tm = rr;
+          slot_p = 0;
+          slot_n = 1;
+        } else {
+          tm = nk - rr;
+          slot_p = 1;
+          slot_n = 0;
+        }
+        double2* rp = R + ((int64_t)(b0 + q) * npos + packed_pos(L, tm, k - tm)) * 2;
+        if (slot_p == slot_n) {  // r == 0: both tones land in bin 0
+          rp[0].x -= v[0] + sg * v[2];
+          rp[0].y -= v[1] + sg * v[3];
+        } else {
+          rp[slot_p].x -= v[0];
+          rp[slot_p].y -= v[1];
+          rp[slot_n].x -= sg * v[2];
+          rp[slot_n].y -= sg * v[3];
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // R must be in the plain [map][pos][+-] layout (maps per team 1, lgG = 0).
 cudaError_t launch_sweep_large(osph_plan* p, int B, double2* flm) {
   const int L = p->L;
-  const int ymaps = (B + SL_MAPS - 1) / SL_MAPS;
+  const bool rowwise = getenv("OSPH_SWEEP_ROWWISE") != nullptr;  // the first (warp-per-row) variant
+  const int mb = B >= 2 ? 2 : 1;
+  const int ymaps = (B + (rowwise ? SL_MAPS : mb) - 1) / (rowwise ? SL_MAPS : mb);
   for (int s = L - 1; s >= 0; --s) {
     const int n = L - s;
-    k_sweep_solve<<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_xt, p->d_xt_off, p->d_w,
-                                                                        p->d_r, p->d_xbuf, flm);
-    if (s >= 1)
-      k_sweep_corr<<<dim3((s + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_pbelow, p->d_pb_off,
-                                                                         p->d_xbuf, p->d_r);
+    if (rowwise) {
+      k_sweep_solve<<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_xt, p->d_xt_off, p->d_w,
+                                                                          p->d_r, p->d_xbuf, flm);
+      if (s >= 1)
+        k_sweep_corr<<<dim3((s + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_pbelow, p->d_pb_off,
+                                                                           p->d_xbuf, p->d_r);
+      continue;
+    }
+    if (mb == 2) {
+      k_sweep_solve_t<2><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_xt, p->d_xt_off,
+                                                                               p->d_w, p->d_r, p->d_xbuf, flm);
+      if (s >= 1)
+        k_sweep_corr_t<2><<<dim3((s + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_pbelow, p->d_pb_off,
+                                                                                p->d_xbuf, p->d_r);
+    } else {
+      k_sweep_solve_t<1><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_xt, p->d_xt_off,
+                                                                               p->d_w, p->d_r, p->d_xbuf, flm);
+      if (s >= 1)
+        k_sweep_corr_t<1><<<dim3((s + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_pbelow, p->d_pb_off,
+                                                                                p->d_xbuf, p->d_r);
+    }
   }
   p->launches += 2 * L - 1;
   return cudaGetLastError();
