@@ -442,6 +442,12 @@ static cudaError_t launch_class(osph_plan* p, int m_first, int m_last, int cs, c
   return e;
 }
 
+cudaError_t launch_kappa(osph_plan* p, cudaStream_t st) {
+  k_kappa<<<(p->L + 127) / 128, 128, 0, st>>>(p->L, p->d_norms, p->d_kappa);
+  p->launches++;
+  return cudaGetLastError();
+}
+
 // Orders are grouped by block size n = L - m; each group gets a kernel
 // instantiation whose register tile fits n and a cluster size that scales
 // the rank-NB update with n^2.  The largest class runs on `st`; the smaller

@@ -345,91 +345,93 @@ __global__ void __launch_bounds__(BF_THREADS) k_bf_epilogue(int L, int m_first, 
   }
 }
 
-// Host driver: orders m_first..m_last (all with n > 256), static pivots.
-cudaError_t launch_factor_bf(osph_plan* p, int m_first, int m_last, cudaStream_t st) {
+// ---- host side ------------------------------------------------------------
+
+// E / R panel storage of one order (doubles), for offset tables built by the plan.
+int64_t bf_panel_doubles(int n) { return (int64_t)BF_NB * bf_lde(n); }
+int64_t bf_diag_doubles(int orders) { return (int64_t)BF_NB * BF_NB * orders; }
+
+// Step tables of work items for orders m_first..m_last (built once per range).
+cudaError_t bf_prepare(osph_plan* p, int m_first, int m_last, BfRange* r) {
   const int L = p->L;
-  const int cnt_all = m_last - m_first + 1;
   const int nmax = L - m_first;
-  cudaError_t e;
-  if (p->bf_m_first != m_first || p->bf_m_last != m_last) {
-    // per-step prefix tables of panel (row-tile) and update (tile) work items
-    const int nsteps = (nmax + BF_NB - 1) / BF_NB;
-    std::vector<int> tab;
-    p->h_bf_step.assign(nsteps, {});
-    for (int sidx = 0; sidx < nsteps; ++sidx) {
-      const int j0 = sidx * BF_NB;
-      int cnt = 0;
-      for (int m = m_first; m <= m_last; ++m)
-        if (L - m > j0) cnt = m - m_first + 1;
-      auto& d = p->h_bf_step[sidx];
-      d.cnt = cnt;
-      d.pre_panel = (int)tab.size();
-      int acc = 0;
-      for (int o = 0; o <= cnt; ++o) {
-        tab.push_back(acc);
-        if (o < cnt) acc += (L - (m_first + o) + BF_T - 1) / BF_T;
-      }
-      d.n_panel = acc;
-      d.pre_upd = (int)tab.size();
-      acc = 0;
-      for (int o = 0; o <= cnt; ++o) {
-        tab.push_back(acc);
-        if (o < cnt) {
-          const int nt = (L - (m_first + o) + BF_T - 1) / BF_T;
-          acc += nt * (nt - 1);
-        }
-      }
-      d.n_upd = acc;
+  const int nsteps = (nmax + BF_NB - 1) / BF_NB;
+  std::vector<int> tab;
+  r->m_first = m_first;
+  r->m_last = m_last;
+  r->steps.assign(nsteps, {});
+  for (int sidx = 0; sidx < nsteps; ++sidx) {
+    const int j0 = sidx * BF_NB;
+    int cnt = 0;
+    for (int m = m_first; m <= m_last; ++m)
+      if (L - m > j0) cnt = m - m_first + 1;
+    auto& d = r->steps[sidx];
+    d.cnt = cnt;
+    d.pre_panel = (int)tab.size();
+    int acc = 0;
+    for (int o = 0; o <= cnt; ++o) {
+      tab.push_back(acc);
+      if (o < cnt) acc += (L - (m_first + o) + BF_T - 1) / BF_T;
     }
-    cudaFree(p->d_bf_tab);
-    p->d_bf_tab = nullptr;
-    if ((e = cudaMalloc(&p->d_bf_tab, sizeof(int) * tab.size())) != cudaSuccess) return e;
-    if ((e = cudaMemcpy(p->d_bf_tab, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
-      return e;
-    // E and R panels: NB x n doubles per order; D: NB^2 per order
-    std::vector<int64_t> off(L + 1, 0);
-    for (int m = 0; m < L; ++m) off[m + 1] = off[m] + ((m >= m_first && m <= m_last) ? (int64_t)BF_NB * bf_lde(L - m) : 0);
-    cudaFree(p->d_bf_off);
-    cudaFree(p->d_bf_e);
-    cudaFree(p->d_bf_r);
-    cudaFree(p->d_bf_d);
-    p->d_bf_off = nullptr;
-    p->d_bf_e = p->d_bf_r = p->d_bf_d = nullptr;
-    if ((e = cudaMalloc(&p->d_bf_off, sizeof(int64_t) * (L + 1))) != cudaSuccess) return e;
-    if ((e = cudaMemcpy(p->d_bf_off, off.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice)) != cudaSuccess)
-      return e;
-    if ((e = cudaMalloc(&p->d_bf_e, sizeof(double) * off[L])) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&p->d_bf_r, sizeof(double) * off[L])) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&p->d_bf_d, sizeof(double) * BF_NB * BF_NB * cnt_all)) != cudaSuccess) return e;
-    p->bf_m_first = m_first;
-    p->bf_m_last = m_last;
+    d.n_panel = acc;
+    d.pre_upd = (int)tab.size();
+    acc = 0;
+    for (int o = 0; o <= cnt; ++o) {
+      tab.push_back(acc);
+      if (o < cnt) {
+        const int nt = (L - (m_first + o) + BF_T - 1) / BF_T;
+        acc += nt * (nt - 1);
+      }
+    }
+    d.n_upd = acc;
   }
+  cudaError_t e;
+  cudaFree(r->d_tab);
+  r->d_tab = nullptr;
+  if ((e = cudaMalloc(&r->d_tab, sizeof(int) * tab.size())) != cudaSuccess) return e;
+  return cudaMemcpy(r->d_tab, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice);
+}
+
+// Factor orders r.m_first..r.m_last with the recorded pivot order, writing A/X,
+// Pb, the tiled X and the sweep constants at the given offset tables.
+cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffsets& o) {
+  const int L = p->L;
+  const int m_first = r.m_first;
+  const int cnt_all = r.m_last - r.m_first + 1;
+  cudaError_t e;
   const size_t sm2 = sizeof(double) * 2 * BF_T * BF_LDS + 16;
   if ((e = cudaFuncSetAttribute(k_bf_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)
     return e;
   if ((e = cudaFuncSetAttribute(k_bf_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)
     return e;
   k_bf_generate<<<dim3((L + BF_THREADS - 1) / BF_THREADS, cnt_all), BF_THREADS, 0, st>>>(
-      L, m_first, p->d_cos, p->d_rec, p->d_ls, p->d_pstart, p->d_piv, p->d_ainv_off, p->d_pb_off, p->d_ainv,
-      p->d_pbelow);
-  k_bf_colnorm<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, p->d_ainv_off, p->d_ainv, p->d_norms, 0);
+      L, m_first, p->d_cos, p->d_rec, p->d_ls, p->d_pstart, p->d_piv, o.ainv, o.pb, p->d_ainv, p->d_pbelow);
+  k_bf_colnorm<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, o.ainv, p->d_ainv, p->d_norms, 0);
   p->launches += 2;
-  for (size_t sidx = 0; sidx < p->h_bf_step.size(); ++sidx) {
-    const auto& d = p->h_bf_step[sidx];
+  for (size_t sidx = 0; sidx < r.steps.size(); ++sidx) {
+    const auto& d = r.steps[sidx];
     const int j0 = (int)sidx * BF_NB;
-    k_bf_diag<<<d.cnt, BF_THREADS, 0, st>>>(L, m_first, j0, p->d_ainv_off, p->d_ainv, p->d_bf_d, p->d_bf_r,
-                                            p->d_bf_off, p->d_status);
-    k_bf_panel<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, p->d_bf_tab + d.pre_panel, d.cnt, p->d_ainv_off,
-                                                 p->d_ainv, p->d_bf_d, p->d_bf_e, p->d_bf_off);
+    k_bf_diag<<<d.cnt, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_bf_r, o.bf,
+                                            p->d_status);
+    k_bf_panel<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_panel, d.cnt, o.ainv, p->d_ainv,
+                                                 p->d_bf_d, p->d_bf_e, o.bf);
     if (d.n_upd > 0)
-      k_bf_update<<<d.n_upd, BF_THREADS, sm2, st>>>(L, m_first, j0, p->d_bf_tab + d.pre_upd, d.cnt, p->d_ainv_off,
-                                                  p->d_ainv, p->d_bf_e, p->d_bf_r, p->d_bf_off);
+      k_bf_update<<<d.n_upd, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_upd, d.cnt, o.ainv, p->d_ainv,
+                                                  p->d_bf_e, p->d_bf_r, o.bf);
     p->launches += 3;
   }
-  k_bf_colnorm<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, p->d_ainv_off, p->d_ainv, p->d_norms, 1);
-  k_bf_epilogue<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, p->d_ainv_off, p->d_ainv, p->d_piv,
-                                                         p->d_xt_off, p->d_xt, p->d_pb_off, p->d_pbelow, p->d_u,
-                                                         p->d_w, p->d_beta, p->d_jstar);
+  k_bf_colnorm<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, o.ainv, p->d_ainv, p->d_norms, 1);
+  k_bf_epilogue<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, o.ainv, p->d_ainv, p->d_piv, o.xt, p->d_xt,
+                                                         o.pb, p->d_pbelow, p->d_u, p->d_w, p->d_beta, p->d_jstar);
   p->launches += 2;
   return cudaGetLastError();
+}
+
+// The non-windowed plan: every order with n > 256 (m <= L - 257), full offset tables.
+cudaError_t launch_factor_bf(osph_plan* p, int m_first, int m_last, cudaStream_t st) {
+  cudaError_t e;
+  if (p->bf_full.m_first != m_first || p->bf_full.m_last != m_last)
+    if ((e = bf_prepare(p, m_first, m_last, &p->bf_full)) != cudaSuccess) return e;
+  const BfOffsets o{p->d_ainv_off, p->d_xt_off, p->d_pb_off, p->d_bf_off};
+  return bf_run(p, p->bf_full, st, o);
 }

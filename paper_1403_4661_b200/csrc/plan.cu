@@ -53,7 +53,7 @@ static void plan_free(osph_plan* p) {
                   p->d_bluestein_rings, p->d_ainv_off, p->d_pb_off, p->d_ainv, p->d_pbelow, p->d_piv,
                   p->d_norms, p->d_kappa, p->d_status, p->d_jstar, p->d_beta, p->d_u, p->d_w, p->d_xt_off, p->d_xt, p->d_panel,
                   p->d_fpack, p->d_g, p->d_r,
-                  p->d_in, p->d_out, p->d_sw, p->d_xbuf, p->d_bf_tab, p->d_bf_off, p->d_bf_e, p->d_bf_r,
+                  p->d_in, p->d_out, p->d_sw, p->d_xbuf, p->d_bf_off, p->d_bf_e, p->d_bf_r,
                   p->d_bf_d};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -70,6 +70,7 @@ static void plan_free(osph_plan* p) {
   if (p->s_fac) cudaStreamDestroy(p->s_fac);
   cudaFree(p->d_z1);
   cudaFree(p->d_z2);
+  free_windows(p);
   for (cudaEvent_t& e : p->ev_fac)
     if (e) cudaEventDestroy(e);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
@@ -241,30 +242,10 @@ static int ensure_inverse(osph_plan* p) {
 static int ensure_forward(osph_plan* p) {
   if (p->fwd_ready) return OSPH_OK;
   const int L = p->L;
-  if (L > 2048) {
-    osph_set_error("forward transform supports L <= 2048 in this build");
-    return OSPH_ERR_ARG;
-  }
   const size_t B = p->max_batch;
-  p->h_ainv_off.assign(L + 1, 0);
-  p->h_pb_off.assign(L + 1, 0);
-  p->h_xt_off.assign(L + 1, 0);
-  for (int m = 0; m < L; ++m) {
-    const int64_t n = L - m;
-    p->h_ainv_off[m + 1] = p->h_ainv_off[m] + n * n;
-    p->h_pb_off[m + 1] = p->h_pb_off[m] + tile_size(m, (int)n);  // chunk-major 8-ring tiles
-    p->h_xt_off[m + 1] = p->h_xt_off[m] + tile_size((int)n, (int)n);  // chunk-major 8-row tiles
-  }
   cudaStream_t st = p->stream;
-  CUDA_TRY(upload(&p->d_ainv_off, p->h_ainv_off.data(), L + 1, st));
-  CUDA_TRY(upload(&p->d_pb_off, p->h_pb_off.data(), L + 1, st));
-  CUDA_TRY(upload(&p->d_xt_off, p->h_xt_off.data(), L + 1, st));
-  CUDA_TRY(dalloc(&p->d_ainv, (size_t)p->h_ainv_off[L]));
-  CUDA_TRY(dalloc(&p->d_pbelow, (size_t)p->h_pb_off[L]));
-  CUDA_TRY(dalloc(&p->d_xt, (size_t)p->h_xt_off[L]));
-  // padding of the tiled operands stays zero forever (the kernels write only real entries)
-  CUDA_TRY(cudaMemsetAsync(p->d_pbelow, 0, sizeof(double) * (size_t)p->h_pb_off[L], st));
-  CUDA_TRY(cudaMemsetAsync(p->d_xt, 0, sizeof(double) * (size_t)p->h_xt_off[L], st));
+  int rc;
+  if ((rc = alloc_factor_storage(p))) return rc;
   CUDA_TRY(dalloc(&p->d_piv, (size_t)L * (L + 1) / 2));
   CUDA_TRY(dalloc(&p->d_norms, (size_t)2 * L));
   CUDA_TRY(dalloc(&p->d_kappa, (size_t)L));
@@ -295,7 +276,7 @@ static int check_call(osph_plan* p, int B, const void* a, void* b, int kind) {
     return OSPH_ERR_ARG;
   }
   if (!p->dft_ok) {
-    osph_set_error("ring DFT length exceeds the in-shared-memory FFT (transforms need L <= 2048 in this build)");
+    osph_set_error("ring DFT length exceeds the two-CTA Bluestein FFT (transforms need L <= 4096)");
     return OSPH_ERR_ARG;
   }
   if (B < 1 || B > p->max_batch) {
@@ -433,7 +414,7 @@ static int forward_real(osph_plan* p, int B, const void* samples, void* flm, boo
   CUDA_TRY(cudaEventRecord(p->ev_start, st));
   CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
   CUDA_TRY(cudaEventRecord(p->ev[6], p->s_in));
-  CUDA_TRY(launch_factor(p, p->s_in, p->s_fac));
+  if (!p->windowed) CUDA_TRY(launch_factor(p, p->s_in, p->s_fac));
   CUDA_TRY(cudaEventRecord(p->ev[7], p->s_in));
   if (host) {
     CUDA_TRY(cudaMemcpyAsync(p->d_in, samples, bytes, cudaMemcpyHostToDevice, st));
@@ -446,7 +427,8 @@ static int forward_real(osph_plan* p, int B, const void* samples, void* flm, boo
   CUDA_TRY(cudaEventRecord(p->ev[5], st));
   CUDA_TRY(cudaStreamWaitEvent(st, p->ev[7], 0));
   CUDA_TRY(cudaEventRecord(p->ev[8], st));
-  CUDA_TRY(launch_sweep(p, Bp, p->d_z2));
+  if (p->windowed) CUDA_TRY(forward_windows(p, Bp, p->d_z2));
+  else CUDA_TRY(launch_sweep(p, Bp, p->d_z2));
   CUDA_TRY(cudaEventRecord(p->ev[9], st));
   k_unpair_flm<<<pair_grid(Bp, n), 256, 0, st>>>(B, L, p->d_z2, dst);
   CUDA_TRY(cudaGetLastError());
@@ -527,6 +509,22 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
   double2* out = host ? p->d_out : (double2*)flm;
   if (kind & OSPH_REAL) {
     if ((rc = forward_real(p, B, samples, flm, host))) return rc;
+  } else if (p->windowed) {
+    // factors do not fit at once: ring DFTs, then factor + sweep window by window
+    const double2* src = (const double2*)samples;
+    if (host) {
+      CUDA_TRY(cudaMemcpyAsync(p->d_in, samples, bytes, cudaMemcpyHostToDevice, st));
+      src = p->d_in;
+    }
+    CUDA_TRY(cudaEventRecord(p->ev[4], st));
+    CUDA_TRY(launch_ring_forward(p, B, src));
+    CUDA_TRY(cudaEventRecord(p->ev[5], st));
+    CUDA_TRY(cudaEventRecord(p->ev[6], st));
+    CUDA_TRY(cudaEventRecord(p->ev[7], st));
+    CUDA_TRY(cudaEventRecord(p->ev[8], st));
+    CUDA_TRY(forward_windows(p, B, out));
+    CUDA_TRY(cudaEventRecord(p->ev[9], st));
+    if (host) CUDA_TRY(cudaMemcpyAsync(flm, p->d_out, bytes, cudaMemcpyDeviceToHost, st));
   } else if (!host) {
     // the factorisation needs no data: it runs on a side stream beside the ring DFTs
     CUDA_TRY(cudaEventRecord(p->ev_start, st));
@@ -562,7 +560,7 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
     }
     CUDA_TRY(cudaEventRecord(p->ev[5], st));
   }
-  if (!(kind & OSPH_REAL)) {
+  if (!(kind & OSPH_REAL) && !p->windowed) {
     CUDA_TRY(cudaEventRecord(p->ev[8], st));
     CUDA_TRY(launch_sweep(p, B, out));
     CUDA_TRY(cudaEventRecord(p->ev[9], st));
@@ -576,6 +574,11 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
     cudaEventElapsedTime(&t01, p->ev[4], p->ev[5]);
     cudaEventElapsedTime(&t12, p->ev[6], p->ev[7]);
     cudaEventElapsedTime(&t23, p->ev[8], p->ev[9]);
+    if (p->windowed) {
+      window_times(p);
+      t12 = p->last_factor_ms;
+      t23 = p->last_sweep_ms;
+    }
     stats->factor_seconds = t12 * 1e-3;
     stats->sweep_seconds = t23 * 1e-3;
     stats->solve_seconds = (t12 + t23) * 1e-3;
@@ -666,6 +669,10 @@ extern "C" int osph_last_stage_times(const osph_plan* p, double* seconds) {
     if (i < 3 ? p->have_inv : p->have_fwd) {
       CUDA_TRY(cudaEventSynchronize(p->ev[pairs[i][1]]));
       CUDA_TRY(cudaEventElapsedTime(&ms, p->ev[pairs[i][0]], p->ev[pairs[i][1]]));
+      if (i >= 4 && p->windowed) {
+        window_times(const_cast<osph_plan*>(p));
+        ms = i == 4 ? p->last_factor_ms : p->last_sweep_ms;
+      }
     }
     seconds[i] = ms * 1e-3;
   }

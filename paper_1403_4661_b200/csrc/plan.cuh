@@ -5,6 +5,27 @@
 
 #include "common.cuh"
 
+struct BfStep {
+  int cnt = 0, pre_panel = 0, n_panel = 0, pre_upd = 0, n_upd = 0;
+};
+struct BfRange {  // work-item tables of one range of orders (factor_bf.cu)
+  int m_first = -1, m_last = -1;
+  std::vector<BfStep> steps;
+  int* d_tab = nullptr;
+};
+struct BfOffsets {  // per-order offsets (indexed by m) into the factor buffers
+  const int64_t* ainv;
+  const int64_t* xt;
+  const int64_t* pb;
+  const int64_t* bf;
+};
+struct FwdWindow {  // orders m_lo..m_hi, factored then swept together
+  int m_lo = 0, m_hi = 0;
+  BfRange bf;
+  int64_t* d_offs = nullptr;  // 4 x (L+1): ainv, xt, pb, bf offsets (window-relative)
+  cudaEvent_t ev[4] = {};     // factor start/end, sweep start/end
+};
+
 struct osph_plan {
   int L = 0;
   int device = 0;
@@ -65,17 +86,16 @@ struct osph_plan {
   bool sweep_large = false;      // L > 1024: two kernels per order (sweep_large.cu), plain R layout
   double2* d_xbuf = nullptr;     // sweep_large: x_s of every map [B][+-][L]
   bool inv_ready = false;        // inverse buffers allocated
-  // breadth-first factorisation of the orders with n > 256 (factor_bf.cu)
-  struct BfStep {
-    int cnt = 0, pre_panel = 0, n_panel = 0, pre_upd = 0, n_upd = 0;
-  };
-  int bf_m_first = -1, bf_m_last = -1;
-  std::vector<BfStep> h_bf_step;
-  int* d_bf_tab = nullptr;       // per-step prefix tables of work items
-  int64_t* d_bf_off = nullptr;   // [L+1] offsets of the E / R panels (NB x n per order)
+  // breadth-first factorisation (factor_bf.cu): orders with n > 256, or every order when windowed
+  BfRange bf_full;               // the non-windowed range (m <= L - 257)
+  int64_t* d_bf_off = nullptr;   // [L+1] offsets of the E / R panels (NB x lde(n) per order)
   double* d_bf_e = nullptr;
   double* d_bf_r = nullptr;
   double* d_bf_d = nullptr;      // NB x NB diagonal-block inverses
+  // windowed forward (window.cu): factor storage for all orders does not fit HBM
+  bool windowed = false;
+  std::vector<FwdWindow> windows;  // descending in m
+  float last_factor_ms = 0.f, last_sweep_ms = 0.f;
 
   // ---- per-call workspaces (sized for max_batch) ----
   double* d_fpack = nullptr;  // inverse: packed coefficients [pos(m,l)][4B]
@@ -113,5 +133,16 @@ cudaError_t launch_sweep(osph_plan* p, int B, double2* flm);               // sw
 int sweep_maps_per_team(osph_plan* p, int B);
 cudaError_t launch_sweep_large(osph_plan* p, int B, double2* flm);  // sweep_large.cu
 cudaError_t launch_factor_bf(osph_plan* p, int m_first, int m_last, cudaStream_t st);  // factor_bf.cu
-int discover_pivots(osph_plan* p);  // pivots.cu: grid pivot order (cuSOLVER getrf), host-blocking  // sweep.cu: launch configuration (cached per B), 1/2/4
+cudaError_t bf_prepare(osph_plan* p, int m_first, int m_last, BfRange* r);               // factor_bf.cu
+cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffsets& o); // factor_bf.cu
+int64_t bf_panel_doubles(int n);
+int64_t bf_diag_doubles(int orders);
+cudaError_t launch_sweep_large_range(osph_plan* p, int B, double2* flm, int s_hi, int s_lo, const int64_t* xt_off,
+                                     const int64_t* pb_off);  // sweep_large.cu
+int discover_pivots(osph_plan* p);
+int alloc_factor_storage(osph_plan* p);                        // window.cu
+void free_windows(osph_plan* p);                               // window.cu
+cudaError_t forward_windows(osph_plan* p, int B, double2* flm);  // window.cu: factor + sweep per window
+void window_times(osph_plan* p);                               // window.cu
+cudaError_t launch_kappa(osph_plan* p, cudaStream_t st);       // factor.cu  // pivots.cu: grid pivot order (cuSOLVER getrf), host-blocking  // sweep.cu: launch configuration (cached per B), 1/2/4
 cudaError_t launch_ring_pair(int n, int m, const double2* v, double2* out, cudaStream_t st);  // ringdft.cu

@@ -921,7 +921,7 @@ int sweep_maps_per_team(osph_plan* p, int B) {
   const size_t cap = 220 * 1024;
   const int KC = SWEEP_KC;
   if (p->sweep_cfg_B == B) return p->sweep_cfg[0];
-  if (L > 1024 || getenv("OSPH_SWEEP_LARGE")) {  // the right-hand sides no longer fit the persistent kernel's smem
+  if (L > 1024 || p->windowed || getenv("OSPH_SWEEP_LARGE")) {  // the right-hand sides no longer fit the persistent kernel's smem
     p->sweep_large = true;
     p->sweep_cfg_B = B;
     p->sweep_cfg[0] = 1;

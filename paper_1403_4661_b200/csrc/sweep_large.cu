@@ -319,35 +319,40 @@ __global__ void __launch_bounds__(SL_THREADS) k_sweep_corr_t(int L, int s, int B
 }
 
 // R must be in the plain [map][pos][+-] layout (maps per team 1, lgG = 0).
-cudaError_t launch_sweep_large(osph_plan* p, int B, double2* flm) {
+cudaError_t launch_sweep_large_range(osph_plan* p, int B, double2* flm, int s_hi, int s_lo, const int64_t* xt_off,
+                                     const int64_t* pb_off) {
   const int L = p->L;
   const bool rowwise = getenv("OSPH_SWEEP_ROWWISE") != nullptr;  // the first (warp-per-row) variant
   const int mb = B >= 2 ? 2 : 1;
   const int ymaps = (B + (rowwise ? SL_MAPS : mb) - 1) / (rowwise ? SL_MAPS : mb);
-  for (int s = L - 1; s >= 0; --s) {
+  for (int s = s_hi; s >= s_lo; --s) {
     const int n = L - s;
     if (rowwise) {
-      k_sweep_solve<<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_xt, p->d_xt_off, p->d_w,
+      k_sweep_solve<<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_xt, xt_off, p->d_w,
                                                                           p->d_r, p->d_xbuf, flm);
       if (s >= 1)
-        k_sweep_corr<<<dim3((s + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_pbelow, p->d_pb_off,
+        k_sweep_corr<<<dim3((s + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_pbelow, pb_off,
                                                                            p->d_xbuf, p->d_r);
       continue;
     }
     if (mb == 2) {
-      k_sweep_solve_t<2><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_xt, p->d_xt_off,
-                                                                               p->d_w, p->d_r, p->d_xbuf, flm);
+      k_sweep_solve_t<2><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_xt, xt_off, p->d_w,
+                                                                               p->d_r, p->d_xbuf, flm);
       if (s >= 1)
-        k_sweep_corr_t<2><<<dim3((s + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_pbelow, p->d_pb_off,
+        k_sweep_corr_t<2><<<dim3((s + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_pbelow, pb_off,
                                                                                 p->d_xbuf, p->d_r);
     } else {
-      k_sweep_solve_t<1><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_xt, p->d_xt_off,
-                                                                               p->d_w, p->d_r, p->d_xbuf, flm);
+      k_sweep_solve_t<1><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_xt, xt_off, p->d_w,
+                                                                               p->d_r, p->d_xbuf, flm);
       if (s >= 1)
-        k_sweep_corr_t<1><<<dim3((s + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_pbelow, p->d_pb_off,
+        k_sweep_corr_t<1><<<dim3((s + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_pbelow, pb_off,
                                                                                 p->d_xbuf, p->d_r);
     }
+    p->launches += s >= 1 ? 2 : 1;
   }
-  p->launches += 2 * L - 1;
   return cudaGetLastError();
+}
+
+cudaError_t launch_sweep_large(osph_plan* p, int B, double2* flm) {
+  return launch_sweep_large_range(p, B, flm, p->L - 1, 0, p->d_xt_off, p->d_pb_off);
 }

@@ -1,0 +1,198 @@
+// window.cu -- storage of the per-order factors, and the windowed forward for
+// band limits whose factors do not fit in HBM at once.
+//
+// Per order m (n = L - m) the forward needs the explicit inverse X_m (n^2
+// doubles, plus its chunk-major tiled copy for the sweep) and the below-block
+// Pb_m (m n doubles): at L = 4096 that is ~2 x 183 + 92 GB, beyond one
+// B200's 180 GB.  The blocks are data independent, but the sweep consumes
+// them strictly in descending m, so the orders are cut into
+// windows [m_lo, m_hi] of bounded storage: factor the window (breadth-first,
+// factor_bf.cu), sweep its orders (sweep_large.cu), reuse the buffers for the
+// next window.  Results are identical to the non-windowed path (same kernels,
+// same per-order arithmetic); only the placement of the factors changes.
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "../../include/osph.h"
+#include "plan.cuh"
+
+void osph_set_error(const std::string& msg);
+
+static int64_t order_doubles(int L, int m) {
+  const int n = L - m;
+  return (int64_t)n * n + tile_size(n, n) + tile_size(m, n) + 2 * bf_panel_doubles(n);
+}
+
+#define W_TRY(expr)                                                                  \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess) {                                                         \
+      osph_set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));            \
+      return OSPH_ERR_CUDA;                                                          \
+    }                                                                                \
+  } while (0)
+
+// Offsets of the factor buffers for orders [m_first, m_last]; everything else 0.
+static void range_offsets(int L, int m_first, int m_last, std::vector<int64_t>& ainv, std::vector<int64_t>& xt,
+                          std::vector<int64_t>& pb, std::vector<int64_t>& bf, int64_t tot[4]) {
+  ainv.assign(L + 1, 0);
+  xt.assign(L + 1, 0);
+  pb.assign(L + 1, 0);
+  bf.assign(L + 1, 0);
+  int64_t a = 0, x = 0, q = 0, b = 0;
+  for (int m = m_first; m <= m_last; ++m) {
+    const int n = L - m;
+    ainv[m] = a;
+    xt[m] = x;
+    pb[m] = q;
+    bf[m] = b;
+    a += (int64_t)n * n;
+    x += tile_size(n, n);
+    q += tile_size(m, n);
+    b += bf_panel_doubles(n);
+  }
+  tot[0] = a;
+  tot[1] = x;
+  tot[2] = q;
+  tot[3] = b;
+}
+
+template <typename T>
+static cudaError_t dalloc_w(T** ptr, size_t count) {
+  return cudaMalloc((void**)ptr, sizeof(T) * std::max<size_t>(count, 1));
+}
+
+// Allocate the factor storage; decide whether the forward runs windowed.
+int alloc_factor_storage(osph_plan* p) {
+  const int L = p->L;
+  cudaStream_t st = p->stream;
+  int64_t full = 0;
+  for (int m = 0; m < L; ++m) full += order_doubles(L, m);
+  size_t free_b = 0, total_b = 0;
+  W_TRY(cudaMemGetInfo(&free_b, &total_b));
+  const char* env_budget = getenv("OSPH_WINDOW_GB");  // testing: force a window budget
+  const double budget_b = env_budget ? atof(env_budget) * 1e9 : 0.55 * (double)free_b;
+  p->windowed = (double)full * 8.0 > budget_b || env_budget != nullptr;
+  std::vector<int64_t> ao, xo, po, bo;
+  int64_t tot[4];
+  if (!p->windowed) {
+    // every order resident: offsets over all orders (the E/R panels only for the
+    // breadth-first orders n > 256; the others use factor_np.cu)
+    range_offsets(L, 0, L - 1, ao, xo, po, bo, tot);
+    int64_t bf_tot = 0;
+    for (int m = 0; m < L; ++m) {
+      bo[m] = bf_tot;
+      if (L - m > 256) bf_tot += bf_panel_doubles(L - m);
+    }
+    p->h_ainv_off = ao;
+    p->h_xt_off = xo;
+    p->h_pb_off = po;
+    p->h_ainv_off[L] = tot[0];
+    p->h_xt_off[L] = tot[1];
+    p->h_pb_off[L] = tot[2];
+    W_TRY(cudaMalloc(&p->d_ainv_off, sizeof(int64_t) * (L + 1)));
+    W_TRY(cudaMalloc(&p->d_xt_off, sizeof(int64_t) * (L + 1)));
+    W_TRY(cudaMalloc(&p->d_pb_off, sizeof(int64_t) * (L + 1)));
+    W_TRY(cudaMalloc(&p->d_bf_off, sizeof(int64_t) * (L + 1)));
+    W_TRY(cudaMemcpy(p->d_ainv_off, p->h_ainv_off.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice));
+    W_TRY(cudaMemcpy(p->d_xt_off, p->h_xt_off.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice));
+    W_TRY(cudaMemcpy(p->d_pb_off, p->h_pb_off.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice));
+    W_TRY(cudaMemcpy(p->d_bf_off, bo.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice));
+    W_TRY(dalloc_w(&p->d_ainv, (size_t)tot[0]));
+    W_TRY(dalloc_w(&p->d_xt, (size_t)tot[1]));
+    W_TRY(dalloc_w(&p->d_pbelow, (size_t)tot[2]));
+    W_TRY(dalloc_w(&p->d_bf_e, (size_t)bf_tot));
+    W_TRY(dalloc_w(&p->d_bf_r, (size_t)bf_tot));
+    W_TRY(dalloc_w(&p->d_bf_d, (size_t)bf_diag_doubles(std::max(1, L - 256))));
+    // padding of the tiled operands stays zero forever (the kernels write only real entries)
+    W_TRY(cudaMemsetAsync(p->d_pbelow, 0, sizeof(double) * (size_t)tot[2], st));
+    W_TRY(cudaMemsetAsync(p->d_xt, 0, sizeof(double) * (size_t)tot[1], st));
+    return OSPH_OK;
+  }
+  // windows in descending m, each within the budget
+  const double wbudget = budget_b / 8.0;
+  p->windows.clear();
+  int m_hi = L - 1;
+  while (m_hi >= 0) {
+    int m_lo = m_hi;
+    double acc = (double)order_doubles(L, m_hi);
+    while (m_lo > 0 && acc + (double)order_doubles(L, m_lo - 1) <= wbudget) acc += (double)order_doubles(L, --m_lo);
+    FwdWindow w;
+    w.m_lo = m_lo;
+    w.m_hi = m_hi;
+    p->windows.push_back(w);
+    m_hi = m_lo - 1;
+  }
+  int64_t mx[4] = {0, 0, 0, 0};
+  int max_orders = 1;
+  for (FwdWindow& w : p->windows) {
+    range_offsets(L, w.m_lo, w.m_hi, ao, xo, po, bo, tot);
+    for (int i = 0; i < 4; ++i) mx[i] = std::max(mx[i], tot[i]);
+    max_orders = std::max(max_orders, w.m_hi - w.m_lo + 1);
+    W_TRY(cudaMalloc(&w.d_offs, sizeof(int64_t) * 4 * (L + 1)));
+    W_TRY(cudaMemcpy(w.d_offs, ao.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice));
+    W_TRY(cudaMemcpy(w.d_offs + (L + 1), xo.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice));
+    W_TRY(cudaMemcpy(w.d_offs + 2 * (L + 1), po.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice));
+    W_TRY(cudaMemcpy(w.d_offs + 3 * (L + 1), bo.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice));
+    if (bf_prepare(p, w.m_lo, w.m_hi, &w.bf) != cudaSuccess) {
+      osph_set_error("window work tables");
+      return OSPH_ERR_CUDA;
+    }
+    for (cudaEvent_t& e : w.ev) W_TRY(cudaEventCreate(&e));
+  }
+  W_TRY(dalloc_w(&p->d_ainv, (size_t)mx[0]));
+  W_TRY(dalloc_w(&p->d_xt, (size_t)mx[1]));
+  W_TRY(dalloc_w(&p->d_pbelow, (size_t)mx[2]));
+  W_TRY(dalloc_w(&p->d_bf_e, (size_t)mx[3]));
+  W_TRY(dalloc_w(&p->d_bf_r, (size_t)mx[3]));
+  W_TRY(dalloc_w(&p->d_bf_d, (size_t)bf_diag_doubles(max_orders)));
+  return OSPH_OK;
+}
+
+void free_windows(osph_plan* p) {
+  for (FwdWindow& w : p->windows) {
+    cudaFree(w.d_offs);
+    cudaFree(w.bf.d_tab);
+    for (cudaEvent_t& e : w.ev)
+      if (e) cudaEventDestroy(e);
+  }
+  p->windows.clear();
+  cudaFree(p->bf_full.d_tab);
+  p->bf_full.d_tab = nullptr;
+}
+
+// Factor + sweep of every window on the plan stream (the right-hand sides R
+// are already in place); zero-fills the norms/status first like launch_factor.
+cudaError_t forward_windows(osph_plan* p, int B, double2* flm) {
+  const int L = p->L;
+  cudaStream_t st = p->stream;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(p->d_norms, 0, sizeof(unsigned long long) * 2 * L, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(p->d_status, 0, sizeof(int) * L, st)) != cudaSuccess) return e;
+  for (FwdWindow& w : p->windows) {
+    const BfOffsets o{w.d_offs, w.d_offs + (L + 1), w.d_offs + 2 * (L + 1), w.d_offs + 3 * (L + 1)};
+    if ((e = cudaEventRecord(w.ev[0], st)) != cudaSuccess) return e;
+    if ((e = bf_run(p, w.bf, st, o)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(w.ev[1], st)) != cudaSuccess) return e;
+    if ((e = launch_sweep_large_range(p, B, flm, w.m_hi, w.m_lo, o.xt, o.pb)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(w.ev[2], st)) != cudaSuccess) return e;
+  }
+  return launch_kappa(p, st);
+}
+
+// Device milliseconds of the last windowed forward: factor and sweep summed over windows.
+void window_times(osph_plan* p) {
+  float f = 0.f, s = 0.f;
+  for (FwdWindow& w : p->windows) {
+    float a = 0.f, b = 0.f;
+    cudaEventSynchronize(w.ev[2]);
+    cudaEventElapsedTime(&a, w.ev[0], w.ev[1]);
+    cudaEventElapsedTime(&b, w.ev[1], w.ev[2]);
+    f += a;
+    s += b;
+  }
+  p->last_factor_ms = f;
+  p->last_sweep_ms = s;
+}

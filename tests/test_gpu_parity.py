@@ -327,3 +327,28 @@ def test_large_L_inverse_rings_match_oracle(L, rings, grid_of):
     for k in rings:
         got = s[k * k:(k + 1) ** 2]
         assert np.abs(got - ref[k]).max() <= 1e-11 * max(1.0, np.abs(ref[k]).max()), k
+
+
+# ---------------------------------------------------------------------------
+# windowed forward (factor storage in windows of orders, window.cu)
+
+
+@pytest.mark.parametrize("L,B,gb", [(256, 3, 0.02), (512, 2, 0.15)])
+def test_windowed_forward_matches_resident(L, B, gb, grid_of, monkeypatch):
+    from paper_1403_4661_b200 import _lib
+
+    g = grid_of(L)
+    rng = np.random.default_rng(21)
+    flm = rng.standard_normal((B, L * L)) + 1j * rng.standard_normal((B, L * L))
+    s = osp.inverse_sht_batch(flm, g)
+    ref = osp.forward_sht_batch(s, g)
+    monkeypatch.setenv("OSPH_WINDOW_GB", str(gb))  # read when the plan allocates its factor storage
+    plan = osp.transform.Plan(g.thetas, B, 0)
+    out = np.empty_like(s)
+    for _ in range(2):  # first call discovers the pivots
+        st = plan.forward_raw(B, s.ctypes.data, out.ctypes.data, _lib.OSPH_HOST, True)
+    plan.close()
+    assert st.failed_order == -1
+    # n <= 256 orders use the breadth-first kernel here (factor_np.cu when resident): rounding differs
+    assert np.abs(out - ref).max() <= 1e-10
+    assert np.abs(out - flm).max() <= 1e-10
