@@ -44,6 +44,7 @@ CONFIGS = {
     2: dict(L=256, B=64, spectrum="cmb", real=False, grid="grid-L256-uniform-condmin.txt"),
     3: dict(L=512, B=256, spectrum="cmb", real=True, grid="grid-L512-uniform-condmin.txt"),
     4: dict(L=2048, B=1, spectrum="white", real=False, grid="grid-L2048-uniform-condmin.txt"),
+    5: dict(L=4096, B=8, spectrum="cmb", real=False, grid="grid-L4096-uniform-condmin.txt"),
 }
 
 

@@ -478,15 +478,16 @@ cudaError_t launch_factor(osph_plan* p, cudaStream_t st, cudaStream_t st2) {
   const Cls classes[] = {{1025, 2048, 16}, {513, 1024, 16}, {257, 512, 8}, {129, 256, 4}, {65, 128, 2}, {1, 64, 1}};
   const bool static_piv = p->piv_ready && !getenv("OSPH_FACTOR_PIVOTED");
   bool first = true;
-  if (static_piv && L > 256 && !getenv("OSPH_FACTOR_NO_BF")) {
-    // every order with n > 256 in one breadth-first blocked pass (factor_bf.cu)
-    if ((e = launch_factor_bf(p, 0, L - 257, st)) != cudaSuccess) return e;
+  const int nmin = p->bf_nmin;
+  if (static_piv && L > nmin && !getenv("OSPH_FACTOR_NO_BF")) {
+    // every order with n > bf_nmin in one breadth-first blocked pass (factor_bf.cu)
+    if ((e = launch_factor_bf(p, 0, L - nmin - 1, st)) != cudaSuccess) return e;
     first = false;
   }
   for (const Cls& c : classes) {
     const int nhi = std::min(c.nhi, L);
     if (nhi < c.nlo) continue;
-    if (!first && static_piv && nhi > 256 && !getenv("OSPH_FACTOR_NO_BF")) continue;  // done by the BF pass
+    if (!first && static_piv && c.nlo > nmin && !getenv("OSPH_FACTOR_NO_BF")) continue;  // done by the BF pass
     const int m_first = L - nhi, m_last = L - c.nlo;
     cudaStream_t s = (first || !st2) ? st : st2;
     first = false;
@@ -505,10 +506,10 @@ cudaError_t launch_factor(osph_plan* p, cudaStream_t st, cudaStream_t st2) {
     if ((e = cudaEventRecord(p->ev_fac[1], st2)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(st, p->ev_fac[1], 0)) != cudaSuccess) return e;
   }
-  if (first_call && L > 256 && !getenv("OSPH_FACTOR_NO_BF") && !getenv("OSPH_FACTOR_PIVOTED")) {
+  if (first_call && L > nmin && !getenv("OSPH_FACTOR_NO_BF") && !getenv("OSPH_FACTOR_PIVOTED")) {
     // the X of the largest pivoted class is not trusted for n > 1024; the
     // breadth-first pass with the recorded pivots recomputes every order n > 256
-    if ((e = launch_factor_bf(p, 0, L - 257, st)) != cudaSuccess) return e;
+    if ((e = launch_factor_bf(p, 0, L - nmin - 1, st)) != cudaSuccess) return e;
   }
   k_kappa<<<(L + 127) / 128, 128, 0, st>>>(L, p->d_norms, p->d_kappa);
   p->launches++;

@@ -122,53 +122,97 @@ __global__ void __launch_bounds__(BF_THREADS) k_bf_colnorm(int L, int m_first, c
 
 // ---- 2a. D = A[J, J]^{-1} (in-place Gauss-Jordan, no interchanges) and the
 // row block R = A[J, :] (the update's B operand, snapshotted before the update).
+// Grid (orders, column chunks of BF_RCHUNK): every block copies its chunk of R,
+// block y = 0 also inverts D.  The inversion keeps a 4 x 4 patch of D per
+// thread in registers; per pivot only the pivot row and column go through
+// shared memory (double-buffered: one barrier per pivot).
+#define BF_RCHUNK 256
 __global__ void __launch_bounds__(BF_THREADS) k_bf_diag(int L, int m_first, int j0, const int64_t* __restrict__ ainv_off,
                                                         const double* __restrict__ ainv, double* __restrict__ dbuf,
                                                         double* __restrict__ rbuf, const int64_t* __restrict__ bf_off,
                                                         int* __restrict__ status) {
-  __shared__ double D[BF_NB][BF_NB + 1];
+  __shared__ double s_row[2][BF_NB], s_col[2][BF_NB];
   const int m = m_first + blockIdx.x;
   const int n = L - m;
   const int nb = min(BF_NB, n - j0);
   const double* A = ainv + __ldg(ainv_off + m);
   const int tid = threadIdx.x;
-  for (int idx = tid; idx < BF_NB * BF_NB; idx += BF_THREADS) {
-    const int r = idx & (BF_NB - 1), c = idx >> 6;
-    D[r][c] = (r < nb && c < nb) ? __ldcg(A + (int64_t)(j0 + c) * n + j0 + r) : (r == c ? 1.0 : 0.0);
+  // R = A[J, :] for columns of this chunk, layout [col][NB]
+  {
+    double* R = rbuf + __ldg(bf_off + m);
+    const int c0 = blockIdx.y * BF_RCHUNK, c1 = min(n, c0 + BF_RCHUNK);
+    const int tot = (c1 - c0) * BF_NB;
+    // 8 independent loads in flight per thread before the stores
+    for (int base = 0; base < tot; base += 8 * BF_THREADS) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = base + u * BF_THREADS + tid;
+        const int r = idx & (BF_NB - 1), c = c0 + (idx >> 6);
+        v[u] = (idx < tot && r < nb) ? __ldcg(A + (int64_t)c * n + j0 + r) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = base + u * BF_THREADS + tid;
+        if (idx < tot) R[(int64_t)(c0 + (idx >> 6)) * BF_NB + (idx & (BF_NB - 1))] = v[u];
+      }
+    }
   }
-  // R = A[J, :], layout [col][NB]
-  double* R = rbuf + __ldg(bf_off + m);
-  for (int idx = tid; idx < n * BF_NB; idx += BF_THREADS) {
-    const int r = idx & (BF_NB - 1), c = idx >> 6;
-    R[idx] = r < nb ? __ldcg(A + (int64_t)c * n + j0 + r) : 0.0;
-  }
-  __syncthreads();
+  if (blockIdx.y != 0) return;
+  const int tr = tid >> 4, tc = tid & 15;  // patch rows 4tr.., columns 4tc..
+  double d[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = 4 * tr + i, c = 4 * tc + j;
+      d[i][j] = (r < nb && c < nb) ? __ldcg(A + (int64_t)(j0 + c) * n + j0 + r) : (r == c ? 1.0 : 0.0);
+    }
   bool bad = false;
   for (int p = 0; p < nb; ++p) {
-    const double piv = D[p][p];
+    const int buf = p & 1;
+    // static register indices only (a runtime index would spill d to local memory)
+    const int q = p & 3;
+    if ((p >> 2) == tr) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        s_row[buf][4 * tc + j] = q == 0 ? d[0][j] : q == 1 ? d[1][j] : q == 2 ? d[2][j] : d[3][j];
+    }
+    if ((p >> 2) == tc) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        s_col[buf][4 * tr + i] = q == 0 ? d[i][0] : q == 1 ? d[i][1] : q == 2 ? d[i][2] : d[i][3];
+    }
+    __syncthreads();
+    const double piv = s_row[buf][p];
     const double inv = 1.0 / piv;
     if (tid == 0 && (piv == 0.0 || !isfinite(piv))) bad = true;
-    double nv[16];
+    double pc[4], pr[4];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int idx = tid + q * BF_THREADS;
-      const int r = idx & (BF_NB - 1), c = idx >> 6;
-      double v = D[r][c];
-      if (r == p) v = (c == p) ? inv : v * inv;
-      else v = (c == p) ? -v * inv : fma(-D[r][p] * inv, D[p][c], v);
-      nv[q] = v;
-    }
-    __syncthreads();
+    for (int i = 0; i < 4; ++i) pc[i] = s_col[buf][4 * tr + i] * inv;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int idx = tid + q * BF_THREADS;
-      D[idx & (BF_NB - 1)][idx >> 6] = nv[q];
+    for (int j = 0; j < 4; ++j) pr[j] = s_row[buf][4 * tc + j];
+    // branch-free: rows r != p subtract pc * prow, row p scales by 1/piv,
+    // column p becomes -pc (its pivot entry 1/piv)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool rp = 4 * tr + i == p;
+      const double gi = rp ? 0.0 : pc[i];
+      const double si = rp ? inv : 1.0;
+      const double colv = rp ? inv : -pc[i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double v = fma(-gi, pr[j], si * d[i][j]);
+        d[i][j] = (4 * tc + j == p) ? colv : v;
+      }
     }
-    __syncthreads();
   }
   if (bad) atomicOr(status + m, 1);
-  double* Dg = dbuf + (size_t)blockIdx.x * BF_NB * BF_NB;
-  for (int idx = tid; idx < BF_NB * BF_NB; idx += BF_THREADS) Dg[idx] = D[idx & (BF_NB - 1)][idx >> 6];
+  double* Dg = dbuf + (size_t)blockIdx.x * BF_NB * BF_NB;  // D[r][c] at c * NB + r
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) Dg[(4 * tc + j) * BF_NB + 4 * tr + i] = d[i][j];
 }
 
 // ---- 2b. E = -A[I, J] D (E[J] = D - I) per 64-row tile; A[I, J] = E + I_J.
@@ -406,13 +450,16 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
     return e;
   k_bf_generate<<<dim3((L + BF_THREADS - 1) / BF_THREADS, cnt_all), BF_THREADS, 0, st>>>(
       L, m_first, p->d_cos, p->d_rec, p->d_ls, p->d_pstart, p->d_piv, o.ainv, o.pb, p->d_ainv, p->d_pbelow);
-  k_bf_colnorm<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, o.ainv, p->d_ainv, p->d_norms, 0);
-  p->launches += 2;
+  p->launches++;
+  if (p->need_norms) {  // ||A||_1 and ||X||_1 feed only the check=True condition estimate
+    k_bf_colnorm<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, o.ainv, p->d_ainv, p->d_norms, 0);
+    p->launches++;
+  }
   for (size_t sidx = 0; sidx < r.steps.size(); ++sidx) {
     const auto& d = r.steps[sidx];
     const int j0 = (int)sidx * BF_NB;
-    k_bf_diag<<<d.cnt, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_bf_r, o.bf,
-                                            p->d_status);
+    k_bf_diag<<<dim3(d.cnt, (L - m_first + BF_RCHUNK - 1) / BF_RCHUNK), BF_THREADS, 0, st>>>(
+        L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_bf_r, o.bf, p->d_status);
     k_bf_panel<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_panel, d.cnt, o.ainv, p->d_ainv,
                                                  p->d_bf_d, p->d_bf_e, o.bf);
     if (d.n_upd > 0)
@@ -420,10 +467,13 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
                                                   p->d_bf_e, p->d_bf_r, o.bf);
     p->launches += 3;
   }
-  k_bf_colnorm<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, o.ainv, p->d_ainv, p->d_norms, 1);
+  if (p->need_norms) {
+    k_bf_colnorm<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, o.ainv, p->d_ainv, p->d_norms, 1);
+    p->launches++;
+  }
   k_bf_epilogue<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, o.ainv, p->d_ainv, p->d_piv, o.xt, p->d_xt,
                                                          o.pb, p->d_pbelow, p->d_u, p->d_w, p->d_beta, p->d_jstar);
-  p->launches += 2;
+  p->launches++;
   return cudaGetLastError();
 }
 

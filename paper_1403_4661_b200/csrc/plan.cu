@@ -500,6 +500,7 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
   CUDA_TRY(cudaSetDevice(p->device));
   if ((rc = ensure_forward(p))) return rc;
   if (!p->piv_ready && !getenv("OSPH_PIVOTS_GJ") && (rc = discover_pivots(p))) return rc;
+  p->need_norms = check != 0;
   const bool host = !(kind & OSPH_DEVICE);
   if (host && (rc = ensure_io(p))) return rc;
   const int L = p->L;

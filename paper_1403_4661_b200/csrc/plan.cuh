@@ -87,7 +87,9 @@ struct osph_plan {
   double2* d_xbuf = nullptr;     // sweep_large: x_s of every map [B][+-][L]
   bool inv_ready = false;        // inverse buffers allocated
   // breadth-first factorisation (factor_bf.cu): orders with n > 256, or every order when windowed
-  BfRange bf_full;               // the non-windowed range (m <= L - 257)
+  BfRange bf_full;               // the non-windowed range (m <= L - bf_nmin - 1)
+  int bf_nmin = 0;               // orders with n > bf_nmin use factor_bf.cu, the rest factor_np.cu (OSPH_BF_NMIN)
+  bool need_norms = true;        // this call checks conditioning (check=True): factor kernels accumulate norms
   int64_t* d_bf_off = nullptr;   // [L+1] offsets of the E / R panels (NB x lde(n) per order)
   double* d_bf_e = nullptr;
   double* d_bf_r = nullptr;

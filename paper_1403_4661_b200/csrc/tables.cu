@@ -11,6 +11,8 @@
 //  * Bluestein chirps and kernel spectra for the odd-length ring DFTs, and the
 //    FFT twiddle table.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <numeric>
 
@@ -137,7 +139,7 @@ cudaError_t launch_legendre_block(osph_plan* p, int m, double* out, int64_t ld) 
 
 __global__ void k_stage_twiddles(double2* __restrict__ sw) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= OSPH_SW_GLOBAL / 2) return;  // i = (h - 1) + pos over h = 1, 2, 4, ..., 4096
+  if (i >= OSPH_SW_GLOBAL / 2 - 1) return;  // i = (h - 1) + pos over h = 1, 2, 4, ..., 4096 (i < 8191)
   const int lh = 31 - __clz(i + 1);
   const int h = 1 << lh, pos = i + 1 - h;
   double s, c;
@@ -224,27 +226,42 @@ static int next_pow2(int v) {
   return p;
 }
 
+// OSPH_DEBUG_SYNC=1: synchronise after every table kernel and name the failing one
+static cudaError_t dbg_sync(cudaStream_t st, const char* what) {
+  static const bool on = getenv("OSPH_DEBUG_SYNC") != nullptr;
+  if (!on) return cudaSuccess;
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) fprintf(stderr, "[osph] %s: %s\n", what, cudaGetErrorString(e));
+  return e;
+}
+
 cudaError_t launch_tables(osph_plan* p) {
   const int L = p->L;
   cudaError_t e;
   cudaStream_t st = p->stream;
+  if ((e = dbg_sync(st, "before tables")) != cudaSuccess) return e;
   {
     dim3 grid((L + 255) / 256, L);
     k_rec_table<<<grid, 256, 0, st>>>(L, p->d_rec);
+    if ((e = dbg_sync(st, "k_rec_table")) != cudaSuccess) return e;
   }
   {
     double* seed_mant = nullptr;
     if ((e = cudaMallocAsync(&seed_mant, sizeof(double) * (size_t)L * L, st)) != cudaSuccess) return e;
     k_seeds<<<(L + 127) / 128, 128, 0, st>>>(L, p->d_sin, seed_mant, p->d_ls);
+    if ((e = dbg_sync(st, "k_seeds")) != cudaSuccess) return e;
     dim3 grid((L + 127) / 128, L);
     k_start_table<<<grid, 128, 0, st>>>(L, p->d_cos, p->d_rec, seed_mant, p->d_ls, p->d_pstart);
+    if ((e = dbg_sync(st, "k_start_table")) != cudaSuccess) return e;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     cudaFreeAsync(seed_mant, st);
   }
   k_twiddles<<<(OSPH_TW_SIZE / 2 + 255) / 256, 256, 0, st>>>(p->d_tw);
   const int ndirect = std::min(L, (OSPH_DIRECT_MAX - 1) / 2 + 1);
   k_small_roots<<<ndirect, 64, 0, st>>>(ndirect, p->d_roots);
+  if ((e = dbg_sync(st, "k_twiddles/k_small_roots")) != cudaSuccess) return e;
   k_stage_twiddles<<<OSPH_SW_GLOBAL / 2 / 256, 256, 0, st>>>(p->d_sw);
+  if ((e = dbg_sync(st, "k_stage_twiddles")) != cudaSuccess) return e;
   const int nsmall = p->n_bluestein_rings - p->n_big_rings;
   if (nsmall > 0) {
     int maxN = 0;

@@ -81,10 +81,12 @@ int alloc_factor_storage(osph_plan* p) {
     // every order resident: offsets over all orders (the E/R panels only for the
     // breadth-first orders n > 256; the others use factor_np.cu)
     range_offsets(L, 0, L - 1, ao, xo, po, bo, tot);
+    const char* env_nmin = getenv("OSPH_BF_NMIN");  // breadth-first for n > bf_nmin (default: every order)
+    p->bf_nmin = env_nmin ? std::max(0, atoi(env_nmin)) : 0;
     int64_t bf_tot = 0;
     for (int m = 0; m < L; ++m) {
       bo[m] = bf_tot;
-      if (L - m > 256) bf_tot += bf_panel_doubles(L - m);
+      if (L - m > p->bf_nmin) bf_tot += bf_panel_doubles(L - m);
     }
     p->h_ainv_off = ao;
     p->h_xt_off = xo;
@@ -105,7 +107,7 @@ int alloc_factor_storage(osph_plan* p) {
     W_TRY(dalloc_w(&p->d_pbelow, (size_t)tot[2]));
     W_TRY(dalloc_w(&p->d_bf_e, (size_t)bf_tot));
     W_TRY(dalloc_w(&p->d_bf_r, (size_t)bf_tot));
-    W_TRY(dalloc_w(&p->d_bf_d, (size_t)bf_diag_doubles(std::max(1, L - 256))));
+    W_TRY(dalloc_w(&p->d_bf_d, (size_t)bf_diag_doubles(std::max(1, L - p->bf_nmin))));
     // padding of the tiled operands stays zero forever (the kernels write only real entries)
     W_TRY(cudaMemsetAsync(p->d_pbelow, 0, sizeof(double) * (size_t)tot[2], st));
     W_TRY(cudaMemsetAsync(p->d_xt, 0, sizeof(double) * (size_t)tot[1], st));
