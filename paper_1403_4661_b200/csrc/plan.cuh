@@ -85,6 +85,8 @@ struct osph_plan {
   int sweep_cfg[3] = {0, 0, 0};  // maps per team, cluster width, ring stages
   bool sweep_large = false;      // L > 1024: two kernels per order (sweep_large.cu), plain R layout
   double2* d_xbuf = nullptr;     // sweep_large: x_s of every map [B][+-][L]
+  double2* d_rres = nullptr;     // sweep_large refinement: residual [B][L][+-]
+  bool refine = false;           // one iterative-refinement step per order in sweep_large (L > 1024 default)
   bool inv_ready = false;        // inverse buffers allocated
   // breadth-first factorisation (factor_bf.cu): orders with n > 256, or every order when windowed
   BfRange bf_full;               // the non-windowed range (m <= L - bf_nmin - 1)

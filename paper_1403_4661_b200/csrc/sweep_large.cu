@@ -146,18 +146,20 @@ __global__ void __launch_bounds__(SL_THREADS) k_sweep_corr(int L, int s, int B, 
 // Tile-coalesced variants: one block per 8-row tile, warps split the 32-column
 // chunks, lane = column: a lane reads its column's 8 rows as one contiguous
 // 64-byte run, so a warp consumes a whole 2 KB tile block per step.
+// rhs of map b, ring offset j, slot: R[(b * npos + p0 + j) * 2 + slot]; accumulate: x += X rhs
+// (the refinement step, whose rhs is the residual in a scratch with npos = L, p0 = 0)
 template <int MB>
 __global__ void __launch_bounds__(SL_THREADS) k_sweep_solve_t(int L, int s, int B, const double* __restrict__ xt,
                                                               const int64_t* __restrict__ xt_off,
                                                               const double* __restrict__ w_all,
                                                               const double2* __restrict__ R,
-                                                              double2* __restrict__ xbuf, double2* __restrict__ flm) {
+                                                              double2* __restrict__ xbuf, double2* __restrict__ flm,
+                                                              int64_t npos, int64_t p0, int accumulate) {
   __shared__ double red[SL_THREADS / 32][8][4 * MB];
   const int n = L - s, nrt = (n + 7) >> 3;
   const int rt = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double* X = xt + __ldg(xt_off + s);
-  const int64_t npos = (int64_t)L * (L + 1) / 2, p0 = packed_pos(L, s, 0);
   const int nch = (n + 31) >> 5;
   for (int b0 = blockIdx.y * MB; b0 < B; b0 += gridDim.y * MB) {
     double acc[8][4 * MB];
@@ -212,10 +214,16 @@ __global__ void __launch_bounds__(SL_THREADS) k_sweep_solve_t(int L, int s, int 
         const double2* rp = R + ((int64_t)(b0 + q) * npos + p0) * 2;
         const double2 gp = rp[0], gn = rp[1];
         const double sg = (s & 1) ? -1.0 : 1.0;
-        const double2 xp = make_double2(fma(w, gp.x, v[0]), fma(w, gp.y, v[1]));
-        const double2 xn = make_double2(sg * fma(w, gn.x, v[2]), sg * fma(w, gn.y, v[3]));
-        xbuf[((int64_t)(b0 + q) * 2 + 0) * L + row] = xp;
-        xbuf[((int64_t)(b0 + q) * 2 + 1) * L + row] = xn;
+        double2 xp = make_double2(fma(w, gp.x, v[0]), fma(w, gp.y, v[1]));
+        double2 xn = make_double2(sg * fma(w, gn.x, v[2]), sg * fma(w, gn.y, v[3]));
+        double2* xb = xbuf + ((int64_t)(b0 + q) * 2) * L + row;
+        if (accumulate) {
+          const double2 op = xb[0], on = xb[L];
+          xp = make_double2(op.x + xp.x, op.y + xp.y);
+          xn = make_double2(on.x + xn.x, on.y + xn.y);
+        }
+        xb[0] = xp;
+        xb[L] = xn;
         const int64_t ell = s + row;
         double2* f = flm + (int64_t)(b0 + q) * L * L + ell * ell + ell;
         f[s] = xp;
@@ -224,6 +232,50 @@ __global__ void __launch_bounds__(SL_THREADS) k_sweep_solve_t(int L, int s, int 
     }
     __syncthreads();
   }
+}
+
+// One step of iterative refinement's residual (fixed precision): for ring
+// j = k - s of the block, r+ = g+ - A x+,  r- = g- - (-1)^s A x- (so that
+// (-1)^s X r- is the correction of x-), A[j][l] = 2pi Y_(s+l),s(theta_k)
+// generated by the recurrence from the start table.  One thread per ring.
+__global__ void __launch_bounds__(128) k_sweep_resid(int L, int s, int B, const double* __restrict__ costh,
+                                                     const double2* __restrict__ rec, const int* __restrict__ ls_tab,
+                                                     const double2* __restrict__ pstart,
+                                                     const double2* __restrict__ R, const double2* __restrict__ xbuf,
+                                                     double2* __restrict__ rres) {
+  const int n = L - s;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (j >= n || b >= B) return;
+  const int k = s + j;
+  const int64_t ts = (int64_t)s * L + k;
+  const int ls = __ldg(ls_tab + ts);
+  const double2 pp = __ldg(pstart + ts);
+  double p0 = pp.x, p1 = pp.y;
+  const double x = __ldg(costh + k);
+  const double2* recs = rec + packed_pos(L, s, 0);
+  const double2* xp = xbuf + ((int64_t)b * 2) * L;
+  const double2* xn = xp + L;
+  double apr = 0.0, api = 0.0, anr = 0.0, ani = 0.0;
+  for (int l = max(ls, s); l < L; ++l) {
+    const double a = OSPH_TWO_PI * p1;
+    const double2 vp = __ldg(xp + (l - s)), vn = __ldg(xn + (l - s));
+    apr = fma(a, vp.x, apr);
+    api = fma(a, vp.y, api);
+    anr = fma(a, vn.x, anr);
+    ani = fma(a, vn.y, ani);
+    const double2 ar = __ldg(recs + (l - s));
+    const double nxt = fma(x, p1, -ar.x * p0) * ar.y;
+    p0 = p1;
+    p1 = nxt;
+  }
+  const double sg = (s & 1) ? -1.0 : 1.0;
+  const int64_t npos = (int64_t)L * (L + 1) / 2;
+  const double2* rp = R + ((int64_t)b * npos + packed_pos(L, s, j)) * 2;
+  const double2 gp = rp[0], gn = rp[1];
+  double2* o = rres + ((int64_t)b * L + j) * 2;
+  o[0] = make_double2(gp.x - apr, gp.y - api);
+  o[1] = make_double2(gn.x - sg * anr, gn.y - sg * ani);
 }
 
 template <int MB>
@@ -335,20 +387,32 @@ cudaError_t launch_sweep_large_range(osph_plan* p, int B, double2* flm, int s_hi
                                                                            p->d_xbuf, p->d_r);
       continue;
     }
-    if (mb == 2) {
-      k_sweep_solve_t<2><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_xt, xt_off, p->d_w,
-                                                                               p->d_r, p->d_xbuf, flm);
-      if (s >= 1)
+    const int64_t npos = (int64_t)L * (L + 1) / 2, p0 = packed_pos(L, s, 0);
+    auto solve = [&](const double2* rhs, int64_t np, int64_t q0, int acc) {
+      if (mb == 2)
+        k_sweep_solve_t<2><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(
+            L, s, B, p->d_xt, xt_off, p->d_w, rhs, p->d_xbuf, flm, np, q0, acc);
+      else
+        k_sweep_solve_t<1><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(
+            L, s, B, p->d_xt, xt_off, p->d_w, rhs, p->d_xbuf, flm, np, q0, acc);
+      p->launches++;
+    };
+    solve(p->d_r, npos, p0, 0);
+    if (p->refine) {  // x += X (b - A x): one fixed-precision refinement step per order
+      k_sweep_resid<<<dim3((n + 127) / 128, B), 128, 0, p->stream>>>(L, s, B, p->d_cos, p->d_rec, p->d_ls,
+                                                                      p->d_pstart, p->d_r, p->d_xbuf, p->d_rres);
+      solve(p->d_rres, L, 0, 1);
+      p->launches++;
+    }
+    if (s >= 1) {
+      if (mb == 2)
         k_sweep_corr_t<2><<<dim3((s + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_pbelow, pb_off,
                                                                                 p->d_xbuf, p->d_r);
-    } else {
-      k_sweep_solve_t<1><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_xt, xt_off, p->d_w,
-                                                                               p->d_r, p->d_xbuf, flm);
-      if (s >= 1)
+      else
         k_sweep_corr_t<1><<<dim3((s + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_pbelow, pb_off,
                                                                                 p->d_xbuf, p->d_r);
+      p->launches++;
     }
-    p->launches += s >= 1 ? 2 : 1;
   }
   return cudaGetLastError();
 }
