@@ -47,6 +47,22 @@ __host__ __device__ __forceinline__ int bf_lde(int n) { return (n + 1) & ~1; }
 
 // Work item lookup: order index within the launch from a prefix table of
 // per-order item counts (binary search; pre[0] = 0, pre[cnt] = total).
+// Warp-cooperative variant (a full warp calls it): 32-ary search, <= 3 rounds
+// of one load per lane instead of ~11 dependent loads in one thread.
+__device__ __forceinline__ int bf_find_warp(const int* __restrict__ pre, int cnt, int item) {
+  const int lane = threadIdx.x & 31;
+  int lo = 0, hi = cnt;  // pre[lo] <= item < pre[hi]
+  while (hi - lo > 1) {
+    const int stride = (hi - lo + 31) >> 5;
+    const int idx = lo + lane * stride;
+    const bool ok = idx < hi && __ldg(pre + idx) <= item;
+    const unsigned mask = __ballot_sync(0xffffffffu, ok);  // lane 0 (idx = lo) is always set
+    lo += (31 - __clz(mask)) * stride;
+    hi = min(hi, lo + stride);
+  }
+  return lo;
+}
+
 __device__ __forceinline__ int bf_find(const int* __restrict__ pre, int cnt, int item) {
   int lo = 0, hi = cnt;  // pre[lo] <= item < pre[hi]
   while (hi - lo > 1) {
@@ -98,6 +114,40 @@ __global__ void __launch_bounds__(BF_THREADS) k_bf_generate(int L, int m_first, 
     }
     if (row >= 0) A[(int64_t)(l - m) * n + row] = v;
     else Pb[tile_index(k, l - m, nrtpb)] = v;
+  }
+}
+
+// A_m in natural ring order as chunk-major 8-ring tiles (the layout of X),
+// for the large-L sweep's iterative refinement: thread = ring offset j.
+__global__ void __launch_bounds__(BF_THREADS) k_bf_generate_at(int L, int m_first, const double* __restrict__ costh,
+                                                               const double2* __restrict__ rec,
+                                                               const int* __restrict__ ls_tab,
+                                                               const double2* __restrict__ pstart,
+                                                               const int64_t* __restrict__ at_off,
+                                                               double* __restrict__ at) {
+  const int m = m_first + blockIdx.y;
+  const int n = L - m;
+  const int j = blockIdx.x * BF_THREADS + threadIdx.x;
+  if (j >= n) return;
+  const int k = m + j;
+  double* At = at + __ldg(at_off + m);
+  const int nrt = (n + 7) >> 3;
+  const int64_t ts = (int64_t)m * L + k;
+  const int ls = __ldg(ls_tab + ts);
+  const double2 pp = __ldg(pstart + ts);
+  double p0 = pp.x, p1 = pp.y;
+  const double x = __ldg(costh + k);
+  const double2* recm = rec + packed_pos(L, m, 0);
+  for (int l = m; l < L; ++l) {
+    double v = 0.0;
+    if (l >= ls) {
+      v = OSPH_TWO_PI * p1;
+      const double2 ar = __ldg(recm + (l - m));
+      const double nxt = fma(x, p1, -ar.x * p0) * ar.y;
+      p0 = p1;
+      p1 = nxt;
+    }
+    At[tile_index(j, l - m, nrt)] = v;
   }
 }
 
@@ -224,7 +274,10 @@ __global__ void __launch_bounds__(BF_THREADS) k_bf_panel(int L, int m_first, int
   double(*At)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm);                 // [k][row]
   double(*Ds)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm + BF_NB * BF_LDS);  // [k][c]
   __shared__ int s_oi;
-  if (threadIdx.x == 0) s_oi = bf_find(pre, cnt, blockIdx.x);
+  if (threadIdx.x < 32) {
+    const int oi_w = bf_find_warp(pre, cnt, blockIdx.x);
+    if (threadIdx.x == 0) s_oi = oi_w;
+  }
   __syncthreads();
   const int oi = s_oi;
   const int m = m_first + oi;
@@ -279,7 +332,10 @@ __global__ void __launch_bounds__(BF_THREADS, 3) k_bf_update(int L, int m_first,
   double(*Et)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm);                 // [k][row]
   double(*Rt)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm + BF_NB * BF_LDS);  // [col][k]
   __shared__ int s_oi;
-  if (threadIdx.x == 0) s_oi = bf_find(pre, cnt, blockIdx.x);
+  if (threadIdx.x < 32) {
+    const int oi_w = bf_find_warp(pre, cnt, blockIdx.x);
+    if (threadIdx.x == 0) s_oi = oi_w;
+  }
   __syncthreads();
   const int oi = s_oi;
   const int m = m_first + oi;
@@ -450,6 +506,11 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
     return e;
   k_bf_generate<<<dim3((L + BF_THREADS - 1) / BF_THREADS, cnt_all), BF_THREADS, 0, st>>>(
       L, m_first, p->d_cos, p->d_rec, p->d_ls, p->d_pstart, p->d_piv, o.ainv, o.pb, p->d_ainv, p->d_pbelow);
+  if (p->d_at) {  // the blocks themselves for the sweep's refinement step, natural ring order
+    k_bf_generate_at<<<dim3((L + BF_THREADS - 1) / BF_THREADS, cnt_all), BF_THREADS, 0, st>>>(
+        L, m_first, p->d_cos, p->d_rec, p->d_ls, p->d_pstart, o.xt, p->d_at);
+    p->launches++;
+  }
   p->launches++;
   if (p->need_norms) {  // ||A||_1 and ||X||_1 feed only the check=True condition estimate
     k_bf_colnorm<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, o.ainv, p->d_ainv, p->d_norms, 0);

@@ -53,7 +53,7 @@ static void plan_free(osph_plan* p) {
                   p->d_bluestein_rings, p->d_ainv_off, p->d_pb_off, p->d_ainv, p->d_pbelow, p->d_piv,
                   p->d_norms, p->d_kappa, p->d_status, p->d_jstar, p->d_beta, p->d_u, p->d_w, p->d_xt_off, p->d_xt, p->d_panel,
                   p->d_fpack, p->d_g, p->d_r,
-                  p->d_in, p->d_out, p->d_sw, p->d_xbuf, p->d_rres, p->d_bf_off, p->d_bf_e, p->d_bf_r,
+                  p->d_in, p->d_out, p->d_sw, p->d_xbuf, p->d_rres, p->d_at, p->d_bf_off, p->d_bf_e, p->d_bf_r,
                   p->d_bf_d};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -258,10 +258,7 @@ static int ensure_forward(osph_plan* p) {
   CUDA_TRY(dalloc(&p->d_beta, (size_t)L));
   CUDA_TRY(dalloc(&p->d_xbuf, (size_t)2 * L * B));
   CUDA_TRY(dalloc(&p->d_rres, (size_t)2 * L * B));
-  {
-    const char* r = getenv("OSPH_REFINE");
-    p->refine = r ? atoi(r) != 0 : L > 1024;
-  }
+
   // [L][L] + 2: the sweep's bulk copies round their sizes up to 16 bytes
   CUDA_TRY(dalloc(&p->d_u, (size_t)L * L + 2));
   CUDA_TRY(dalloc(&p->d_w, (size_t)L * L + 2));

@@ -86,6 +86,7 @@ struct osph_plan {
   bool sweep_large = false;      // L > 1024: two kernels per order (sweep_large.cu), plain R layout
   double2* d_xbuf = nullptr;     // sweep_large: x_s of every map [B][+-][L]
   double2* d_rres = nullptr;     // sweep_large refinement: residual [B][L][+-]
+  double* d_at = nullptr;        // refinement: the blocks A_m themselves, tiled like X (offsets of X)
   bool refine = false;           // one iterative-refinement step per order in sweep_large (L > 1024 default)
   bool inv_ready = false;        // inverse buffers allocated
   // breadth-first factorisation (factor_bf.cu): orders with n > 256, or every order when windowed

@@ -370,6 +370,84 @@ __global__ void __launch_bounds__(SL_THREADS) k_sweep_corr_t(int L, int s, int B
   }
 }
 
+// Residual from the stored block A_s (chunk-major 8-ring tiles, natural ring
+// order, written by the factor's generate pass): one block per 8-ring tile,
+// the same coalesced pattern as k_sweep_corr_t.  r+ = g+ - A x+,
+// r- = g- - (-1)^s A x-.
+template <int MB>
+__global__ void __launch_bounds__(SL_THREADS) k_sweep_resid_t(int L, int s, int B, const double* __restrict__ at,
+                                                              const int64_t* __restrict__ at_off,
+                                                              const double2* __restrict__ R,
+                                                              const double2* __restrict__ xbuf,
+                                                              double2* __restrict__ rres) {
+  __shared__ double red[SL_THREADS / 32][8][4 * MB];
+  const int n = L - s, nrt = (n + 7) >> 3;
+  const int rt = blockIdx.x;  // rings s + 8 rt .. s + 8 rt + 7
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* A = at + __ldg(at_off + s);
+  const int64_t npos = (int64_t)L * (L + 1) / 2, p0 = packed_pos(L, s, 0);
+  const int nch = (n + 31) >> 5;
+  for (int b0 = blockIdx.y * MB; b0 < B; b0 += gridDim.y * MB) {
+    double acc[8][4 * MB];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int q = 0; q < 4 * MB; ++q) acc[r][q] = 0.0;
+    for (int c = warp; c < nch; c += SL_THREADS / 32) {
+      const int l = c * 32 + lane;
+      if (l < n) {
+        const double2* pp = reinterpret_cast<const double2*>(A + ((int64_t)c * nrt + rt) * 256 + lane * 8);
+        double ar[8];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const double2 v = __ldg(pp + h);
+          ar[2 * h] = v.x;
+          ar[2 * h + 1] = v.y;
+        }
+#pragma unroll
+        for (int q = 0; q < MB; ++q) {
+          if (b0 + q < B) {
+            const double2 xp = __ldg(xbuf + ((int64_t)(b0 + q) * 2 + 0) * L + l);
+            const double2 xn = __ldg(xbuf + ((int64_t)(b0 + q) * 2 + 1) * L + l);
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              acc[r][4 * q + 0] = fma(ar[r], xp.x, acc[r][4 * q + 0]);
+              acc[r][4 * q + 1] = fma(ar[r], xp.y, acc[r][4 * q + 1]);
+              acc[r][4 * q + 2] = fma(ar[r], xn.x, acc[r][4 * q + 2]);
+              acc[r][4 * q + 3] = fma(ar[r], xn.y, acc[r][4 * q + 3]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int q = 0; q < 4 * MB; ++q) {
+        const double v = warp_sum(acc[r][q]);
+        if (lane == 0) red[warp][r][q] = v;
+      }
+    __syncthreads();
+    if (threadIdx.x < 8 * MB) {
+      const int r = threadIdx.x & 7, q = threadIdx.x >> 3;
+      const int j = rt * 8 + r;
+      if (j < n && b0 + q < B) {
+        double v[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int w = 0; w < SL_THREADS / 32; ++w)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] += red[w][r][4 * q + u];
+        const double sg = (s & 1) ? -1.0 : 1.0;
+        const double2* rp = R + ((int64_t)(b0 + q) * npos + p0 + j) * 2;
+        const double2 gp = rp[0], gn = rp[1];
+        double2* o = rres + ((int64_t)(b0 + q) * L + j) * 2;
+        o[0] = make_double2(gp.x - v[0], gp.y - v[1]);
+        o[1] = make_double2(gn.x - sg * v[2], gn.y - sg * v[3]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // R must be in the plain [map][pos][+-] layout (maps per team 1, lgG = 0).
 cudaError_t launch_sweep_large_range(osph_plan* p, int B, double2* flm, int s_hi, int s_lo, const int64_t* xt_off,
                                      const int64_t* pb_off) {
@@ -399,8 +477,17 @@ cudaError_t launch_sweep_large_range(osph_plan* p, int B, double2* flm, int s_hi
     };
     solve(p->d_r, npos, p0, 0);
     if (p->refine) {  // x += X (b - A x): one fixed-precision refinement step per order
-      k_sweep_resid<<<dim3((n + 127) / 128, B), 128, 0, p->stream>>>(L, s, B, p->d_cos, p->d_rec, p->d_ls,
-                                                                      p->d_pstart, p->d_r, p->d_xbuf, p->d_rres);
+      if (p->d_at) {  // stored block (tiled like X)
+        if (mb == 2)
+          k_sweep_resid_t<2><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_at, xt_off, p->d_r,
+                                                                                   p->d_xbuf, p->d_rres);
+        else
+          k_sweep_resid_t<1><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_at, xt_off, p->d_r,
+                                                                                   p->d_xbuf, p->d_rres);
+      } else {
+        k_sweep_resid<<<dim3((n + 127) / 128, B), 128, 0, p->stream>>>(L, s, B, p->d_cos, p->d_rec, p->d_ls,
+                                                                        p->d_pstart, p->d_r, p->d_xbuf, p->d_rres);
+      }
       solve(p->d_rres, L, 0, 1);
       p->launches++;
     }

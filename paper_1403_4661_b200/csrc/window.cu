@@ -20,9 +20,9 @@
 
 void osph_set_error(const std::string& msg);
 
-static int64_t order_doubles(int L, int m) {
+static int64_t order_doubles(int L, int m, bool refine) {
   const int n = L - m;
-  return (int64_t)n * n + tile_size(n, n) + tile_size(m, n) + 2 * bf_panel_doubles(n);
+  return (int64_t)n * n + tile_size(n, n) * (refine ? 2 : 1) + tile_size(m, n) + 2 * bf_panel_doubles(n);
 }
 
 #define W_TRY(expr)                                                                  \
@@ -68,8 +68,13 @@ static cudaError_t dalloc_w(T** ptr, size_t count) {
 int alloc_factor_storage(osph_plan* p) {
   const int L = p->L;
   cudaStream_t st = p->stream;
+  {
+    const char* r = getenv("OSPH_REFINE");  // refinement step in the large-L sweep (default L > 1024)
+    p->refine = r ? atoi(r) != 0 : L > 1024;
+  }
+  const bool rf = p->refine;
   int64_t full = 0;
-  for (int m = 0; m < L; ++m) full += order_doubles(L, m);
+  for (int m = 0; m < L; ++m) full += order_doubles(L, m, rf);
   size_t free_b = 0, total_b = 0;
   W_TRY(cudaMemGetInfo(&free_b, &total_b));
   const char* env_budget = getenv("OSPH_WINDOW_GB");  // testing: force a window budget
@@ -104,6 +109,7 @@ int alloc_factor_storage(osph_plan* p) {
     W_TRY(cudaMemcpy(p->d_bf_off, bo.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice));
     W_TRY(dalloc_w(&p->d_ainv, (size_t)tot[0]));
     W_TRY(dalloc_w(&p->d_xt, (size_t)tot[1]));
+    if (rf) W_TRY(dalloc_w(&p->d_at, (size_t)tot[1]));
     W_TRY(dalloc_w(&p->d_pbelow, (size_t)tot[2]));
     W_TRY(dalloc_w(&p->d_bf_e, (size_t)bf_tot));
     W_TRY(dalloc_w(&p->d_bf_r, (size_t)bf_tot));
@@ -119,8 +125,9 @@ int alloc_factor_storage(osph_plan* p) {
   int m_hi = L - 1;
   while (m_hi >= 0) {
     int m_lo = m_hi;
-    double acc = (double)order_doubles(L, m_hi);
-    while (m_lo > 0 && acc + (double)order_doubles(L, m_lo - 1) <= wbudget) acc += (double)order_doubles(L, --m_lo);
+    double acc = (double)order_doubles(L, m_hi, rf);
+    while (m_lo > 0 && acc + (double)order_doubles(L, m_lo - 1, rf) <= wbudget)
+      acc += (double)order_doubles(L, --m_lo, rf);
     FwdWindow w;
     w.m_lo = m_lo;
     w.m_hi = m_hi;
@@ -146,6 +153,7 @@ int alloc_factor_storage(osph_plan* p) {
   }
   W_TRY(dalloc_w(&p->d_ainv, (size_t)mx[0]));
   W_TRY(dalloc_w(&p->d_xt, (size_t)mx[1]));
+  if (rf) W_TRY(dalloc_w(&p->d_at, (size_t)mx[1]));
   W_TRY(dalloc_w(&p->d_pbelow, (size_t)mx[2]));
   W_TRY(dalloc_w(&p->d_bf_e, (size_t)mx[3]));
   W_TRY(dalloc_w(&p->d_bf_r, (size_t)mx[3]));
