@@ -83,7 +83,8 @@ struct osph_plan {
   double* d_panel = nullptr;     // static-pivot factorisation: panel hand-off buffers
   int sweep_cfg_B = -1;          // cached sweep launch configuration for batch sweep_cfg_B
   int sweep_cfg[3] = {0, 0, 0};  // maps per team, cluster width, ring stages
-  bool sweep_large = false;      // L > 1024: two kernels per order (sweep_large.cu), plain R layout
+  bool sweep_large = false;
+  bool sweep_gemm = false;       // large batches: two GEMM launches per order (sweep_gemm.cu), plain R layout      // L > 1024: two kernels per order (sweep_large.cu), plain R layout
   double2* d_xbuf = nullptr;     // sweep_large: x_s of every map [B][+-][L]
   double2* d_rres = nullptr;     // sweep_large refinement: residual [B][L][+-]
   double* d_at = nullptr;        // refinement: the blocks A_m themselves, tiled like X (offsets of X)
@@ -137,6 +138,7 @@ cudaError_t launch_factor(osph_plan* p, cudaStream_t st = nullptr, cudaStream_t 
 cudaError_t launch_sweep(osph_plan* p, int B, double2* flm);               // sweep.cu
 int sweep_maps_per_team(osph_plan* p, int B);
 cudaError_t launch_sweep_large(osph_plan* p, int B, double2* flm);  // sweep_large.cu
+cudaError_t launch_sweep_gemm(osph_plan* p, int B, double2* flm);   // sweep_gemm.cu
 cudaError_t launch_factor_bf(osph_plan* p, int m_first, int m_last, cudaStream_t st);  // factor_bf.cu
 cudaError_t bf_prepare(osph_plan* p, int m_first, int m_last, BfRange* r);               // factor_bf.cu
 cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffsets& o); // factor_bf.cu

@@ -921,6 +921,7 @@ int sweep_maps_per_team(osph_plan* p, int B) {
   const size_t cap = 220 * 1024;
   const int KC = SWEEP_KC;
   if (p->sweep_cfg_B == B) return p->sweep_cfg[0];
+  p->sweep_gemm = false;
   if (L > 1024 || p->windowed || getenv("OSPH_SWEEP_LARGE")) {  // the right-hand sides no longer fit the persistent kernel's smem
     p->sweep_large = true;
     p->sweep_cfg_B = B;
@@ -970,6 +971,15 @@ int sweep_maps_per_team(osph_plan* p, int B) {
     if (gg == 1) break;
   }
   if (found) g = best_g;
+  if (!found && B >= 16 && !getenv("OSPH_SWEEP_NO_GEMM")) {
+    // teams would run in waves: one GEMM pair per order over the whole GPU instead (sweep_gemm.cu)
+    p->sweep_gemm = true;
+    p->sweep_large = false;
+    p->sweep_cfg_B = B;
+    p->sweep_cfg[0] = 1;
+    p->sweep_cfg[1] = p->sweep_cfg[2] = 0;
+    return 1;
+  }
   if (!found) {
     // several waves of teams: over (g, T) that fit, maximise the maps in flight
     // (resident teams x maps per team); ties go to the narrower team
@@ -1011,6 +1021,7 @@ int sweep_maps_per_team(osph_plan* p, int B) {
 
 cudaError_t launch_sweep(osph_plan* p, int B, double2* flm) {
   const int g = sweep_maps_per_team(p, B), T = p->sweep_cfg[1], S = p->sweep_cfg[2];
+  if (p->sweep_gemm) return launch_sweep_gemm(p, B, flm);
   if (p->sweep_large) return launch_sweep_large(p, B, flm);
   if (g == 4) return launch_sweep_cc<16>(p, B, 4, T, SWEEP_KC, S, flm);
   if (g == 2) return launch_sweep_cc<8>(p, B, 2, T, SWEEP_KC, S, flm);
