@@ -8,14 +8,17 @@
 // (s x n) x (n x 4B) for the corrections -- so each order runs as two
 // fp64 tensor-core GEMM launches over the whole GPU instead of the persistent
 // per-team kernel (whose teams no longer fit the GPU at once for large B).
-// Tiles: 32 rows x 64 columns (16 maps x {+,-} x {re, im}) per CTA, K in
+// Tiles: 16 rows x 64 columns (16 maps x {+,-} x {re, im}) per CTA (twice
+// the CTAs of 32-row tiles: measured 14.3 -> 12.4 ms at config 3), K in
 // 32-wide chunks double-buffered by 16-byte cp.async; A operands are the
-// chunk-major 8-row tiles the factorisation writes (a 32-row x 32-k chunk is
-// one contiguous 8 KB run), B operands come straight from R / xbuf.
+// chunk-major 8-row tiles the factorisation writes (each 8-row x 32-k piece
+// is one contiguous 2 KB run), B operands come straight from R / xbuf.
 #include "plan.cuh"
 
 #define SG_THREADS 256
-#define SG_TM 32   // rows per CTA
+#ifndef SG_TM
+#define SG_TM 16   // rows per CTA (16: twice the CTAs of 32 at these per-order GEMM sizes)
+#endif
 #define SG_MAPS 16 // maps per CTA (64 real columns)
 #define SG_KC 32
 
@@ -28,7 +31,7 @@ __device__ __forceinline__ void sg_wait1() { asm volatile("cp.async.wait_group 1
 __device__ __forceinline__ void sg_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 struct SgStage {
-  double a[SG_TM / 8][SG_KC][8];          // 4 row tiles, as stored: [k][row % 8]
+  double a[SG_TM / 8][SG_KC][8];          // row tiles as stored: [k][row % 8]
   double b[SG_MAPS][SG_KC][4];            // [map][k][+re, +im, -re, -im]
 };
 
@@ -54,7 +57,7 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
 
   auto load = [&](int buf, int c) {
     SgStage& S = st[buf];
-    // A: 4 row tiles x 2 KB, contiguous within chunk c (zero past the last tile)
+    // A: SG_TM / 8 row tiles x 2 KB, contiguous within chunk c (zero past the last tile)
     for (int i = tid; i < (SG_TM / 8) * 128; i += SG_THREADS) {  // 128 16-byte pieces per tile
       const int t = i >> 7, q = i & 127;
       double* dst = &S.a[t][0][0] + 2 * q;
@@ -77,11 +80,12 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
     sg_commit();
   };
 
-  // warp tile: rows (warp & 1) * 16 .. +16 (2 blocks of 8), columns (warp >> 1) * 16 .. +16 (2 blocks)
-  const int wr = (warp & 1) * 16, wc = (warp >> 1) * 16;
-  double acc[2][2][2];
+  // warp tile: rows (warp & 1) * (SG_TM / 2) .. (RB blocks of 8), columns (warp >> 1) * 16 .. +16 (2 blocks)
+  constexpr int RB = SG_TM / 16;
+  const int wr = (warp & 1) * (SG_TM / 2), wc = (warp >> 1) * 16;
+  double acc[RB][2][2];
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < RB; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
@@ -97,9 +101,9 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
     const SgStage& S = st[c & 1];
 #pragma unroll
     for (int k0 = 0; k0 < SG_KC; k0 += 4) {
-      double a[2], b[2];
+      double a[RB], b[2];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < RB; ++i) {
         const int row = wr + 8 * i + g;
         a[i] = S.a[row >> 3][k0 + tq][row & 7];
       }
@@ -109,7 +113,7 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
         b[j] = S.b[col >> 2][k0 + tq][col & 3];
       }
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < RB; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
@@ -118,7 +122,7 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
 
   const double sg = (s & 1) ? -1.0 : 1.0;
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < RB; ++i) {
     const int row = rt0 * 8 + wr + 8 * i + g;
     if (row >= M) continue;
 #pragma unroll
