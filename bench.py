@@ -91,6 +91,27 @@ def flops(L: int, B: int) -> dict:
     }
 
 
+# ncu DRAM traffic of the dominant kernel (one `ncu --set full` capture of the same
+# workload, summarised under profiles/ by tools/ncu_summary.py), bytes per launch
+
+NCU_PROFILES = {  # (stage, L, B) -> summary file
+    ("sweep", 256, 64): "sweep_r01c_full.txt",
+}
+
+
+def ncu_traffic(stage: str, L: int, B: int):
+    name = NCU_PROFILES.get((stage, L, B))
+    if not name or not (ROOT / "profiles" / name).exists():
+        return None, None
+    units = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total = 0.0
+    for line in (ROOT / "profiles" / name).read_text().splitlines():
+        parts = line.split()
+        if len(parts) >= 3 and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            total += float(parts[1]) * units.get(parts[2], 1.0)
+    return (total or None), f"profiles/{name} (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"
+
+
 # ---------------------------------------------------------------------------
 # clocks
 
@@ -330,8 +351,10 @@ def run_ours(args, cfg):
         roof = None
         if top in alg:
             achieved = alg[top] / stages[top] / 1e12
+            traffic, tsrc = ncu_traffic(top, L, B)
             roof = {"bound": "tensor", "kernel": top, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                    "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                    "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                    "traffic_source": tsrc,
                     "peak_source": "own fp64 DMMA microbenchmark (MEASURED_PEAKS.json has no fp64 entry)"}
         cpu = None
         if world == 1 and not args.no_cpu:

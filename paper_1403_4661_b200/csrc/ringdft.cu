@@ -16,6 +16,7 @@
 // the FFT stage barriers are shared; global accesses run map-fastest, which
 // is the contiguous direction of G and R.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "fft.cuh"
 #include "plan.cuh"
@@ -23,7 +24,7 @@
 namespace cg = cooperative_groups;
 
 #define RING_THREADS 256
-#define RING_SMEM_BUDGET (96 * 1024)
+#define RING_SMEM_BUDGET (48 * 1024)  // measured (config 2): 48 KB + 16 waves beats 96 KB + 4 waves by 11-15%
 
 // Fold G (layout [m][k][4B]) of ring k, map b into bin t (t < n).
 __device__ __forceinline__ double2 fold_bin(const double* __restrict__ G, int L, int B, int k, int n, int b, int t) {
@@ -395,16 +396,19 @@ static int max_fft(const osph_plan* p) {  // largest single-CTA Bluestein FFT
   return N;
 }
 
-// maps per block: enough blocks for ~4 waves on 148 SMs, at least 1
+// maps per block: enough blocks for ~16 waves on 148 SMs (OSPH_RING_WAVES), at least 1
 static int maps_per_block_for(int B, int rings) {
+  static const int waves = getenv("OSPH_RING_WAVES") ? atoi(getenv("OSPH_RING_WAVES")) : 16;
   int mpb = B;
-  while (mpb > 1 && (int64_t)rings * ((B + mpb - 1) / mpb) < 148 * 4) mpb = (mpb + 1) / 2;
+  while (mpb > 1 && (int64_t)rings * ((B + mpb - 1) / mpb) < 148 * waves) mpb = (mpb + 1) / 2;
   return mpb;
 }
 
 static size_t ring_smem(const osph_plan* p) {
+  static const size_t budget = getenv("OSPH_RING_SMEM_KB") ? (size_t)atoi(getenv("OSPH_RING_SMEM_KB")) * 1024
+                                                            : (size_t)RING_SMEM_BUDGET;
   const size_t need = sizeof(double2) * ((size_t)max_fft(p) + OSPH_SW_SMEM);
-  return need > RING_SMEM_BUDGET ? need : RING_SMEM_BUDGET;
+  return need > budget ? need : budget;
 }
 
 cudaError_t launch_ring_inverse(osph_plan* p, int B, double2* samples) {
