@@ -179,6 +179,58 @@ def _cpu_worker(args):
     return nmaps, time.perf_counter() - t0
 
 
+def cpu_round_trip_estimate(cfg: dict) -> tuple[float, str]:
+    """Seconds per map round trip of the oracle port on one core, for L too large to time whole.
+
+    A bounded sample, scaled up (SURVEY 8(d) "CPU baseline protocol"):
+    * inverse: the reference's synthesis on 8 evenly spaced rings
+      (oracle.inverse_rings, same C kernels), x L/8 -- every ring costs O(L^2);
+    * forward: one order of _forward_direct (legendre_table, ring analysis,
+      the gelsy solve, the k < m correction and ring update; the reference
+      benchmark's method) timed at 6 orders spread over n = L - m, a cubic in
+      n fitted through them and summed over all L orders.
+    """
+    from threadpoolctl import threadpool_limits
+
+    from oracle import optisph_oracle as O
+
+    O.build()
+    L = cfg["L"]
+    _, _, thetas = O.load_grid_file(str(ROOT / "tests" / "golden" / "grids" / cfg["grid"]))
+    rng = np.random.default_rng(5)
+    with threadpool_limits(limits=1):
+        flm = rng.standard_normal(L * L) + 1j * rng.standard_normal(L * L)
+        rings = [int(k) for k in np.linspace(0, L - 1, 8)]
+        t0 = time.perf_counter()
+        O.inverse_rings(flm, thetas, rings)
+        t_inv = (time.perf_counter() - t0) * L / len(rings)
+        buf = rng.standard_normal(L * L) + 1j * rng.standard_normal(L * L)
+        roots = O.ring_roots_flat(L)
+        lib = O._clib()
+        ns = sorted({max(1, int(round(L * f))) for f in (1 / 32, 1 / 16, 1 / 8, 1 / 4, 1 / 2, 1.0)})
+        ts = []
+        for n in ns:  # one order of _forward_direct (transform.py:415-429), as the reference benchmark runs it
+            m = L - n
+            t0 = time.perf_counter()
+            table = O.legendre_table(m, thetas, L)
+            g_p = np.empty(n, dtype=np.complex128)
+            g_n = np.empty(n, dtype=np.complex128)
+            lib.oracle_peel_analyze(O._p(buf), O._p(roots), m, L, O._p(g_p), O._p(g_n))
+            f_p, f_n = O._solve_pair(2.0 * np.pi * table[m:], g_p, g_n, m, 1.0, False)
+            if m:
+                cols = np.column_stack([f_p.real, f_p.imag, f_n.real, f_n.imag])
+                gg = 2.0 * np.pi * (table[:m] @ cols)
+                big_gp = np.ascontiguousarray(gg[:, 0] + 1j * gg[:, 1])
+                big_gn = np.ascontiguousarray(gg[:, 2] + 1j * gg[:, 3])
+                lib.oracle_peel_update(O._p(buf), O._p(roots), m, m, O._p(big_gp), O._p(big_gn))
+            ts.append(time.perf_counter() - t0)
+    coef = np.polyfit(np.array(ns, float), np.array(ts), 3)
+    t_fwd = float(np.clip(np.polyval(coef, np.arange(1, L + 1, dtype=float)), 0.0, None).sum())
+    how = (f"oracle port, 1 core, L={L}: inverse timed on 8 rings x L/8 ({t_inv:.2f} s/map); forward per-order "
+           f"work timed at n={ns}, cubic fit summed over L orders ({t_fwd:.2f} s/map); extrapolated")
+    return t_inv + t_fwd, how
+
+
 def cpu_round_trips(cfg: dict, procs: int, maps_per_proc: int, seed: int) -> tuple[float, float]:
     """(maps, wall seconds) for procs processes x maps_per_proc round trips each."""
     import multiprocessing as mp
@@ -357,12 +409,15 @@ def run_ours(args, cfg):
                     "traffic_source": tsrc,
                     "peak_source": "own fp64 DMMA microbenchmark (MEASURED_PEAKS.json has no fp64 entry)"}
         cpu = None
-        if world == 1 and not args.no_cpu:
+        if world == 1 and not args.no_cpu and L <= 256:
             procs = 1
             maps, wall = cpu_round_trips(cfg, procs, args.cpu_maps, seed=99)
             cpu = {"value": maps / wall, "unit": UNIT, "cores": procs, "kind": "port",
                    "sample": f"{args.cpu_maps} map round trip(s), L={L}, 1 core, oracle port "
                              f"(C kernels + numpy.fft + scipy gelsy), check=False as experiments.benchmark"}
+        elif world == 1 and not args.no_cpu:
+            t_map, how = cpu_round_trip_estimate(cfg)
+            cpu = {"value": 1.0 / t_map, "unit": UNIT, "cores": 1, "kind": "port", "sample": how}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
