@@ -450,6 +450,136 @@ __global__ void __launch_bounds__(BF_THREADS, 3) k_bf_update(int L, int m_first,
     }
 }
 
+// ---- 2c'. Persistent, software-pipelined variant of the update: one CTA per
+// SM walks a contiguous range of work items (consecutive items share the
+// order, so the item -> order mapping advances incrementally instead of being
+// searched), and while it multiplies item i out of shared memory the
+// 16-/8-byte async copies of item i+1's E, R and C tiles are in flight.  Two
+// stages of (E, R, C) = 207 KB of shared memory.  Opt-in (OSPH_BF_PERSISTENT=1):
+// slower than three independent CTAs per SM at L = 2048 (691 vs 549 ms).
+#define BF_LDC (BF_T + 2)
+struct BfStageP {
+  double e[BF_NB][BF_LDS];  // [k][row]
+  double r[BF_T][BF_LDS];   // [col][k]
+  double c[BF_T][BF_LDC];   // [col][row]
+};
+__device__ __forceinline__ void bf_cp8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(bf_smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void bf_cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void bf_cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+
+__global__ void __launch_bounds__(BF_THREADS, 1) k_bf_update_p(int L, int m_first, int j0, const int* __restrict__ pre,
+                                                               int cnt, int total, const int64_t* __restrict__ ainv_off,
+                                                               double* __restrict__ ainv,
+                                                               const double* __restrict__ ebuf,
+                                                               const double* __restrict__ rbuf,
+                                                               const int64_t* __restrict__ bf_off) {
+  extern __shared__ __align__(16) unsigned char bfp_raw[];
+  BfStageP* stg = reinterpret_cast<BfStageP*>(bfp_raw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int per = (total + gridDim.x - 1) / gridDim.x;
+  const int it0 = blockIdx.x * per, it1 = min(total, it0 + per);
+  if (it0 >= it1) return;
+  __shared__ int s_oi0;
+  if (warp == 0) {
+    const int o = bf_find_warp(pre, cnt, it0);
+    if (lane == 0) s_oi0 = o;
+  }
+  __syncthreads();
+  // item cursor (identical in every thread)
+  int oi = s_oi0, base = __ldg(pre + oi), next = __ldg(pre + oi + 1);
+  auto item = [&](int it, int& m, int& n, int& i0, int& c0) {
+    while (it >= next) {
+      ++oi;
+      base = next;
+      next = __ldg(pre + oi + 1);
+    }
+    m = m_first + oi;
+    n = L - m;
+    const int nt = (n + BF_T - 1) / BF_T;
+    const int local = it - base;
+    int ct = local / nt;
+    if (ct >= j0 / BF_T) ++ct;
+    i0 = (local % nt) * BF_T;
+    c0 = ct * BF_T;
+  };
+  auto issue = [&](BfStageP& S, int m, int n, int i0, int c0) {
+    const int lde = bf_lde(n), nb = min(BF_NB, n - j0);
+    const double* A = ainv + __ldg(ainv_off + m);
+    const double* E = ebuf + __ldg(bf_off + m);
+    const double* R = rbuf + __ldg(bf_off + m);
+    for (int idx = tid; idx < BF_T * BF_NB / 2; idx += BF_THREADS) {
+      const int k = idx >> 5, r2 = (idx & 31) * 2;  // E: column k, rows r2, r2 + 1
+      if (k < nb && i0 + r2 + 1 < lde) bf_cp16(&S.e[k][r2], E + (int64_t)k * lde + i0 + r2);
+      else {
+        S.e[k][r2] = 0.0;
+        S.e[k][r2 + 1] = 0.0;
+      }
+      const int c = idx >> 5, k2 = (idx & 31) * 2;  // R: column c0 + c, k2, k2 + 1
+      if (c0 + c < n) bf_cp16(&S.r[c][k2], R + (int64_t)(c0 + c) * BF_NB + k2);
+      else {
+        S.r[c][k2] = 0.0;
+        S.r[c][k2 + 1] = 0.0;
+      }
+    }
+    for (int idx = tid; idx < BF_T * BF_T; idx += BF_THREADS) {  // C: column c0 + c, row i0 + r (8-byte pieces)
+      const int c = idx >> 6, r = idx & 63;
+      if (i0 + r < n && c0 + c < n) bf_cp8(&S.c[c][r], A + (int64_t)(c0 + c) * n + i0 + r);
+      else S.c[c][r] = 0.0;
+    }
+    bf_cp_commit();
+  };
+  const int wr = (warp & 1) * 32, wc = (warp >> 1) * 16;
+  int m, n, i0, c0;
+  item(it0, m, n, i0, c0);
+  issue(stg[0], m, n, i0, c0);
+  for (int it = it0; it < it1; ++it) {
+    const int cm = m, cn = n, ci0 = i0, cc0 = c0;
+    if (it + 1 < it1) {
+      item(it + 1, m, n, i0, c0);
+      issue(stg[(it + 1 - it0) & 1], m, n, i0, c0);
+      bf_cp_wait1();
+    } else {
+      bf_cp_wait_all();
+    }
+    __syncthreads();
+    const BfStageP& S = stg[(it - it0) & 1];
+    double acc[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int r = wr + 8 * i + g, c = wc + 8 * j + 2 * t;
+        acc[i][j][0] = S.c[c][r];
+        acc[i][j][1] = S.c[c + 1][r];
+      }
+#pragma unroll 4
+    for (int k0 = 0; k0 < BF_NB; k0 += 4) {
+      double a[4], b[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = S.e[k0 + t][wr + 8 * i + g];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = S.r[wc + 8 * j + g][k0 + t];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    double* A = ainv + __ldg(ainv_off + cm);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int row = ci0 + wr + 8 * i + g, col = cc0 + wc + 8 * j + 2 * t;
+        if (row < cn && col < cn) A[(int64_t)col * cn + row] = acc[i][j][0];
+        if (row < cn && col + 1 < cn) A[(int64_t)(col + 1) * cn + row] = acc[i][j][1];
+      }
+    __syncthreads();  // stage (it - it0) & 1 is refilled by the next iteration's issue
+  }
+}
+
 // ---- 3. sweep operands from X (column c = pivot position, ring perm[c]):
 // chunk-major tiles with natural-order columns (the late ring's column zero),
 // u_m[perm[c]] = Pb_m[m-1, :] X[:, c], and for c = j* (perm = 0): w_m, beta_m, j*.
@@ -551,6 +681,14 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
     return e;
   if ((e = cudaFuncSetAttribute(k_bf_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)
     return e;
+  if ((e = cudaFuncSetAttribute(k_bf_update_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(BfStageP) * 2))) != cudaSuccess)
+    return e;
+  if (p->num_sms == 0) {
+    cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device);
+    // measured at L = 2048: 691 ms persistent vs 549 ms one CTA per tile (3 CTAs/SM hide latency better)
+    p->bf_persistent = getenv("OSPH_BF_PERSISTENT") ? atoi(getenv("OSPH_BF_PERSISTENT")) != 0 : false;
+  }
   k_bf_generate<<<dim3((L + BF_THREADS - 1) / BF_THREADS, cnt_all), BF_THREADS, 0, st>>>(
       L, m_first, p->d_cos, p->d_rec, p->d_ls, p->d_pstart, p->d_piv, o.ainv, o.pb, p->d_ainv, p->d_pbelow);
   if (p->d_at) {  // the blocks themselves for the sweep's refinement step, natural ring order
@@ -577,7 +715,12 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
                                                    p->d_ainv, p->d_bf_d, p->d_bf_e, o.bf);
       p->launches++;
     }
-    if (d.n_upd > 0)
+    if (d.n_upd > 0 && p->bf_persistent) {
+      const int ctas = std::min(d.n_upd, p->num_sms);
+      k_bf_update_p<<<ctas, BF_THREADS, sizeof(BfStageP) * 2, st>>>(L, m_first, j0, r.d_tab + d.pre_upd, d.cnt,
+                                                                   d.n_upd, o.ainv, p->d_ainv, p->d_bf_e, p->d_bf_r,
+                                                                   o.bf);
+    } else if (d.n_upd > 0)
       k_bf_update<<<d.n_upd, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_upd, d.cnt, o.ainv, p->d_ainv,
                                                   p->d_bf_e, p->d_bf_r, o.bf);
     p->launches += 2;

@@ -92,6 +92,8 @@ struct osph_plan {
   bool inv_ready = false;        // inverse buffers allocated
   // breadth-first factorisation (factor_bf.cu): orders with n > 256, or every order when windowed
   BfRange bf_full;               // the non-windowed range (m <= L - bf_nmin - 1)
+  int num_sms = 0;
+  bool bf_persistent = false;    // persistent pipelined update kernel (opt-in: OSPH_BF_PERSISTENT=1)
   int bf_nmin = 0;               // orders with n > bf_nmin use factor_bf.cu, the rest factor_np.cu (OSPH_BF_NMIN)
   bool need_norms = true;        // this call checks conditioning (check=True): factor kernels accumulate norms
   int64_t* d_bf_off = nullptr;   // [L+1] offsets of the E / R panels (NB x lde(n) per order)
