@@ -164,5 +164,54 @@ def main(argv=None) -> None:
     print(f"[gridopt] L={args.L} written to {args.out} in {time.time() - t0:.1f} s", flush=True)
 
 
+# ---------------------------------------------------------------------------
+# reference-shaped entry points (sampling.py:217-313)
+
+
+def optimize_order_like_reference(cands, band_limit: int, block_builder=None, measure=None,
+                                  tie_rtol: float = 1e-9, device: int = 0) -> ColatitudeGrid:
+    """``optimize_order(cands, band_limit, ...)`` with the reference's signature.
+
+    Only the uniform measure's equiangular candidates are on this package's
+    path; a custom ``block_builder`` is not supported (the blocks are built on
+    the device).
+    """
+    from .sampling import Measure
+
+    if measure not in (None, Measure.UNIFORM):
+        raise NotImplementedError("only the uniform measure is supported")
+    if block_builder is not None:
+        raise NotImplementedError("custom block builders are not supported (blocks are built on the GPU)")
+    if not np.array_equal(np.asarray(cands, dtype=np.float64), equiangular_candidates(band_limit)):
+        raise ValueError("candidates must be the uniform measure's equiangular candidates")
+    return optimize_order(band_limit, device, tie_rtol=tie_rtol)
+
+
+def make_grid(band_limit: int, measure=None, ordering=None, cache_dir=None, device: int = 0) -> ColatitudeGrid:
+    """``make_grid`` (sampling.py:281-313): interleaved, or condition-minimised with an on-disk cache."""
+    from pathlib import Path
+
+    from .sampling import Measure, Ordering, interleaved_grid, load_grid
+
+    measure = Measure.UNIFORM if measure is None else measure
+    ordering = Ordering.INTERLEAVED if ordering is None else ordering
+    if measure is not Measure.UNIFORM:
+        raise NotImplementedError("only the uniform measure is supported")
+    if ordering is Ordering.INTERLEAVED:
+        return interleaved_grid(band_limit)
+    path = None
+    if cache_dir is not None:
+        path = Path(cache_dir) / f"grid-L{band_limit}-{measure.value}-{ordering.value}.txt"
+        if path.exists():
+            grid = load_grid(path)
+            if grid.band_limit == band_limit and grid.ordering is ordering:
+                return grid
+    grid = optimize_order(band_limit, device)
+    if path is not None:
+        path.parent.mkdir(parents=True, exist_ok=True)
+        save_grid(grid, path)
+    return grid
+
+
 if __name__ == "__main__":
     main()
