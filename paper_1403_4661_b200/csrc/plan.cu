@@ -65,6 +65,7 @@ static void plan_free(osph_plan* p) {
   }
   if (p->ev_start) cudaEventDestroy(p->ev_start);
   if (p->ev_out) cudaEventDestroy(p->ev_out);
+  if (p->ev_sweep_done) cudaEventDestroy(p->ev_sweep_done);
   if (p->s_in) cudaStreamDestroy(p->s_in);
   if (p->s_out) cudaStreamDestroy(p->s_out);
   if (p->s_fac) cudaStreamDestroy(p->s_fac);
@@ -136,9 +137,14 @@ extern "C" int osph_plan_create(int L, const double* thetas, int max_batch, int 
   PLAN_TRY(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
   p->own_stream = true;
   for (cudaEvent_t& e : p->ev) PLAN_TRY(cudaEventCreate(&e));
-  PLAN_TRY(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
+  // the factorisation streams run at the highest priority: the factor is the
+  // critical path into the sweep, the work beside it (inverse, ring DFTs) is not
+  int prio_lo = 0, prio_hi = 0;
+  PLAN_TRY(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  if (getenv("OSPH_NO_STREAM_PRIORITY")) prio_hi = prio_lo;
+  PLAN_TRY(cudaStreamCreateWithPriority(&p->s_in, cudaStreamNonBlocking, prio_hi));
   PLAN_TRY(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
-  PLAN_TRY(cudaStreamCreateWithFlags(&p->s_fac, cudaStreamNonBlocking));
+  PLAN_TRY(cudaStreamCreateWithPriority(&p->s_fac, cudaStreamNonBlocking, prio_hi));
   for (cudaEvent_t& e : p->ev_fac) PLAN_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (int c = 0; c < osph_plan::kIoChunks; ++c) {
     PLAN_TRY(cudaEventCreateWithFlags(&p->ev_in[c], cudaEventDisableTiming));
@@ -146,6 +152,7 @@ extern "C" int osph_plan_create(int L, const double* thetas, int max_batch, int 
   }
   PLAN_TRY(cudaEventCreateWithFlags(&p->ev_start, cudaEventDisableTiming));
   PLAN_TRY(cudaEventCreateWithFlags(&p->ev_out, cudaEventDisableTiming));
+  PLAN_TRY(cudaEventCreateWithFlags(&p->ev_sweep_done, cudaEventDisableTiming));
   cudaStream_t st = p->stream;
 
   std::vector<double> c(L), s(L);
@@ -413,8 +420,13 @@ static int forward_real(osph_plan* p, int B, const void* samples, void* flm, boo
   const double2* src = (const double2*)samples;
   double2* dst = (double2*)flm;
   // the factorisation needs no data: side streams, beside the copy, pairing and ring DFTs
-  CUDA_TRY(cudaEventRecord(p->ev_start, st));
-  CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
+  // (it waits only for the previous forward's sweep, see osph_forward)
+  if (p->have_sweep_ev && !p->windowed) {
+    CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_sweep_done, 0));
+  } else {
+    CUDA_TRY(cudaEventRecord(p->ev_start, st));
+    CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
+  }
   CUDA_TRY(cudaEventRecord(p->ev[6], p->s_in));
   if (!p->windowed) CUDA_TRY(launch_factor(p, p->s_in, p->s_fac));
   CUDA_TRY(cudaEventRecord(p->ev[7], p->s_in));
@@ -432,6 +444,8 @@ static int forward_real(osph_plan* p, int B, const void* samples, void* flm, boo
   if (p->windowed) CUDA_TRY(forward_windows(p, Bp, p->d_z2));
   else CUDA_TRY(launch_sweep(p, Bp, p->d_z2));
   CUDA_TRY(cudaEventRecord(p->ev[9], st));
+  CUDA_TRY(cudaEventRecord(p->ev_sweep_done, st));
+  p->have_sweep_ev = true;
   k_unpair_flm<<<pair_grid(Bp, n), 256, 0, st>>>(B, L, p->d_z2, dst);
   CUDA_TRY(cudaGetLastError());
   p->launches += 2;
@@ -527,11 +541,20 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
     CUDA_TRY(cudaEventRecord(p->ev[8], st));
     CUDA_TRY(forward_windows(p, B, out));
     CUDA_TRY(cudaEventRecord(p->ev[9], st));
+    CUDA_TRY(cudaEventRecord(p->ev_sweep_done, st));
+    p->have_sweep_ev = true;
     if (host) CUDA_TRY(cudaMemcpyAsync(flm, p->d_out, bytes, cudaMemcpyDeviceToHost, st));
   } else if (!host) {
-    // the factorisation needs no data: it runs on a side stream beside the ring DFTs
-    CUDA_TRY(cudaEventRecord(p->ev_start, st));
-    CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
+    // The factorisation reads nothing this call or earlier calls produce, so it
+    // only waits for the previous forward's sweep (the last reader of the factor
+    // buffers) and runs on a side stream beside whatever precedes this call on
+    // the plan stream (e.g. the inverse of the same batch) and the ring DFTs.
+    if (p->have_sweep_ev) {
+      CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_sweep_done, 0));
+    } else {
+      CUDA_TRY(cudaEventRecord(p->ev_start, st));
+      CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
+    }
     CUDA_TRY(cudaEventRecord(p->ev[6], p->s_in));
     CUDA_TRY(launch_factor(p, p->s_in, p->s_fac));
     CUDA_TRY(cudaEventRecord(p->ev[7], p->s_in));
@@ -567,6 +590,8 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
     CUDA_TRY(cudaEventRecord(p->ev[8], st));
     CUDA_TRY(launch_sweep(p, B, out));
     CUDA_TRY(cudaEventRecord(p->ev[9], st));
+    CUDA_TRY(cudaEventRecord(p->ev_sweep_done, st));
+    p->have_sweep_ev = true;
     if (host) CUDA_TRY(cudaMemcpyAsync(flm, p->d_out, bytes, cudaMemcpyDeviceToHost, st));
   }
   p->have_fwd = true;

@@ -121,6 +121,8 @@ struct osph_plan {
   cudaStream_t s_in = nullptr, s_out = nullptr, s_fac = nullptr;
   cudaEvent_t ev_fac[2] = {};
   cudaEvent_t ev_in[kIoChunks] = {}, ev_done[kIoChunks] = {}, ev_start = nullptr, ev_out = nullptr;
+  cudaEvent_t ev_sweep_done = nullptr;  // last forward's sweep: the factor buffers are free again
+  bool have_sweep_ev = false;
   bool have_inv = false, have_fwd = false;
 };
 
