@@ -94,8 +94,9 @@ def flops(L: int, B: int) -> dict:
 # ncu DRAM traffic of the dominant kernel (one `ncu --set full` capture of the same
 # workload, summarised under profiles/ by tools/ncu_summary.py), bytes per launch
 
-NCU_PROFILES = {  # (stage, L, B) -> summary file
+NCU_PROFILES = {  # (stage, L, B) -> summary file (a multi-kernel stage sums its kernels of one call)
     ("sweep", 256, 64): "sweep_r01c_full.txt",
+    ("factor", 256, 64): "launches_r01c_summary.txt",
 }
 
 
@@ -109,6 +110,9 @@ def ncu_traffic(stage: str, L: int, B: int):
         parts = line.split()
         if len(parts) >= 3 and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             total += float(parts[1]) * units.get(parts[2], 1.0)
+        elif len(parts) == 2 and parts[0] == "factor_chain_dram_bytes":
+            total = float(parts[1])
+            return total, f"profiles/{name} (DRAM bytes of the breadth-first factor chain of one forward call)"
     return (total or None), f"profiles/{name} (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"
 
 

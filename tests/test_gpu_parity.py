@@ -352,3 +352,23 @@ def test_windowed_forward_matches_resident(L, B, gb, grid_of, monkeypatch):
     # n <= 256 orders use the breadth-first kernel here (factor_np.cu when resident): rounding differs
     assert np.abs(out - ref).max() <= 1e-10
     assert np.abs(out - flm).max() <= 1e-10
+
+
+# ---------------------------------------------------------------------------
+# smallest band limits (the reference accepts any L >= 1)
+
+
+@pytest.mark.parametrize("L", [1, 2, 3, 5, 7])
+def test_tiny_band_limits_match_oracle(L):
+    from oracle import optisph_oracle as O
+    from paper_1403_4661_b200 import gridopt
+
+    grid = gridopt.make_grid(L, ordering=osp.Ordering.CONDITION_MINIMIZED)
+    rng = np.random.default_rng(L)
+    flm = rng.standard_normal((2, L * L)) + 1j * rng.standard_normal((2, L * L))
+    s = osp.inverse_sht_batch(flm, grid)
+    f = osp.forward_sht_batch(s, grid)
+    for b in range(2):
+        ref_s = O.inverse_sht(flm[b], grid.thetas)
+        assert np.abs(s[b] - ref_s).max() <= 1e-12
+        assert np.abs(f[b] - flm[b]).max() <= 1e-11
