@@ -26,6 +26,10 @@ __host__ __device__ __forceinline__ int64_t packed_pos(int L, int m, int i) {
   return (int64_t)m * L - ((int64_t)m * (m - 1)) / 2 + i;
 }
 
+// Row stride of the per-order sweep vectors w_m and u_m ([L][uw_ld(L)] doubles):
+// even, so every row starts 16-byte aligned for the sweep's bulk copies.
+__host__ __device__ __forceinline__ int64_t uw_ld(int L) { return (int64_t)((L + 1) & ~1); }
+
 // Forward right-hand side / ring spectra R, TEAM-MAJOR: the maps are grouped in
 // teams of G = 2^lgG (the sweep's maps per team) and a team's slab
 // [pos][+-][map] is contiguous, so a team reads the right-hand side of order m

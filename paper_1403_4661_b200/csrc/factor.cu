@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(FAC_THREADS, 1) k_factor_gj(
   // u_m[j] = Pb_m[ring m-1, :] . X[:, j] for own columns, stored in natural ring
   // order: the sweep's chain partial a_{m-1} = Pb_m[m-1, :] . x'_m is u_m . rhs_m
   {
-    double* u = u_out + (size_t)m * L;
+    double* u = u_out + (size_t)m * uw_ld(L);
     const int nrtpb = (m + 7) >> 3;
     for (int col = cown0 + warp; col < cown1; col += FAC_THREADS / 32) {
       double s = 0.0;
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(FAC_THREADS, 1) k_factor_gj(
       beta_out[m] = b;
       jstar_out[m] = js;
     }
-    for (int l = tid; l < n; l += FAC_THREADS) w_out[(size_t)m * L + l] = __ldcg(A + (int64_t)js * n + l);
+    for (int l = tid; l < n; l += FAC_THREADS) w_out[(size_t)m * uw_ld(L) + l] = __ldcg(A + (int64_t)js * n + l);
   }
 }
 

@@ -608,12 +608,12 @@ __global__ void __launch_bounds__(BF_THREADS) k_bf_epilogue(int L, int m_first, 
       const double v = __ldcg(col + i);
       Xt[tile_index(i, cn, nrt)] = cn != 0 ? v : 0.0;
       if (m >= 1) s = fma(__ldcg(Pb + tile_index(m - 1, i, nrtpb)), v, s);
-      if (cn == 0) w_out[(size_t)m * L + i] = v;
+      if (cn == 0) w_out[(size_t)m * uw_ld(L) + i] = v;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) {
-      u_out[(size_t)m * L + cn] = cn != 0 ? s : 0.0;
+      u_out[(size_t)m * uw_ld(L) + cn] = cn != 0 ? s : 0.0;
       if (cn == 0) {
         beta_out[m] = s;
         jstar_out[m] = c;

@@ -348,14 +348,14 @@ __global__ void __launch_bounds__(FNP_THREADS, 1) k_factor_np(
     }
     const int jl = pinv[0];  // w_m = X[:, j*], the late ring's column
     if (jl >= c0 && jl < c1)
-      for (int i = tid; i < n; i += FNP_THREADS) w_out[(size_t)m * L + i] = slice[(size_t)(jl - c0) * ldn + i];
+      for (int i = tid; i < n; i += FNP_THREADS) w_out[(size_t)m * uw_ld(L) + i] = slice[(size_t)(jl - c0) * ldn + i];
   }
   if (tid == 0 && s_bad) atomicOr(status_out + m, 1);
   cluster.sync();  // the below-block rows of every rank are in global memory
   // u_m[j] = Pb_m[ring m-1, :] . X[:, j] for own columns, stored in natural ring
   // order: the sweep's chain partial a_{m-1} = Pb_m[m-1, :] . x'_m is u_m . rhs_m
   {
-    double* u = u_out + (size_t)m * L;
+    double* u = u_out + (size_t)m * uw_ld(L);
     const double* Pb = pbelow + pb_off[m];
     const int nrtpb = (m + 7) >> 3;
     for (int c = warp; c < cw; c += FNP_WARPS) {

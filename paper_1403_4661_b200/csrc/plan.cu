@@ -267,10 +267,11 @@ static int ensure_forward(osph_plan* p) {
   CUDA_TRY(dalloc(&p->d_rres, (size_t)2 * L * B));
 
   // [L][L] + 2: the sweep's bulk copies round their sizes up to 16 bytes
-  CUDA_TRY(dalloc(&p->d_u, (size_t)L * L + 2));
-  CUDA_TRY(dalloc(&p->d_w, (size_t)L * L + 2));
-  CUDA_TRY(cudaMemsetAsync(p->d_u, 0, sizeof(double) * ((size_t)L * L + 2), st));
-  CUDA_TRY(cudaMemsetAsync(p->d_w, 0, sizeof(double) * ((size_t)L * L + 2), st));
+  const size_t nuw = (size_t)L * uw_ld(L) + 2;  // even row stride: aligned rows for bulk copies
+  CUDA_TRY(dalloc(&p->d_u, nuw));
+  CUDA_TRY(dalloc(&p->d_w, nuw));
+  CUDA_TRY(cudaMemsetAsync(p->d_u, 0, sizeof(double) * nuw, st));
+  CUDA_TRY(cudaMemsetAsync(p->d_w, 0, sizeof(double) * nuw, st));
   // teams of up to 4 maps: the last team's padding maps stay zero
   CUDA_TRY(dalloc(&p->d_r, (size_t)L * (L + 1) * (B + 3)));
   CUDA_TRY(cudaMemsetAsync(p->d_r, 0, sizeof(double2) * (size_t)L * (L + 1) * (B + 3), st));

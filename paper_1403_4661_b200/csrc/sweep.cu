@@ -511,8 +511,8 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
     uint64_t* bar = inB + (s & 1);
     mbar_arrive_expect_tx(bar, rb + wb + ub);
     bulk_g2s(gst + (size_t)(s & 1) * cfg.ldx * CC, Rt + packed_pos(L, s, 0) * 2 * G, rb, bar);
-    if (wb) bulk_g2s(wv + (size_t)(s & 3) * ldr, w_all + (size_t)s * L + r0, wb, bar);
-    bulk_g2s(ubuf + (size_t)(s & 1) * cfg.ldx, u_all + (size_t)s * L, ub, bar);
+    if (wb) bulk_g2s(wv + (size_t)(s & 3) * ldr, w_all + (size_t)s * uw_ld(L) + r0, wb, bar);
+    bulk_g2s(ubuf + (size_t)(s & 1) * cfg.ldx, u_all + (size_t)s * uw_ld(L), ub, bar);
   };
 
   // ======================= producers =======================

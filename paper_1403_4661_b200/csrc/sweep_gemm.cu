@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
       double vr = acc[i][j][0], vi = acc[i][j][1];
       if (MODE == 0) {
         // late ring's column (zeroed in X tiles): + w[row] * rhs[0]
-        const double w = __ldg(w_all + (int64_t)s * L + row);
+        const double w = __ldg(w_all + (int64_t)s * uw_ld(L) + row);
         const double2 g0 = R[((int64_t)b * npos + p0) * 2 + slot];
         vr = fma(w, g0.x, vr);
         vi = fma(w, g0.y, vi);

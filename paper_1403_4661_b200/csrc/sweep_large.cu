@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(SL_THREADS) k_sweep_solve(int L, int s, int B,
         }
       }
     }
-    const double w = __ldg(w_all + (int64_t)s * L + r);  // X[:, j*]: the late ring's column
+    const double w = __ldg(w_all + (int64_t)s * uw_ld(L) + r);  // X[:, j*]: the late ring's column
 #pragma unroll
     for (int q = 0; q < SL_MAPS; ++q) {
       if (b0 + q >= B) break;
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(SL_THREADS) k_sweep_solve_t(int L, int s, int 
         for (int w = 0; w < SL_THREADS / 32; ++w)
 #pragma unroll
           for (int u = 0; u < 4; ++u) v[u] += red[w][r][4 * q + u];
-        const double w = __ldg(w_all + (int64_t)s * L + row);  // X[:, j*]: the late ring's column
+        const double w = __ldg(w_all + (int64_t)s * uw_ld(L) + row);  // X[:, j*]: the late ring's column
         const double2* rp = R + ((int64_t)(b0 + q) * npos + p0) * 2;
         const double2 gp = rp[0], gn = rp[1];
         const double sg = (s & 1) ? -1.0 : 1.0;

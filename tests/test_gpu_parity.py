@@ -358,7 +358,7 @@ def test_windowed_forward_matches_resident(L, B, gb, grid_of, monkeypatch):
 # smallest band limits (the reference accepts any L >= 1)
 
 
-@pytest.mark.parametrize("L", [1, 2, 3, 5, 7])
+@pytest.mark.parametrize("L", [1, 2, 3, 5, 7, 33, 127])
 def test_tiny_band_limits_match_oracle(L):
     from oracle import optisph_oracle as O
     from paper_1403_4661_b200 import gridopt
@@ -370,5 +370,5 @@ def test_tiny_band_limits_match_oracle(L):
     f = osp.forward_sht_batch(s, grid)
     for b in range(2):
         ref_s = O.inverse_sht(flm[b], grid.thetas)
-        assert np.abs(s[b] - ref_s).max() <= 1e-12
+        assert np.abs(s[b] - ref_s).max() <= 1e-12 * max(1.0, np.abs(ref_s).max())
         assert np.abs(f[b] - flm[b]).max() <= 1e-11
