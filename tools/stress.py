@@ -1,0 +1,55 @@
+"""Randomised GPU parity sweep: many (L, B, real/complex, host/device) cases.
+
+Small L: inverse and forward against the oracle; larger L: round trip and
+inverse on sampled rings.  Prints one line per case and a summary; exit code
+1 on any failure.  Run on the GPU box: python tools/stress.py [n_cases]
+"""
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import paper_1403_4661_b200 as osp  # noqa: E402
+from oracle import optisph_oracle as O  # noqa: E402
+from paper_1403_4661_b200 import gridopt  # noqa: E402
+
+rng = np.random.default_rng(int(time.time()) % 100000)
+n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+grids = {}
+fails = 0
+for case in range(n_cases):
+    L = int(rng.choice([1, 2, 3, 4, 6, 9, 16, 31, 40, 64, 65, 100, 128, 129, 200, 256, 300, 383, 512]))
+    B = int(rng.choice([1, 2, 3, 5, 8, 17, 33, 64]))
+    if L >= 300:
+        B = min(B, 8)
+    real = bool(rng.integers(2))
+    device = bool(rng.integers(2))
+    if L not in grids:
+        grids[L] = gridopt.make_grid(L, ordering=osp.Ordering.CONDITION_MINIMIZED)
+    g = grids[L]
+    flm = np.stack([O.config_coefficients(L, rng, spectrum="cmb", real=real) for _ in range(B)])
+    x = torch.from_numpy(flm).cuda() if device else flm
+    try:
+        s = osp.inverse_sht_batch(x, g, real=real)
+        f = osp.forward_sht_batch(s, g, real=real)
+        if device:
+            torch.cuda.synchronize()
+            s, f = s.cpu().numpy(), f.cpu().numpy()
+        rt = float(np.abs(f - flm).max())
+        b = int(rng.integers(B))
+        rings = sorted({0, L - 1, int(rng.integers(L))})
+        ref = O.inverse_rings(flm[b], g.thetas, rings)
+        inv = max(float(np.abs(s[b, k * k:(k + 1) ** 2] - ref[k]).max()) for k in rings)
+        ok = rt <= 1e-10 and inv <= 1e-12
+    except Exception as e:  # noqa: BLE001
+        ok, rt, inv = False, float("nan"), float("nan")
+        print("  exception:", e)
+    fails += not ok
+    print(f"{'ok ' if ok else 'BAD'} L={L:4d} B={B:3d} real={int(real)} device={int(device)} rt={rt:.2e} inv={inv:.2e}",
+          flush=True)
+print(f"{n_cases - fails}/{n_cases} passed")
+sys.exit(1 if fails else 0)
