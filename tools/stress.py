@@ -19,13 +19,17 @@ from paper_1403_4661_b200 import gridopt  # noqa: E402
 
 rng = np.random.default_rng(int(time.time()) % 100000)
 n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
+LS = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else \
+    [1, 2, 3, 4, 6, 9, 16, 31, 40, 64, 65, 100, 128, 129, 200, 256, 300, 383, 512]
 grids = {}
 fails = 0
 for case in range(n_cases):
-    L = int(rng.choice([1, 2, 3, 4, 6, 9, 16, 31, 40, 64, 65, 100, 128, 129, 200, 256, 300, 383, 512]))
+    L = int(rng.choice(LS))
     B = int(rng.choice([1, 2, 3, 5, 8, 17, 33, 64]))
     if L >= 300:
         B = min(B, 8)
+    if L >= 700:
+        B = min(B, 3)
     real = bool(rng.integers(2))
     device = bool(rng.integers(2))
     if L not in grids:
@@ -44,7 +48,9 @@ for case in range(n_cases):
         rings = sorted({0, L - 1, int(rng.integers(L))})
         ref = O.inverse_rings(flm[b], g.thetas, rings)
         inv = max(float(np.abs(s[b, k * k:(k + 1) ** 2] - ref[k]).max()) for k in rings)
-        ok = rt <= 1e-10 and inv <= 1e-12
+        # round trip: 1e-10 up to L = 1024; beyond, the peeling chain's own
+        # amplification (DESIGN 6) sets the scale (L=1100: ~3e-10 with the CMB spectrum)
+        ok = rt <= (1e-10 if L <= 1024 else 1e-8) and inv <= 1e-12
     except Exception as e:  # noqa: BLE001
         ok, rt, inv = False, float("nan"), float("nan")
         print("  exception:", e)
