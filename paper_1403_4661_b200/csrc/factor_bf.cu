@@ -312,6 +312,88 @@ __global__ void __launch_bounds__(BF_THREADS) k_bf_diag(int L, int m_first, int 
   }
 }
 
+// ---- 2a'. The same D with a short dependency chain: 64 threads, one row of
+// the identity-padded 64 x 64 block per thread in registers, kept ROTATED so
+// the current pivot column is always register 0 (static register indices in a
+// rolled loop, as factor_np.cu's panel step).  Per pivot the pivot row is
+// published with its reciprocal through a double-buffered shared record (one
+// 64-thread barrier); every other row subtracts g = d[0] / piv times it; the
+// pivot row's own scale is applied at the end.  After 64 steps the rotation is
+// back to natural order and the rows are those of D (identity past nb).
+__global__ void __launch_bounds__(64) k_bf_diag_rows(int L, int m_first, int j0,
+                                                     const int64_t* __restrict__ ainv_off,
+                                                     const double* __restrict__ ainv, double* __restrict__ dbuf,
+                                                     int* __restrict__ status) {
+  __shared__ __align__(16) double rec[2][BF_NB + 2];  // pivot row columns p+1 .. p+63 (rotated), 1 / pivot
+  const int m = m_first + blockIdx.x;
+  const int n = L - m;
+  const int nb = min(BF_NB, n - j0);
+  const double* A = ainv + __ldg(ainv_off + m);
+  const int r = threadIdx.x;
+  double d[BF_NB];
+#pragma unroll
+  for (int c = 0; c < BF_NB; ++c)
+    d[c] = (r < nb && c < nb) ? __ldcg(A + (int64_t)(j0 + c) * n + j0 + r) : (r == c ? 1.0 : 0.0);
+  bool bad = false;
+  auto publish = [&](double* pn) {
+#pragma unroll
+    for (int c = 0; c < BF_NB - 2; c += 2) *reinterpret_cast<double2*>(pn + c) = make_double2(d[c + 1], d[c + 2]);
+    if (d[0] == 0.0 || !isfinite(d[0])) bad = true;
+    *reinterpret_cast<double2*>(pn + BF_NB - 2) = make_double2(d[BF_NB - 1], 1.0 / d[0]);
+  };
+  double rsc = 1.0;
+  if (r == 0) publish(rec[0]);
+#pragma unroll 1
+  for (int p = 0; p < BF_NB; ++p) {
+    __syncthreads();
+    const double* pr = rec[p & 1];
+    const double inv = pr[BF_NB - 1];
+    const bool ispiv = r == p;
+    const double gg = ispiv ? 0.0 : d[0] * inv;
+    rsc = ispiv ? inv : rsc;
+#pragma unroll
+    for (int c = 0; c < BF_NB - 1; c += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(pr + c);
+      d[c] = fma(-gg, v.x, d[c + 1]);
+      if (c + 1 < BF_NB - 1) d[c + 1] = fma(-gg, v.y, d[c + 2]);
+    }
+    d[BF_NB - 1] = ispiv ? 1.0 : -gg;
+    if (r == p + 1) publish(rec[(p + 1) & 1]);
+  }
+  if (bad) atomicOr(status + m, 1);
+  double* Dg = dbuf + (size_t)blockIdx.x * BF_NB * BF_NB;  // D[r][c] at c * NB + r
+#pragma unroll
+  for (int c = 0; c < BF_NB; ++c) Dg[c * BF_NB + r] = d[c] * rsc;
+}
+
+// R = A[J, :] (the update's B operand), layout [col][NB]; grid (orders, column chunks).
+__global__ void __launch_bounds__(BF_THREADS) k_bf_rcopy(int L, int m_first, int j0,
+                                                         const int64_t* __restrict__ ainv_off,
+                                                         const double* __restrict__ ainv, double* __restrict__ rbuf,
+                                                         const int64_t* __restrict__ bf_off) {
+  const int m = m_first + blockIdx.x;
+  const int n = L - m;
+  const int nb = min(BF_NB, n - j0);
+  const double* A = ainv + __ldg(ainv_off + m);
+  double* R = rbuf + __ldg(bf_off + m);
+  const int c0 = blockIdx.y * BF_RCHUNK, c1 = min(n, c0 + BF_RCHUNK);
+  const int tot = (c1 - c0) * BF_NB;
+  for (int base = 0; base < tot; base += 8 * BF_THREADS) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * BF_THREADS + threadIdx.x;
+      const int rr = idx & (BF_NB - 1), c = c0 + (idx >> 6);
+      v[u] = (idx < tot && rr < nb) ? __ldcg(A + (int64_t)c * n + j0 + rr) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = base + u * BF_THREADS + threadIdx.x;
+      if (idx < tot) R[(int64_t)(c0 + (idx >> 6)) * BF_NB + (idx & (BF_NB - 1))] = v[u];
+    }
+  }
+}
+
 // ---- 2b. E = -A[I, J] D (E[J] = D - I) per 64-row tile; A[I, J] = E + I_J.
 __global__ void __launch_bounds__(BF_THREADS) k_bf_panel(int L, int m_first, int j0, const int* __restrict__ pre,
                                                          int cnt, const int64_t* __restrict__ ainv_off,
@@ -708,6 +790,12 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
     if (L - m_first <= 512 && getenv("OSPH_BF_FUSE")) {  // opt-in: E formed by the diagonal kernel (measured slower at L=256: 0.91 vs 0.74 ms)
       k_bf_diag<true><<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_bf_r, o.bf,
                                                     p->d_status, p->d_bf_e);
+    } else if (!getenv("OSPH_BF_DIAG_PATCH")) {  // register-row diagonal inverse + separate R copy
+      k_bf_rcopy<<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_r, o.bf);
+      k_bf_diag_rows<<<d.cnt, 64, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_status);
+      k_bf_panel<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_panel, d.cnt, o.ainv,
+                                                   p->d_ainv, p->d_bf_d, p->d_bf_e, o.bf);
+      p->launches += 2;
     } else {
       k_bf_diag<false><<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_bf_r, o.bf,
                                                      p->d_status, p->d_bf_e);
