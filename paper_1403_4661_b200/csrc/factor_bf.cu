@@ -177,17 +177,12 @@ __global__ void __launch_bounds__(BF_THREADS) k_bf_colnorm(int L, int m_first, c
 // block y = 0 also inverts D.  The inversion keeps a 4 x 4 patch of D per
 // thread in registers; per pivot only the pivot row and column go through
 // shared memory (double-buffered: one barrier per pivot).
-// FUSE (opt-in, OSPH_BF_FUSE, n <= 512): block y = 0 also forms the panel E = -A[:, J] D
-// itself (E[J] = D - I, A[:, J] = E + I_J), saving the k_bf_panel launch; one CTA
-// per order is slower than the row-parallel panel kernel even at L = 256.
 #define BF_RCHUNK 256
-template <bool FUSE>
 __global__ void __launch_bounds__(BF_THREADS) k_bf_diag(int L, int m_first, int j0, const int64_t* __restrict__ ainv_off,
-                                                        double* __restrict__ ainv, double* __restrict__ dbuf,
+                                                        const double* __restrict__ ainv, double* __restrict__ dbuf,
                                                         double* __restrict__ rbuf, const int64_t* __restrict__ bf_off,
-                                                        int* __restrict__ status, double* __restrict__ ebuf) {
+                                                        int* __restrict__ status) {
   __shared__ double s_row[2][BF_NB], s_col[2][BF_NB];
-  __shared__ double s_D[FUSE ? BF_NB : 1][BF_NB + 1];
   const int m = m_first + blockIdx.x;
   const int n = L - m;
   const int nb = min(BF_NB, n - j0);
@@ -264,52 +259,11 @@ __global__ void __launch_bounds__(BF_THREADS) k_bf_diag(int L, int m_first, int 
     }
   }
   if (bad) atomicOr(status + m, 1);
-  if (!FUSE) {
-    double* Dg = dbuf + (size_t)blockIdx.x * BF_NB * BF_NB;  // D[r][c] at c * NB + r
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) Dg[(4 * tc + j) * BF_NB + 4 * tr + i] = d[i][j];
-    return;
-  }
+  double* Dg = dbuf + (size_t)blockIdx.x * BF_NB * BF_NB;  // D[r][c] at c * NB + r
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) s_D[FUSE ? 4 * tr + i : 0][4 * tc + j] = d[i][j];
-  __syncthreads();
-  double* Am = ainv + __ldg(ainv_off + m);
-  double* E = ebuf + __ldg(bf_off + m);
-  const int lde = bf_lde(n);
-  for (int row = tid; row < n; row += BF_THREADS) {
-    const bool inJ = row >= j0 && row < j0 + nb;
-#pragma unroll 1
-    for (int cg = 0; cg < BF_NB / 16; ++cg) {
-      double acc[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) acc[q] = 0.0;
-      if (!inJ) {
-        for (int k = 0; k < nb; ++k) {
-          const double a = __ldcg(Am + (int64_t)(j0 + k) * n + row);
-#pragma unroll
-          for (int q = 0; q < 16; ++q) acc[q] = fma(a, s_D[FUSE ? k : 0][cg * 16 + q], acc[q]);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int c = cg * 16 + q;
-        if (c >= nb) continue;
-        const double v = inJ ? s_D[FUSE ? row - j0 : 0][c] - ((row - j0 == c) ? 1.0 : 0.0) : -acc[q];
-        E[(int64_t)c * lde + row] = v;
-        acc[q] = v;
-      }
-    }
-  }
-  // A[:, J] = E + I_J only after every row's A[:, J] has been read
-  __syncthreads();
-  for (int idx = tid; idx < n * nb; idx += BF_THREADS) {
-    const int c = idx / n, row = idx - c * n;
-    Am[(int64_t)(j0 + c) * n + row] = E[(int64_t)c * lde + row] + ((row - j0 == c) ? 1.0 : 0.0);
-  }
+    for (int j = 0; j < 4; ++j) Dg[(4 * tc + j) * BF_NB + 4 * tr + i] = d[i][j];
 }
 
 // ---- 2a'. The same D with a short dependency chain: 64 threads, one row of
@@ -787,22 +741,18 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
     const auto& d = r.steps[sidx];
     const int j0 = (int)sidx * BF_NB;
     const dim3 dgrid(d.cnt, (L - m_first + BF_RCHUNK - 1) / BF_RCHUNK);
-    if (L - m_first <= 512 && getenv("OSPH_BF_FUSE")) {  // opt-in: E formed by the diagonal kernel (measured slower at L=256: 0.91 vs 0.74 ms)
-      k_bf_diag<true><<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_bf_r, o.bf,
-                                                    p->d_status, p->d_bf_e);
-    } else if (!getenv("OSPH_BF_DIAG_PATCH")) {  // register-row diagonal inverse + separate R copy
+    if (!getenv("OSPH_BF_DIAG_PATCH")) {  // register-row diagonal inverse + separate R copy
       k_bf_rcopy<<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_r, o.bf);
       k_bf_diag_rows<<<d.cnt, 64, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_status);
-      k_bf_panel<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_panel, d.cnt, o.ainv,
-                                                   p->d_ainv, p->d_bf_d, p->d_bf_e, o.bf);
       p->launches += 2;
-    } else {
-      k_bf_diag<false><<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_bf_r, o.bf,
-                                                     p->d_status, p->d_bf_e);
-      k_bf_panel<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_panel, d.cnt, o.ainv,
-                                                   p->d_ainv, p->d_bf_d, p->d_bf_e, o.bf);
+    } else {  // 4 x 4 register patch per thread, R copied by the same kernel
+      k_bf_diag<<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_bf_r, o.bf,
+                                              p->d_status);
       p->launches++;
     }
+    k_bf_panel<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_panel, d.cnt, o.ainv, p->d_ainv,
+                                                 p->d_bf_d, p->d_bf_e, o.bf);
+    p->launches++;
     if (d.n_upd > 0 && p->bf_persistent) {
       const int ctas = std::min(d.n_upd, p->num_sms);
       k_bf_update_p<<<ctas, BF_THREADS, sizeof(BfStageP) * 2, st>>>(L, m_first, j0, r.d_tab + d.pre_upd, d.cnt,
@@ -811,7 +761,7 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
     } else if (d.n_upd > 0)
       k_bf_update<<<d.n_upd, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_upd, d.cnt, o.ainv, p->d_ainv,
                                                   p->d_bf_e, p->d_bf_r, o.bf);
-    p->launches += 2;
+    if (d.n_upd > 0) p->launches++;
   }
   if (p->need_norms) {
     k_bf_colnorm<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, o.ainv, p->d_ainv, p->d_norms, 1);
