@@ -403,6 +403,83 @@ __global__ void __launch_bounds__(BF_THREADS) k_bf_panel(int L, int m_first, int
   }
 }
 
+// ---- 2b'. The panel on the tensor cores: one 64-row tile per CTA computes
+// A[I, J] D (64 x 64 x 64, DMMA, operands in shared memory: A[I, J] k-major,
+// D column-major as stored), then E = -A[I, J] D (E[J] = D - I) and
+// A[I, J] = E + I_J as k_bf_panel does.
+__global__ void __launch_bounds__(BF_THREADS, 3) k_bf_panel_mma(int L, int m_first, int j0, const int* __restrict__ pre,
+                                                                int cnt, const int64_t* __restrict__ ainv_off,
+                                                                double* __restrict__ ainv,
+                                                                const double* __restrict__ dbuf,
+                                                                double* __restrict__ ebuf,
+                                                                const int64_t* __restrict__ bf_off) {
+  extern __shared__ __align__(16) double bf_sm[];
+  double(*At)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm);                 // [k][row]
+  double(*Dt)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm + BF_NB * BF_LDS);  // [c][k] = D[k][c]
+  __shared__ int s_oi;
+  if (threadIdx.x < 32) {
+    const int oi_w = bf_find_warp(pre, cnt, blockIdx.x);
+    if (threadIdx.x == 0) s_oi = oi_w;
+  }
+  __syncthreads();
+  const int oi = s_oi;
+  const int m = m_first + oi;
+  const int n = L - m, lde = bf_lde(n);
+  const int nb = min(BF_NB, n - j0);
+  const int i0 = (blockIdx.x - __ldg(pre + oi)) * BF_T;
+  double* A = ainv + __ldg(ainv_off + m);
+  const double* Dg = dbuf + (size_t)oi * BF_NB * BF_NB;
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < BF_NB * BF_NB / 2; idx += BF_THREADS) {  // D: column c, k2, k2 + 1
+    const int c = idx >> 5, k2 = (idx & 31) * 2;
+    bf_cp16(&Dt[c][k2], Dg + c * BF_NB + k2);
+  }
+  for (int idx = tid; idx < BF_T * BF_NB; idx += BF_THREADS) {  // A[I, J]: column k, row r
+    const int r = idx & (BF_T - 1), k = idx >> 6;
+    At[k][r] = (i0 + r < n && k < nb) ? __ldcg(A + (int64_t)(j0 + k) * n + i0 + r) : 0.0;
+  }
+  bf_cp_wait_all();
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = (warp & 1) * 32, wc = (warp >> 1) * 16;
+  double acc[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll 4
+  for (int k0 = 0; k0 < BF_NB; k0 += 4) {
+    double a[4], b[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = At[k0 + t][wr + 8 * i + g];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) b[j] = Dt[wc + 8 * j + g][k0 + t];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+  double* E = ebuf + __ldg(bf_off + m);  // [col][lde]
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = i0 + wr + 8 * i + g;
+    if (row >= n) continue;
+    const bool inJ = row >= j0 && row < j0 + nb;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = wc + 8 * j + 2 * t + h;
+        if (c >= nb) continue;
+        const bool diag = inJ && row - j0 == c;
+        const double v = inJ ? Dt[c][row - j0] - (diag ? 1.0 : 0.0) : -acc[i][j][h];
+        E[(int64_t)c * lde + row] = v;
+        A[(int64_t)(j0 + c) * n + row] = v + (diag ? 1.0 : 0.0);
+      }
+  }
+}
+
 // ---- 2c. A[I, K] += E[I, :] R[:, K] for every 64 x 64 tile outside column block J.
 // E and R are staged by 16-byte async copies (k-major / column-major in smem,
 // matching their global layouts) while the C fragments load from global.
@@ -715,6 +792,9 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
   const size_t sm2 = sizeof(double) * 2 * BF_T * BF_LDS + 16;
   if ((e = cudaFuncSetAttribute(k_bf_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)
     return e;
+  if ((e = cudaFuncSetAttribute(k_bf_panel_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) !=
+      cudaSuccess)
+    return e;
   if ((e = cudaFuncSetAttribute(k_bf_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)
     return e;
   if ((e = cudaFuncSetAttribute(k_bf_update_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -750,8 +830,12 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
                                               p->d_status);
       p->launches++;
     }
-    k_bf_panel<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_panel, d.cnt, o.ainv, p->d_ainv,
-                                                 p->d_bf_d, p->d_bf_e, o.bf);
+    if (!getenv("OSPH_BF_PANEL_FMA"))
+      k_bf_panel_mma<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_panel, d.cnt, o.ainv,
+                                                       p->d_ainv, p->d_bf_d, p->d_bf_e, o.bf);
+    else
+      k_bf_panel<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_panel, d.cnt, o.ainv,
+                                                   p->d_ainv, p->d_bf_d, p->d_bf_e, o.bf);
     p->launches++;
     if (d.n_upd > 0 && p->bf_persistent) {
       const int ctas = std::min(d.n_upd, p->num_sms);
