@@ -88,7 +88,7 @@ struct osph_plan {
   double2* d_xbuf = nullptr;     // sweep_large: x_s of every map [B][+-][L]
   double2* d_rres = nullptr;     // sweep_large refinement: residual [B][L][+-]
   double* d_at = nullptr;        // refinement: the blocks A_m themselves, tiled like X (offsets of X)
-  bool refine = false;           // one iterative-refinement step per order in sweep_large (L > 1024 default)
+  int refine = 0;                // iterative-refinement steps per order in sweep_large (default 1 for L > 512)
   bool inv_ready = false;        // inverse buffers allocated
   // breadth-first factorisation (factor_bf.cu): orders with n > 256, or every order when windowed
   BfRange bf_full;               // the non-windowed range (m <= L - bf_nmin - 1)

@@ -476,7 +476,7 @@ cudaError_t launch_sweep_large_range(osph_plan* p, int B, double2* flm, int s_hi
       p->launches++;
     };
     solve(p->d_r, npos, p0, 0);
-    if (p->refine) {  // x += X (b - A x): one fixed-precision refinement step per order
+    for (int rstep = 0; rstep < p->refine; ++rstep) {  // x += X (b - A x): fixed-precision refinement
       if (p->d_at) {  // stored block (tiled like X)
         if (mb == 2)
           k_sweep_resid_t<2><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_at, xt_off, p->d_r,
