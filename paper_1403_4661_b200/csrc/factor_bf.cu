@@ -84,37 +84,47 @@ __global__ void __launch_bounds__(BF_THREADS) k_bf_generate(int L, int m_first, 
                                                             const int64_t* __restrict__ ainv_off,
                                                             const int64_t* __restrict__ pb_off,
                                                             double* __restrict__ ainv, double* __restrict__ pbelow) {
+  __shared__ double2 s_rec[BF_THREADS];  // recurrence factors of the current degree chunk (broadcast reads)
   const int m = m_first + blockIdx.y;
   const int n = L - m;
   const int t = blockIdx.x * BF_THREADS + threadIdx.x;
-  if (t >= L) return;
-  int k, row = -1;
-  if (t < n) {
-    row = t;
-    k = m + __ldg(perm_all + packed_pos(L, m, t));
-  } else {
-    k = t - n;  // ring below the block
+  const bool active = t < L;
+  int k = 0, row = -1;
+  if (active) {
+    if (t < n) {
+      row = t;
+      k = m + __ldg(perm_all + packed_pos(L, m, t));
+    } else {
+      k = t - n;  // ring below the block
+    }
   }
   double* A = ainv + __ldg(ainv_off + m);
   double* Pb = pbelow + __ldg(pb_off + m);
   const int64_t ts = (int64_t)m * L + k;
-  const int ls = __ldg(ls_tab + ts);
-  const double2 pp = __ldg(pstart + ts);
+  const int ls = active ? __ldg(ls_tab + ts) : L;
+  const double2 pp = active ? __ldg(pstart + ts) : make_double2(0.0, 0.0);
   double p0 = pp.x, p1 = pp.y;
-  const double x = __ldg(costh + k);
+  const double x = active ? __ldg(costh + k) : 0.0;
   const double2* recm = rec + packed_pos(L, m, 0);
   const int nrtpb = (m + 7) >> 3;
-  for (int l = m; l < L; ++l) {
-    double v = 0.0;
-    if (l >= ls) {
-      v = OSPH_TWO_PI * p1;
-      const double2 ar = __ldg(recm + (l - m));
-      const double nxt = fma(x, p1, -ar.x * p0) * ar.y;
-      p0 = p1;
-      p1 = nxt;
+  for (int l0 = m; l0 < L; l0 += BF_THREADS) {
+    __syncthreads();
+    if (l0 + threadIdx.x < L) s_rec[threadIdx.x] = __ldg(recm + (l0 + threadIdx.x - m));
+    __syncthreads();
+    if (!active) continue;
+    const int l1 = min(L, l0 + BF_THREADS);
+    for (int l = l0; l < l1; ++l) {
+      double v = 0.0;
+      if (l >= ls) {
+        v = OSPH_TWO_PI * p1;
+        const double2 ar = s_rec[l - l0];
+        const double nxt = fma(x, p1, -ar.x * p0) * ar.y;
+        p0 = p1;
+        p1 = nxt;
+      }
+      if (row >= 0) A[(int64_t)(l - m) * n + row] = v;
+      else Pb[tile_index(k, l - m, nrtpb)] = v;
     }
-    if (row >= 0) A[(int64_t)(l - m) * n + row] = v;
-    else Pb[tile_index(k, l - m, nrtpb)] = v;
   }
 }
 
