@@ -186,17 +186,28 @@ __global__ void __launch_bounds__(SYN_THREADS, TN > 128 ? 1 : 2) k_synth_dmma(
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
     if (tid < SYN_TM) {
-      for (int j = 0; j < SYN_TK; ++j) {
-        const int l = ks + j;
-        double v = 0.0;
-        if (l < L && l >= ls) {
-          v = p1;
-          const double2 ar = __ldg(recm + (l - m));
-          const double nxt = fma(x, p1, -ar.x * p0) * ar.y;
-          p0 = p1;
-          p1 = nxt;
+      // recurrence factors of the chunk fetched 8 at a time (independent loads,
+      // one exposed latency per batch instead of one per degree)
+#pragma unroll
+      for (int j8 = 0; j8 < SYN_TK; j8 += 8) {
+        double2 ar[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int l = ks + j8 + u;
+          ar[u] = l < L ? __ldg(recm + (l - m)) : make_double2(0.0, 0.0);
         }
-        Ps[buf][j][tid] = v;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int l = ks + j8 + u;
+          double v = 0.0;
+          if (l < L && l >= ls) {
+            v = p1;
+            const double nxt = fma(x, p1, -ar[u].x * p0) * ar[u].y;
+            p0 = p1;
+            p1 = nxt;
+          }
+          Ps[buf][j8 + u][tid] = v;
+        }
       }
     }
   };
