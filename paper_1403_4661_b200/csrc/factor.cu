@@ -389,12 +389,6 @@ __global__ void __launch_bounds__(FAC_THREADS, 1) k_factor_gj(
   }
 }
 
-__global__ void k_identity_perm(int L, int* __restrict__ perm) {
-  const int m = blockIdx.y;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L - m; i += gridDim.x * blockDim.x)
-    perm[packed_pos(L, m, i)] = i;
-}
-
 // Finalise kappa per order once every cluster has finished.
 __global__ void k_kappa(int L, const unsigned long long* __restrict__ norms, double* __restrict__ kappa) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
@@ -457,10 +451,6 @@ cudaError_t launch_factor(osph_plan* p, cudaStream_t st, cudaStream_t st2) {
   const int L = p->L;
   cudaError_t e;
   if (!st) st = p->stream;
-  if (!p->piv_ready && getenv("OSPH_FACTOR_IDENTITY_PIV")) {  // experiment: natural row order, no pivoting
-    k_identity_perm<<<dim3((L + 255) / 256, L), 256, 0, st>>>(L, p->d_piv);
-    p->piv_ready = true;
-  }
   const bool first_call = !p->piv_ready;
   // first call: the partial-pivoting kernels record the pivot order (grid-determined);
   // run them serially, then redo the large orders with the breadth-first kernel below
