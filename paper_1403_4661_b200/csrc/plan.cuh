@@ -83,8 +83,8 @@ struct osph_plan {
   double* d_panel = nullptr;     // static-pivot factorisation: panel hand-off buffers
   int sweep_cfg_B = -1;          // cached sweep launch configuration for batch sweep_cfg_B
   int sweep_cfg[3] = {0, 0, 0};  // maps per team, cluster width, ring stages
-  bool sweep_large = false;
-  bool sweep_gemm = false;       // large batches: two GEMM launches per order (sweep_gemm.cu), plain R layout      // L > 1024: two kernels per order (sweep_large.cu), plain R layout
+  bool sweep_large = false;      // L > 1024 or nothing fits: two kernels per order (sweep_large.cu), plain R layout
+  bool sweep_gemm = false;       // large batches: two GEMM launches per order (sweep_gemm.cu), plain R layout
   double2* d_xbuf = nullptr;     // sweep_large: x_s of every map [B][+-][L]
   double2* d_rres = nullptr;     // sweep_large refinement: residual [B][L][+-]
   double* d_at = nullptr;        // refinement: the blocks A_m themselves, tiled like X (offsets of X)
