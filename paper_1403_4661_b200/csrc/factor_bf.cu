@@ -422,7 +422,8 @@ __global__ void __launch_bounds__(BF_THREADS, 3) k_bf_panel_mma(int L, int m_fir
                                                                 double* __restrict__ ainv,
                                                                 const double* __restrict__ dbuf,
                                                                 double* __restrict__ ebuf,
-                                                                const int64_t* __restrict__ bf_off) {
+                                                                const int64_t* __restrict__ bf_off,
+                                                                double* __restrict__ rnext) {
   extern __shared__ __align__(16) double bf_sm[];
   double(*At)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm);                 // [k][row]
   double(*Dt)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm + BF_NB * BF_LDS);  // [c][k] = D[k][c]
@@ -486,6 +487,9 @@ __global__ void __launch_bounds__(BF_THREADS, 3) k_bf_panel_mma(int L, int m_fir
         const double v = inJ ? Dt[c][row - j0] - (diag ? 1.0 : 0.0) : -acc[i][j][h];
         E[(int64_t)c * lde + row] = v;
         A[(int64_t)(j0 + c) * n + row] = v + (diag ? 1.0 : 0.0);
+        // next step's R = A[J', :] (J' = the next 64 rows): its J columns are final here
+        if (rnext && row >= j0 + BF_NB && row < j0 + 2 * BF_NB)
+          rnext[__ldg(bf_off + m) + (int64_t)(j0 + c) * BF_NB + (row - j0 - BF_NB)] = v;
       }
   }
 }
@@ -497,7 +501,8 @@ __global__ void __launch_bounds__(BF_THREADS, 3) k_bf_update(int L, int m_first,
                                                              int cnt, const int64_t* __restrict__ ainv_off,
                                                              double* __restrict__ ainv, const double* __restrict__ ebuf,
                                                              const double* __restrict__ rbuf,
-                                                             const int64_t* __restrict__ bf_off) {
+                                                             const int64_t* __restrict__ bf_off,
+                                                             double* __restrict__ rnext) {
   extern __shared__ __align__(16) double bf_sm[];
   double(*Et)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm);                 // [k][row]
   double(*Rt)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm + BF_NB * BF_LDS);  // [col][k]
@@ -570,6 +575,11 @@ __global__ void __launch_bounds__(BF_THREADS, 3) k_bf_update(int L, int m_first,
       const int row = i0 + wr + 8 * i + g, col = c0 + wc + 8 * j + 2 * t;
       if (row < n && col < n) A[(int64_t)col * n + row] = acc[i][j][0];
       if (row < n && col + 1 < n) A[(int64_t)(col + 1) * n + row] = acc[i][j][1];
+      if (rnext && i0 == j0 + BF_T && row < n) {  // the next step's R = A[J', :] from the J' row tile
+        double* Rn = rnext + __ldg(bf_off + m);
+        if (col < n) Rn[(int64_t)col * BF_NB + (row - i0)] = acc[i][j][0];
+        if (col + 1 < n) Rn[(int64_t)(col + 1) * BF_NB + (row - i0)] = acc[i][j][1];
+      }
     }
 }
 
@@ -831,18 +841,27 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
     const auto& d = r.steps[sidx];
     const int j0 = (int)sidx * BF_NB;
     const dim3 dgrid(d.cnt, (L - m_first + BF_RCHUNK - 1) / BF_RCHUNK);
-    if (!getenv("OSPH_BF_DIAG_PATCH")) {  // register-row diagonal inverse + separate R copy
-      k_bf_rcopy<<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_r, o.bf);
+    // R = A[J, :] of this step: copied at step 0; afterwards written by the
+    // previous step's panel (J columns) and update (J-row tiles) into the
+    // other of two buffers (the variants below copy it every step instead)
+    const bool fused_r = !getenv("OSPH_BF_DIAG_PATCH") && !getenv("OSPH_BF_PANEL_FMA") && !p->bf_persistent;
+    double* rcur = p->d_bf_r + (fused_r ? (int64_t)(sidx & 1) * p->bf_r_half : 0);
+    double* rnext = fused_r ? p->d_bf_r + (int64_t)((sidx + 1) & 1) * p->bf_r_half : nullptr;
+    if (!getenv("OSPH_BF_DIAG_PATCH")) {  // register-row diagonal inverse (+ R copy when needed)
+      if (sidx == 0 || !fused_r) {
+        k_bf_rcopy<<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, rcur, o.bf);
+        p->launches++;
+      }
       k_bf_diag_rows<<<d.cnt, 64, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_status);
-      p->launches += 2;
+      p->launches++;
     } else {  // 4 x 4 register patch per thread, R copied by the same kernel
-      k_bf_diag<<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_bf_r, o.bf,
+      k_bf_diag<<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, rcur, o.bf,
                                               p->d_status);
       p->launches++;
     }
     if (!getenv("OSPH_BF_PANEL_FMA"))
       k_bf_panel_mma<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_panel, d.cnt, o.ainv,
-                                                       p->d_ainv, p->d_bf_d, p->d_bf_e, o.bf);
+                                                       p->d_ainv, p->d_bf_d, p->d_bf_e, o.bf, rnext);
     else
       k_bf_panel<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_panel, d.cnt, o.ainv,
                                                    p->d_ainv, p->d_bf_d, p->d_bf_e, o.bf);
@@ -850,11 +869,11 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
     if (d.n_upd > 0 && p->bf_persistent) {
       const int ctas = std::min(d.n_upd, p->num_sms);
       k_bf_update_p<<<ctas, BF_THREADS, sizeof(BfStageP) * 2, st>>>(L, m_first, j0, r.d_tab + d.pre_upd, d.cnt,
-                                                                   d.n_upd, o.ainv, p->d_ainv, p->d_bf_e, p->d_bf_r,
+                                                                   d.n_upd, o.ainv, p->d_ainv, p->d_bf_e, rcur,
                                                                    o.bf);
     } else if (d.n_upd > 0)
       k_bf_update<<<d.n_upd, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_upd, d.cnt, o.ainv, p->d_ainv,
-                                                  p->d_bf_e, p->d_bf_r, o.bf);
+                                                  p->d_bf_e, rcur, o.bf, rnext);
     if (d.n_upd > 0) p->launches++;
   }
   if (p->need_norms) {

@@ -98,7 +98,8 @@ struct osph_plan {
   bool need_norms = true;        // this call checks conditioning (check=True): factor kernels accumulate norms
   int64_t* d_bf_off = nullptr;   // [L+1] offsets of the E / R panels (NB x lde(n) per order)
   double* d_bf_e = nullptr;
-  double* d_bf_r = nullptr;
+  double* d_bf_r = nullptr;      // two R buffers of bf_r_half doubles (alternating steps)
+  int64_t bf_r_half = 0;
   double* d_bf_d = nullptr;      // NB x NB diagonal-block inverses
   // windowed forward (window.cu): factor storage for all orders does not fit HBM
   bool windowed = false;

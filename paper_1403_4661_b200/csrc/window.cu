@@ -114,7 +114,9 @@ int alloc_factor_storage(osph_plan* p) {
     if (rf) W_TRY(dalloc_w(&p->d_at, (size_t)tot[1]));
     W_TRY(dalloc_w(&p->d_pbelow, (size_t)tot[2]));
     W_TRY(dalloc_w(&p->d_bf_e, (size_t)bf_tot));
-    W_TRY(dalloc_w(&p->d_bf_r, (size_t)bf_tot));
+    W_TRY(dalloc_w(&p->d_bf_r, (size_t)(2 * bf_tot)));  // two R buffers (alternating steps), zeroed once
+    W_TRY(cudaMemsetAsync(p->d_bf_r, 0, sizeof(double) * (size_t)(2 * bf_tot), st));
+    p->bf_r_half = bf_tot;
     W_TRY(dalloc_w(&p->d_bf_d, (size_t)bf_diag_doubles(std::max(1, L - p->bf_nmin))));
     // padding of the tiled operands stays zero forever (the kernels write only real entries)
     W_TRY(cudaMemsetAsync(p->d_pbelow, 0, sizeof(double) * (size_t)tot[2], st));
@@ -158,7 +160,9 @@ int alloc_factor_storage(osph_plan* p) {
   if (rf) W_TRY(dalloc_w(&p->d_at, (size_t)mx[1]));
   W_TRY(dalloc_w(&p->d_pbelow, (size_t)mx[2]));
   W_TRY(dalloc_w(&p->d_bf_e, (size_t)mx[3]));
-  W_TRY(dalloc_w(&p->d_bf_r, (size_t)mx[3]));
+  W_TRY(dalloc_w(&p->d_bf_r, (size_t)(2 * mx[3])));
+  W_TRY(cudaMemsetAsync(p->d_bf_r, 0, sizeof(double) * (size_t)(2 * mx[3]), st));
+  p->bf_r_half = mx[3];
   W_TRY(dalloc_w(&p->d_bf_d, (size_t)bf_diag_doubles(max_orders)));
   return OSPH_OK;
 }
