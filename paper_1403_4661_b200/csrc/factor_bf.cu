@@ -299,14 +299,16 @@ __global__ void __launch_bounds__(64) k_bf_diag_rows(int L, int m_first, int j0,
   for (int c = 0; c < BF_NB; ++c)
     d[c] = (r < nb && c < nb) ? __ldcg(A + (int64_t)(j0 + c) * n + j0 + r) : (r == c ? 1.0 : 0.0);
   bool bad = false;
-  auto publish = [&](double* pn) {
+  // rinv = 1 / d[0], computed by every row as soon as its new d[0] exists so
+  // the division's latency hides under the row update (only row p + 1 uses it)
+  auto publish = [&](double* pn, double rinv) {
 #pragma unroll
     for (int c = 0; c < BF_NB - 2; c += 2) *reinterpret_cast<double2*>(pn + c) = make_double2(d[c + 1], d[c + 2]);
     if (d[0] == 0.0 || !isfinite(d[0])) bad = true;
-    *reinterpret_cast<double2*>(pn + BF_NB - 2) = make_double2(d[BF_NB - 1], 1.0 / d[0]);
+    *reinterpret_cast<double2*>(pn + BF_NB - 2) = make_double2(d[BF_NB - 1], rinv);
   };
   double rsc = 1.0;
-  if (r == 0) publish(rec[0]);
+  if (r == 0) publish(rec[0], 1.0 / d[0]);
 #pragma unroll 1
   for (int p = 0; p < BF_NB; ++p) {
     __syncthreads();
@@ -315,14 +317,18 @@ __global__ void __launch_bounds__(64) k_bf_diag_rows(int L, int m_first, int j0,
     const bool ispiv = r == p;
     const double gg = ispiv ? 0.0 : d[0] * inv;
     rsc = ispiv ? inv : rsc;
+    const double2 v0 = *reinterpret_cast<const double2*>(pr);
+    d[0] = fma(-gg, v0.x, d[1]);
+    const double rinv = 1.0 / d[0];
+    d[1] = fma(-gg, v0.y, d[2]);
 #pragma unroll
-    for (int c = 0; c < BF_NB - 1; c += 2) {
+    for (int c = 2; c < BF_NB - 1; c += 2) {
       const double2 v = *reinterpret_cast<const double2*>(pr + c);
       d[c] = fma(-gg, v.x, d[c + 1]);
       if (c + 1 < BF_NB - 1) d[c + 1] = fma(-gg, v.y, d[c + 2]);
     }
     d[BF_NB - 1] = ispiv ? 1.0 : -gg;
-    if (r == p + 1) publish(rec[(p + 1) & 1]);
+    if (r == p + 1) publish(rec[(p + 1) & 1], rinv);
   }
   if (bad) atomicOr(status + m, 1);
   double* Dg = dbuf + (size_t)blockIdx.x * BF_NB * BF_NB;  // D[r][c] at c * NB + r
@@ -583,6 +589,100 @@ __global__ void __launch_bounds__(BF_THREADS, 3) k_bf_update(int L, int m_first,
     }
 }
 
+// ---- 2c (wide). The same update on 128 x 64 tiles: eight warps of 32 x 32,
+// so each k-step loads 8 fragments for 16 DMMAs (the 64 x 64 tile: 6 for 8)
+// and every E / R element staged in shared memory feeds twice the math.
+// 101 KB of shared memory, two CTAs per SM.  Default (OSPH_BF_UPD_ROWS=64
+// selects the 64 x 64 kernel above).
+#define BF_TW 128
+#define BF_LDW (BF_TW + 4)
+__global__ void __launch_bounds__(BF_THREADS, 2) k_bf_update_w(int L, int m_first, int j0, const int* __restrict__ pre,
+                                                               int cnt, const int64_t* __restrict__ ainv_off,
+                                                               double* __restrict__ ainv, const double* __restrict__ ebuf,
+                                                               const double* __restrict__ rbuf,
+                                                               const int64_t* __restrict__ bf_off,
+                                                               double* __restrict__ rnext) {
+  extern __shared__ __align__(16) double bf_sm[];
+  double(*Et)[BF_LDW] = reinterpret_cast<double(*)[BF_LDW]>(bf_sm);                  // [k][row]
+  double(*Rt)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm + BF_NB * BF_LDW);  // [col][k]
+  __shared__ int s_oi;
+  if (threadIdx.x < 32) {
+    const int oi_w = bf_find_warp(pre, cnt, blockIdx.x);
+    if (threadIdx.x == 0) s_oi = oi_w;
+  }
+  __syncthreads();
+  const int oi = s_oi;
+  const int m = m_first + oi;
+  const int n = L - m, lde = bf_lde(n);
+  const int nb = min(BF_NB, n - j0);
+  const int nt = (n + BF_TW - 1) / BF_TW;
+  const int local = blockIdx.x - __ldg(pre + oi);
+  const int rt = local % nt;
+  int ct = local / nt;
+  if (ct >= j0 / BF_T) ++ct;  // skip the panel's column tile
+  const int i0 = rt * BF_TW, c0 = ct * BF_T;
+  double* A = ainv + __ldg(ainv_off + m);
+  const double* E = ebuf + __ldg(bf_off + m);
+  const double* R = rbuf + __ldg(bf_off + m);
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < BF_TW * BF_NB / 2; idx += BF_THREADS) {
+    const int k = idx >> 6, r2 = (idx & 63) * 2;  // E: column k, rows r2, r2+1
+    if (k < nb && i0 + r2 + 1 < lde) bf_cp16(&Et[k][r2], E + (int64_t)k * lde + i0 + r2);
+    else {
+      Et[k][r2] = 0.0;
+      Et[k][r2 + 1] = 0.0;
+    }
+  }
+  for (int idx = tid; idx < BF_T * BF_NB / 2; idx += BF_THREADS) {
+    const int c = idx >> 5, k2 = (idx & 31) * 2;  // R: column c0 + c, k2, k2+1
+    if (c0 + c < n) bf_cp16(&Rt[c][k2], R + (int64_t)(c0 + c) * BF_NB + k2);
+    else {
+      Rt[c][k2] = 0.0;
+      Rt[c][k2 + 1] = 0.0;
+    }
+  }
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = (warp & 3) * 32, wc = (warp >> 2) * 32;  // warp tile 32 rows x 32 cols
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int row = i0 + wr + 8 * i + g, col = c0 + wc + 8 * j + 2 * t;
+      acc[i][j][0] = (row < n && col < n) ? __ldcg(A + (int64_t)col * n + row) : 0.0;
+      acc[i][j][1] = (row < n && col + 1 < n) ? __ldcg(A + (int64_t)(col + 1) * n + row) : 0.0;
+    }
+  bf_cp_wait_all();
+  __syncthreads();
+#pragma unroll 2
+  for (int k0 = 0; k0 < BF_NB; k0 += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = Et[k0 + t][wr + 8 * i + g];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = Rt[wc + 8 * j + g][k0 + t];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+  double* Rn = rnext ? rnext + __ldg(bf_off + m) : nullptr;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int row = i0 + wr + 8 * i + g, col = c0 + wc + 8 * j + 2 * t;
+      if (row < n && col < n) A[(int64_t)col * n + row] = acc[i][j][0];
+      if (row < n && col + 1 < n) A[(int64_t)(col + 1) * n + row] = acc[i][j][1];
+      // the next step's R = A[J', :] (rows j0 + 64 .. j0 + 127; never split across 128-row tiles)
+      if (Rn && row >= j0 + BF_NB && row < j0 + 2 * BF_NB && row < n) {
+        if (col < n) Rn[(int64_t)col * BF_NB + (row - j0 - BF_NB)] = acc[i][j][0];
+        if (col + 1 < n) Rn[(int64_t)(col + 1) * BF_NB + (row - j0 - BF_NB)] = acc[i][j][1];
+      }
+    }
+}
+
 // ---- 2c'. Persistent, software-pipelined variant of the update: one CTA per
 // SM walks a contiguous range of work items (consecutive items share the
 // order, so the item -> order mapping advances incrementally instead of being
@@ -794,6 +894,16 @@ cudaError_t bf_prepare(osph_plan* p, int m_first, int m_last, BfRange* r) {
       }
     }
     d.n_upd = acc;
+    d.pre_updw = (int)tab.size();
+    acc = 0;
+    for (int o = 0; o <= cnt; ++o) {
+      tab.push_back(acc);
+      if (o < cnt) {
+        const int n = L - (m_first + o);
+        acc += ((n + BF_TW - 1) / BF_TW) * ((n + BF_T - 1) / BF_T - 1);
+      }
+    }
+    d.n_updw = acc;
   }
   cudaError_t e;
   cudaFree(r->d_tab);
@@ -817,6 +927,11 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
     return e;
   if ((e = cudaFuncSetAttribute(k_bf_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)
     return e;
+  const size_t smw = sizeof(double) * (BF_NB * BF_LDW + BF_T * BF_LDS) + 16;
+  if ((e = cudaFuncSetAttribute(k_bf_update_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw)) !=
+      cudaSuccess)
+    return e;
+  static const bool upd_wide = !(getenv("OSPH_BF_UPD_ROWS") && atoi(getenv("OSPH_BF_UPD_ROWS")) == 64);
   if ((e = cudaFuncSetAttribute(k_bf_update_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(sizeof(BfStageP) * 2))) != cudaSuccess)
     return e;
@@ -871,7 +986,10 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
       k_bf_update_p<<<ctas, BF_THREADS, sizeof(BfStageP) * 2, st>>>(L, m_first, j0, r.d_tab + d.pre_upd, d.cnt,
                                                                    d.n_upd, o.ainv, p->d_ainv, p->d_bf_e, rcur,
                                                                    o.bf);
-    } else if (d.n_upd > 0)
+    } else if (d.n_upd > 0 && upd_wide)
+      k_bf_update_w<<<d.n_updw, BF_THREADS, smw, st>>>(L, m_first, j0, r.d_tab + d.pre_updw, d.cnt, o.ainv,
+                                                      p->d_ainv, p->d_bf_e, rcur, o.bf, rnext);
+    else if (d.n_upd > 0)
       k_bf_update<<<d.n_upd, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_upd, d.cnt, o.ainv, p->d_ainv,
                                                   p->d_bf_e, rcur, o.bf, rnext);
     if (d.n_upd > 0) p->launches++;

@@ -6,7 +6,7 @@
 #include "common.cuh"
 
 struct BfStep {
-  int cnt = 0, pre_panel = 0, n_panel = 0, pre_upd = 0, n_upd = 0;
+  int cnt = 0, pre_panel = 0, n_panel = 0, pre_upd = 0, n_upd = 0, pre_updw = 0, n_updw = 0;  // updw: 128-row tiles
 };
 struct BfRange {  // work-item tables of one range of orders (factor_bf.cu)
   int m_first = -1, m_last = -1;
