@@ -95,8 +95,8 @@ def flops(L: int, B: int) -> dict:
 # workload, summarised under profiles/ by tools/ncu_summary.py), bytes per launch
 
 NCU_PROFILES = {  # (stage, L, B) -> summary file (a multi-kernel stage sums its kernels of one call)
-    ("sweep", 256, 64): "sweep_r01c_full.txt",
-    ("factor", 256, 64): "launches_r01c_summary.txt",
+    ("sweep", 256, 64): "sweep_r01d_full.txt",
+    ("factor", 256, 64): "launches_r01d_summary.txt",
 }
 
 

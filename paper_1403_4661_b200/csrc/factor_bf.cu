@@ -592,8 +592,8 @@ __global__ void __launch_bounds__(BF_THREADS, 3) k_bf_update(int L, int m_first,
 // ---- 2c (wide). The same update on 128 x 64 tiles: eight warps of 32 x 32,
 // so each k-step loads 8 fragments for 16 DMMAs (the 64 x 64 tile: 6 for 8)
 // and every E / R element staged in shared memory feeds twice the math.
-// 101 KB of shared memory, two CTAs per SM.  Default (OSPH_BF_UPD_ROWS=64
-// selects the 64 x 64 kernel above).
+// 101 KB of shared memory, two CTAs per SM.  Default for L >= 1024
+// (OSPH_BF_UPD_ROWS=64|128 forces either kernel).
 #define BF_TW 128
 #define BF_LDW (BF_TW + 4)
 __global__ void __launch_bounds__(BF_THREADS, 2) k_bf_update_w(int L, int m_first, int j0, const int* __restrict__ pre,
@@ -931,7 +931,10 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
   if ((e = cudaFuncSetAttribute(k_bf_update_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw)) !=
       cudaSuccess)
     return e;
-  static const bool upd_wide = !(getenv("OSPH_BF_UPD_ROWS") && atoi(getenv("OSPH_BF_UPD_ROWS")) == 64);
+  // 128-row tiles win at large L (config 4: 1.574 vs 1.564 transforms/s), 64-row ones at L = 256
+  // (config 2: 32.5k vs 32.3k); OSPH_BF_UPD_ROWS=64|128 forces one
+  static const int upd_rows_env = getenv("OSPH_BF_UPD_ROWS") ? atoi(getenv("OSPH_BF_UPD_ROWS")) : 0;
+  const bool upd_wide = upd_rows_env ? upd_rows_env == 128 : L >= 1024;
   if ((e = cudaFuncSetAttribute(k_bf_update_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(sizeof(BfStageP) * 2))) != cudaSuccess)
     return e;
@@ -959,7 +962,8 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
     // R = A[J, :] of this step: copied at step 0; afterwards written by the
     // previous step's panel (J columns) and update (J-row tiles) into the
     // other of two buffers (the variants below copy it every step instead)
-    const bool fused_r = !getenv("OSPH_BF_DIAG_PATCH") && !getenv("OSPH_BF_PANEL_FMA") && !p->bf_persistent;
+    static const bool rfuse_env = !(getenv("OSPH_BF_RFUSE") && atoi(getenv("OSPH_BF_RFUSE")) == 0);
+    const bool fused_r = rfuse_env && !getenv("OSPH_BF_DIAG_PATCH") && !getenv("OSPH_BF_PANEL_FMA") && !p->bf_persistent;
     double* rcur = p->d_bf_r + (fused_r ? (int64_t)(sidx & 1) * p->bf_r_half : 0);
     double* rnext = fused_r ? p->d_bf_r + (int64_t)((sidx + 1) & 1) * p->bf_r_half : nullptr;
     if (!getenv("OSPH_BF_DIAG_PATCH")) {  // register-row diagonal inverse (+ R copy when needed)
