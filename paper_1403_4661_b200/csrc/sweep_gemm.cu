@@ -10,7 +10,7 @@
 // per-team kernel (whose teams no longer fit the GPU at once for large B).
 // Tiles: 16 rows x 64 columns (16 maps x {+,-} x {re, im}) per CTA (twice
 // the CTAs of 32-row tiles: measured 14.3 -> 12.4 ms at config 3), K in
-// 32-wide chunks double-buffered by 16-byte cp.async; A operands are the
+// 32-wide chunks in a 3-stage 16-byte cp.async ring; A operands are the
 // chunk-major 8-row tiles the factorisation writes (each 8-row x 32-k piece
 // is one contiguous 2 KB run), B operands come straight from R / xbuf.
 #include "plan.cuh"
@@ -27,8 +27,6 @@ __device__ __forceinline__ void sg_cp16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sg_smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void sg_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void sg_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
-__device__ __forceinline__ void sg_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 struct SgStage {
   double a[SG_TM / 8][SG_KC][8];          // row tiles as stored: [k][row % 8]
@@ -37,7 +35,10 @@ struct SgStage {
 
 // MODE 0: solve (A = X_s tiles, rows = degrees, K = rings, B = R slab of order s)
 // MODE 1: corrections (A = Pb_s tiles, rows = rings k < s, K = degrees, B = xbuf)
-template <int MODE>
+template <int N>
+__device__ __forceinline__ void sg_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int MODE, int NS>
 __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, const double* __restrict__ atiles,
                                                            const int64_t* __restrict__ a_off,
                                                            const double* __restrict__ w_all, double2* __restrict__ R,
@@ -89,16 +90,19 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
 #pragma unroll
     for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  load(0, 0);
+  // NS-stage cp.async ring: chunks c+1 .. c+NS-1 in flight while chunk c multiplies
+  // (empty commit groups past the last chunk keep the group count uniform)
+#pragma unroll
+  for (int c = 0; c < NS - 1; ++c) {
+    if (c < nch) load(c, c);
+    else sg_commit();
+  }
   for (int c = 0; c < nch; ++c) {
-    if (c + 1 < nch) {
-      load((c + 1) & 1, c + 1);
-      sg_wait1();
-    } else {
-      sg_wait0();
-    }
-    __syncthreads();
-    const SgStage& S = st[c & 1];
+    sg_wait<NS - 2>();
+    __syncthreads();  // chunk c visible to all; stage (c - 1) % NS free
+    if (c + NS - 1 < nch) load((c + NS - 1) % NS, c + NS - 1);
+    else sg_commit();
+    const SgStage& S = st[c % NS];
 #pragma unroll
     for (int k0 = 0; k0 < SG_KC; k0 += 4) {
       double a[RB], b[2];
@@ -117,7 +121,6 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
 #pragma unroll
         for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
-    __syncthreads();
   }
 
   const double sg = (s & 1) ? -1.0 : 1.0;
@@ -173,25 +176,36 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
   }
 }
 
-cudaError_t launch_sweep_gemm(osph_plan* p, int B, double2* flm) {
+template <int NS>
+static cudaError_t sweep_gemm_run(osph_plan* p, int B, double2* flm) {
   const int L = p->L;
-  const size_t smem = 2 * sizeof(SgStage);
+  const size_t smem = NS * sizeof(SgStage);
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(k_sweep_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+  if ((e = cudaFuncSetAttribute(k_sweep_gemm<0, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
       cudaSuccess)
     return e;
-  if ((e = cudaFuncSetAttribute(k_sweep_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+  if ((e = cudaFuncSetAttribute(k_sweep_gemm<1, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
       cudaSuccess)
     return e;
   const int ny = (B + SG_MAPS - 1) / SG_MAPS;
   for (int s = L - 1; s >= 0; --s) {
     const int n = L - s;
-    k_sweep_gemm<0><<<dim3((n + SG_TM - 1) / SG_TM, ny), SG_THREADS, smem, p->stream>>>(
+    k_sweep_gemm<0, NS><<<dim3((n + SG_TM - 1) / SG_TM, ny), SG_THREADS, smem, p->stream>>>(
         L, s, B, p->d_xt, p->d_xt_off, p->d_w, p->d_r, p->d_xbuf, flm);
     if (s >= 1)
-      k_sweep_gemm<1><<<dim3((s + SG_TM - 1) / SG_TM, ny), SG_THREADS, smem, p->stream>>>(
+      k_sweep_gemm<1, NS><<<dim3((s + SG_TM - 1) / SG_TM, ny), SG_THREADS, smem, p->stream>>>(
           L, s, B, p->d_pbelow, p->d_pb_off, p->d_w, p->d_r, p->d_xbuf, flm);
   }
   p->launches += 2 * L - 1;
   return cudaGetLastError();
+}
+
+// cp.async stages of the K loop (OSPH_SG_STAGES=2|3|4).  Config 3 sweep:
+// 13.06 / 12.24 / 12.34 ms for 2 / 3 / 4 stages -- the loop is bound by the
+// L2 reads of the B chunks (every row-tile CTA re-reads them), not latency
+cudaError_t launch_sweep_gemm(osph_plan* p, int B, double2* flm) {
+  static const int ns = getenv("OSPH_SG_STAGES") ? atoi(getenv("OSPH_SG_STAGES")) : 3;
+  if (ns == 2) return sweep_gemm_run<2>(p, B, flm);
+  if (ns == 3) return sweep_gemm_run<3>(p, B, flm);
+  return sweep_gemm_run<4>(p, B, flm);
 }
