@@ -8,18 +8,14 @@
 // (s x n) x (n x 4B) for the corrections -- so each order runs as two
 // fp64 tensor-core GEMM launches over the whole GPU instead of the persistent
 // per-team kernel (whose teams no longer fit the GPU at once for large B).
-// Tiles: 16 rows x 64 columns (16 maps x {+,-} x {re, im}) per CTA (twice
-// the CTAs of 32-row tiles: measured 14.3 -> 12.4 ms at config 3), K in
-// 32-wide chunks in a 3-stage 16-byte cp.async ring; A operands are the
+// Tiles: 64 rows x 16 columns (4 maps x {+,-} x {re, im}) per CTA by
+// default (launch_sweep_gemm lists the measured shapes), K in 32-wide
+// chunks in a 4-stage 16-byte cp.async ring; A operands are the
 // chunk-major 8-row tiles the factorisation writes (each 8-row x 32-k piece
 // is one contiguous 2 KB run), B operands come straight from R / xbuf.
 #include "plan.cuh"
 
 #define SG_THREADS 256
-#ifndef SG_TM
-#define SG_TM 16   // rows per CTA (16: twice the CTAs of 32 at these per-order GEMM sizes)
-#endif
-#define SG_MAPS 16 // maps per CTA (64 real columns)
 #define SG_KC 32
 
 __device__ __forceinline__ uint32_t sg_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -28,9 +24,11 @@ __device__ __forceinline__ void sg_cp16(void* dst, const void* src) {
 }
 __device__ __forceinline__ void sg_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 
+// CTA tile: TM rows x MAPS maps (4 real columns per map)
+template <int TM, int MAPS>
 struct SgStage {
-  double a[SG_TM / 8][SG_KC][8];          // row tiles as stored: [k][row % 8]
-  double b[SG_MAPS][SG_KC][4];            // [map][k][+re, +im, -re, -im]
+  double a[TM / 8][SG_KC][8];          // row tiles as stored: [k][row % 8]
+  double b[MAPS][SG_KC][4];            // [map][k][+re, +im, -re, -im]
 };
 
 // MODE 0: solve (A = X_s tiles, rows = degrees, K = rings, B = R slab of order s)
@@ -38,18 +36,19 @@ struct SgStage {
 template <int N>
 __device__ __forceinline__ void sg_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-template <int MODE, int NS>
+template <int MODE, int NS, int TM, int MAPS>
 __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, const double* __restrict__ atiles,
                                                            const int64_t* __restrict__ a_off,
                                                            const double* __restrict__ w_all, double2* __restrict__ R,
                                                            double2* __restrict__ xbuf, double2* __restrict__ flm) {
   extern __shared__ __align__(16) unsigned char sg_raw[];
-  SgStage* st = reinterpret_cast<SgStage*>(sg_raw);
+  using Stage = SgStage<TM, MAPS>;
+  Stage* st = reinterpret_cast<Stage*>(sg_raw);
   const int n = L - s;
   const int M = MODE == 0 ? n : s;            // output rows
   const int nrt = MODE == 0 ? (n + 7) >> 3 : (s + 7) >> 3;
-  const int rt0 = blockIdx.x * (SG_TM / 8);   // first 8-row tile
-  const int b0 = blockIdx.y * SG_MAPS;
+  const int rt0 = blockIdx.x * (TM / 8);   // first 8-row tile
+  const int b0 = blockIdx.y * MAPS;
   const double* A = atiles + __ldg(a_off + s);
   const int64_t npos = (int64_t)L * (L + 1) / 2, p0 = packed_pos(L, s, 0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -57,16 +56,16 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
   const int nch = (n + SG_KC - 1) / SG_KC;
 
   auto load = [&](int buf, int c) {
-    SgStage& S = st[buf];
-    // A: SG_TM / 8 row tiles x 2 KB, contiguous within chunk c (zero past the last tile)
-    for (int i = tid; i < (SG_TM / 8) * 128; i += SG_THREADS) {  // 128 16-byte pieces per tile
+    Stage& S = st[buf];
+    // A: TM / 8 row tiles x 2 KB, contiguous within chunk c (zero past the last tile)
+    for (int i = tid; i < (TM / 8) * 128; i += SG_THREADS) {  // 128 16-byte pieces per tile
       const int t = i >> 7, q = i & 127;
       double* dst = &S.a[t][0][0] + 2 * q;
       if (rt0 + t < nrt) sg_cp16(dst, A + ((int64_t)c * nrt + rt0 + t) * 256 + 2 * q);
       else *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
     }
     // B: per map, 32 K-entries x {+, -} complex
-    for (int i = tid; i < SG_MAPS * SG_KC * 2; i += SG_THREADS) {
+    for (int i = tid; i < MAPS * SG_KC * 2; i += SG_THREADS) {
       const int mp = i / (SG_KC * 2), rem = i % (SG_KC * 2), k = rem >> 1, slot = rem & 1;
       const int kk = c * SG_KC + k, b = b0 + mp;
       double* dst = &S.b[mp][k][2 * slot];
@@ -81,9 +80,10 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
     sg_commit();
   };
 
-  // warp tile: rows (warp & 1) * (SG_TM / 2) .. (RB blocks of 8), columns (warp >> 1) * 16 .. +16 (2 blocks)
-  constexpr int RB = SG_TM / 16;
-  const int wr = (warp & 1) * (SG_TM / 2), wc = (warp >> 1) * 16;
+  // warps: WCG column groups of 16 (2 blocks of 8) x WRG row groups of RB blocks of 8
+  constexpr int WCG = MAPS / 4, WRG = 8 / WCG, RB = TM / (8 * WRG);
+  static_assert(WCG * WRG == 8 && RB >= 1 && RB * 8 * WRG == TM, "CTA tile does not map onto 8 warps");
+  const int wr = (warp % WRG) * (TM / WRG), wc = (warp / WRG) * 16;
   double acc[RB][2][2];
 #pragma unroll
   for (int i = 0; i < RB; ++i)
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
     __syncthreads();  // chunk c visible to all; stage (c - 1) % NS free
     if (c + NS - 1 < nch) load((c + NS - 1) % NS, c + NS - 1);
     else sg_commit();
-    const SgStage& S = st[c % NS];
+    const Stage& S = st[c % NS];
 #pragma unroll
     for (int k0 = 0; k0 < SG_KC; k0 += 4) {
       double a[RB], b[2];
@@ -176,36 +176,51 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
   }
 }
 
-template <int NS>
+template <int NS, int TM, int MAPS>
 static cudaError_t sweep_gemm_run(osph_plan* p, int B, double2* flm) {
   const int L = p->L;
-  const size_t smem = NS * sizeof(SgStage);
+  const size_t smem = NS * sizeof(SgStage<TM, MAPS>);
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(k_sweep_gemm<0, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
-      cudaSuccess)
+  if ((e = cudaFuncSetAttribute(k_sweep_gemm<0, NS, TM, MAPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem)) != cudaSuccess)
     return e;
-  if ((e = cudaFuncSetAttribute(k_sweep_gemm<1, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
-      cudaSuccess)
+  if ((e = cudaFuncSetAttribute(k_sweep_gemm<1, NS, TM, MAPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem)) != cudaSuccess)
     return e;
-  const int ny = (B + SG_MAPS - 1) / SG_MAPS;
+  const int ny = (B + MAPS - 1) / MAPS;
   for (int s = L - 1; s >= 0; --s) {
     const int n = L - s;
-    k_sweep_gemm<0, NS><<<dim3((n + SG_TM - 1) / SG_TM, ny), SG_THREADS, smem, p->stream>>>(
+    k_sweep_gemm<0, NS, TM, MAPS><<<dim3((n + TM - 1) / TM, ny), SG_THREADS, smem, p->stream>>>(
         L, s, B, p->d_xt, p->d_xt_off, p->d_w, p->d_r, p->d_xbuf, flm);
     if (s >= 1)
-      k_sweep_gemm<1, NS><<<dim3((s + SG_TM - 1) / SG_TM, ny), SG_THREADS, smem, p->stream>>>(
+      k_sweep_gemm<1, NS, TM, MAPS><<<dim3((s + TM - 1) / TM, ny), SG_THREADS, smem, p->stream>>>(
           L, s, B, p->d_pbelow, p->d_pb_off, p->d_w, p->d_r, p->d_xbuf, flm);
   }
   p->launches += 2 * L - 1;
   return cudaGetLastError();
 }
 
-// cp.async stages of the K loop (OSPH_SG_STAGES=2|3|4).  Config 3 sweep:
-// 13.06 / 12.24 / 12.34 ms for 2 / 3 / 4 stages -- the loop is bound by the
-// L2 reads of the B chunks (every row-tile CTA re-reads them), not latency
+// CTA tile rows x maps (OSPH_SG_SHAPE) and cp.async stages of the K loop
+// (OSPH_SG_STAGES).  The loop is bound by the L2 reads of the operand chunks
+// -- every CTA of a map group re-reads the B chunk, every map group the A
+// chunk -- so the tile shape decides.  Config 3 sweep (ms):
+//   16x16: 13.06 / 12.24 / 12.34 with 2 / 3 / 4 stages
+//   32x8: 11.25 / 10.99 / 11.12 with 3 / 4 / 6;  64x4: 11.07 / 10.79 / 12.34 with 3 / 4 / 6
+//   64x8: 13.21, 32x16: 14.02 with 3 (fewer CTAs)
 cudaError_t launch_sweep_gemm(osph_plan* p, int B, double2* flm) {
-  static const int ns = getenv("OSPH_SG_STAGES") ? atoi(getenv("OSPH_SG_STAGES")) : 3;
-  if (ns == 2) return sweep_gemm_run<2>(p, B, flm);
-  if (ns == 3) return sweep_gemm_run<3>(p, B, flm);
-  return sweep_gemm_run<4>(p, B, flm);
+  static const int ns = getenv("OSPH_SG_STAGES") ? atoi(getenv("OSPH_SG_STAGES")) : 4;
+  static const std::string shape = getenv("OSPH_SG_SHAPE") ? getenv("OSPH_SG_SHAPE") : "64x4";
+  if (shape == "32x8") {
+    if (ns == 6) return sweep_gemm_run<6, 32, 8>(p, B, flm);
+    return ns == 4 ? sweep_gemm_run<4, 32, 8>(p, B, flm) : sweep_gemm_run<3, 32, 8>(p, B, flm);
+  }
+  if (shape == "64x8") return ns == 4 ? sweep_gemm_run<4, 64, 8>(p, B, flm) : sweep_gemm_run<3, 64, 8>(p, B, flm);
+  if (shape == "32x16") return sweep_gemm_run<3, 32, 16>(p, B, flm);
+  if (shape == "64x4") {
+    if (ns == 6) return sweep_gemm_run<6, 64, 4>(p, B, flm);
+    return ns == 4 ? sweep_gemm_run<4, 64, 4>(p, B, flm) : sweep_gemm_run<3, 64, 4>(p, B, flm);
+  }
+  if (ns == 2) return sweep_gemm_run<2, 16, 16>(p, B, flm);
+  if (ns == 4) return sweep_gemm_run<4, 16, 16>(p, B, flm);
+  return sweep_gemm_run<3, 16, 16>(p, B, flm);
 }
