@@ -97,6 +97,8 @@ def flops(L: int, B: int) -> dict:
 NCU_PROFILES = {  # (stage, L, B) -> summary file (a multi-kernel stage sums its kernels of one call)
     ("sweep", 256, 64): "sweep_r01d_full.txt",
     ("factor", 256, 64): "launches_r01d_summary.txt",
+    ("sweep", 512, 256): "sweepgemm_r01e_launches.txt",
+    ("factor", 2048, 1): "launches_bf2048_r01e_summary.txt",
 }
 
 
@@ -113,6 +115,8 @@ def ncu_traffic(stage: str, L: int, B: int):
         elif len(parts) == 2 and parts[0] == "factor_chain_dram_bytes":
             total = float(parts[1])
             return total, f"profiles/{name} (DRAM bytes of the breadth-first factor chain of one forward call)"
+        elif len(parts) == 2 and parts[0] == "stage_dram_bytes":
+            return float(parts[1]), f"profiles/{name} (DRAM bytes of the stage's launches in one forward call)"
     return (total or None), f"profiles/{name} (dram__bytes_read.sum + dram__bytes_write.sum, one launch)"
 
 
