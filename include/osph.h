@@ -119,6 +119,27 @@ int osph_last_stage_times(const osph_plan* plan, double* seconds /* [6] */);
 /* Number of kernel launches enqueued by the last osph_inverse/osph_forward call. */
 int osph_last_launch_count(const osph_plan* plan);
 
+/* Which order-peeling sweep the last osph_forward ran (the chain of
+ * transform.py:441-463), or -1 before the first forward:
+ *   OSPH_SWEEP_PERSISTENT  one persistent cluster kernel (sweep.cu; L <= 1024, teams resident)
+ *   OSPH_SWEEP_GEMM        two whole-GPU DMMA GEMM launches per order (sweep_gemm.cu; large batches)
+ *   OSPH_SWEEP_LARGE       two launches per order + refinement (sweep_large.cu; L > 1024)
+ *   OSPH_SWEEP_WINDOWED    factor + large sweep window by window (window.cu; factors exceed HBM) */
+#define OSPH_SWEEP_PERSISTENT 0
+#define OSPH_SWEEP_GEMM 1
+#define OSPH_SWEEP_LARGE 2
+#define OSPH_SWEEP_WINDOWED 3
+int osph_last_sweep_kind(const osph_plan* plan);
+
+/* The grid's pivot order: perm[L(L+1)/2] (may be NULL), packed by order as
+ * perm[m*L - m(m-1)/2 + i] = ring offset (k - m) of pivot position i of order
+ * m's block -- the row order LU with partial pivoting (LAPACK getrf) picks for
+ * 2pi Y_lm(theta_k), k, l >= m (the blocks gelsy solves in blocks.py:88-116).
+ * Found on the first call that needs it (hand-written kernels, pivots.cu) and
+ * cached per grid; *seconds (may be NULL) = wall time this plan spent finding
+ * it (0 when the grid's order was already cached). */
+int osph_plan_pivots(osph_plan* plan, int32_t* perm, double* seconds);
+
 /* Thread-local description of the last error (empty string if none). */
 const char* osph_last_error(void);
 

@@ -18,6 +18,7 @@ LIB_PATH = _HERE / "libosph.so"
 
 OSPH_OK, OSPH_ERR_ARG, OSPH_ERR_ILLCOND, OSPH_ERR_CUDA, OSPH_ERR_NCCL = 0, 1, 2, 3, 4
 OSPH_HOST, OSPH_DEVICE, OSPH_ASYNC, OSPH_REAL = 0, 1, 2, 4
+SWEEP_KINDS = {0: "persistent", 1: "gemm", 2: "large", 3: "windowed"}
 ABI_VERSION = 1
 
 
@@ -46,6 +47,8 @@ SIGNATURES = {
     "osph_ring_analysis": (_I, [_P, _I, _I, _P, _I]),
     "osph_legendre_block": (_I, [_P, _I, _P, ctypes.c_int64, _I]),
     "osph_last_launch_count": (_I, [_P]),
+    "osph_last_sweep_kind": (_I, [_P]),
+    "osph_plan_pivots": (_I, [_P, _P, _P]),
     "osph_last_stage_times": (_I, [_P, _P]),
     "osph_last_error": (ctypes.c_char_p, []),
     "osph_abi_version": (_I, []),

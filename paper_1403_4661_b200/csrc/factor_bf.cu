@@ -1,11 +1,11 @@
-// factor_bf.cu -- batched, breadth-first blocked Gauss-Jordan inversion of the
-// large per-order blocks (n = L - m > 256) with the grid-determined pivot order.
+// factor_bf.cu -- batched, breadth-first blocked Gauss-Jordan inversion of
+// every per-order block with the grid-determined pivot order.
 //
-// Same result as factor.cu / factor_np.cu (explicit X = (P A_m)^{-1}, A_m =
-// 2pi Y_lm(theta_k), k >= m, l >= m; transform.py:416-429, blocks.py:88-116),
-// organised for throughput instead of per-order latency.  With the pivot
-// order known (recorded by the partial-pivoting kernel on the plan's first
-// call; it depends only on the grid), row i of the working matrix is ring
+// Explicit X = (P A_m)^{-1}, A_m = 2pi Y_lm(theta_k), k >= m, l >= m
+// (transform.py:416-429, blocks.py:88-116), organised for throughput instead
+// of per-order latency.  With the pivot order known (found once per grid by
+// pivots.cu, which runs these same kernels with a partial-pivoting search in
+// front of every panel step), row i of the working matrix is ring
 // m + perm[i] and Gauss-Jordan needs no interchanges, so a panel step on the
 // column block J = [j0, j0 + nb) is purely block-algebraic:
 //     D = A[J, J]^{-1}                 (nb x nb, one CTA per order)
@@ -16,7 +16,7 @@
 // The update (2 n^2 nb flops per order and step, nb = 64) is the bulk of the
 // work: 64 x 64 output tiles on the fp64 tensor cores (mma.sync m8n8k4 ->
 // DMMA.8x8x4), operands staged in shared memory.  After the last step the
-// epilogue emits the sweep operands exactly as factor_np.cu does (X in
+// epilogue emits the sweep operands (X in
 // chunk-major 8-row tiles with natural-order columns, w_m, u_m, j*, beta_m)
 // plus ||X||_1 for the condition estimate.
 #include <algorithm>
@@ -181,105 +181,13 @@ __global__ void __launch_bounds__(BF_THREADS) k_bf_colnorm(int L, int m_first, c
   if (lane == 0 && cmax > 0.0) bf_atomic_max_pos(norms + 2 * m + which, cmax);
 }
 
-// ---- 2a. D = A[J, J]^{-1} (in-place Gauss-Jordan, no interchanges) and the
-// row block R = A[J, :] (the update's B operand, snapshotted before the update).
-// Grid (orders, column chunks of BF_RCHUNK): every block copies its chunk of R,
-// block y = 0 also inverts D.  The inversion keeps a 4 x 4 patch of D per
-// thread in registers; per pivot only the pivot row and column go through
-// shared memory (double-buffered: one barrier per pivot).
-#define BF_RCHUNK 256
-__global__ void __launch_bounds__(BF_THREADS) k_bf_diag(int L, int m_first, int j0, const int64_t* __restrict__ ainv_off,
-                                                        const double* __restrict__ ainv, double* __restrict__ dbuf,
-                                                        double* __restrict__ rbuf, const int64_t* __restrict__ bf_off,
-                                                        int* __restrict__ status) {
-  __shared__ double s_row[2][BF_NB], s_col[2][BF_NB];
-  const int m = m_first + blockIdx.x;
-  const int n = L - m;
-  const int nb = min(BF_NB, n - j0);
-  const double* A = ainv + __ldg(ainv_off + m);
-  const int tid = threadIdx.x;
-  // R = A[J, :] for columns of this chunk, layout [col][NB]
-  {
-    double* R = rbuf + __ldg(bf_off + m);
-    const int c0 = blockIdx.y * BF_RCHUNK, c1 = min(n, c0 + BF_RCHUNK);
-    const int tot = (c1 - c0) * BF_NB;
-    // 8 independent loads in flight per thread before the stores
-    for (int base = 0; base < tot; base += 8 * BF_THREADS) {
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int idx = base + u * BF_THREADS + tid;
-        const int r = idx & (BF_NB - 1), c = c0 + (idx >> 6);
-        v[u] = (idx < tot && r < nb) ? __ldcg(A + (int64_t)c * n + j0 + r) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int idx = base + u * BF_THREADS + tid;
-        if (idx < tot) R[(int64_t)(c0 + (idx >> 6)) * BF_NB + (idx & (BF_NB - 1))] = v[u];
-      }
-    }
-  }
-  if (blockIdx.y != 0) return;
-  const int tr = tid >> 4, tc = tid & 15;  // patch rows 4tr.., columns 4tc..
-  double d[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int r = 4 * tr + i, c = 4 * tc + j;
-      d[i][j] = (r < nb && c < nb) ? __ldcg(A + (int64_t)(j0 + c) * n + j0 + r) : (r == c ? 1.0 : 0.0);
-    }
-  bool bad = false;
-  for (int p = 0; p < nb; ++p) {
-    const int buf = p & 1;
-    // static register indices only (a runtime index would spill d to local memory)
-    const int q = p & 3;
-    if ((p >> 2) == tr) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        s_row[buf][4 * tc + j] = q == 0 ? d[0][j] : q == 1 ? d[1][j] : q == 2 ? d[2][j] : d[3][j];
-    }
-    if ((p >> 2) == tc) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        s_col[buf][4 * tr + i] = q == 0 ? d[i][0] : q == 1 ? d[i][1] : q == 2 ? d[i][2] : d[i][3];
-    }
-    __syncthreads();
-    const double piv = s_row[buf][p];
-    const double inv = 1.0 / piv;
-    if (tid == 0 && (piv == 0.0 || !isfinite(piv))) bad = true;
-    double pc[4], pr[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) pc[i] = s_col[buf][4 * tr + i] * inv;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) pr[j] = s_row[buf][4 * tc + j];
-    // branch-free: rows r != p subtract pc * prow, row p scales by 1/piv,
-    // column p becomes -pc (its pivot entry 1/piv)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const bool rp = 4 * tr + i == p;
-      const double gi = rp ? 0.0 : pc[i];
-      const double si = rp ? inv : 1.0;
-      const double colv = rp ? inv : -pc[i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const double v = fma(-gi, pr[j], si * d[i][j]);
-        d[i][j] = (4 * tc + j == p) ? colv : v;
-      }
-    }
-  }
-  if (bad) atomicOr(status + m, 1);
-  double* Dg = dbuf + (size_t)blockIdx.x * BF_NB * BF_NB;  // D[r][c] at c * NB + r
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) Dg[(4 * tc + j) * BF_NB + 4 * tr + i] = d[i][j];
-}
 
-// ---- 2a'. The same D with a short dependency chain: 64 threads, one row of
+#define BF_RCHUNK 256  // columns per R-copy block
+
+// ---- 2a. D = A[J, J]^{-1} (in-place Gauss-Jordan, no interchanges): 64 threads, one row of
 // the identity-padded 64 x 64 block per thread in registers, kept ROTATED so
 // the current pivot column is always register 0 (static register indices in a
-// rolled loop, as factor_np.cu's panel step).  Per pivot the pivot row is
+// rolled loop).  Per pivot the pivot row is
 // published with its reciprocal through a double-buffered shared record (one
 // 64-thread barrier); every other row subtracts g = d[0] / piv times it; the
 // pivot row's own scale is applied at the end.  After 64 steps the rotation is
@@ -364,65 +272,10 @@ __global__ void __launch_bounds__(BF_THREADS) k_bf_rcopy(int L, int m_first, int
   }
 }
 
-// ---- 2b. E = -A[I, J] D (E[J] = D - I) per 64-row tile; A[I, J] = E + I_J.
-__global__ void __launch_bounds__(BF_THREADS) k_bf_panel(int L, int m_first, int j0, const int* __restrict__ pre,
-                                                         int cnt, const int64_t* __restrict__ ainv_off,
-                                                         double* __restrict__ ainv, const double* __restrict__ dbuf,
-                                                         double* __restrict__ ebuf, const int64_t* __restrict__ bf_off) {
-  extern __shared__ double bf_sm[];
-  double(*At)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm);                 // [k][row]
-  double(*Ds)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm + BF_NB * BF_LDS);  // [k][c]
-  __shared__ int s_oi;
-  if (threadIdx.x < 32) {
-    const int oi_w = bf_find_warp(pre, cnt, blockIdx.x);
-    if (threadIdx.x == 0) s_oi = oi_w;
-  }
-  __syncthreads();
-  const int oi = s_oi;
-  const int m = m_first + oi;
-  const int n = L - m, lde = bf_lde(n);
-  const int nb = min(BF_NB, n - j0);
-  const int i0 = (blockIdx.x - __ldg(pre + oi)) * BF_T;
-  double* A = ainv + __ldg(ainv_off + m);
-  const double* Dg = dbuf + (size_t)oi * BF_NB * BF_NB;
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < BF_T * BF_NB; idx += BF_THREADS) {
-    const int r = idx & (BF_T - 1), c = idx >> 6;
-    At[c][r] = (i0 + r < n && c < nb) ? __ldcg(A + (int64_t)(j0 + c) * n + i0 + r) : 0.0;
-    Ds[c][r] = __ldcg(Dg + idx);  // D[r][c] is stored at c * NB + r
-  }
-  __syncthreads();
-  double* E = ebuf + __ldg(bf_off + m);  // [col][lde]
-  const int r = tid & (BF_T - 1), cg4 = tid >> 6;  // row r, columns cg4*16 .. +16
-  const int gi = i0 + r;
-  const bool inJ = gi >= j0 && gi < j0 + nb;
-  double acc[16];
-#pragma unroll
-  for (int q = 0; q < 16; ++q) acc[q] = 0.0;
-  if (!inJ) {
-#pragma unroll 4
-    for (int k = 0; k < BF_NB; ++k) {
-      const double a = At[k][r];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) acc[q] = fma(a, Ds[cg4 * 16 + q][k], acc[q]);
-    }
-  }
-  if (gi < n) {
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int c = cg4 * 16 + q;
-      if (c >= nb) continue;
-      const double v = inJ ? Ds[c][gi - j0] - ((gi - j0 == c) ? 1.0 : 0.0) : -acc[q];
-      E[(int64_t)c * lde + gi] = v;
-      A[(int64_t)(j0 + c) * n + gi] = v + ((inJ && gi - j0 == c) ? 1.0 : 0.0);
-    }
-  }
-}
-
-// ---- 2b'. The panel on the tensor cores: one 64-row tile per CTA computes
+// ---- 2b. The panel on the tensor cores: one 64-row tile per CTA computes
 // A[I, J] D (64 x 64 x 64, DMMA, operands in shared memory: A[I, J] k-major,
 // D column-major as stored), then E = -A[I, J] D (E[J] = D - I) and
-// A[I, J] = E + I_J as k_bf_panel does.
+// A[I, J] = E + I_J.
 __global__ void __launch_bounds__(BF_THREADS, 3) k_bf_panel_mma(int L, int m_first, int j0, const int* __restrict__ pre,
                                                                 int cnt, const int64_t* __restrict__ ainv_off,
                                                                 double* __restrict__ ainv,
@@ -683,136 +536,6 @@ __global__ void __launch_bounds__(BF_THREADS, 2) k_bf_update_w(int L, int m_firs
     }
 }
 
-// ---- 2c'. Persistent, software-pipelined variant of the update: one CTA per
-// SM walks a contiguous range of work items (consecutive items share the
-// order, so the item -> order mapping advances incrementally instead of being
-// searched), and while it multiplies item i out of shared memory the
-// 16-/8-byte async copies of item i+1's E, R and C tiles are in flight.  Two
-// stages of (E, R, C) = 207 KB of shared memory.  Opt-in (OSPH_BF_PERSISTENT=1):
-// slower than three independent CTAs per SM at L = 2048 (691 vs 549 ms).
-#define BF_LDC (BF_T + 2)
-struct BfStageP {
-  double e[BF_NB][BF_LDS];  // [k][row]
-  double r[BF_T][BF_LDS];   // [col][k]
-  double c[BF_T][BF_LDC];   // [col][row]
-};
-__device__ __forceinline__ void bf_cp8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(bf_smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void bf_cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
-__device__ __forceinline__ void bf_cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-
-__global__ void __launch_bounds__(BF_THREADS, 1) k_bf_update_p(int L, int m_first, int j0, const int* __restrict__ pre,
-                                                               int cnt, int total, const int64_t* __restrict__ ainv_off,
-                                                               double* __restrict__ ainv,
-                                                               const double* __restrict__ ebuf,
-                                                               const double* __restrict__ rbuf,
-                                                               const int64_t* __restrict__ bf_off) {
-  extern __shared__ __align__(16) unsigned char bfp_raw[];
-  BfStageP* stg = reinterpret_cast<BfStageP*>(bfp_raw);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int per = (total + gridDim.x - 1) / gridDim.x;
-  const int it0 = blockIdx.x * per, it1 = min(total, it0 + per);
-  if (it0 >= it1) return;
-  __shared__ int s_oi0;
-  if (warp == 0) {
-    const int o = bf_find_warp(pre, cnt, it0);
-    if (lane == 0) s_oi0 = o;
-  }
-  __syncthreads();
-  // item cursor (identical in every thread)
-  int oi = s_oi0, base = __ldg(pre + oi), next = __ldg(pre + oi + 1);
-  auto item = [&](int it, int& m, int& n, int& i0, int& c0) {
-    while (it >= next) {
-      ++oi;
-      base = next;
-      next = __ldg(pre + oi + 1);
-    }
-    m = m_first + oi;
-    n = L - m;
-    const int nt = (n + BF_T - 1) / BF_T;
-    const int local = it - base;
-    int ct = local / nt;
-    if (ct >= j0 / BF_T) ++ct;
-    i0 = (local % nt) * BF_T;
-    c0 = ct * BF_T;
-  };
-  auto issue = [&](BfStageP& S, int m, int n, int i0, int c0) {
-    const int lde = bf_lde(n), nb = min(BF_NB, n - j0);
-    const double* A = ainv + __ldg(ainv_off + m);
-    const double* E = ebuf + __ldg(bf_off + m);
-    const double* R = rbuf + __ldg(bf_off + m);
-    for (int idx = tid; idx < BF_T * BF_NB / 2; idx += BF_THREADS) {
-      const int k = idx >> 5, r2 = (idx & 31) * 2;  // E: column k, rows r2, r2 + 1
-      if (k < nb && i0 + r2 + 1 < lde) bf_cp16(&S.e[k][r2], E + (int64_t)k * lde + i0 + r2);
-      else {
-        S.e[k][r2] = 0.0;
-        S.e[k][r2 + 1] = 0.0;
-      }
-      const int c = idx >> 5, k2 = (idx & 31) * 2;  // R: column c0 + c, k2, k2 + 1
-      if (c0 + c < n) bf_cp16(&S.r[c][k2], R + (int64_t)(c0 + c) * BF_NB + k2);
-      else {
-        S.r[c][k2] = 0.0;
-        S.r[c][k2 + 1] = 0.0;
-      }
-    }
-    for (int idx = tid; idx < BF_T * BF_T; idx += BF_THREADS) {  // C: column c0 + c, row i0 + r (8-byte pieces)
-      const int c = idx >> 6, r = idx & 63;
-      if (i0 + r < n && c0 + c < n) bf_cp8(&S.c[c][r], A + (int64_t)(c0 + c) * n + i0 + r);
-      else S.c[c][r] = 0.0;
-    }
-    bf_cp_commit();
-  };
-  const int wr = (warp & 1) * 32, wc = (warp >> 1) * 16;
-  int m, n, i0, c0;
-  item(it0, m, n, i0, c0);
-  issue(stg[0], m, n, i0, c0);
-  for (int it = it0; it < it1; ++it) {
-    const int cm = m, cn = n, ci0 = i0, cc0 = c0;
-    if (it + 1 < it1) {
-      item(it + 1, m, n, i0, c0);
-      issue(stg[(it + 1 - it0) & 1], m, n, i0, c0);
-      bf_cp_wait1();
-    } else {
-      bf_cp_wait_all();
-    }
-    __syncthreads();
-    const BfStageP& S = stg[(it - it0) & 1];
-    double acc[4][2][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int r = wr + 8 * i + g, c = wc + 8 * j + 2 * t;
-        acc[i][j][0] = S.c[c][r];
-        acc[i][j][1] = S.c[c + 1][r];
-      }
-#pragma unroll 4
-    for (int k0 = 0; k0 < BF_NB; k0 += 4) {
-      double a[4], b[2];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = S.e[k0 + t][wr + 8 * i + g];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) b[j] = S.r[wc + 8 * j + g][k0 + t];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-    }
-    double* A = ainv + __ldg(ainv_off + cm);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int row = ci0 + wr + 8 * i + g, col = cc0 + wc + 8 * j + 2 * t;
-        if (row < cn && col < cn) A[(int64_t)col * cn + row] = acc[i][j][0];
-        if (row < cn && col + 1 < cn) A[(int64_t)(col + 1) * cn + row] = acc[i][j][1];
-      }
-    __syncthreads();  // stage (it - it0) & 1 is refilled by the next iteration's issue
-  }
-}
-
 // ---- 3. sweep operands from X (column c = pivot position, ring perm[c]):
 // chunk-major tiles with natural-order columns (the late ring's column zero),
 // u_m[perm[c]] = Pb_m[m-1, :] X[:, c], and for c = j* (perm = 0): w_m, beta_m, j*.
@@ -912,6 +635,71 @@ cudaError_t bf_prepare(osph_plan* p, int m_first, int m_last, BfRange* r) {
   return cudaMemcpy(r->d_tab, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice);
 }
 
+static cudaError_t bf_attrs(int device) {
+  static bool done[64] = {};  // per device (function attributes are per context)
+  if (device >= 0 && device < 64 && done[device]) return cudaSuccess;
+  const size_t sm2 = sizeof(double) * 2 * BF_T * BF_LDS + 16;
+  const size_t smw = sizeof(double) * (BF_NB * BF_LDW + BF_T * BF_LDS) + 16;
+  cudaError_t e = cudaFuncSetAttribute(k_bf_panel_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_bf_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_bf_update_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
+  if (e == cudaSuccess && device >= 0 && device < 64) done[device] = true;
+  return e;
+}
+
+// The blocks of orders r.m_first..r.m_last, rows in the order p->d_piv gives
+// (plus, with the refinement buffer, the blocks in natural ring order).
+cudaError_t bf_generate(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffsets& o, bool with_at) {
+  const int L = p->L;
+  const int cnt_all = r.m_last - r.m_first + 1;
+  k_bf_generate<<<dim3((L + BF_THREADS - 1) / BF_THREADS, cnt_all), BF_THREADS, 0, st>>>(
+      L, r.m_first, p->d_cos, p->d_rec, p->d_ls, p->d_pstart, p->d_piv, o.ainv, o.pb, p->d_ainv, p->d_pbelow);
+  p->launches++;
+  if (with_at && p->d_at) {  // the blocks themselves for the sweep's refinement step, natural ring order
+    k_bf_generate_at<<<dim3((L + BF_THREADS - 1) / BF_THREADS, cnt_all), BF_THREADS, 0, st>>>(
+        L, r.m_first, p->d_cos, p->d_rec, p->d_ls, p->d_pstart, o.xt, p->d_at);
+    p->launches++;
+  }
+  return cudaGetLastError();
+}
+
+// One panel step (column block J = [j0, j0 + 64)) of every order with n > j0:
+// R = A[J, :] (copied, or handed off by the previous step when fused_r),
+// D = A[J, J]^{-1}, the panel E and the rank-64 update.
+cudaError_t bf_step(osph_plan* p, const BfRange& r, int sidx, cudaStream_t st, const BfOffsets& o, bool fused_r) {
+  const int L = p->L;
+  const int m_first = r.m_first;
+  cudaError_t e;
+  if ((e = bf_attrs(p->device)) != cudaSuccess) return e;
+  const size_t sm2 = sizeof(double) * 2 * BF_T * BF_LDS + 16;
+  const size_t smw = sizeof(double) * (BF_NB * BF_LDW + BF_T * BF_LDS) + 16;
+  // 128-row tiles win at large L (config 4: 1.574 vs 1.564 transforms/s), 64-row ones at L = 256
+  // (config 2: 32.5k vs 32.3k); OSPH_BF_UPD_ROWS=64|128 forces one
+  static const int upd_rows_env = getenv("OSPH_BF_UPD_ROWS") ? atoi(getenv("OSPH_BF_UPD_ROWS")) : 0;
+  const bool upd_wide = upd_rows_env ? upd_rows_env == 128 : L >= 1024;
+  const auto& d = r.steps[sidx];
+  const int j0 = sidx * BF_NB;
+  const dim3 dgrid(d.cnt, (L - m_first + BF_RCHUNK - 1) / BF_RCHUNK);
+  double* rcur = p->d_bf_r + (fused_r ? (int64_t)(sidx & 1) * p->bf_r_half : 0);
+  double* rnext = fused_r ? p->d_bf_r + (int64_t)((sidx + 1) & 1) * p->bf_r_half : nullptr;
+  if (sidx == 0 || !fused_r) {
+    k_bf_rcopy<<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, rcur, o.bf);
+    p->launches++;
+  }
+  k_bf_diag_rows<<<d.cnt, 64, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_status);
+  k_bf_panel_mma<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_panel, d.cnt, o.ainv,
+                                                     p->d_ainv, p->d_bf_d, p->d_bf_e, o.bf, rnext);
+  p->launches += 2;
+  if (d.n_upd > 0 && upd_wide)
+    k_bf_update_w<<<d.n_updw, BF_THREADS, smw, st>>>(L, m_first, j0, r.d_tab + d.pre_updw, d.cnt, o.ainv,
+                                                    p->d_ainv, p->d_bf_e, rcur, o.bf, rnext);
+  else if (d.n_upd > 0)
+    k_bf_update<<<d.n_upd, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_upd, d.cnt, o.ainv, p->d_ainv,
+                                                p->d_bf_e, rcur, o.bf, rnext);
+  if (d.n_upd > 0) p->launches++;
+  return cudaGetLastError();
+}
+
 // Factor orders r.m_first..r.m_last with the recorded pivot order, writing A/X,
 // Pb, the tiled X and the sweep constants at the given offset tables.
 cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffsets& o) {
@@ -919,85 +707,17 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
   const int m_first = r.m_first;
   const int cnt_all = r.m_last - r.m_first + 1;
   cudaError_t e;
-  const size_t sm2 = sizeof(double) * 2 * BF_T * BF_LDS + 16;
-  if ((e = cudaFuncSetAttribute(k_bf_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)
-    return e;
-  if ((e = cudaFuncSetAttribute(k_bf_panel_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) !=
-      cudaSuccess)
-    return e;
-  if ((e = cudaFuncSetAttribute(k_bf_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2)) != cudaSuccess)
-    return e;
-  const size_t smw = sizeof(double) * (BF_NB * BF_LDW + BF_T * BF_LDS) + 16;
-  if ((e = cudaFuncSetAttribute(k_bf_update_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw)) !=
-      cudaSuccess)
-    return e;
-  // 128-row tiles win at large L (config 4: 1.574 vs 1.564 transforms/s), 64-row ones at L = 256
-  // (config 2: 32.5k vs 32.3k); OSPH_BF_UPD_ROWS=64|128 forces one
-  static const int upd_rows_env = getenv("OSPH_BF_UPD_ROWS") ? atoi(getenv("OSPH_BF_UPD_ROWS")) : 0;
-  const bool upd_wide = upd_rows_env ? upd_rows_env == 128 : L >= 1024;
-  if ((e = cudaFuncSetAttribute(k_bf_update_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(sizeof(BfStageP) * 2))) != cudaSuccess)
-    return e;
-  if (p->num_sms == 0) {
-    cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device);
-    // measured at L = 2048: 691 ms persistent vs 549 ms one CTA per tile (3 CTAs/SM hide latency better)
-    p->bf_persistent = getenv("OSPH_BF_PERSISTENT") ? atoi(getenv("OSPH_BF_PERSISTENT")) != 0 : false;
-  }
-  k_bf_generate<<<dim3((L + BF_THREADS - 1) / BF_THREADS, cnt_all), BF_THREADS, 0, st>>>(
-      L, m_first, p->d_cos, p->d_rec, p->d_ls, p->d_pstart, p->d_piv, o.ainv, o.pb, p->d_ainv, p->d_pbelow);
-  if (p->d_at) {  // the blocks themselves for the sweep's refinement step, natural ring order
-    k_bf_generate_at<<<dim3((L + BF_THREADS - 1) / BF_THREADS, cnt_all), BF_THREADS, 0, st>>>(
-        L, m_first, p->d_cos, p->d_rec, p->d_ls, p->d_pstart, o.xt, p->d_at);
-    p->launches++;
-  }
-  p->launches++;
+  if ((e = bf_generate(p, r, st, o, true)) != cudaSuccess) return e;
   if (p->need_norms) {  // ||A||_1 and ||X||_1 feed only the check=True condition estimate
     k_bf_colnorm<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, o.ainv, p->d_ainv, p->d_norms, 0);
     p->launches++;
   }
-  for (size_t sidx = 0; sidx < r.steps.size(); ++sidx) {
-    const auto& d = r.steps[sidx];
-    const int j0 = (int)sidx * BF_NB;
-    const dim3 dgrid(d.cnt, (L - m_first + BF_RCHUNK - 1) / BF_RCHUNK);
-    // R = A[J, :] of this step: copied at step 0; afterwards written by the
-    // previous step's panel (J columns) and update (J-row tiles) into the
-    // other of two buffers (the variants below copy it every step instead)
-    static const bool rfuse_env = !(getenv("OSPH_BF_RFUSE") && atoi(getenv("OSPH_BF_RFUSE")) == 0);
-    const bool fused_r = rfuse_env && !getenv("OSPH_BF_DIAG_PATCH") && !getenv("OSPH_BF_PANEL_FMA") && !p->bf_persistent;
-    double* rcur = p->d_bf_r + (fused_r ? (int64_t)(sidx & 1) * p->bf_r_half : 0);
-    double* rnext = fused_r ? p->d_bf_r + (int64_t)((sidx + 1) & 1) * p->bf_r_half : nullptr;
-    if (!getenv("OSPH_BF_DIAG_PATCH")) {  // register-row diagonal inverse (+ R copy when needed)
-      if (sidx == 0 || !fused_r) {
-        k_bf_rcopy<<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, rcur, o.bf);
-        p->launches++;
-      }
-      k_bf_diag_rows<<<d.cnt, 64, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_status);
-      p->launches++;
-    } else {  // 4 x 4 register patch per thread, R copied by the same kernel
-      k_bf_diag<<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, rcur, o.bf,
-                                              p->d_status);
-      p->launches++;
-    }
-    if (!getenv("OSPH_BF_PANEL_FMA"))
-      k_bf_panel_mma<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_panel, d.cnt, o.ainv,
-                                                       p->d_ainv, p->d_bf_d, p->d_bf_e, o.bf, rnext);
-    else
-      k_bf_panel<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_panel, d.cnt, o.ainv,
-                                                   p->d_ainv, p->d_bf_d, p->d_bf_e, o.bf);
-    p->launches++;
-    if (d.n_upd > 0 && p->bf_persistent) {
-      const int ctas = std::min(d.n_upd, p->num_sms);
-      k_bf_update_p<<<ctas, BF_THREADS, sizeof(BfStageP) * 2, st>>>(L, m_first, j0, r.d_tab + d.pre_upd, d.cnt,
-                                                                   d.n_upd, o.ainv, p->d_ainv, p->d_bf_e, rcur,
-                                                                   o.bf);
-    } else if (d.n_upd > 0 && upd_wide)
-      k_bf_update_w<<<d.n_updw, BF_THREADS, smw, st>>>(L, m_first, j0, r.d_tab + d.pre_updw, d.cnt, o.ainv,
-                                                      p->d_ainv, p->d_bf_e, rcur, o.bf, rnext);
-    else if (d.n_upd > 0)
-      k_bf_update<<<d.n_upd, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_upd, d.cnt, o.ainv, p->d_ainv,
-                                                  p->d_bf_e, rcur, o.bf, rnext);
-    if (d.n_upd > 0) p->launches++;
-  }
+  // R = A[J, :] of a step: copied at step 0; afterwards written by the previous
+  // step's panel (J columns) and update (J-row tiles) into the other of two
+  // buffers (OSPH_BF_RFUSE=0 copies it every step instead; bit-identical)
+  static const bool fused_r = !(getenv("OSPH_BF_RFUSE") && atoi(getenv("OSPH_BF_RFUSE")) == 0);
+  for (size_t sidx = 0; sidx < r.steps.size(); ++sidx)
+    if ((e = bf_step(p, r, (int)sidx, st, o, fused_r)) != cudaSuccess) return e;
   if (p->need_norms) {
     k_bf_colnorm<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, o.ainv, p->d_ainv, p->d_norms, 1);
     p->launches++;
@@ -1008,7 +728,7 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
   return cudaGetLastError();
 }
 
-// The non-windowed plan: every order with n > 256 (m <= L - 257), full offset tables.
+// The non-windowed plan: orders m_first..m_last, full offset tables.
 cudaError_t launch_factor_bf(osph_plan* p, int m_first, int m_last, cudaStream_t st) {
   cudaError_t e;
   if (p->bf_full.m_first != m_first || p->bf_full.m_last != m_last)

@@ -51,7 +51,7 @@ static void plan_free(osph_plan* p) {
   void* ptrs[] = {p->d_cos, p->d_sin, p->d_rec, p->d_ls, p->d_pstart, p->d_ring_order, p->d_fft_n,
                   p->d_chirp_off, p->d_bhat_off, p->d_chirp, p->d_bhat, p->d_tw, p->d_roots,
                   p->d_bluestein_rings, p->d_ainv_off, p->d_pb_off, p->d_ainv, p->d_pbelow, p->d_piv,
-                  p->d_norms, p->d_kappa, p->d_status, p->d_jstar, p->d_beta, p->d_u, p->d_w, p->d_xt_off, p->d_xt, p->d_panel,
+                  p->d_norms, p->d_kappa, p->d_status, p->d_jstar, p->d_beta, p->d_u, p->d_w, p->d_xt_off, p->d_xt,
                   p->d_fpack, p->d_g, p->d_r,
                   p->d_in, p->d_out, p->d_sw, p->d_xbuf, p->d_rres, p->d_at, p->d_bf_off, p->d_bf_e, p->d_bf_r,
                   p->d_bf_d};
@@ -68,12 +68,9 @@ static void plan_free(osph_plan* p) {
   if (p->ev_sweep_done) cudaEventDestroy(p->ev_sweep_done);
   if (p->s_in) cudaStreamDestroy(p->s_in);
   if (p->s_out) cudaStreamDestroy(p->s_out);
-  if (p->s_fac) cudaStreamDestroy(p->s_fac);
   cudaFree(p->d_z1);
   cudaFree(p->d_z2);
   free_windows(p);
-  for (cudaEvent_t& e : p->ev_fac)
-    if (e) cudaEventDestroy(e);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   delete p;
 }
@@ -83,6 +80,7 @@ extern "C" int osph_abi_version(void) { return OSPH_ABI_VERSION; }
 extern "C" const char* osph_last_error(void) { return g_last_error.c_str(); }
 
 extern "C" int osph_plan_create(int L, const double* thetas, int max_batch, int device, osph_plan** out) {
+  DeviceGuard guard;
   g_last_error.clear();
   if (!out) {
     osph_set_error("osph_plan_create: out is NULL");
@@ -144,8 +142,6 @@ extern "C" int osph_plan_create(int L, const double* thetas, int max_batch, int 
   if (getenv("OSPH_NO_STREAM_PRIORITY")) prio_hi = prio_lo;
   PLAN_TRY(cudaStreamCreateWithPriority(&p->s_in, cudaStreamNonBlocking, prio_hi));
   PLAN_TRY(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
-  PLAN_TRY(cudaStreamCreateWithPriority(&p->s_fac, cudaStreamNonBlocking, prio_hi));
-  for (cudaEvent_t& e : p->ev_fac) PLAN_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   for (int c = 0; c < osph_plan::kIoChunks; ++c) {
     PLAN_TRY(cudaEventCreateWithFlags(&p->ev_in[c], cudaEventDisableTiming));
     PLAN_TRY(cudaEventCreateWithFlags(&p->ev_done[c], cudaEventDisableTiming));
@@ -195,11 +191,13 @@ extern "C" int osph_plan_create(int L, const double* thetas, int max_batch, int 
 }
 
 extern "C" int osph_plan_destroy(osph_plan* plan) {
+  DeviceGuard guard;
   plan_free(plan);
   return OSPH_OK;
 }
 
 extern "C" int osph_plan_set_stream(osph_plan* p, void* stream) {
+  DeviceGuard guard;
   if (!p) {
     osph_set_error("plan is NULL");
     return OSPH_ERR_ARG;
@@ -258,10 +256,6 @@ static int ensure_forward(osph_plan* p) {
   CUDA_TRY(dalloc(&p->d_kappa, (size_t)L));
   CUDA_TRY(dalloc(&p->d_status, (size_t)L));
   CUDA_TRY(dalloc(&p->d_jstar, (size_t)L));
-  {
-    const size_t nmax = std::min(L, 256);
-    CUDA_TRY(dalloc(&p->d_panel, nmax * 2 * 32 * (((nmax + 15) / 16) * 16 + 4)));
-  }
   CUDA_TRY(dalloc(&p->d_beta, (size_t)L));
   CUDA_TRY(dalloc(&p->d_xbuf, (size_t)2 * L * B));
   CUDA_TRY(dalloc(&p->d_rres, (size_t)2 * L * B));
@@ -278,6 +272,13 @@ static int ensure_forward(osph_plan* p) {
   CUDA_TRY(cudaStreamSynchronize(st));
   p->fwd_ready = true;
   return OSPH_OK;
+}
+
+static int sweep_kind(const osph_plan* p) {
+  if (p->windowed) return OSPH_SWEEP_WINDOWED;
+  if (p->sweep_gemm) return OSPH_SWEEP_GEMM;
+  if (p->sweep_large) return OSPH_SWEEP_LARGE;
+  return OSPH_SWEEP_PERSISTENT;
 }
 
 static int check_call(osph_plan* p, int B, const void* a, void* b, int kind) {
@@ -429,7 +430,7 @@ static int forward_real(osph_plan* p, int B, const void* samples, void* flm, boo
     CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
   }
   CUDA_TRY(cudaEventRecord(p->ev[6], p->s_in));
-  if (!p->windowed) CUDA_TRY(launch_factor(p, p->s_in, p->s_fac));
+  if (!p->windowed) CUDA_TRY(launch_factor(p, p->s_in));
   CUDA_TRY(cudaEventRecord(p->ev[7], p->s_in));
   if (host) {
     CUDA_TRY(cudaMemcpyAsync(p->d_in, samples, bytes, cudaMemcpyHostToDevice, st));
@@ -444,6 +445,7 @@ static int forward_real(osph_plan* p, int B, const void* samples, void* flm, boo
   CUDA_TRY(cudaEventRecord(p->ev[8], st));
   if (p->windowed) CUDA_TRY(forward_windows(p, Bp, p->d_z2));
   else CUDA_TRY(launch_sweep(p, Bp, p->d_z2));
+  p->last_sweep_kind = sweep_kind(p);
   CUDA_TRY(cudaEventRecord(p->ev[9], st));
   CUDA_TRY(cudaEventRecord(p->ev_sweep_done, st));
   p->have_sweep_ev = true;
@@ -455,6 +457,7 @@ static int forward_real(osph_plan* p, int B, const void* samples, void* flm, boo
 }
 
 extern "C" int osph_inverse(osph_plan* p, int B, const void* flm, void* samples, int kind) {
+  DeviceGuard guard;
   g_last_error.clear();
   int rc = check_call(p, B, flm, samples, kind);
   if (rc) return rc;
@@ -507,6 +510,7 @@ extern "C" int osph_inverse(osph_plan* p, int B, const void* flm, void* samples,
 
 extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm, int kind, int check,
                             osph_stats* stats) {
+  DeviceGuard guard;
   g_last_error.clear();
   int rc = check_call(p, B, samples, flm, kind);
   if (rc) return rc;
@@ -516,7 +520,7 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
   }
   CUDA_TRY(cudaSetDevice(p->device));
   if ((rc = ensure_forward(p))) return rc;
-  if (!p->piv_ready && !getenv("OSPH_PIVOTS_GJ") && (rc = discover_pivots(p))) return rc;
+  if (!p->piv_ready && (rc = discover_pivots(p))) return rc;
   p->need_norms = check != 0;
   const bool host = !(kind & OSPH_DEVICE);
   if (host && (rc = ensure_io(p))) return rc;
@@ -541,6 +545,7 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
     CUDA_TRY(cudaEventRecord(p->ev[7], st));
     CUDA_TRY(cudaEventRecord(p->ev[8], st));
     CUDA_TRY(forward_windows(p, B, out));
+    p->last_sweep_kind = OSPH_SWEEP_WINDOWED;
     CUDA_TRY(cudaEventRecord(p->ev[9], st));
     CUDA_TRY(cudaEventRecord(p->ev_sweep_done, st));
     p->have_sweep_ev = true;
@@ -557,7 +562,7 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
       CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
     }
     CUDA_TRY(cudaEventRecord(p->ev[6], p->s_in));
-    CUDA_TRY(launch_factor(p, p->s_in, p->s_fac));
+    CUDA_TRY(launch_factor(p, p->s_in));
     CUDA_TRY(cudaEventRecord(p->ev[7], p->s_in));
     CUDA_TRY(cudaEventRecord(p->ev[4], st));
     CUDA_TRY(launch_ring_forward(p, B, (const double2*)samples));
@@ -577,7 +582,7 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
       CUDA_TRY(cudaEventRecord(p->ev_in[c], p->s_in));
     }
     CUDA_TRY(cudaEventRecord(p->ev[6], st));
-    CUDA_TRY(launch_factor(p, st, p->s_fac));
+    CUDA_TRY(launch_factor(p, st));
     CUDA_TRY(cudaEventRecord(p->ev[7], st));
     for (int c = 0; c < nch; ++c) {
       const int b0 = (int)((int64_t)B * c / nch), b1 = (int)((int64_t)B * (c + 1) / nch);
@@ -590,6 +595,7 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
   if (!(kind & OSPH_REAL) && !p->windowed) {
     CUDA_TRY(cudaEventRecord(p->ev[8], st));
     CUDA_TRY(launch_sweep(p, B, out));
+    p->last_sweep_kind = sweep_kind(p);
     CUDA_TRY(cudaEventRecord(p->ev[9], st));
     CUDA_TRY(cudaEventRecord(p->ev_sweep_done, st));
     p->have_sweep_ev = true;
@@ -639,6 +645,7 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
 }
 
 extern "C" int osph_legendre_block(osph_plan* p, int m, double* out, int64_t ld, int kind) {
+  DeviceGuard guard;
   g_last_error.clear();
   if (!p || !out) {
     osph_set_error("NULL plan or output pointer");
@@ -659,6 +666,7 @@ extern "C" int osph_legendre_block(osph_plan* p, int m, double* out, int64_t ld,
 }
 
 extern "C" int osph_ring_analysis(const double* ring, int n, int m, double* out, int device) {
+  DeviceGuard guard;
   g_last_error.clear();
   if (!ring || !out) {
     osph_set_error("NULL pointer");
@@ -688,6 +696,7 @@ extern "C" int osph_ring_analysis(const double* ring, int n, int m, double* out,
 }
 
 extern "C" int osph_last_stage_times(const osph_plan* p, double* seconds) {
+  DeviceGuard guard;
   if (!p || !seconds) {
     osph_set_error("NULL argument");
     return OSPH_ERR_ARG;
@@ -705,5 +714,26 @@ extern "C" int osph_last_stage_times(const osph_plan* p, double* seconds) {
     }
     seconds[i] = ms * 1e-3;
   }
+  return OSPH_OK;
+}
+
+extern "C" int osph_last_sweep_kind(const osph_plan* p) { return p ? p->last_sweep_kind : -1; }
+
+extern "C" int osph_plan_pivots(osph_plan* p, int32_t* perm, double* seconds) {
+  DeviceGuard guard;
+  g_last_error.clear();
+  if (!p) {
+    osph_set_error("plan is NULL");
+    return OSPH_ERR_ARG;
+  }
+  CUDA_TRY(cudaSetDevice(p->device));
+  int rc;
+  if ((rc = ensure_forward(p))) return rc;
+  if (!p->piv_ready && (rc = discover_pivots(p))) return rc;
+  if (perm) {
+    const size_t npk = (size_t)p->L * (p->L + 1) / 2;
+    CUDA_TRY(cudaMemcpy(perm, p->d_piv, sizeof(int32_t) * npk, cudaMemcpyDeviceToHost));
+  }
+  if (seconds) *seconds = p->pivot_seconds;
   return OSPH_OK;
 }

@@ -80,7 +80,8 @@ struct osph_plan {
   double* d_xt = nullptr;         // X_m in 8-row tiles (sweep operand)
   bool fwd_ready = false;        // forward buffers allocated
   bool piv_ready = false;        // d_piv holds the (grid-determined) pivot order of every order
-  double* d_panel = nullptr;     // static-pivot factorisation: panel hand-off buffers
+  double pivot_seconds = 0.0;    // host wall time of this plan's pivot discovery (0: cached per grid)
+  int last_sweep_kind = -1;      // OSPH_SWEEP_* of the last forward call
   int sweep_cfg_B = -1;          // cached sweep launch configuration for batch sweep_cfg_B
   int sweep_cfg[3] = {0, 0, 0};  // maps per team, cluster width, ring stages
   bool sweep_large = false;      // L > 1024 or nothing fits: two kernels per order (sweep_large.cu), plain R layout
@@ -90,11 +91,9 @@ struct osph_plan {
   double* d_at = nullptr;        // refinement: the blocks A_m themselves, tiled like X (offsets of X)
   int refine = 0;                // iterative-refinement steps per order in sweep_large (default 1 for L > 512)
   bool inv_ready = false;        // inverse buffers allocated
-  // breadth-first factorisation (factor_bf.cu): orders with n > 256, or every order when windowed
-  BfRange bf_full;               // the non-windowed range (m <= L - bf_nmin - 1)
+  // breadth-first factorisation (factor_bf.cu) of every order
+  BfRange bf_full;               // the non-windowed range (every order)
   int num_sms = 0;
-  bool bf_persistent = false;    // persistent pipelined update kernel (opt-in: OSPH_BF_PERSISTENT=1)
-  int bf_nmin = 0;               // orders with n > bf_nmin use factor_bf.cu, the rest factor_np.cu (OSPH_BF_NMIN)
   bool need_norms = true;        // this call checks conditioning (check=True): factor kernels accumulate norms
   int64_t* d_bf_off = nullptr;   // [L+1] offsets of the E / R panels (NB x lde(n) per order)
   double* d_bf_e = nullptr;
@@ -119,12 +118,29 @@ struct osph_plan {
   cudaEvent_t ev[10] = {};
   // host-buffer calls: copies on their own streams, overlapped with compute chunk by chunk
   static constexpr int kIoChunks = 4;
-  cudaStream_t s_in = nullptr, s_out = nullptr, s_fac = nullptr;
-  cudaEvent_t ev_fac[2] = {};
+  cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev_in[kIoChunks] = {}, ev_done[kIoChunks] = {}, ev_start = nullptr, ev_out = nullptr;
   cudaEvent_t ev_sweep_done = nullptr;  // last forward's sweep: the factor buffers are free again
   bool have_sweep_ev = false;
   bool have_inv = false, have_fwd = false;
+};
+
+// Saves the calling thread's current device and restores it on scope exit, so
+// an entry point that switches to the plan's device leaves the caller's
+// device (e.g. torch's current device) untouched.
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      cudaGetLastError();
+      prev = -1;
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
 };
 
 // last-error plumbing (plan.cu)
@@ -132,14 +148,13 @@ void osph_set_error(const std::string& msg);
 
 // ---- launchers (each returns cudaError_t of the launch) ----
 cudaError_t launch_tables(osph_plan* p);
-cudaError_t launch_legendre_block(osph_plan* p, int m, double* out, int64_t ld);  // tables.cu                                   // tables.cu
+cudaError_t launch_legendre_block(osph_plan* p, int m, double* out, int64_t ld);  // tables.cu
 cudaError_t launch_ring_inverse(osph_plan* p, int B, double2* samples);    // ringdft.cu
 // maps [bofs, bofs + nb) of a batch of B (nb < 0: all B)
 cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples, int bofs = 0, int nb = -1);  // ringdft.cu
 cudaError_t launch_pack(osph_plan* p, int B, const double2* flm);          // synth.cu
 cudaError_t launch_synth(osph_plan* p, int B);                             // synth.cu
-// factor classes on st (largest) and st2 (the rest; nullptr = all on st), joined into st
-cudaError_t launch_factor(osph_plan* p, cudaStream_t st = nullptr, cudaStream_t st2 = nullptr);  // factor.cu
+cudaError_t launch_factor(osph_plan* p, cudaStream_t st = nullptr);  // factor.cu: every order, breadth-first
 cudaError_t launch_sweep(osph_plan* p, int B, double2* flm);               // sweep.cu
 int sweep_maps_per_team(osph_plan* p, int B);
 cudaError_t launch_sweep_large(osph_plan* p, int B, double2* flm);  // sweep_large.cu
@@ -147,14 +162,16 @@ cudaError_t launch_sweep_gemm(osph_plan* p, int B, double2* flm);   // sweep_gem
 cudaError_t launch_factor_bf(osph_plan* p, int m_first, int m_last, cudaStream_t st);  // factor_bf.cu
 cudaError_t bf_prepare(osph_plan* p, int m_first, int m_last, BfRange* r);               // factor_bf.cu
 cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffsets& o); // factor_bf.cu
+cudaError_t bf_generate(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffsets& o, bool with_at);
+cudaError_t bf_step(osph_plan* p, const BfRange& r, int sidx, cudaStream_t st, const BfOffsets& o, bool fused_r);
 int64_t bf_panel_doubles(int n);
 int64_t bf_diag_doubles(int orders);
 cudaError_t launch_sweep_large_range(osph_plan* p, int B, double2* flm, int s_hi, int s_lo, const int64_t* xt_off,
                                      const int64_t* pb_off);  // sweep_large.cu
-int discover_pivots(osph_plan* p);
+int discover_pivots(osph_plan* p);  // pivots.cu: the grid's pivot order (once per grid), host-blocking
 int alloc_factor_storage(osph_plan* p);                        // window.cu
 void free_windows(osph_plan* p);                               // window.cu
 cudaError_t forward_windows(osph_plan* p, int B, double2* flm);  // window.cu: factor + sweep per window
 void window_times(osph_plan* p);                               // window.cu
-cudaError_t launch_kappa(osph_plan* p, cudaStream_t st);       // factor.cu  // pivots.cu: grid pivot order (cuSOLVER getrf), host-blocking  // sweep.cu: launch configuration (cached per B), 1/2/4
+cudaError_t launch_kappa(osph_plan* p, cudaStream_t st);       // factor.cu
 cudaError_t launch_ring_pair(int n, int m, const double2* v, double2* out, cudaStream_t st);  // ringdft.cu

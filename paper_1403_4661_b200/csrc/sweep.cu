@@ -701,10 +701,14 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
         const Job j = make_job(1, s, L, lgT, rank, SWEEP_KC, xt, xt_off, pbt, pb_off, false);
         run_job<CC>(j, ringC, cst, cphase, gw, SWEEP_WC, xrow + (size_t)(s & 1) * cfg.ldx * CC, CC, g, tq, lane,
                     [&](int k, int c, double v0, double v1) {
+          // the other tone of the same map sits in lane ^ 1 (columns c and c ^ 2);
+          // both lanes of a pair are always active together
+          const unsigned am = __activemask();
+          const double o0 = __shfl_xor_sync(am, v0, 1), o1 = __shfl_xor_sync(am, v1, 1);
           const int bl = c >> 2;
           if (k >= s - 1 || bl >= gm) return;  // ring s-1 is the chain
           const bool plus = (c & 2) == 0;
-          const double gr = plus ? v0 : ss * v0, gi = plus ? v1 : ss * v1;
+          double gr = plus ? v0 : ss * v0, gi = plus ? v1 : ss * v1;
           if (k == s - 2 && s - 3 >= SWEEP_PF_MIN) {
             // row 1 of order s-3 (ring s-2): its right-hand side was prefetched
             // before this correction, so the correction goes to every CTA's
@@ -722,6 +726,13 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
           }
           int tm, slot;
           corr_target(s, k, plus, tm, slot);
+          if (tm == 0) {
+            // s = 0 mod (2k+1): both tones land in bin 0 -- one reduction from the
+            // + lane (deterministic sum order, no racing pair of REDs)
+            if (!plus) return;
+            gr += ss * o0;
+            gi += ss * o1;
+          }
           // fire-and-forget reductions (RED.ADD.F64)
           double2* rp = Rt + (packed_pos(L, tm, k - tm) * 2 + slot) * G + bl;
           atomicAdd(&rp->x, -gr);

@@ -127,9 +127,12 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
 #pragma unroll
   for (int i = 0; i < RB; ++i) {
     const int row = rt0 * 8 + wr + 8 * i + g;
-    if (row >= M) continue;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
+      // the other slot of the same (row, map) is in lane ^ 1 (column col ^ 2)
+      const double or_ = MODE == 1 ? __shfl_xor_sync(0xffffffffu, acc[i][j][0], 1) : 0.0;
+      const double oi_ = MODE == 1 ? __shfl_xor_sync(0xffffffffu, acc[i][j][1], 1) : 0.0;
+      if (row >= M) continue;
       const int col = wc + 8 * j + 2 * tq;  // even: (re, im) of one (map, slot)
       const int mp = col >> 2, slot = (col >> 1) & 1, b = b0 + mp;
       if (b >= B) continue;
@@ -168,8 +171,15 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
           tm = nk - rr;
           ts = slot ^ 1;
         }
+        if (rr == 0) {
+          // both tones land in bin 0: one reduction from the slot-0 lane
+          // (deterministic sum order instead of two racing REDs)
+          if (slot) continue;
+          vr += sg * or_;
+          vi += sg * oi_;
+        }
         double2* rp = R + ((int64_t)b * npos + packed_pos(L, tm, k - tm)) * 2 + ts;
-        atomicAdd(&rp->x, -vr);  // r == 0 sends both tones to bin 0: reductions
+        atomicAdd(&rp->x, -vr);
         atomicAdd(&rp->y, -vi);
       }
     }

@@ -85,16 +85,8 @@ int alloc_factor_storage(osph_plan* p) {
   std::vector<int64_t> ao, xo, po, bo;
   int64_t tot[4];
   if (!p->windowed) {
-    // every order resident: offsets over all orders (the E/R panels only for the
-    // breadth-first orders n > 256; the others use factor_np.cu)
+    // every order resident: offsets over all orders
     range_offsets(L, 0, L - 1, ao, xo, po, bo, tot);
-    const char* env_nmin = getenv("OSPH_BF_NMIN");  // breadth-first for n > bf_nmin (default: every order)
-    p->bf_nmin = env_nmin ? std::max(0, atoi(env_nmin)) : 0;
-    int64_t bf_tot = 0;
-    for (int m = 0; m < L; ++m) {
-      bo[m] = bf_tot;
-      if (L - m > p->bf_nmin) bf_tot += bf_panel_doubles(L - m);
-    }
     p->h_ainv_off = ao;
     p->h_xt_off = xo;
     p->h_pb_off = po;
@@ -113,11 +105,11 @@ int alloc_factor_storage(osph_plan* p) {
     W_TRY(dalloc_w(&p->d_xt, (size_t)tot[1]));
     if (rf) W_TRY(dalloc_w(&p->d_at, (size_t)tot[1]));
     W_TRY(dalloc_w(&p->d_pbelow, (size_t)tot[2]));
-    W_TRY(dalloc_w(&p->d_bf_e, (size_t)bf_tot));
-    W_TRY(dalloc_w(&p->d_bf_r, (size_t)(2 * bf_tot)));  // two R buffers (alternating steps), zeroed once
-    W_TRY(cudaMemsetAsync(p->d_bf_r, 0, sizeof(double) * (size_t)(2 * bf_tot), st));
-    p->bf_r_half = bf_tot;
-    W_TRY(dalloc_w(&p->d_bf_d, (size_t)bf_diag_doubles(std::max(1, L - p->bf_nmin))));
+    W_TRY(dalloc_w(&p->d_bf_e, (size_t)tot[3]));
+    W_TRY(dalloc_w(&p->d_bf_r, (size_t)(2 * tot[3])));  // two R buffers (alternating steps), zeroed once
+    W_TRY(cudaMemsetAsync(p->d_bf_r, 0, sizeof(double) * (size_t)(2 * tot[3]), st));
+    p->bf_r_half = tot[3];
+    W_TRY(dalloc_w(&p->d_bf_d, (size_t)bf_diag_doubles(L)));
     // padding of the tiled operands stays zero forever (the kernels write only real entries)
     W_TRY(cudaMemsetAsync(p->d_pbelow, 0, sizeof(double) * (size_t)tot[2], st));
     W_TRY(cudaMemsetAsync(p->d_xt, 0, sizeof(double) * (size_t)tot[1], st));

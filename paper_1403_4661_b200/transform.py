@@ -152,6 +152,17 @@ class Plan:
     def last_launch_count(self) -> int:
         return int(self._lib.osph_last_launch_count(self._h))
 
+    def last_sweep_kind(self) -> str | None:
+        """Sweep variant of the last forward call: persistent / gemm / large / windowed."""
+        return _lib.SWEEP_KINDS.get(int(self._lib.osph_last_sweep_kind(self._h)))
+
+    def pivots(self) -> tuple[np.ndarray, float]:
+        """(perm packed by order, seconds this plan spent discovering it) -- osph_plan_pivots."""
+        perm = np.empty(self.L * (self.L + 1) // 2, dtype=np.int32)
+        sec = ctypes.c_double()
+        _lib.raise_for(self._lib.osph_plan_pivots(self._h, perm.ctypes.data_as(ctypes.c_void_p), ctypes.byref(sec)))
+        return perm, float(sec.value)
+
     def last_stage_times(self) -> np.ndarray:
         """Device seconds: last inverse's 3 stages, then last forward's 3 (osph_last_stage_times)."""
         out = np.zeros(6)
@@ -182,8 +193,9 @@ def get_plan(grid_or_thetas, batch: int = 1, device: int = 0) -> Plan:
     with _plans_lock:
         plan = _plans.get(key)
         if plan is None or plan.max_batch < batch:
-            if plan is not None:
-                plan.close()
+            # a smaller cached plan is only dropped from the cache, never closed here:
+            # another thread may hold it (between get_plan and its plan.lock, or inside
+            # a call); it is destroyed by Plan.__del__ when the last reference goes
             plan = Plan(th, max(batch, plan.max_batch * 2 if plan else batch), device)
             _plans[key] = plan
         return plan
@@ -192,7 +204,8 @@ def get_plan(grid_or_thetas, batch: int = 1, device: int = 0) -> Plan:
 def clear_plans() -> None:
     with _plans_lock:
         for p in _plans.values():
-            p.close()
+            with p.lock:  # wait for a call in flight on this plan
+                p.close()
         _plans.clear()
 
 
@@ -211,6 +224,25 @@ def _is_torch_cuda(x) -> bool:
     return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
 
 
+def _check_out(out, shape, device=None):
+    """The library writes B * L^2 complex128 values through ``out``: refuse anything else."""
+    if out is None:
+        return
+    if device is not None:  # torch tensor on the input's device
+        import torch
+
+        if not _is_torch_cuda(out) or out.device != device:
+            raise ValueError(f"out must be a CUDA tensor on {device}")
+        if out.dtype != torch.complex128 or not out.is_contiguous() or tuple(out.shape) != tuple(shape):
+            raise ValueError(f"out must be a contiguous complex128 tensor of shape {tuple(shape)}")
+        return
+    if not isinstance(out, np.ndarray):
+        raise ValueError("out must be a numpy array for host inputs")
+    if out.dtype != np.complex128 or not out.flags.c_contiguous or out.shape != tuple(shape) \
+            or not out.flags.writeable:
+        raise ValueError(f"out must be a writeable C-contiguous complex128 array of shape {tuple(shape)}")
+
+
 def _run(direction: str, data, grid, out=None, check: bool = True, device: int = 0, real: bool = False):
     """Shared driver: numpy (host) or CUDA torch tensor (device) batches of shape (B, L^2)."""
     L = grid.band_limit if hasattr(grid, "band_limit") else len(grid)
@@ -225,6 +257,7 @@ def _run(direction: str, data, grid, out=None, check: bool = True, device: int =
         x = x.contiguous()
         B = x.shape[0]
         dev = x.device.index or 0
+        _check_out(out, x.shape, x.device)
         y = out if out is not None else torch.empty_like(x)
         plan = get_plan(grid, B, dev)
         kind = _lib.OSPH_DEVICE | (_lib.OSPH_REAL if real else 0)
@@ -241,6 +274,7 @@ def _run(direction: str, data, grid, out=None, check: bool = True, device: int =
     if x.shape[-1] != L * L:
         raise BandLimitError(f"expected {L * L} values per map, got {x.shape[-1]}")
     B = x.shape[0]
+    _check_out(out, x.shape)
     y = out if out is not None else np.empty_like(x)
     plan = get_plan(grid, B, device)
     kind = _lib.OSPH_HOST | (_lib.OSPH_REAL if real else 0)

@@ -33,9 +33,9 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 OUT = Path(__file__).resolve().parent
 L = 4096
 SEED = 14034661
-M_STOP = 3968
+M_STOP = 3072
 RINGS = [0, 1, 63, 64, 2047, 2048, 3000, 4095]
-ORDERS = [3968, 3969, 4000, 4064, 4090, 4094, 4095]
+ORDERS = [3072, 3073, 3100, 3333, 3500, 3968, 4000, 4064, 4090, 4094, 4095]
 TMP = Path("/tmp/osph_golden4096_samples.npy")
 
 
