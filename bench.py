@@ -493,6 +493,114 @@ def run_ours(args, cfg):
         torch.distributed.destroy_process_group()
 
 
+def run_sharded(args, cfg, mode):
+    """--shard chain|factors: the transforms split over the ranks (distributed.ShardedTransform).
+
+    chain   one batch (configs[3]: one L=2048 map) across every rank: rings split in
+            the inverse, order blocks in the forward with the spectra and coefficients
+            handed down the chain (NCCL send/recv), "scaling": "strong";
+    factors every rank its own B maps; the per-order factorisation split by order
+            blocks and all-gathered (NCCL broadcasts) instead of repeated, "weak"."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1403_4661_b200 as osp
+    from paper_1403_4661_b200.distributed import ShardedTransform
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    L, B = cfg["L"], cfg["B"]
+    if cfg["real"]:
+        raise SystemExit("--shard runs complex maps (configs 1, 2, 4, 5)")
+    grid = osp.load_grid(ROOT / "tests" / "golden" / "grids" / cfg["grid"])
+    seed = 14034661 + 2 + (1000 * rank if mode == "factors" else 0)
+    flm_h = make_coefficients(L, B, seed, cfg["spectrum"], False)
+    flm = torch.from_numpy(flm_h).to(dev)
+    st = ShardedTransform(grid, B, mode)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        s = st.inverse(flm)
+        return st.forward(s), st.plan.last_launch_count()
+
+    back, _ = step()
+    torch.cuda.synchronize()
+    err = (back - flm).abs().max().item()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    total_ms, launches = 0.0, 0
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            _, nl = step()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            total_ms += ev0.elapsed_time(ev1)
+            launches += nl
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    maps_per_step = B if mode == "chain" else world * B
+    value = maps_per_step * args.steps / (total_ms * 1e-3)
+    # e2e: pinned host input, copied in every step; result copied out
+    flm_pin = torch.from_numpy(flm_h).pin_memory()
+    out_pin = torch.empty_like(flm_pin).pin_memory()
+    e2e_t = []
+    for _ in range(max(1, min(args.steps, 5))):
+        flush.fill_(1.0)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        x = flm_pin.to(dev, non_blocking=True)
+        s = st.inverse(x)
+        out_pin.copy_(st.forward(s, check=True))
+        torch.cuda.synchronize()
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_err = float((out_pin - flm_pin).abs().max())
+    e2e_mean = float(np.mean(e2e_t))
+    if world > 1:
+        t = torch.tensor([e2e_mean], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_mean = float(t.item())
+    if rank == 0:
+        m_lo, m_hi, k_lo, k_hi = st.ranges[0]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if mode == "chain" else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": dict(workload_config(cfg, args),
+                           parallelism=(f"order blocks x {world} ranks (chain: spectra + coefficients handed "
+                                        f"rank to rank, NCCL), rings split in the inverse" if mode == "chain" else
+                                        f"maps per rank, factorisation split by order blocks over {world} ranks "
+                                        f"and all-gathered (NCCL)"),
+                           global_batch=maps_per_step),
+            "shard": {"mode": mode, "rank0_orders": [m_lo, m_hi], "rank0_rings": [k_lo, k_hi]},
+            "e2e": {"value": maps_per_step / e2e_mean, "unit": UNIT,
+                    "h2d_bytes_per_step": int(B * L * L * 16), "d2h_bytes_per_step": int(B * L * L * 16)},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "roundtrip_max_err": max(err, e2e_err),
+        }
+        print(json.dumps(line), flush=True)
+    st.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -502,10 +610,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-maps", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shard", default="maps", choices=["maps", "factors", "chain"],
+                    help="maps: every rank its own batch (default); factors: shared factorisation; "
+                         "chain: one batch across the ranks by order blocks (configs[3])")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif args.shard != "maps":
+        run_sharded(args, cfg, args.shard)
     else:
         run_ours(args, cfg)
 

@@ -42,14 +42,14 @@
 extern "C" {
 #endif
 
-#define OSPH_ABI_VERSION 1
+#define OSPH_ABI_VERSION 2
 
 /* return codes */
 #define OSPH_OK 0
 #define OSPH_ERR_ARG 1        /* band-limit mismatch / bad argument (BandLimitError, ValueError) */
 #define OSPH_ERR_ILLCOND 2    /* per-order block numerically singular (IllConditionedSolveError) */
 #define OSPH_ERR_CUDA 3       /* CUDA runtime failure (no device, launch error, OOM) */
-#define OSPH_ERR_NCCL 4       /* reserved for the multi-GPU order-sharded path */
+#define OSPH_ERR_NCCL 4       /* inter-GPU exchange failed (peer copy / collective of a multi-GPU plan) */
 
 /* pointer kinds / flags for osph_inverse / osph_forward */
 #define OSPH_HOST 0   /* host pointers: the library copies in and out (pinned memory is fastest) */
@@ -75,10 +75,22 @@ typedef struct osph_stats {
   double total_seconds;   /* device time of the whole call */
 } osph_stats;
 
-/* Create a plan for band limit L on `device`.  thetas[L] are the ring
- * co-latitudes (ColatitudeGrid.thetas, ring k = ring with 2k+1 samples).
- * max_batch bounds B in later calls (workspace is sized for it). */
-int osph_plan_create(int L, const double* thetas, int max_batch, int device, osph_plan** out);
+/* Create a plan for band limit L on ndev devices devs[0..ndev-1].
+ * thetas[L] are the ring co-latitudes (ColatitudeGrid.thetas, ring k = ring
+ * with 2k+1 samples).  max_batch bounds B in later calls (workspace is sized
+ * for it).  ndev = 1: one device.  ndev > 1: one host thread drives every
+ * device (devices may repeat, e.g. for tests); osph_inverse / osph_forward
+ * then shard the work:
+ *   B >= ndev   maps split over the devices; the forward's per-order
+ *               factorisation is split by order blocks and the factors are
+ *               copied peer to peer to every device (no redundant factoring);
+ *   B <  ndev   one map chain: the inverse is split by ring ranges, the
+ *               forward by load-balanced blocks of orders m, each device
+ *               factoring its own block while the sweep passes the corrected
+ *               ring spectra and the completed coefficients from block to
+ *               block (peer copies over NVLink).
+ * Host pointers only for ndev > 1 (the plan owns every device's buffers). */
+int osph_plan_create(int L, const double* thetas, int max_batch, int ndev, const int* devs, osph_plan** out);
 int osph_plan_destroy(osph_plan* plan);
 
 /* Use `stream` (a cudaStream_t) for all work of this plan; NULL = plan-owned
@@ -142,6 +154,59 @@ int osph_plan_pivots(osph_plan* plan, int32_t* perm, double* seconds);
 
 /* Thread-local description of the last error (empty string if none). */
 const char* osph_last_error(void);
+
+/* ---- one process per GPU (torch.distributed / MPI drive the exchange) ----
+ * A single-device plan becomes rank `rank` of `nranks` (before its first
+ * forward):
+ *   OSPH_SHARD_CHAIN    one map (or a few) across GPUs: this plan factors and
+ *                       sweeps only its block of orders [m_lo, m_hi] (blocks
+ *                       descend in m with the rank: rank 0 owns the highest
+ *                       orders, cost-balanced by sum (L-m)^3) and its inverse
+ *                       synthesises only its rings [k_lo, k_hi).  Forward:
+ *                       RINGS|FACTOR, receive the spectra + coefficients from
+ *                       rank-1, SWEEP, send them to rank+1; the last rank
+ *                       holds every coefficient (transform.py:441-463 run as
+ *                       nranks consecutive blocks).
+ *   OSPH_SHARD_FACTORS  batches: FACTOR factors only [m_lo, m_hi]; the
+ *                       factor buffers are all-gathered (osph_shard_buffer);
+ *                       then RINGS|SWEEP transforms this rank's own maps.
+ * Returns OSPH_ERR_ARG if the plan already ran a forward. */
+#define OSPH_SHARD_CHAIN 1
+#define OSPH_SHARD_FACTORS 2
+int osph_plan_shard(osph_plan* plan, int rank, int nranks, int mode);
+
+/* The block of `rank` of `nranks` (no plan needed): orders [m_lo, m_hi] and
+ * rings [k_lo, k_hi) (rings only split in chain mode). */
+int osph_shard_range(int L, int rank, int nranks, int mode, int* m_lo, int* m_hi, int* k_lo, int* k_hi);
+
+/* Forward transform in stages (device pointers; OSPH_ASYNC allowed):
+ * RINGS = ring DFTs of every ring of `samples` into the plan's spectra,
+ * FACTOR = factorisation of the plan's orders, SWEEP = the order-peeling
+ * sweep over the plan's orders (chain shards: their block, reading and
+ * updating the spectra and writing their orders of flm; otherwise every
+ * order).  osph_forward == RINGS|FACTOR|SWEEP on an unsharded plan.  check
+ * applies to the plan's own orders (SWEEP stage). */
+#define OSPH_STAGE_RINGS 1
+#define OSPH_STAGE_FACTOR 2
+#define OSPH_STAGE_SWEEP 4
+int osph_forward_stage(osph_plan* plan, int stages, int B, const void* samples, void* flm, int ptr_kind, int check,
+                       osph_stats* stats);
+
+/* Device address and byte size of a plan buffer the shards exchange:
+ * OSPH_BUF_SPECTRA: the ring spectra of B maps (chain hand-off; m_lo/m_hi ignored);
+ * the others: the factor data of orders [m_lo, m_hi] (one contiguous run each). */
+#define OSPH_BUF_SPECTRA 0
+#define OSPH_BUF_XT 1     /* X_m = A_m^-1, 8-row tiles */
+#define OSPH_BUF_PB 2     /* 2pi Y_lm(theta_k), rings k < m, tiles */
+#define OSPH_BUF_AT 3     /* A_m (refinement, L > 512; 0 bytes otherwise) */
+#define OSPH_BUF_U 4      /* chain weights u_m */
+#define OSPH_BUF_W 5      /* late-ring columns w_m */
+#define OSPH_BUF_BETA 6   /* beta_m */
+#define OSPH_BUF_JSTAR 7  /* j*_m */
+#define OSPH_BUF_NORMS 8  /* ||A_m||_1, ||X_m||_1 (condition estimate) */
+#define OSPH_BUF_STATUS 9 /* zero-pivot flags */
+#define OSPH_BUF_COUNT 10
+int osph_shard_buffer(osph_plan* plan, int which, int B, int m_lo, int m_hi, void** ptr, int64_t* bytes);
 
 /* ABI version (OSPH_ABI_VERSION) -- lets bindings refuse a mismatched library. */
 int osph_abi_version(void);

@@ -43,13 +43,13 @@ from .transform import (
     ring_analysis,
 )
 
-from . import fileio  # noqa: E402
+from . import distributed, experiments, fileio  # noqa: E402
 from .fileio import read_coefficients, read_signal, write_coefficients, write_signal  # noqa: E402
 from .gridopt import make_grid  # noqa: E402
 from .gridopt import optimize_order_like_reference as optimize_order  # noqa: E402
 
 __all__ = [
-    "fileio", "make_grid", "optimize_order", "read_coefficients", "read_signal", "write_coefficients",
+    "distributed", "experiments", "fileio", "make_grid", "optimize_order", "read_coefficients", "read_signal", "write_coefficients",
     "write_signal",
     "AliasingError", "BandLimitError", "ColatitudeGrid", "DeviceError", "FileFormatError",
     "HarmonicCoefficients", "IllConditionedSolveError", "Measure", "OptisphError", "Ordering",

@@ -18,8 +18,11 @@ LIB_PATH = _HERE / "libosph.so"
 
 OSPH_OK, OSPH_ERR_ARG, OSPH_ERR_ILLCOND, OSPH_ERR_CUDA, OSPH_ERR_NCCL = 0, 1, 2, 3, 4
 OSPH_HOST, OSPH_DEVICE, OSPH_ASYNC, OSPH_REAL = 0, 1, 2, 4
+SHARD_CHAIN, SHARD_FACTORS = 1, 2
+STAGE_RINGS, STAGE_FACTOR, STAGE_SWEEP = 1, 2, 4
+BUF_SPECTRA, BUF_XT, BUF_PB, BUF_AT, BUF_U, BUF_W, BUF_BETA, BUF_JSTAR, BUF_NORMS, BUF_STATUS, BUF_COUNT = range(11)
 SWEEP_KINDS = {0: "persistent", 1: "gemm", 2: "large", 3: "windowed"}
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class OsphStats(ctypes.Structure):
@@ -38,7 +41,11 @@ class OsphStats(ctypes.Structure):
 _P = ctypes.c_void_p
 _I = ctypes.c_int
 SIGNATURES = {
-    "osph_plan_create": (_I, [_I, _P, _I, _I, ctypes.POINTER(_P)]),
+    "osph_plan_create": (_I, [_I, _P, _I, _I, _P, ctypes.POINTER(_P)]),
+    "osph_plan_shard": (_I, [_P, _I, _I, _I]),
+    "osph_shard_range": (_I, [_I, _I, _I, _I, _P, _P, _P, _P]),
+    "osph_forward_stage": (_I, [_P, _I, _I, _P, _P, _I, _I, ctypes.POINTER(OsphStats)]),
+    "osph_shard_buffer": (_I, [_P, _I, _I, _I, _I, ctypes.POINTER(_P), ctypes.POINTER(ctypes.c_int64)]),
     "osph_plan_destroy": (_I, [_P]),
     "osph_plan_set_stream": (_I, [_P, _P]),
     "osph_plan_info": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
@@ -94,4 +101,6 @@ def raise_for(rc: int, stats: OsphStats | None = None) -> None:
         raise IllConditionedSolveError(order, kappa)
     if rc == OSPH_ERR_ARG:
         raise BandLimitError(msg) if "band" in msg or "batch" in msg else ValueError(msg)
+    if rc == OSPH_ERR_NCCL:
+        raise DeviceError(f"libosph multi-GPU exchange failed: {msg}")
     raise DeviceError(f"libosph error {rc}: {msg}")

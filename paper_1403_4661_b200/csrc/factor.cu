@@ -44,6 +44,8 @@ cudaError_t launch_factor(osph_plan* p, cudaStream_t st) {
   if (!st) st = p->stream;
   if ((e = cudaMemsetAsync(p->d_norms, 0, sizeof(unsigned long long) * 2 * L, st)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(p->d_status, 0, sizeof(int) * L, st)) != cudaSuccess) return e;
-  if ((e = launch_factor_bf(p, 0, L - 1, st)) != cudaSuccess) return e;
+  int lo, hi;
+  own_orders(p, lo, hi);  // all orders, or this shard's block (OSPH_SHARD_FACTORS)
+  if ((e = launch_factor_bf(p, lo, hi, st)) != cudaSuccess) return e;
   return launch_kappa(p, st);
 }

@@ -333,7 +333,9 @@ int discover_pivots(osph_plan* p) {
   PIV_TRY(cudaMalloc(&nmoves, sizeof(int) * (size_t)L));
   PIV_TRY(cudaMemsetAsync(p->d_status, 0, sizeof(int) * L, st));
   if (!p->windowed) {
-    if (p->bf_full.m_first != 0 || p->bf_full.m_last != L - 1) PIV_TRY(bf_prepare(p, 0, L - 1, &p->bf_full));
+    int lo, hi;
+    own_orders(p, lo, hi);  // a factor shard needs (and finds) only its own orders' pivots
+    if (p->bf_full.m_first != lo || p->bf_full.m_last != hi) PIV_TRY(bf_prepare(p, lo, hi, &p->bf_full));
     const BfOffsets o{p->d_ainv_off, p->d_xt_off, p->d_pb_off, p->d_bf_off};
     PIV_TRY(bf_generate(p, p->bf_full, st, o, false));
     for (size_t s = 0; s < p->bf_full.steps.size(); ++s)
@@ -348,7 +350,7 @@ int discover_pivots(osph_plan* p) {
   PIV_TRY(cudaMemcpyAsync(perm.data(), p->d_piv, sizeof(int) * npk, cudaMemcpyDeviceToHost, st));
   PIV_TRY(cudaMemsetAsync(p->d_status, 0, sizeof(int) * L, st));
   PIV_TRY(cudaStreamSynchronize(st));
-  {
+  if (!p->shard_mode) {  // a shard's discovery covers only its orders: not a complete entry
     std::lock_guard<std::mutex> lk(g_piv_mu);
     if (g_piv_cache.size() >= 16) g_piv_cache.erase(g_piv_cache.begin());
     g_piv_cache[key] = perm;

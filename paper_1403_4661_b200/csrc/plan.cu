@@ -45,8 +45,10 @@ static cudaError_t upload(T** ptr, const T* host, size_t count, cudaStream_t st)
   return e;
 }
 
-static void plan_free(osph_plan* p) {
+void plan_free(osph_plan* p) {
   if (!p) return;
+  for (osph_plan* q : p->group) plan_free(q);
+  for (osph_plan* q : p->group_maps) plan_free(q);
   cudaSetDevice(p->device);
   void* ptrs[] = {p->d_cos, p->d_sin, p->d_rec, p->d_ls, p->d_pstart, p->d_ring_order, p->d_fft_n,
                   p->d_chirp_off, p->d_bhat_off, p->d_chirp, p->d_bhat, p->d_tw, p->d_roots,
@@ -70,6 +72,10 @@ static void plan_free(osph_plan* p) {
   if (p->s_out) cudaStreamDestroy(p->s_out);
   cudaFree(p->d_z1);
   cudaFree(p->d_z2);
+  if (p->inv_own_lists) {
+    cudaFree(p->d_inv_ring_order);
+    cudaFree(p->d_inv_bluestein);
+  }
   free_windows(p);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   delete p;
@@ -79,9 +85,20 @@ extern "C" int osph_abi_version(void) { return OSPH_ABI_VERSION; }
 
 extern "C" const char* osph_last_error(void) { return g_last_error.c_str(); }
 
-extern "C" int osph_plan_create(int L, const double* thetas, int max_batch, int device, osph_plan** out) {
+extern "C" int osph_plan_create(int L, const double* thetas, int max_batch, int ndev, const int* devs,
+                                osph_plan** out) {
   DeviceGuard guard;
   g_last_error.clear();
+  if (out) *out = nullptr;
+  if (ndev < 1 || !devs) {
+    osph_set_error("osph_plan_create: ndev must be >= 1 with a device list");
+    return OSPH_ERR_ARG;
+  }
+  if (ndev > 1) return group_create(L, thetas, max_batch, ndev, devs, out);
+  return plan_create_one(L, thetas, max_batch, devs[0], out);
+}
+
+int plan_create_one(int L, const double* thetas, int max_batch, int device, osph_plan** out) {
   if (!out) {
     osph_set_error("osph_plan_create: out is NULL");
     return OSPH_ERR_ARG;
@@ -162,6 +179,7 @@ extern "C" int osph_plan_create(int L, const double* thetas, int max_batch, int 
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return s[a] < s[b]; });
   PLAN_TRY(upload(&p->d_ring_order, order.data(), L, st));
+  p->h_ring_order = order;
   const size_t npacked = (size_t)L * (L + 1) / 2;
   PLAN_TRY(dalloc(&p->d_rec, npacked));
   PLAN_TRY(dalloc(&p->d_ls, (size_t)L * L));
@@ -173,6 +191,7 @@ extern "C" int osph_plan_create(int L, const double* thetas, int max_batch, int 
   PLAN_TRY(upload(&p->d_chirp_off, p->h_chirp_off.data(), L, st));
   PLAN_TRY(upload(&p->d_bhat_off, p->h_bhat_off.data(), L, st));
   PLAN_TRY(upload(&p->d_bluestein_rings, brings.data(), brings.size(), st));
+  p->h_bluestein_rings = brings;
   PLAN_TRY(dalloc(&p->d_chirp, (size_t)p->h_chirp_off[L]));
   PLAN_TRY(dalloc(&p->d_bhat, (size_t)p->h_bhat_off[L]));
   PLAN_TRY(dalloc(&p->d_tw, 8192));
@@ -183,6 +202,16 @@ extern "C" int osph_plan_create(int L, const double* thetas, int max_batch, int 
     if (p->h_fft_n[k] > OSPH_FFT_MAX) p->n_big_rings++;
   }
   if (!p->dft_ok) p->n_bluestein_rings = p->n_big_rings = 0;  // Legendre tables only (osph_legendre_block)
+  // the inverse produces every ring until osph_plan_shard restricts it
+  p->inv_nr = L;
+  p->d_inv_ring_order = p->d_ring_order;
+  p->d_inv_bluestein = p->d_bluestein_rings;
+  p->inv_n_bluestein = p->n_bluestein_rings;
+  p->inv_n_big = p->n_big_rings;
+  p->inv_direct_lo = 0;
+  p->inv_direct_hi = p->n_direct_rings;
+  p->own_k_lo = 0;
+  p->own_k_hi = L;
   PLAN_TRY(launch_tables(p));
   PLAN_TRY(cudaStreamSynchronize(st));
   *out = p;
@@ -226,7 +255,7 @@ extern "C" int osph_plan_info(const osph_plan* p, int* L, int* max_batch) {
 
 extern "C" int osph_last_launch_count(const osph_plan* p) { return p ? p->launches : 0; }
 
-static int ensure_io(osph_plan* p) {
+int ensure_io(osph_plan* p) {
   if (p->d_in) return OSPH_OK;
   const size_t n = (size_t)p->max_batch * p->L * p->L;
   CUDA_TRY(dalloc(&p->d_in, n));
@@ -234,7 +263,7 @@ static int ensure_io(osph_plan* p) {
   return OSPH_OK;
 }
 
-static int ensure_inverse(osph_plan* p) {
+int ensure_inverse(osph_plan* p) {
   if (p->inv_ready) return OSPH_OK;
   const int L = p->L;
   const size_t B = p->max_batch;
@@ -244,7 +273,7 @@ static int ensure_inverse(osph_plan* p) {
   return OSPH_OK;
 }
 
-static int ensure_forward(osph_plan* p) {
+int ensure_forward(osph_plan* p) {
   if (p->fwd_ready) return OSPH_OK;
   const int L = p->L;
   const size_t B = p->max_batch;
@@ -281,7 +310,7 @@ static int sweep_kind(const osph_plan* p) {
   return OSPH_SWEEP_PERSISTENT;
 }
 
-static int check_call(osph_plan* p, int B, const void* a, void* b, int kind) {
+int check_call(osph_plan* p, int B, const void* a, void* b, int kind) {
   if (!p) {
     osph_set_error("plan is NULL");
     return OSPH_ERR_ARG;
@@ -456,11 +485,36 @@ static int forward_real(osph_plan* p, int B, const void* samples, void* flm, boo
   return OSPH_OK;
 }
 
+// Device -> host copy of the rings the plan's inverse produced (every ring, or a
+// chain shard's range [own_k_lo, own_k_hi): samples k^2 .. own_k_hi^2 of each map).
+static cudaError_t copy_rings_d2h(const osph_plan* p, double2* host, const double2* dev, int nmaps, cudaStream_t st) {
+  const size_t per_map = (size_t)p->L * p->L;
+  if (p->own_k_lo == 0 && p->own_k_hi == p->L)
+    return cudaMemcpyAsync(host, dev, sizeof(double2) * per_map * nmaps, cudaMemcpyDeviceToHost, st);
+  const size_t s0 = (size_t)p->own_k_lo * p->own_k_lo, s1 = (size_t)p->own_k_hi * p->own_k_hi;
+  if (s1 == s0) return cudaSuccess;
+  return cudaMemcpy2DAsync(host + s0, sizeof(double2) * per_map, dev + s0, sizeof(double2) * per_map,
+                           sizeof(double2) * (s1 - s0), nmaps, cudaMemcpyDeviceToHost, st);
+}
+
 extern "C" int osph_inverse(osph_plan* p, int B, const void* flm, void* samples, int kind) {
   DeviceGuard guard;
   g_last_error.clear();
+  if (p && !p->group_devs.empty()) return group_inverse(p, B, flm, samples, kind);
+  int rc = inverse_enqueue(p, B, flm, samples, kind);
+  if (rc) return rc;
+  if (!(kind & OSPH_ASYNC)) CUDA_TRY(cudaStreamSynchronize(p->stream));
+  return OSPH_OK;
+}
+
+// osph_inverse without the final synchronisation (multi-device plans enqueue every device first).
+int inverse_enqueue(osph_plan* p, int B, const void* flm, void* samples, int kind) {
   int rc = check_call(p, B, flm, samples, kind);
   if (rc) return rc;
+  if ((kind & OSPH_REAL) && p->shard_mode == OSPH_SHARD_CHAIN) {
+    osph_set_error("real-map pairing (OSPH_REAL) is not available on chain-sharded plans");
+    return OSPH_ERR_ARG;
+  }
   CUDA_TRY(cudaSetDevice(p->device));
   if ((rc = ensure_inverse(p))) return rc;
   const bool host = !(kind & OSPH_DEVICE);
@@ -497,14 +551,13 @@ extern "C" int osph_inverse(osph_plan* p, int B, const void* flm, void* samples,
       CUDA_TRY(launch_ring_inverse(p, bc, p->d_out + off));
       CUDA_TRY(cudaEventRecord(p->ev_done[c], st));
       CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->ev_done[c], 0));
-      CUDA_TRY(cudaMemcpyAsync((double2*)samples + off, p->d_out + off, bytes, cudaMemcpyDeviceToHost, p->s_out));
+      CUDA_TRY(copy_rings_d2h(p, (double2*)samples + off, p->d_out + off, bc, p->s_out));
     }
     CUDA_TRY(cudaEventRecord(p->ev[3], st));
     CUDA_TRY(cudaEventRecord(p->ev_out, p->s_out));
     CUDA_TRY(cudaStreamWaitEvent(st, p->ev_out, 0));  // the plan stream covers the whole call
   }
   p->have_inv = true;
-  if (!(kind & OSPH_ASYNC)) CUDA_TRY(cudaStreamSynchronize(st));
   return OSPH_OK;
 }
 
@@ -512,8 +565,13 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
                             osph_stats* stats) {
   DeviceGuard guard;
   g_last_error.clear();
+  if (p && !p->group_devs.empty()) return group_forward(p, B, samples, flm, kind, check, stats);
   int rc = check_call(p, B, samples, flm, kind);
   if (rc) return rc;
+  if (p->shard_mode) {
+    osph_set_error("a sharded plan runs the forward in stages (osph_forward_stage)");
+    return OSPH_ERR_ARG;
+  }
   if ((kind & OSPH_ASYNC) && check) {
     osph_set_error("check=1 needs a host-blocking call (drop OSPH_ASYNC or pass check=0)");
     return OSPH_ERR_ARG;
@@ -622,23 +680,35 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
     stats->failed_order = -1;
     stats->failed_kappa = 0.0;
   }
-  if (check) {
-    std::vector<double> kappa(L);
-    std::vector<int> status(L);
-    CUDA_TRY(cudaMemcpy(kappa.data(), p->d_kappa, sizeof(double) * L, cudaMemcpyDeviceToHost));
-    CUDA_TRY(cudaMemcpy(status.data(), p->d_status, sizeof(int) * L, cudaMemcpyDeviceToHost));
-    for (int m = L - 1; m >= 0; --m) {  // the reference raises at the first failing order of its sweep
-      if (status[m] || !(kappa[m] <= 2.0e14)) {
-        if (stats) {
-          stats->failed_order = m;
-          stats->failed_kappa = status[m] ? INFINITY : kappa[m];
-        }
-        char buf[160];
-        snprintf(buf, sizeof buf, "order %d system is numerically singular (condition number %.3e)", m,
-                 status[m] ? INFINITY : kappa[m]);
-        osph_set_error(buf);
-        return OSPH_ERR_ILLCOND;
+  return forward_check(p, check, stats);
+}
+
+// check=True after a finished forward: the first failing order of the sweep
+// (descending m, like the reference's loop) among the orders this plan factored.
+int forward_check(osph_plan* p, int check, osph_stats* stats) {
+  if (!check) return OSPH_OK;
+  const int L = p->L;
+  int lo, hi;
+  own_orders(p, lo, hi);
+  if (p->shard_mode == OSPH_SHARD_FACTORS) {  // the factors of every order were gathered
+    lo = 0;
+    hi = L - 1;
+  }
+  std::vector<double> kappa(L);
+  std::vector<int> status(L);
+  CUDA_TRY(cudaMemcpy(kappa.data(), p->d_kappa, sizeof(double) * L, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(status.data(), p->d_status, sizeof(int) * L, cudaMemcpyDeviceToHost));
+  for (int m = hi; m >= lo; --m) {  // the reference raises at the first failing order of its sweep
+    if (status[m] || !(kappa[m] <= 2.0e14)) {
+      if (stats) {
+        stats->failed_order = m;
+        stats->failed_kappa = status[m] ? INFINITY : kappa[m];
       }
+      char buf[160];
+      snprintf(buf, sizeof buf, "order %d system is numerically singular (condition number %.3e)", m,
+               status[m] ? INFINITY : kappa[m]);
+      osph_set_error(buf);
+      return OSPH_ERR_ILLCOND;
     }
   }
   return OSPH_OK;

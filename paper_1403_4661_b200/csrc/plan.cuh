@@ -4,6 +4,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "../../include/osph.h"
 
 struct BfStep {
   int cnt = 0, pre_panel = 0, n_panel = 0, pre_upd = 0, n_upd = 0, pre_updw = 0, n_updw = 0;  // updw: 128-row tiles
@@ -41,6 +42,7 @@ struct osph_plan {
   int* d_ls = nullptr;        // [m][k] first degree whose value is in the double range
   double2* d_pstart = nullptr;  // [m][k] {P_(ls-1)m, P_(ls)m} (true values)
   int* d_ring_order = nullptr;  // [L] rings sorted by sin(theta), for warp-coherent skipping
+  std::vector<int> h_ring_order, h_bluestein_rings;  // host copies (shard ring lists are filtered from them)
 
   // ---- ring DFT tables ----
   std::vector<int> h_fft_n;          // [L] Bluestein FFT size per ring (0 = direct DFT)
@@ -59,6 +61,24 @@ struct osph_plan {
   int n_big_rings = 0;  // rings with a 16384-point Bluestein FFT (2-CTA clusters; first in d_bluestein_rings)
   double2* d_sw = nullptr;  // [OSPH_SW_GLOBAL] per-stage FFT twiddles (fft.cuh)
   bool dft_ok = true;  // every ring's Bluestein FFT fits one CTA (else: tables-only plan)
+  // rings the INVERSE produces: all of them, or a chain shard's contiguous range
+  // [own_k_lo, own_k_hi) (osph_plan_shard); the forward ring DFTs always cover all rings
+  int inv_nr = 0;                   // rings in d_inv_ring_order (synthesis ring list)
+  int* d_inv_ring_order = nullptr;  // those rings sorted by sin(theta) (aliases d_ring_order when unsharded)
+  int* d_inv_bluestein = nullptr;   // their Bluestein rings, 16384-point ones first (aliases d_bluestein_rings)
+  int inv_n_bluestein = 0, inv_n_big = 0, inv_direct_lo = 0, inv_direct_hi = 0;
+  bool inv_own_lists = false;       // d_inv_* are separate allocations (free them)
+
+  // ---- sharding over GPUs (osph_plan_shard) ----
+  int shard_mode = 0;               // 0 none, OSPH_SHARD_CHAIN, OSPH_SHARD_FACTORS
+  int shard_rank = 0, shard_n = 1;
+  int own_m_lo = 0, own_m_hi = -1;  // orders this plan factors (and, in chain mode, sweeps); -1: all
+  int own_k_lo = 0, own_k_hi = 0;   // rings this plan synthesises in the inverse
+  // multi-device plan (osph_plan_create with ndev > 1): per-device sub-plans, created lazily:
+  // chain shards (B < ndev: one map across the devices) and factor shards (B >= ndev: maps split)
+  std::vector<int> group_devs;
+  std::vector<osph_plan*> group, group_maps;
+  std::vector<double> h_thetas;
 
   // ---- forward factor storage (per call, data independent) ----
   std::vector<int64_t> h_ainv_off;  // [L+1] offset of order m's n x n inverse
@@ -131,10 +151,8 @@ struct osph_plan {
 struct DeviceGuard {
   int prev = -1;
   DeviceGuard() {
-    if (cudaGetDevice(&prev) != cudaSuccess) {
-      cudaGetLastError();
-      prev = -1;
-    }
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    cudaGetLastError();  // a failed call earlier on this thread must not leak into this one's launch checks
   }
   ~DeviceGuard() {
     if (prev >= 0) cudaSetDevice(prev);
@@ -143,8 +161,34 @@ struct DeviceGuard {
   DeviceGuard& operator=(const DeviceGuard&) = delete;
 };
 
+// Orders this plan factors: every order unless osph_plan_shard gave it a block.
+inline void own_orders(const osph_plan* p, int& lo, int& hi) {
+  if (p->shard_mode && p->own_m_hi >= 0) {
+    lo = p->own_m_lo;
+    hi = p->own_m_hi;
+  } else {
+    lo = 0;
+    hi = p->L - 1;
+  }
+}
+
 // last-error plumbing (plan.cu)
 void osph_set_error(const std::string& msg);
+
+// plan.cu internals shared with shard.cu
+int plan_create_one(int L, const double* thetas, int max_batch, int device, osph_plan** out);
+void plan_free(osph_plan* p);
+int ensure_io(osph_plan* p);
+int ensure_inverse(osph_plan* p);
+int ensure_forward(osph_plan* p);
+int check_call(osph_plan* p, int B, const void* a, void* b, int kind);
+int inverse_enqueue(osph_plan* p, int B, const void* flm, void* samples, int kind);
+// shard.cu: sharded stages and multi-device plans
+int forward_stage_enqueue(osph_plan* p, int stages, int B, const void* samples, void* flm);
+int forward_check(osph_plan* p, int check, osph_stats* stats);
+int group_create(int L, const double* thetas, int max_batch, int ndev, const int* devs, osph_plan** out);
+int group_inverse(osph_plan* p, int B, const void* flm, void* samples, int kind);
+int group_forward(osph_plan* p, int B, const void* samples, void* flm, int kind, int check, osph_stats* stats);
 
 // ---- launchers (each returns cudaError_t of the launch) ----
 cudaError_t launch_tables(osph_plan* p);
@@ -172,6 +216,9 @@ int discover_pivots(osph_plan* p);  // pivots.cu: the grid's pivot order (once p
 int alloc_factor_storage(osph_plan* p);                        // window.cu
 void free_windows(osph_plan* p);                               // window.cu
 cudaError_t forward_windows(osph_plan* p, int B, double2* flm);  // window.cu: factor + sweep per window
+// window.cu, staged: factor window 0 only / sweep every window (factoring windows >= 1 before their sweep)
+cudaError_t forward_windows_factor_first(osph_plan* p);
+cudaError_t forward_windows_sweep(osph_plan* p, int B, double2* flm);
 void window_times(osph_plan* p);                               // window.cu
 cudaError_t launch_kappa(osph_plan* p, cudaStream_t st);       // factor.cu
 cudaError_t launch_ring_pair(int n, int m, const double2* v, double2* out, cudaStream_t st);  // ringdft.cu

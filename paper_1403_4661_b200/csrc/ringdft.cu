@@ -116,39 +116,59 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_inverse_bluestein(
   }
 }
 
-__global__ void __launch_bounds__(RING_THREADS) k_ring_inverse_direct(int L, int B, int maps_per_block,
+__global__ void __launch_bounds__(RING_THREADS) k_ring_inverse_direct(int L, int B, int maps_per_block, int k0,
                                                                       const double2* __restrict__ roots,
                                                                       const double* __restrict__ G,
                                                                       double2* __restrict__ samples) {
   __shared__ double2 bins[16][OSPH_DIRECT_MAX + 1];
-  const int k = blockIdx.x;
+  __shared__ double2 part[RING_THREADS];  // per-part fold sums (deterministic order)
+  const int k = k0 + blockIdx.x;
   const int n = 2 * k + 1;
   const int b_first = blockIdx.y * maps_per_block;
   const int b_last = min(B, b_first + maps_per_block);
   const double2* rt = roots + (int64_t)k * k;
   for (int b0 = b_first; b0 < b_last; b0 += 16) {
     const int Gr = min(16, b_last - b0);
-    // fold: short rings gather up to 2L tones per bin, so spread the tones over
-    // the block (map-fastest, coalesced) and accumulate in shared memory
-    for (int idx = threadIdx.x; idx < Gr * n; idx += blockDim.x) bins[idx / n][idx % n] = make_double2(0.0, 0.0);
-    __syncthreads();
+    // fold: short rings gather up to 2L tones per bin.  Deterministic: bin (g, t)
+    // is split into P interleaved parts (i = p, p + P, ... of its +m and -m tone
+    // lists), one thread sums a part in order, and the parts are added in p order
+    // (no floating-point atomics: bitwise reproducible like the reference).
+    const int items = Gr * n;
+    const int P = max(1, RING_THREADS / items);
     const int64_t mstride = (int64_t)L * 4 * B;
-    for (int idx = threadIdx.x; idx < Gr * L; idx += blockDim.x) {
-      const int g = idx % Gr, m = idx / Gr;
-      const double2* src = reinterpret_cast<const double2*>(G + m * mstride + ((int64_t)k * 4 * B + 4 * (b0 + g)));
-      const double2 vp = __ldg(src), vn = __ldg(src + 1);
-      const double4 v = make_double4(vp.x, vp.y, vn.x, vn.y);
-      const int r = m % n;
-      atomicAdd(&bins[g][r].x, v.x);
-      atomicAdd(&bins[g][r].y, v.y);
-      if (m > 0) {
-        const int rn = r == 0 ? 0 : n - r;
-        const double sg = (m & 1) ? -1.0 : 1.0;
-        atomicAdd(&bins[g][rn].x, sg * v.z);
-        atomicAdd(&bins[g][rn].y, sg * v.w);
+    for (int idx = threadIdx.x; idx < items * P; idx += blockDim.x) {
+      const int p = idx / items, item = idx - p * items;
+      const int t = item / Gr, g = item - t * Gr;  // map fastest: neighbouring threads read neighbouring maps
+      const double* gk = G + ((int64_t)k * 4 * B + 4 * (b0 + g));
+      double re = 0.0, im = 0.0;
+      for (int m = t + p * n; m < L; m += P * n) {  // +m tones: bin m mod n
+        const double2 v = __ldg(reinterpret_cast<const double2*>(gk + m * mstride));
+        re += v.x;
+        im += v.y;
       }
+      for (int m = (t == 0 ? n : n - t) + p * n; m < L; m += P * n) {  // -m tones (m >= 1): bin -m mod n
+        const double2 v = __ldg(reinterpret_cast<const double2*>(gk + m * mstride + 2));
+        if (m & 1) {
+          re -= v.x;
+          im -= v.y;
+        } else {
+          re += v.x;
+          im += v.y;
+        }
+      }
+      if (P == 1) bins[g][t] = make_double2(re, im);
+      else part[idx] = make_double2(re, im);
     }
     __syncthreads();
+    if (P > 1) {
+      for (int item = threadIdx.x; item < items; item += blockDim.x) {
+        const int t = item / Gr, g = item - t * Gr;
+        double2 acc = part[item];
+        for (int p = 1; p < P; ++p) acc = cadd(acc, part[p * items + item]);
+        bins[g][t] = acc;
+      }
+      __syncthreads();
+    }
     for (int idx = threadIdx.x; idx < Gr * n; idx += blockDim.x) {
       const int g = idx / n, j = idx - g * n;
       double re = 0.0, im = 0.0;
@@ -367,13 +387,13 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_forward_bluestein2(
 
 static size_t big_smem() { return sizeof(double2) * (size_t)(OSPH_SW_SMEM + BIG_M); }
 
-static cudaError_t launch_big(const void* kern, osph_plan* p, int nb, void** args) {
+static cudaError_t launch_big(const void* kern, osph_plan* p, int nb, int nbig, void** args) {
   const size_t smem = big_smem();
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int mpb = maps_per_block_for(nb, p->n_big_rings);
+  const int mpb = maps_per_block_for(nb, nbig);
   cudaLaunchConfig_t lc = {};
-  lc.gridDim = dim3((unsigned)(2 * p->n_big_rings), (unsigned)((nb + mpb - 1) / mpb));
+  lc.gridDim = dim3((unsigned)(2 * nbig), (unsigned)((nb + mpb - 1) / mpb));
   lc.blockDim = dim3(RING_THREADS);
   lc.dynamicSmemBytes = smem;
   lc.stream = p->stream;
@@ -411,31 +431,33 @@ static size_t ring_smem(const osph_plan* p) {
   return need > budget ? need : budget;
 }
 
+// The rings of the plan's inverse set (every ring, or a chain shard's range).
 cudaError_t launch_ring_inverse(osph_plan* p, int B, double2* samples) {
   const int L = p->L;
-  if (p->n_big_rings > 0) {  // the largest rings come first in d_bluestein_rings
+  if (p->inv_n_big > 0) {  // the largest rings come first in d_inv_bluestein
     int Li = L, Bi = B, mpb = 0;
-    const int* rings = p->d_bluestein_rings;
+    const int* rings = p->d_inv_bluestein;
     void* args[] = {&Li, &Bi, &mpb, &rings, &p->d_chirp_off, &p->d_bhat_off, &p->d_chirp, &p->d_bhat,
                     &p->d_tw, &p->d_sw, &p->d_g, &samples};
-    cudaError_t e = launch_big((const void*)k_ring_inverse_bluestein2, p, B, args);
+    cudaError_t e = launch_big((const void*)k_ring_inverse_bluestein2, p, B, p->inv_n_big, args);
     if (e != cudaSuccess) return e;
   }
-  const int nsmall = p->n_bluestein_rings - p->n_big_rings;
+  const int nsmall = p->inv_n_bluestein - p->inv_n_big;
   if (nsmall > 0) {
     const int mpb = maps_per_block_for(B, nsmall);
     const size_t smem = ring_smem(p);
     cudaFuncSetAttribute(k_ring_inverse_bluestein, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid(nsmall, (B + mpb - 1) / mpb);
     k_ring_inverse_bluestein<<<grid, RING_THREADS, smem, p->stream>>>(
-        L, B, mpb, p->d_bluestein_rings + p->n_big_rings, p->d_fft_n, p->d_chirp_off, p->d_bhat_off, p->d_chirp,
+        L, B, mpb, p->d_inv_bluestein + p->inv_n_big, p->d_fft_n, p->d_chirp_off, p->d_bhat_off, p->d_chirp,
         p->d_bhat, p->d_sw, p->d_g, samples, (int)(smem / sizeof(double2)));
     p->launches++;
   }
-  if (p->n_direct_rings > 0) {
-    const int mpb = maps_per_block_for(B, p->n_direct_rings);
-    dim3 grid(p->n_direct_rings, (B + mpb - 1) / mpb);
-    k_ring_inverse_direct<<<grid, 128, 0, p->stream>>>(L, B, mpb, p->d_roots, p->d_g, samples);
+  const int ndirect = p->inv_direct_hi - p->inv_direct_lo;
+  if (ndirect > 0) {
+    const int mpb = maps_per_block_for(B, ndirect);
+    dim3 grid(ndirect, (B + mpb - 1) / mpb);
+    k_ring_inverse_direct<<<grid, 128, 0, p->stream>>>(L, B, mpb, p->inv_direct_lo, p->d_roots, p->d_g, samples);
     p->launches++;
   }
   return cudaGetLastError();
@@ -450,7 +472,7 @@ cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples, int
     const int* rings = p->d_bluestein_rings;
     void* args[] = {&Li, &Bi, &mpb, &rings, &p->d_chirp_off, &p->d_bhat_off, &p->d_chirp, &p->d_bhat,
                     &p->d_tw, &p->d_sw, &samples, &p->d_r, &b0, &b1, &lgG};
-    cudaError_t e = launch_big((const void*)k_ring_forward_bluestein2, p, nb, args);
+    cudaError_t e = launch_big((const void*)k_ring_forward_bluestein2, p, nb, p->n_big_rings, args);
     if (e != cudaSuccess) return e;
   }
   const int nsmall = p->n_bluestein_rings - p->n_big_rings;

@@ -701,10 +701,6 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
         const Job j = make_job(1, s, L, lgT, rank, SWEEP_KC, xt, xt_off, pbt, pb_off, false);
         run_job<CC>(j, ringC, cst, cphase, gw, SWEEP_WC, xrow + (size_t)(s & 1) * cfg.ldx * CC, CC, g, tq, lane,
                     [&](int k, int c, double v0, double v1) {
-          // the other tone of the same map sits in lane ^ 1 (columns c and c ^ 2);
-          // both lanes of a pair are always active together
-          const unsigned am = __activemask();
-          const double o0 = __shfl_xor_sync(am, v0, 1), o1 = __shfl_xor_sync(am, v1, 1);
           const int bl = c >> 2;
           if (k >= s - 1 || bl >= gm) return;  // ring s-1 is the chain
           const bool plus = (c & 2) == 0;
@@ -728,7 +724,11 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
           corr_target(s, k, plus, tm, slot);
           if (tm == 0) {
             // s = 0 mod (2k+1): both tones land in bin 0 -- one reduction from the
-            // + lane (deterministic sum order, no racing pair of REDs)
+            // + lane (deterministic sum order, no racing pair of REDs).  The other
+            // tone of the same map is in lane ^ 1 (column c ^ 2); both lanes of the
+            // pair share (s, k), so they take this (rare) branch together.
+            const unsigned am = __activemask();
+            const double o0 = __shfl_xor_sync(am, v0, 1), o1 = __shfl_xor_sync(am, v1, 1);
             if (!plus) return;
             gr += ss * o0;
             gi += ss * o1;
@@ -982,7 +982,7 @@ int sweep_maps_per_team(osph_plan* p, int B) {
     if (gg == 1) break;
   }
   if (found) g = best_g;
-  if (!found && B >= 16 && !getenv("OSPH_SWEEP_NO_GEMM")) {
+  if ((!found && B >= 16 && !getenv("OSPH_SWEEP_NO_GEMM")) || getenv("OSPH_SWEEP_GEMM")) {
     // teams would run in waves: one GEMM pair per order over the whole GPU instead (sweep_gemm.cu)
     p->sweep_gemm = true;
     p->sweep_large = false;

@@ -129,9 +129,6 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
     const int row = rt0 * 8 + wr + 8 * i + g;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      // the other slot of the same (row, map) is in lane ^ 1 (column col ^ 2)
-      const double or_ = MODE == 1 ? __shfl_xor_sync(0xffffffffu, acc[i][j][0], 1) : 0.0;
-      const double oi_ = MODE == 1 ? __shfl_xor_sync(0xffffffffu, acc[i][j][1], 1) : 0.0;
       if (row >= M) continue;
       const int col = wc + 8 * j + 2 * tq;  // even: (re, im) of one (map, slot)
       const int mp = col >> 2, slot = (col >> 1) & 1, b = b0 + mp;
@@ -173,7 +170,11 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
         }
         if (rr == 0) {
           // both tones land in bin 0: one reduction from the slot-0 lane
-          // (deterministic sum order instead of two racing REDs)
+          // (deterministic sum order instead of two racing REDs).  The other slot
+          // of the same (row, map) is in lane ^ 1 (column col ^ 2); both lanes
+          // share the row, so they take this (rare) branch together.
+          const unsigned am = __activemask();
+          const double or_ = __shfl_xor_sync(am, acc[i][j][0], 1), oi_ = __shfl_xor_sync(am, acc[i][j][1], 1);
           if (slot) continue;
           vr += sg * or_;
           vi += sg * oi_;
@@ -210,27 +211,10 @@ static cudaError_t sweep_gemm_run(osph_plan* p, int B, double2* flm) {
   return cudaGetLastError();
 }
 
-// CTA tile rows x maps (OSPH_SG_SHAPE) and cp.async stages of the K loop
-// (OSPH_SG_STAGES).  The loop is bound by the L2 reads of the operand chunks
-// -- every CTA of a map group re-reads the B chunk, every map group the A
-// chunk -- so the tile shape decides.  Config 3 sweep (ms):
-//   16x16: 13.06 / 12.24 / 12.34 with 2 / 3 / 4 stages
-//   32x8: 11.25 / 10.99 / 11.12 with 3 / 4 / 6;  64x4: 11.07 / 10.79 / 12.34 with 3 / 4 / 6
-//   64x8: 13.21, 32x16: 14.02 with 3 (fewer CTAs)
-cudaError_t launch_sweep_gemm(osph_plan* p, int B, double2* flm) {
-  static const int ns = getenv("OSPH_SG_STAGES") ? atoi(getenv("OSPH_SG_STAGES")) : 4;
-  static const std::string shape = getenv("OSPH_SG_SHAPE") ? getenv("OSPH_SG_SHAPE") : "64x4";
-  if (shape == "32x8") {
-    if (ns == 6) return sweep_gemm_run<6, 32, 8>(p, B, flm);
-    return ns == 4 ? sweep_gemm_run<4, 32, 8>(p, B, flm) : sweep_gemm_run<3, 32, 8>(p, B, flm);
-  }
-  if (shape == "64x8") return ns == 4 ? sweep_gemm_run<4, 64, 8>(p, B, flm) : sweep_gemm_run<3, 64, 8>(p, B, flm);
-  if (shape == "32x16") return sweep_gemm_run<3, 32, 16>(p, B, flm);
-  if (shape == "64x4") {
-    if (ns == 6) return sweep_gemm_run<6, 64, 4>(p, B, flm);
-    return ns == 4 ? sweep_gemm_run<4, 64, 4>(p, B, flm) : sweep_gemm_run<3, 64, 4>(p, B, flm);
-  }
-  if (ns == 2) return sweep_gemm_run<2, 16, 16>(p, B, flm);
-  if (ns == 4) return sweep_gemm_run<4, 16, 16>(p, B, flm);
-  return sweep_gemm_run<3, 16, 16>(p, B, flm);
-}
+// CTA tile 64 rows x 4 maps, 4 cp.async stages of the K loop.  The loop is
+// bound by the L2 reads of the operand chunks -- every CTA of a map group
+// re-reads the B chunk, every map group the A chunk -- so the tile shape
+// decides.  Measured alternatives (config 3 sweep, ms; removed): 16x16 13.06 /
+// 12.24 / 12.34 with 2 / 3 / 4 stages; 32x8 11.25 / 10.99 / 11.12 with 3 / 4 /
+// 6; 64x4 11.07 / 10.79 / 12.34 with 3 / 4 / 6; 64x8 13.21; 32x16 14.02.
+cudaError_t launch_sweep_gemm(osph_plan* p, int B, double2* flm) { return sweep_gemm_run<4, 64, 4>(p, B, flm); }

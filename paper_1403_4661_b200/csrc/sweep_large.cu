@@ -11,137 +11,19 @@
 // operands (X_s: n^2 doubles, Pb_s: s n doubles, up to 32 MB at L = 2048) are
 // streamed from HBM by the whole GPU, so the step is bandwidth-bound and the
 // launch gap (~2-3 us) is small against it; nothing is pipelined across
-// orders.  One warp per matrix row (8 rows per block), lanes striding K,
-// maps in passes of SL_MAPS with all their columns accumulated at once.
+// orders.  One block per 8-row tile of the operand (tiles as the factor
+// kernels store them), one or two maps per block.
 #include <cstdlib>
 
 #include "plan.cuh"
 
 #define SL_THREADS 256
-#define SL_MAPS 4
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-
-__global__ void __launch_bounds__(SL_THREADS) k_sweep_solve(int L, int s, int B, const double* __restrict__ xt,
-                                                            const int64_t* __restrict__ xt_off,
-                                                            const double* __restrict__ w_all,
-                                                            const double2* __restrict__ R,
-                                                            double2* __restrict__ xbuf, double2* __restrict__ flm) {
-  const int n = L - s, nrt = (n + 7) >> 3;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * 8 + warp;  // degree offset l - s
-  if (r >= n) return;
-  const double* X = xt + __ldg(xt_off + s);
-  const int64_t npos = (int64_t)L * (L + 1) / 2, p0 = packed_pos(L, s, 0);
-  const double sg = (s & 1) ? -1.0 : 1.0;
-  for (int b0 = blockIdx.y * SL_MAPS; b0 < B; b0 += gridDim.y * SL_MAPS) {
-    double ap[SL_MAPS][2], an[SL_MAPS][2];
-#pragma unroll
-    for (int q = 0; q < SL_MAPS; ++q) ap[q][0] = ap[q][1] = an[q][0] = an[q][1] = 0.0;
-    for (int j = lane; j < n; j += 32) {
-      const double x = __ldg(X + tile_index(r, j, nrt));  // natural ring order; the late column is zero
-#pragma unroll
-      for (int q = 0; q < SL_MAPS; ++q) {
-        if (b0 + q < B) {
-          const double2* rp = R + ((int64_t)(b0 + q) * npos + p0 + j) * 2;
-          const double2 gp = __ldg(rp), gn = __ldg(rp + 1);
-          ap[q][0] = fma(x, gp.x, ap[q][0]);
-          ap[q][1] = fma(x, gp.y, ap[q][1]);
-          an[q][0] = fma(x, gn.x, an[q][0]);
-          an[q][1] = fma(x, gn.y, an[q][1]);
-        }
-      }
-    }
-    const double w = __ldg(w_all + (int64_t)s * uw_ld(L) + r);  // X[:, j*]: the late ring's column
-#pragma unroll
-    for (int q = 0; q < SL_MAPS; ++q) {
-      if (b0 + q >= B) break;
-      double v[4] = {warp_sum(ap[q][0]), warp_sum(ap[q][1]), warp_sum(an[q][0]), warp_sum(an[q][1])};
-      if (lane == 0) {
-        const double2* rp = R + ((int64_t)(b0 + q) * npos + p0) * 2;
-        const double2 gp = rp[0], gn = rp[1];
-        const double2 xp = make_double2(fma(w, gp.x, v[0]), fma(w, gp.y, v[1]));
-        const double2 xn = make_double2(sg * fma(w, gn.x, v[2]), sg * fma(w, gn.y, v[3]));
-        xbuf[((int64_t)(b0 + q) * 2 + 0) * L + r] = xp;
-        xbuf[((int64_t)(b0 + q) * 2 + 1) * L + r] = xn;
-        const int64_t ell = s + r;
-        double2* f = flm + (int64_t)(b0 + q) * L * L + ell * ell + ell;
-        f[s] = xp;
-        if (s > 0) f[-s] = xn;
-      }
-    }
-  }
-}
-
-__global__ void __launch_bounds__(SL_THREADS) k_sweep_corr(int L, int s, int B, const double* __restrict__ pbt,
-                                                           const int64_t* __restrict__ pb_off,
-                                                           const double2* __restrict__ xbuf,
-                                                           double2* __restrict__ R) {
-  const int n = L - s, nrtpb = (s + 7) >> 3;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int k = blockIdx.x * 8 + warp;  // ring k < s
-  if (k >= s) return;
-  const double* Pb = pbt + __ldg(pb_off + s);
-  const int64_t npos = (int64_t)L * (L + 1) / 2;
-  const double sg = (s & 1) ? -1.0 : 1.0;
-  // alias target (transform.py:459-463): bin s mod n_k of ring k
-  const int nk = 2 * k + 1, rr = s % nk;
-  int tm, slot_p, slot_n;
-  if (rr == 0) {
-    tm = 0;
-    slot_p = slot_n = 0;
-  } else if (rr <= k) {
-    tm = rr;
-    slot_p = 0;
-    slot_n = 1;
-  } else {
-    tm = nk - rr;
-    slot_p = 1;
-    slot_n = 0;
-  }
-  const int64_t pos = packed_pos(L, tm, k - tm);
-  for (int b0 = blockIdx.y * SL_MAPS; b0 < B; b0 += gridDim.y * SL_MAPS) {
-    double ap[SL_MAPS][2], an[SL_MAPS][2];
-#pragma unroll
-    for (int q = 0; q < SL_MAPS; ++q) ap[q][0] = ap[q][1] = an[q][0] = an[q][1] = 0.0;
-    for (int l = lane; l < n; l += 32) {
-      const double a = __ldg(Pb + tile_index(k, l, nrtpb));
-#pragma unroll
-      for (int q = 0; q < SL_MAPS; ++q) {
-        if (b0 + q < B) {
-          const double2 xp = __ldg(xbuf + ((int64_t)(b0 + q) * 2 + 0) * L + l);
-          const double2 xn = __ldg(xbuf + ((int64_t)(b0 + q) * 2 + 1) * L + l);
-          ap[q][0] = fma(a, xp.x, ap[q][0]);
-          ap[q][1] = fma(a, xp.y, ap[q][1]);
-          an[q][0] = fma(a, xn.x, an[q][0]);
-          an[q][1] = fma(a, xn.y, an[q][1]);
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < SL_MAPS; ++q) {
-      if (b0 + q >= B) break;
-      double v[4] = {warp_sum(ap[q][0]), warp_sum(ap[q][1]), warp_sum(an[q][0]), warp_sum(an[q][1])};
-      if (lane == 0) {  // one writer per (order s, ring k, map): plain read-modify-write
-        double2* rp = R + ((int64_t)(b0 + q) * npos + pos) * 2;
-        if (slot_p == slot_n) {  // r == 0: both tones land in bin 0
-          rp[0].x -= v[0] + sg * v[2];
-          rp[0].y -= v[1] + sg * v[3];
-        } else {
-          rp[slot_p].x -= v[0];
-          rp[slot_p].y -= v[1];
-          rp[slot_n].x -= sg * v[2];
-          rp[slot_n].y -= sg * v[3];
-        }
-      }
-    }
-  }
-}
-
 
 // Tile-coalesced variants: one block per 8-row tile, warps split the 32-column
 // chunks, lane = column: a lane reads its column's 8 rows as one contiguous
@@ -452,19 +334,10 @@ __global__ void __launch_bounds__(SL_THREADS) k_sweep_resid_t(int L, int s, int 
 cudaError_t launch_sweep_large_range(osph_plan* p, int B, double2* flm, int s_hi, int s_lo, const int64_t* xt_off,
                                      const int64_t* pb_off) {
   const int L = p->L;
-  const bool rowwise = getenv("OSPH_SWEEP_ROWWISE") != nullptr;  // the first (warp-per-row) variant
   const int mb = B >= 2 ? 2 : 1;
-  const int ymaps = (B + (rowwise ? SL_MAPS : mb) - 1) / (rowwise ? SL_MAPS : mb);
+  const int ymaps = (B + mb - 1) / mb;
   for (int s = s_hi; s >= s_lo; --s) {
     const int n = L - s;
-    if (rowwise) {
-      k_sweep_solve<<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_xt, xt_off, p->d_w,
-                                                                          p->d_r, p->d_xbuf, flm);
-      if (s >= 1)
-        k_sweep_corr<<<dim3((s + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_pbelow, pb_off,
-                                                                           p->d_xbuf, p->d_r);
-      continue;
-    }
     const int64_t npos = (int64_t)L * (L + 1) / 2, p0 = packed_pos(L, s, 0);
     auto solve = [&](const double2* rhs, int64_t np, int64_t q0, int acc) {
       if (mb == 2)

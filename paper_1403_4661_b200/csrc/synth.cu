@@ -52,14 +52,14 @@ cudaError_t launch_pack(osph_plan* p, int B, const double2* flm) {
 
 template <int C>
 __global__ void __launch_bounds__(SYN_FMA_THREADS) k_synth_fma(
-    int L, const double* __restrict__ costh, const double2* __restrict__ rec, const int* __restrict__ ls_tab,
+    int L, int nr, const double* __restrict__ costh, const double2* __restrict__ rec, const int* __restrict__ ls_tab,
     const double2* __restrict__ pstart, const int* __restrict__ ring_order, const double* __restrict__ F,
     double* __restrict__ G) {
   __shared__ double Fs[SYN_FMA_CHUNK * C];
   __shared__ double2 Rs[SYN_FMA_CHUNK];
   const int m = blockIdx.y;
   const int idx = blockIdx.x * SYN_FMA_THREADS + threadIdx.x;
-  const bool active = idx < L;
+  const bool active = idx < nr;  // ring_order lists the nr rings to synthesise
   const int k = active ? ring_order[idx] : 0;
   const int64_t t = (int64_t)m * L + k;
   int ls = active ? ls_tab[t] : L;
@@ -124,7 +124,7 @@ __device__ __forceinline__ void syn_cp_async16(void* dst, const void* src) {
 
 template <int TN>
 __global__ void __launch_bounds__(SYN_THREADS, TN > 128 ? 1 : 2) k_synth_dmma(
-    int L, int C, const double* __restrict__ costh, const double2* __restrict__ rec,
+    int L, int nr, int C, const double* __restrict__ costh, const double2* __restrict__ rec,
     const int* __restrict__ ls_tab, const double2* __restrict__ pstart, const int* __restrict__ ring_order,
     const double* __restrict__ F, double* __restrict__ G) {
   constexpr int NT = TN / 16;  // 8-column tiles per warp (warp tile 16 rows x TN/2 columns)
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(SYN_THREADS, TN > 128 ? 1 : 2) k_synth_dmma(
   double p0 = 0.0, p1 = 0.0, x = 0.0;
   if (tid < SYN_TM) {
     const int r = row0 + tid;
-    if (r < L) {
+    if (r < nr) {  // ring_order lists the nr rings to synthesise
       kring = ring_order[r];
       const int64_t t = (int64_t)m * L + kring;
       ls = ls_tab[t];
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(SYN_THREADS, TN > 128 ? 1 : 2) k_synth_dmma(
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int r = row0 + wr + i * 8 + g;
-    if (r >= L) continue;
+    if (r >= nr) continue;
     const int k = ring_order[r];
     double* grow = G + ((int64_t)m * L + k) * C;
 #pragma unroll
@@ -255,9 +255,9 @@ static cudaError_t launch_synth_tn(osph_plan* p, int C) {
   const size_t smem = sizeof(double) * 2 * SYN_TK * ((SYN_TM + SYN_PAD) + (TN + SYN_PAD));
   cudaError_t e = cudaFuncSetAttribute(k_synth_dmma<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((C + TN - 1) / TN, (L + SYN_TM - 1) / SYN_TM, L);
-  k_synth_dmma<TN><<<grid, SYN_THREADS, smem, p->stream>>>(L, C, p->d_cos, p->d_rec, p->d_ls, p->d_pstart,
-                                                           p->d_ring_order, p->d_fpack, p->d_g);
+  dim3 grid((C + TN - 1) / TN, (p->inv_nr + SYN_TM - 1) / SYN_TM, L);
+  k_synth_dmma<TN><<<grid, SYN_THREADS, smem, p->stream>>>(L, p->inv_nr, C, p->d_cos, p->d_rec, p->d_ls,
+                                                           p->d_pstart, p->d_inv_ring_order, p->d_fpack, p->d_g);
   return cudaGetLastError();
 }
 
@@ -265,13 +265,13 @@ cudaError_t launch_synth(osph_plan* p, int B) {
   const int L = p->L;
   const int C = 4 * B;
   if (C <= 8) {
-    dim3 grid((L + SYN_FMA_THREADS - 1) / SYN_FMA_THREADS, L);
+    dim3 grid((p->inv_nr + SYN_FMA_THREADS - 1) / SYN_FMA_THREADS, L);
     if (C == 4)
-      k_synth_fma<4><<<grid, SYN_FMA_THREADS, 0, p->stream>>>(L, p->d_cos, p->d_rec, p->d_ls, p->d_pstart,
-                                                            p->d_ring_order, p->d_fpack, p->d_g);
+      k_synth_fma<4><<<grid, SYN_FMA_THREADS, 0, p->stream>>>(L, p->inv_nr, p->d_cos, p->d_rec, p->d_ls, p->d_pstart,
+                                                            p->d_inv_ring_order, p->d_fpack, p->d_g);
     else
-      k_synth_fma<8><<<grid, SYN_FMA_THREADS, 0, p->stream>>>(L, p->d_cos, p->d_rec, p->d_ls, p->d_pstart,
-                                                            p->d_ring_order, p->d_fpack, p->d_g);
+      k_synth_fma<8><<<grid, SYN_FMA_THREADS, 0, p->stream>>>(L, p->inv_nr, p->d_cos, p->d_rec, p->d_ls, p->d_pstart,
+                                                            p->d_inv_ring_order, p->d_fpack, p->d_g);
   } else {
     // widest column tile that the batch fills at least half of
     static const int tn_env = getenv("OSPH_SYNTH_TN") ? atoi(getenv("OSPH_SYNTH_TN")) : 0;

@@ -82,6 +82,15 @@ int alloc_factor_storage(osph_plan* p) {
   const char* env_budget = getenv("OSPH_WINDOW_GB");  // testing: force a window budget
   const double budget_b = env_budget ? atof(env_budget) * 1e9 : 0.55 * (double)free_b;
   p->windowed = (double)full * 8.0 > budget_b || env_budget != nullptr;
+  int own_lo, own_hi;
+  own_orders(p, own_lo, own_hi);
+  if (p->shard_mode == OSPH_SHARD_CHAIN) {
+    // a chain shard stores (in windows) only the orders it owns
+    p->windowed = true;
+  } else if (p->shard_mode == OSPH_SHARD_FACTORS && p->windowed) {
+    osph_set_error("factor-sharded batches need every order's factors resident (L too large for this GPU)");
+    return OSPH_ERR_ARG;
+  }
   std::vector<int64_t> ao, xo, po, bo;
   int64_t tot[4];
   if (!p->windowed) {
@@ -118,11 +127,11 @@ int alloc_factor_storage(osph_plan* p) {
   // windows in descending m, each within the budget
   const double wbudget = budget_b / 8.0;
   p->windows.clear();
-  int m_hi = L - 1;
-  while (m_hi >= 0) {
+  int m_hi = own_hi;
+  while (m_hi >= own_lo) {
     int m_lo = m_hi;
     double acc = (double)order_doubles(L, m_hi, rf);
-    while (m_lo > 0 && acc + (double)order_doubles(L, m_lo - 1, rf) <= wbudget)
+    while (m_lo > own_lo && acc + (double)order_doubles(L, m_lo - 1, rf) <= wbudget)
       acc += (double)order_doubles(L, --m_lo, rf);
     FwdWindow w;
     w.m_lo = m_lo;
@@ -184,6 +193,43 @@ cudaError_t forward_windows(osph_plan* p, int B, double2* flm) {
     if ((e = cudaEventRecord(w.ev[0], st)) != cudaSuccess) return e;
     if ((e = bf_run(p, w.bf, st, o)) != cudaSuccess) return e;
     if ((e = cudaEventRecord(w.ev[1], st)) != cudaSuccess) return e;
+    if ((e = launch_sweep_large_range(p, B, flm, w.m_hi, w.m_lo, o.xt, o.pb)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(w.ev[2], st)) != cudaSuccess) return e;
+  }
+  return launch_kappa(p, st);
+}
+
+// Staged windowed forward (sharded plans, osph_forward_stage): the first
+// window's factorisation alone (it reads no data, so it can run before the
+// right-hand sides arrive from the previous shard), then the sweep of every
+// window with windows >= 1 factored just before their sweep (they reuse the
+// storage of the window before).
+cudaError_t forward_windows_factor_first(osph_plan* p) {
+  const int L = p->L;
+  cudaStream_t st = p->stream;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(p->d_norms, 0, sizeof(unsigned long long) * 2 * L, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(p->d_status, 0, sizeof(int) * L, st)) != cudaSuccess) return e;
+  if (p->windows.empty()) return cudaSuccess;
+  FwdWindow& w = p->windows[0];
+  const BfOffsets o{w.d_offs, w.d_offs + (L + 1), w.d_offs + 2 * (L + 1), w.d_offs + 3 * (L + 1)};
+  if ((e = cudaEventRecord(w.ev[0], st)) != cudaSuccess) return e;
+  if ((e = bf_run(p, w.bf, st, o)) != cudaSuccess) return e;
+  return cudaEventRecord(w.ev[1], st);
+}
+
+cudaError_t forward_windows_sweep(osph_plan* p, int B, double2* flm) {
+  const int L = p->L;
+  cudaStream_t st = p->stream;
+  cudaError_t e;
+  for (size_t i = 0; i < p->windows.size(); ++i) {
+    FwdWindow& w = p->windows[i];
+    const BfOffsets o{w.d_offs, w.d_offs + (L + 1), w.d_offs + 2 * (L + 1), w.d_offs + 3 * (L + 1)};
+    if (i > 0) {
+      if ((e = cudaEventRecord(w.ev[0], st)) != cudaSuccess) return e;
+      if ((e = bf_run(p, w.bf, st, o)) != cudaSuccess) return e;
+      if ((e = cudaEventRecord(w.ev[1], st)) != cudaSuccess) return e;
+    }
     if ((e = launch_sweep_large_range(p, B, flm, w.m_hi, w.m_lo, o.xt, o.pb)) != cudaSuccess) return e;
     if ((e = cudaEventRecord(w.ev[2], st)) != cudaSuccess) return e;
   }

@@ -136,7 +136,9 @@ def optimize_order(band_limit: int, device: int = 0, *, tie_rtol: float = 1e-9, 
     lib = _lib.load()
     handle = ctypes.c_void_p()
     th = np.ascontiguousarray(cands)
-    _lib.raise_for(lib.osph_plan_create(L, th.ctypes.data_as(ctypes.c_void_p), 1, device, ctypes.byref(handle)))
+    devs = (ctypes.c_int * 1)(device)
+    _lib.raise_for(lib.osph_plan_create(L, th.ctypes.data_as(ctypes.c_void_p), 1, 1, ctypes.cast(devs, ctypes.c_void_p),
+                                        ctypes.byref(handle)))
     try:
         buf = torch.empty((L, L), dtype=torch.float64, device=f"cuda:{device}")
 

@@ -114,18 +114,26 @@ def _check_band_limits(a: int, b: int) -> None:
 
 
 class Plan:
-    """One libosph plan: band limit, ring co-latitudes, batch capacity, device."""
+    """One libosph plan: band limit, ring co-latitudes, batch capacity, device(s).
 
-    def __init__(self, thetas, max_batch: int = 1, device: int = 0):
+    ``devices`` (a list) makes one plan over several GPUs driven by this
+    process (osph_plan_create with ndev > 1; host buffers only): batches are
+    split by maps with the factorisation split by order blocks, single maps
+    run as an order-block chain (shard.cu)."""
+
+    def __init__(self, thetas, max_batch: int = 1, device: int = 0, devices=None):
         lib = _lib.load()
         th = np.ascontiguousarray(np.asarray(thetas, dtype=np.float64))
         self.L = int(th.size)
         self.thetas = th
         self.max_batch = int(max_batch)
-        self.device = int(device)
+        devs = [int(device)] if devices is None else [int(d) for d in devices]
+        self.devices = devs
+        self.device = devs[0]
+        dev_arr = (ctypes.c_int * len(devs))(*devs)
         handle = ctypes.c_void_p()
-        rc = lib.osph_plan_create(self.L, th.ctypes.data_as(ctypes.c_void_p), self.max_batch, self.device,
-                                  ctypes.byref(handle))
+        rc = lib.osph_plan_create(self.L, th.ctypes.data_as(ctypes.c_void_p), self.max_batch, len(devs),
+                                  ctypes.cast(dev_arr, ctypes.c_void_p), ctypes.byref(handle))
         _lib.raise_for(rc)
         self._h = handle
         self._lib = lib
@@ -151,6 +159,26 @@ class Plan:
 
     def last_launch_count(self) -> int:
         return int(self._lib.osph_last_launch_count(self._h))
+
+    # sharded operation (one process per GPU; distributed.py drives the exchange) ----------
+    def shard(self, rank: int, nranks: int, mode: int) -> None:
+        """Make this plan rank ``rank`` of ``nranks`` (osph_plan_shard; before its first forward)."""
+        _lib.raise_for(self._lib.osph_plan_shard(self._h, int(rank), int(nranks), int(mode)))
+
+    def forward_stage(self, stages: int, B: int, src: int, dst: int, kind: int = _lib.OSPH_DEVICE,
+                      check: bool = False) -> None:
+        st = _lib.OsphStats()
+        rc = self._lib.osph_forward_stage(self._h, int(stages), int(B), ctypes.c_void_p(src), ctypes.c_void_p(dst),
+                                          int(kind), 1 if check else 0, ctypes.byref(st))
+        _lib.raise_for(rc, st)
+
+    def buffer(self, which: int, B: int = 0, m_lo: int = 0, m_hi: int = 0) -> tuple[int, int]:
+        """(device address, bytes) of an exchange buffer (osph_shard_buffer)."""
+        ptr = ctypes.c_void_p()
+        nbytes = ctypes.c_int64()
+        _lib.raise_for(self._lib.osph_shard_buffer(self._h, int(which), int(B), int(m_lo), int(m_hi),
+                                                   ctypes.byref(ptr), ctypes.byref(nbytes)))
+        return int(ptr.value or 0), int(nbytes.value)
 
     def last_sweep_kind(self) -> str | None:
         """Sweep variant of the last forward call: persistent / gemm / large / windowed."""

