@@ -21,6 +21,7 @@
 // plus ||X||_1 for the condition estimate.
 #include <algorithm>
 #include <cstdlib>
+#include <tuple>
 #include <vector>
 
 #include "plan.cuh"
@@ -353,80 +354,118 @@ __global__ void __launch_bounds__(BF_THREADS, 3) k_bf_panel_mma(int L, int m_fir
   }
 }
 
-// ---- 2c. A[I, K] += E[I, :] R[:, K] for every 64 x 64 tile outside column block J.
-// E and R are staged by 16-byte async copies (k-major / column-major in smem,
-// matching their global layouts) while the C fragments load from global.
-__global__ void __launch_bounds__(BF_THREADS, 3) k_bf_update(int L, int m_first, int j0, const int* __restrict__ pre,
-                                                             int cnt, const int64_t* __restrict__ ainv_off,
-                                                             double* __restrict__ ainv, const double* __restrict__ ebuf,
-                                                             const double* __restrict__ rbuf,
-                                                             const int64_t* __restrict__ bf_off,
-                                                             double* __restrict__ rnext) {
+// ---- 2c. The rank-64 (or paired rank-128) trailing update A[I, K] += E R[:, K].
+//
+// Arguments of the update kernels.  Modes of k_bf_update (64 x 64 tiles):
+//   normal      every tile outside the panel's column block(s): rt, ct from the work item;
+//   ct_fixed    one column tile, every row tile (the paired step's narrow updates);
+//   rt_fixed    one row tile, every column tile outside J1 and J2, the result also
+//               copied to rnext (the paired step's R2 = A[J2, :]).
+// PAIR: the two panels of a paired step (J1 = [j0, j0 + 64), J2 = [j0 + 64,
+// j0 + 128)) in one pass over C: C += E1' R1 + E2 R2, K = 128 in two staged
+// halves, with the J2 rows of E1 masked (rows J2 of C already hold A[J2, K] + E1[J2] R1).
+struct BfUpdArgs {
+  int L, m_first, j0;
+  const int* pre;
+  int cnt;
+  const int64_t* ainv_off;
+  double* ainv;
+  const double* ebuf;
+  const double* rbuf;
+  const int64_t* bf_off;
+  double* rnext;
+  const double* ebuf2;
+  const double* rbuf2;
+  int rt_fixed, ct_fixed;
+};
+
+template <bool PAIR>
+__global__ void __launch_bounds__(BF_THREADS, 3) k_bf_update(BfUpdArgs a) {
   extern __shared__ __align__(16) double bf_sm[];
   double(*Et)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm);                 // [k][row]
   double(*Rt)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm + BF_NB * BF_LDS);  // [col][k]
   __shared__ int s_oi;
   if (threadIdx.x < 32) {
-    const int oi_w = bf_find_warp(pre, cnt, blockIdx.x);
+    const int oi_w = bf_find_warp(a.pre, a.cnt, blockIdx.x);
     if (threadIdx.x == 0) s_oi = oi_w;
   }
   __syncthreads();
+  const int L = a.L, j0 = a.j0;
   const int oi = s_oi;
-  const int m = m_first + oi;
+  const int m = a.m_first + oi;
   const int n = L - m, lde = bf_lde(n);
-  const int nb = min(BF_NB, n - j0);
   const int nt = (n + BF_T - 1) / BF_T;
-  const int local = blockIdx.x - __ldg(pre + oi);
-  const int rt = local % nt;
-  int ct = local / nt;
-  if (ct >= j0 / BF_T) ++ct;  // skip the panel's column tile
-  const int i0 = rt * BF_T, c0 = ct * BF_T;
-  double* A = ainv + __ldg(ainv_off + m);
-  const double* E = ebuf + __ldg(bf_off + m);
-  const double* R = rbuf + __ldg(bf_off + m);
-  const int tid = threadIdx.x;
-  // async staging: 64 x 64 doubles each = 2048 16-byte chunks, 8 per thread per operand
-  for (int idx = tid; idx < BF_T * BF_NB / 2; idx += BF_THREADS) {
-    const int k = idx >> 5, r2 = (idx & 31) * 2;  // E: column k, rows r2, r2+1
-    if (k < nb && i0 + r2 + 1 < lde) bf_cp16(&Et[k][r2], E + (int64_t)k * lde + i0 + r2);
-    else {
-      Et[k][r2] = 0.0;
-      Et[k][r2 + 1] = 0.0;
-    }
-    const int c = idx >> 5, k2 = (idx & 31) * 2;  // R: column c0 + c, k2, k2+1
-    if (c0 + c < n) bf_cp16(&Rt[c][k2], R + (int64_t)(c0 + c) * BF_NB + k2);
-    else {
-      Rt[c][k2] = 0.0;
-      Rt[c][k2 + 1] = 0.0;
-    }
+  const int local = blockIdx.x - __ldg(a.pre + oi);
+  const int jt = j0 / BF_T;
+  int rt, ct;
+  if (a.ct_fixed >= 0) {
+    rt = local;
+    ct = a.ct_fixed;
+  } else if (a.rt_fixed >= 0) {
+    rt = a.rt_fixed;
+    ct = local;
+    if (ct >= jt) ct += 2;  // skip J1 and J2
+  } else {
+    rt = local % nt;
+    ct = local / nt;
+    if (ct >= jt) ct += PAIR ? 2 : 1;  // skip the panel's column tile(s)
   }
+  const int i0 = rt * BF_T, c0 = ct * BF_T;
+  double* A = a.ainv + __ldg(a.ainv_off + m);
+  const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wr = (warp & 1) * 32, wc = (warp >> 1) * 16;  // warp tile 32 rows x 16 cols
   double acc[4][2][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int row = i0 + wr + 8 * i + g, col = c0 + wc + 8 * j + 2 * t;
-      acc[i][j][0] = (row < n && col < n) ? __ldcg(A + (int64_t)col * n + row) : 0.0;
-      acc[i][j][1] = (row < n && col + 1 < n) ? __ldcg(A + (int64_t)(col + 1) * n + row) : 0.0;
+  for (int h = 0; h < (PAIR ? 2 : 1); ++h) {
+    const double* E = (h ? a.ebuf2 : a.ebuf) + __ldg(a.bf_off + m);
+    const double* R = (h ? a.rbuf2 : a.rbuf) + __ldg(a.bf_off + m);
+    const int nb = min(BF_NB, n - j0 - h * BF_NB);
+    const int mlo = PAIR && h == 0 ? j0 + BF_NB : 0, mhi = PAIR && h == 0 ? j0 + 2 * BF_NB : 0;
+    if (h) __syncthreads();  // the first half's operands are consumed
+    // async staging: 64 x 64 doubles each = 2048 16-byte chunks, 8 per thread per operand
+    for (int idx = tid; idx < BF_T * BF_NB / 2; idx += BF_THREADS) {
+      const int k = idx >> 5, r2 = (idx & 31) * 2;  // E: column k, rows r2, r2+1
+      const int row = i0 + r2;
+      if (k < nb && row + 1 < lde && !(row >= mlo && row < mhi)) bf_cp16(&Et[k][r2], E + (int64_t)k * lde + row);
+      else {
+        Et[k][r2] = 0.0;
+        Et[k][r2 + 1] = 0.0;
+      }
+      const int c = idx >> 5, k2 = (idx & 31) * 2;  // R: column c0 + c, k2, k2+1
+      if (c0 + c < n) bf_cp16(&Rt[c][k2], R + (int64_t)(c0 + c) * BF_NB + k2);
+      else {
+        Rt[c][k2] = 0.0;
+        Rt[c][k2 + 1] = 0.0;
+      }
     }
-  bf_cp_wait_all();
-  __syncthreads();
-  // rows of E beyond n (padding) are zero in E only if i0 + r < n: mask them here
+    if (h == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int row = i0 + wr + 8 * i + g, col = c0 + wc + 8 * j + 2 * t;
+          acc[i][j][0] = (row < n && col < n) ? __ldcg(A + (int64_t)col * n + row) : 0.0;
+          acc[i][j][1] = (row < n && col + 1 < n) ? __ldcg(A + (int64_t)(col + 1) * n + row) : 0.0;
+        }
+    }
+    bf_cp_wait_all();
+    __syncthreads();
 #pragma unroll 4
-  for (int k0 = 0; k0 < BF_NB; k0 += 4) {
-    double a[4], b[2];
+    for (int k0 = 0; k0 < BF_NB; k0 += 4) {
+      double av[4], bv[2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = Et[k0 + t][wr + 8 * i + g];
+      for (int i = 0; i < 4; ++i) av[i] = Et[k0 + t][wr + 8 * i + g];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) b[j] = Rt[wc + 8 * j + g][k0 + t];
+      for (int j = 0; j < 2; ++j) bv[j] = Rt[wc + 8 * j + g][k0 + t];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+    }
   }
+  double* Rn = a.rnext ? a.rnext + __ldg(a.bf_off + m) : nullptr;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -434,8 +473,7 @@ __global__ void __launch_bounds__(BF_THREADS, 3) k_bf_update(int L, int m_first,
       const int row = i0 + wr + 8 * i + g, col = c0 + wc + 8 * j + 2 * t;
       if (row < n && col < n) A[(int64_t)col * n + row] = acc[i][j][0];
       if (row < n && col + 1 < n) A[(int64_t)(col + 1) * n + row] = acc[i][j][1];
-      if (rnext && i0 == j0 + BF_T && row < n) {  // the next step's R = A[J', :] from the J' row tile
-        double* Rn = rnext + __ldg(bf_off + m);
+      if (Rn && i0 == j0 + BF_T && row < n) {  // the next panel's R = A[J', :] from the J' row tile
         if (col < n) Rn[(int64_t)col * BF_NB + (row - i0)] = acc[i][j][0];
         if (col + 1 < n) Rn[(int64_t)(col + 1) * BF_NB + (row - i0)] = acc[i][j][1];
       }
@@ -446,81 +484,86 @@ __global__ void __launch_bounds__(BF_THREADS, 3) k_bf_update(int L, int m_first,
 // so each k-step loads 8 fragments for 16 DMMAs (the 64 x 64 tile: 6 for 8)
 // and every E / R element staged in shared memory feeds twice the math.
 // 101 KB of shared memory, two CTAs per SM.  Default for L >= 1024
-// (OSPH_BF_UPD_ROWS=64|128 forces either kernel).
+// (OSPH_BF_UPD_ROWS=64|128 forces either kernel).  Normal and PAIR modes.
 #define BF_TW 128
 #define BF_LDW (BF_TW + 4)
-__global__ void __launch_bounds__(BF_THREADS, 2) k_bf_update_w(int L, int m_first, int j0, const int* __restrict__ pre,
-                                                               int cnt, const int64_t* __restrict__ ainv_off,
-                                                               double* __restrict__ ainv, const double* __restrict__ ebuf,
-                                                               const double* __restrict__ rbuf,
-                                                               const int64_t* __restrict__ bf_off,
-                                                               double* __restrict__ rnext) {
+template <bool PAIR>
+__global__ void __launch_bounds__(BF_THREADS, 2) k_bf_update_w(BfUpdArgs a) {
   extern __shared__ __align__(16) double bf_sm[];
   double(*Et)[BF_LDW] = reinterpret_cast<double(*)[BF_LDW]>(bf_sm);                  // [k][row]
   double(*Rt)[BF_LDS] = reinterpret_cast<double(*)[BF_LDS]>(bf_sm + BF_NB * BF_LDW);  // [col][k]
   __shared__ int s_oi;
   if (threadIdx.x < 32) {
-    const int oi_w = bf_find_warp(pre, cnt, blockIdx.x);
+    const int oi_w = bf_find_warp(a.pre, a.cnt, blockIdx.x);
     if (threadIdx.x == 0) s_oi = oi_w;
   }
   __syncthreads();
+  const int L = a.L, j0 = a.j0;
   const int oi = s_oi;
-  const int m = m_first + oi;
+  const int m = a.m_first + oi;
   const int n = L - m, lde = bf_lde(n);
-  const int nb = min(BF_NB, n - j0);
   const int nt = (n + BF_TW - 1) / BF_TW;
-  const int local = blockIdx.x - __ldg(pre + oi);
+  const int local = blockIdx.x - __ldg(a.pre + oi);
   const int rt = local % nt;
   int ct = local / nt;
-  if (ct >= j0 / BF_T) ++ct;  // skip the panel's column tile
+  if (ct >= j0 / BF_T) ct += PAIR ? 2 : 1;  // skip the panel's column tile(s)
   const int i0 = rt * BF_TW, c0 = ct * BF_T;
-  double* A = ainv + __ldg(ainv_off + m);
-  const double* E = ebuf + __ldg(bf_off + m);
-  const double* R = rbuf + __ldg(bf_off + m);
+  double* A = a.ainv + __ldg(a.ainv_off + m);
   const int tid = threadIdx.x;
-  for (int idx = tid; idx < BF_TW * BF_NB / 2; idx += BF_THREADS) {
-    const int k = idx >> 6, r2 = (idx & 63) * 2;  // E: column k, rows r2, r2+1
-    if (k < nb && i0 + r2 + 1 < lde) bf_cp16(&Et[k][r2], E + (int64_t)k * lde + i0 + r2);
-    else {
-      Et[k][r2] = 0.0;
-      Et[k][r2 + 1] = 0.0;
-    }
-  }
-  for (int idx = tid; idx < BF_T * BF_NB / 2; idx += BF_THREADS) {
-    const int c = idx >> 5, k2 = (idx & 31) * 2;  // R: column c0 + c, k2, k2+1
-    if (c0 + c < n) bf_cp16(&Rt[c][k2], R + (int64_t)(c0 + c) * BF_NB + k2);
-    else {
-      Rt[c][k2] = 0.0;
-      Rt[c][k2 + 1] = 0.0;
-    }
-  }
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wr = (warp & 3) * 32, wc = (warp >> 2) * 32;  // warp tile 32 rows x 32 cols
   double acc[4][4][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int row = i0 + wr + 8 * i + g, col = c0 + wc + 8 * j + 2 * t;
-      acc[i][j][0] = (row < n && col < n) ? __ldcg(A + (int64_t)col * n + row) : 0.0;
-      acc[i][j][1] = (row < n && col + 1 < n) ? __ldcg(A + (int64_t)(col + 1) * n + row) : 0.0;
+  for (int h = 0; h < (PAIR ? 2 : 1); ++h) {
+    const double* E = (h ? a.ebuf2 : a.ebuf) + __ldg(a.bf_off + m);
+    const double* R = (h ? a.rbuf2 : a.rbuf) + __ldg(a.bf_off + m);
+    const int nb = min(BF_NB, n - j0 - h * BF_NB);
+    const int mlo = PAIR && h == 0 ? j0 + BF_NB : 0, mhi = PAIR && h == 0 ? j0 + 2 * BF_NB : 0;
+    if (h) __syncthreads();
+    for (int idx = tid; idx < BF_TW * BF_NB / 2; idx += BF_THREADS) {
+      const int k = idx >> 6, r2 = (idx & 63) * 2;  // E: column k, rows r2, r2+1
+      const int row = i0 + r2;
+      if (k < nb && row + 1 < lde && !(row >= mlo && row < mhi)) bf_cp16(&Et[k][r2], E + (int64_t)k * lde + row);
+      else {
+        Et[k][r2] = 0.0;
+        Et[k][r2 + 1] = 0.0;
+      }
     }
-  bf_cp_wait_all();
-  __syncthreads();
+    for (int idx = tid; idx < BF_T * BF_NB / 2; idx += BF_THREADS) {
+      const int c = idx >> 5, k2 = (idx & 31) * 2;  // R: column c0 + c, k2, k2+1
+      if (c0 + c < n) bf_cp16(&Rt[c][k2], R + (int64_t)(c0 + c) * BF_NB + k2);
+      else {
+        Rt[c][k2] = 0.0;
+        Rt[c][k2 + 1] = 0.0;
+      }
+    }
+    if (h == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int row = i0 + wr + 8 * i + g, col = c0 + wc + 8 * j + 2 * t;
+          acc[i][j][0] = (row < n && col < n) ? __ldcg(A + (int64_t)col * n + row) : 0.0;
+          acc[i][j][1] = (row < n && col + 1 < n) ? __ldcg(A + (int64_t)(col + 1) * n + row) : 0.0;
+        }
+    }
+    bf_cp_wait_all();
+    __syncthreads();
 #pragma unroll 2
-  for (int k0 = 0; k0 < BF_NB; k0 += 4) {
-    double a[4], b[4];
+    for (int k0 = 0; k0 < BF_NB; k0 += 4) {
+      double av[4], bv[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = Et[k0 + t][wr + 8 * i + g];
+      for (int i = 0; i < 4; ++i) av[i] = Et[k0 + t][wr + 8 * i + g];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = Rt[wc + 8 * j + g][k0 + t];
+      for (int j = 0; j < 4; ++j) bv[j] = Rt[wc + 8 * j + g][k0 + t];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+    }
   }
-  double* Rn = rnext ? rnext + __ldg(bf_off + m) : nullptr;
+  double* Rn = a.rnext ? a.rnext + __ldg(a.bf_off + m) : nullptr;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -628,6 +671,37 @@ cudaError_t bf_prepare(osph_plan* p, int m_first, int m_last, BfRange* r) {
     }
     d.n_updw = acc;
   }
+  // paired steps (rank-128 trailing updates)
+  const int npsteps = (nmax + 2 * BF_NB - 1) / (2 * BF_NB);
+  r->psteps.assign(npsteps, {});
+  auto prefix = [&](int o0, int o1, auto items) {  // prefix table of orders m_first+o0 .. m_first+o1-1
+    const int at = (int)tab.size();
+    int acc = 0;
+    for (int o = o0; o <= o1; ++o) {
+      tab.push_back(acc);
+      if (o < o1) acc += items(L - (m_first + o));
+    }
+    return std::make_pair(at, acc);
+  };
+  auto tiles = [](int n, int t) { return (n + t - 1) / t; };
+  for (int ps = 0; ps < npsteps; ++ps) {
+    auto& d = r->psteps[ps];
+    d.j0 = ps * 2 * BF_NB;
+    for (int m = m_first; m <= m_last; ++m) {
+      if (L - m > d.j0) d.cnt = m - m_first + 1;
+      if (L - m > d.j0 + BF_NB) d.cnt2 = m - m_first + 1;
+    }
+    std::tie(d.pre_panel, d.n_panel) = prefix(0, d.cnt, [&](int n) { return tiles(n, BF_T); });
+    d.n_panel2 = tab[d.pre_panel + d.cnt2];
+    std::tie(d.pre_row, d.n_row) = prefix(0, d.cnt2, [&](int n) { return tiles(n, BF_T) - 2; });
+    std::tie(d.pre_upd2, d.n_upd2) = prefix(0, d.cnt2, [&](int n) { return tiles(n, BF_T) * (tiles(n, BF_T) - 2); });
+    std::tie(d.pre_updw2, d.n_updw2) =
+        prefix(0, d.cnt2, [&](int n) { return tiles(n, BF_TW) * (tiles(n, BF_T) - 2); });
+    std::tie(d.pre_single, d.n_single) =
+        prefix(d.cnt2, d.cnt, [&](int n) { return tiles(n, BF_T) * (tiles(n, BF_T) - 1); });
+    std::tie(d.pre_singlew, d.n_singlew) =
+        prefix(d.cnt2, d.cnt, [&](int n) { return tiles(n, BF_TW) * (tiles(n, BF_T) - 1); });
+  }
   cudaError_t e;
   cudaFree(r->d_tab);
   r->d_tab = nullptr;
@@ -641,8 +715,14 @@ static cudaError_t bf_attrs(int device) {
   const size_t sm2 = sizeof(double) * 2 * BF_T * BF_LDS + 16;
   const size_t smw = sizeof(double) * (BF_NB * BF_LDW + BF_T * BF_LDS) + 16;
   cudaError_t e = cudaFuncSetAttribute(k_bf_panel_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_bf_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_bf_update_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_bf_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_bf_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_bf_update_w<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_bf_update_w<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
   if (e == cudaSuccess && device >= 0 && device < 64) done[device] = true;
   return e;
 }
@@ -690,13 +770,87 @@ cudaError_t bf_step(osph_plan* p, const BfRange& r, int sidx, cudaStream_t st, c
   k_bf_panel_mma<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_panel, d.cnt, o.ainv,
                                                      p->d_ainv, p->d_bf_d, p->d_bf_e, o.bf, rnext);
   p->launches += 2;
-  if (d.n_upd > 0 && upd_wide)
-    k_bf_update_w<<<d.n_updw, BF_THREADS, smw, st>>>(L, m_first, j0, r.d_tab + d.pre_updw, d.cnt, o.ainv,
-                                                    p->d_ainv, p->d_bf_e, rcur, o.bf, rnext);
-  else if (d.n_upd > 0)
-    k_bf_update<<<d.n_upd, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_upd, d.cnt, o.ainv, p->d_ainv,
-                                                p->d_bf_e, rcur, o.bf, rnext);
+  BfUpdArgs ua{L, m_first, j0, nullptr, d.cnt, o.ainv, p->d_ainv, p->d_bf_e, rcur, o.bf, rnext, nullptr, nullptr,
+               -1, -1};
+  if (d.n_upd > 0 && upd_wide) {
+    ua.pre = r.d_tab + d.pre_updw;
+    k_bf_update_w<false><<<d.n_updw, BF_THREADS, smw, st>>>(ua);
+  } else if (d.n_upd > 0) {
+    ua.pre = r.d_tab + d.pre_upd;
+    k_bf_update<false><<<d.n_upd, BF_THREADS, sm2, st>>>(ua);
+  }
   if (d.n_upd > 0) p->launches++;
+  return cudaGetLastError();
+}
+
+// One paired step: the panels J1 = [j0, j0+64) and J2 = [j0+64, j0+128) of every
+// order with n > j0 (J2 only where n > j0 + 64), with ONE pass of the trailing
+// update over the matrix for both (rank 128) instead of two:
+//   1  R1 = A[J1, :]                          6  D2 = A[J2, J2]^-1
+//   2  D1 = A[J1, J1]^-1                      7  E2 = -A[:, J2] D2;  A[:, J2] = E2 + I
+//   3  E1 = -A[:, J1] D1;  A[:, J1] = E1 + I  8  A[:, J1] += E2 R2[:, J1]
+//      (and R2[:, J1] = A[J2, J1])            9  A[:, K] += E1' R1[:, K] + E2 R2[:, K]
+//   4  A[:, J2] += E1 R1[:, J2]                  (K = outside J1, J2; E1' = E1 without the J2
+//   5  A[J2, K] += E1[J2] R1[:, K];              rows, which step 5 already applied)
+//      R2[:, K] = A[J2, K]
+// Steps 4, 5 and 8 are 64-wide; step 9 is the bulk (2 n^2 128 flops per order).
+// Orders whose n ends inside J2's range take the rank-64 update of J1 instead.
+static cudaError_t bf_pair_step(osph_plan* p, const BfRange& r, int ps, cudaStream_t st, const BfOffsets& o,
+                                bool upd_wide) {
+  const int L = p->L;
+  const int m_first = r.m_first;
+  const BfPairStep& d = r.psteps[ps];
+  const int j0 = d.j0, jt = j0 / BF_T;
+  const size_t sm2 = sizeof(double) * 2 * BF_T * BF_LDS + 16;
+  const size_t smw = sizeof(double) * (BF_NB * BF_LDW + BF_T * BF_LDS) + 16;
+  double* R1 = p->d_bf_r;
+  double* R2 = p->d_bf_r + p->bf_r_half;
+  const int* tab = r.d_tab;
+  const dim3 dgrid(d.cnt, (L - m_first + BF_RCHUNK - 1) / BF_RCHUNK);
+  k_bf_rcopy<<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, R1, o.bf);                // 1
+  k_bf_diag_rows<<<d.cnt, 64, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_status);     // 2
+  k_bf_panel_mma<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, tab + d.pre_panel, d.cnt, o.ainv,  // 3
+                                                     p->d_ainv, p->d_bf_d, p->d_bf_e, o.bf, d.cnt2 ? R2 : nullptr);
+  p->launches += 3;
+  if (d.cnt2 > 0) {
+    BfUpdArgs u{L, m_first, j0, tab + d.pre_panel, d.cnt2, o.ainv, p->d_ainv, p->d_bf_e, R1, o.bf, nullptr,
+                nullptr, nullptr, -1, jt + 1};
+    k_bf_update<false><<<d.n_panel2, BF_THREADS, sm2, st>>>(u);  // 4
+    u.pre = tab + d.pre_row;
+    u.ct_fixed = -1;
+    u.rt_fixed = jt + 1;
+    u.rnext = R2;
+    if (d.n_row > 0) k_bf_update<false><<<d.n_row, BF_THREADS, sm2, st>>>(u);  // 5
+    k_bf_diag_rows<<<d.cnt2, 64, 0, st>>>(L, m_first, j0 + BF_NB, o.ainv, p->d_ainv, p->d_bf_d, p->d_status);  // 6
+    k_bf_panel_mma<<<d.n_panel2, BF_THREADS, sm2, st>>>(L, m_first, j0 + BF_NB, tab + d.pre_panel, d.cnt2,     // 7
+                                                        o.ainv, p->d_ainv, p->d_bf_d, p->d_bf_e2, o.bf, nullptr);
+    BfUpdArgs v{L, m_first, j0 + BF_NB, tab + d.pre_panel, d.cnt2, o.ainv, p->d_ainv, p->d_bf_e2, R2, o.bf,
+                nullptr, nullptr, nullptr, -1, jt};
+    k_bf_update<false><<<d.n_panel2, BF_THREADS, sm2, st>>>(v);  // 8
+    BfUpdArgs w{L, m_first, j0, nullptr, d.cnt2, o.ainv, p->d_ainv, p->d_bf_e, R1, o.bf, nullptr, p->d_bf_e2, R2,
+                -1, -1};
+    if (upd_wide && d.n_updw2 > 0) {  // 9
+      w.pre = tab + d.pre_updw2;
+      k_bf_update_w<true><<<d.n_updw2, BF_THREADS, smw, st>>>(w);
+    } else if (d.n_upd2 > 0) {
+      w.pre = tab + d.pre_upd2;
+      k_bf_update<true><<<d.n_upd2, BF_THREADS, sm2, st>>>(w);
+    }
+    p->launches += 6;
+  }
+  if (d.cnt > d.cnt2) {  // orders without a J2 panel in this step: the rank-64 update of J1
+    BfUpdArgs u{L, m_first + d.cnt2, j0, nullptr, d.cnt - d.cnt2, o.ainv, p->d_ainv, p->d_bf_e, R1, o.bf, nullptr,
+                nullptr, nullptr, -1, -1};
+    if (upd_wide && d.n_singlew > 0) {
+      u.pre = tab + d.pre_singlew;
+      k_bf_update_w<false><<<d.n_singlew, BF_THREADS, smw, st>>>(u);
+      p->launches++;
+    } else if (d.n_single > 0) {
+      u.pre = tab + d.pre_single;
+      k_bf_update<false><<<d.n_single, BF_THREADS, sm2, st>>>(u);
+      p->launches++;
+    }
+  }
   return cudaGetLastError();
 }
 
@@ -716,8 +870,20 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
   // step's panel (J columns) and update (J-row tiles) into the other of two
   // buffers (OSPH_BF_RFUSE=0 copies it every step instead; bit-identical)
   static const bool fused_r = !(getenv("OSPH_BF_RFUSE") && atoi(getenv("OSPH_BF_RFUSE")) == 0);
-  for (size_t sidx = 0; sidx < r.steps.size(); ++sidx)
-    if ((e = bf_step(p, r, (int)sidx, st, o, fused_r)) != cudaSuccess) return e;
+  // paired (rank-128) steps: half the passes of the trailing update over every matrix
+  // (OSPH_BF_PAIR=0|1 forces the rank-64 steps / the paired ones)
+  static const int pair_env = getenv("OSPH_BF_PAIR") ? atoi(getenv("OSPH_BF_PAIR")) : -1;
+  const bool paired = pair_env >= 0 ? pair_env != 0 : L >= 512;
+  if (paired) {
+    if ((e = bf_attrs(p->device)) != cudaSuccess) return e;
+    static const int upd_rows_env = getenv("OSPH_BF_UPD_ROWS") ? atoi(getenv("OSPH_BF_UPD_ROWS")) : 0;
+    const bool upd_wide = upd_rows_env ? upd_rows_env == 128 : L >= 1024;
+    for (size_t ps = 0; ps < r.psteps.size(); ++ps)
+      if ((e = bf_pair_step(p, r, (int)ps, st, o, upd_wide)) != cudaSuccess) return e;
+  } else {
+    for (size_t sidx = 0; sidx < r.steps.size(); ++sidx)
+      if ((e = bf_step(p, r, (int)sidx, st, o, fused_r)) != cudaSuccess) return e;
+  }
   if (p->need_norms) {
     k_bf_colnorm<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, o.ainv, p->d_ainv, p->d_norms, 1);
     p->launches++;

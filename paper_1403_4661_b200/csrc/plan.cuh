@@ -9,9 +9,17 @@
 struct BfStep {
   int cnt = 0, pre_panel = 0, n_panel = 0, pre_upd = 0, n_upd = 0, pre_updw = 0, n_updw = 0;  // updw: 128-row tiles
 };
+struct BfPairStep {  // one paired (rank-128) step of factor_bf.cu: panels J1 = [j0, j0+64), J2 = [j0+64, j0+128)
+  int j0 = 0, cnt = 0, cnt2 = 0;  // orders with n > j0 / with n > j0 + 64 (the first ones of the range)
+  int pre_panel = 0, n_panel = 0, n_panel2 = 0;  // 64-row tiles per order (n_panel2: first cnt2 orders)
+  int pre_row = 0, n_row = 0;                    // column tiles outside J1, J2 (cnt2 orders)
+  int pre_upd2 = 0, n_upd2 = 0, pre_updw2 = 0, n_updw2 = 0;        // paired update, 64- / 128-row tiles
+  int pre_single = 0, n_single = 0, pre_singlew = 0, n_singlew = 0;  // orders cnt2..cnt-1: rank-64 update
+};
 struct BfRange {  // work-item tables of one range of orders (factor_bf.cu)
   int m_first = -1, m_last = -1;
   std::vector<BfStep> steps;
+  std::vector<BfPairStep> psteps;
   int* d_tab = nullptr;
 };
 struct BfOffsets {  // per-order offsets (indexed by m) into the factor buffers
@@ -117,6 +125,7 @@ struct osph_plan {
   bool need_norms = true;        // this call checks conditioning (check=True): factor kernels accumulate norms
   int64_t* d_bf_off = nullptr;   // [L+1] offsets of the E / R panels (NB x lde(n) per order)
   double* d_bf_e = nullptr;
+  double* d_bf_e2 = nullptr;     // the second panel's E of a paired step
   double* d_bf_r = nullptr;      // two R buffers of bf_r_half doubles (alternating steps)
   int64_t bf_r_half = 0;
   double* d_bf_d = nullptr;      // NB x NB diagonal-block inverses

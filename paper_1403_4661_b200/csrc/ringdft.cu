@@ -201,7 +201,10 @@ __device__ __forceinline__ void scatter_rhs_multi(const double2* X, int lstride,
     const double2 xn = X[(g << lstride) + (SWZ ? fsw(qn) : qn)];
     const int64_t base = r_index(packed_pos(L, m, k - m), 0, b0 + g, lgG, npos);
     R[base] = make_double2(scale * xp.x, scale * xp.y);
-    R[base + (1 << lgG)] = make_double2(scale * xn.x, scale * xn.y);
+    // order 0 solves its + column only (f_{l,-0} = f_{l,0}, transform.py:451): its - slot
+    // starts at zero and collects the sweep's -tone corrections that alias to bin 0
+    // (s = 0 mod 2k+1), folded into the + slot before order 0 is solved (sweep.cu)
+    R[base + (1 << lgG)] = m == 0 ? make_double2(0.0, 0.0) : make_double2(scale * xn.x, scale * xn.y);
   }
 }
 

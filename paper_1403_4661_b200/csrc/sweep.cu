@@ -139,14 +139,18 @@ __device__ __forceinline__ void step_barrier() {
 }
 __device__ __forceinline__ void cluster_sync_all() { step_barrier<0>(); }
 // Alias target of a correction of order s on ring k: R[pos(tm, k - tm)][slot]
-// (transform.py:459-463 in the order-major layout; r == 0 puts both tones in bin 0)
+// (transform.py:459-463 in the order-major layout).  r == 0 puts both tones in
+// bin 0 (order 0): the + tone into its + slot, the - tone into order 0's unused
+// - slot (zeroed by the ring DFT scatter), so the two reductions never race on
+// one address (bitwise-reproducible sums); the slots are added before order 0
+// is solved.
 __device__ __forceinline__ int mod_small(int a, int n);
 __device__ __forceinline__ void corr_target(int s, int k, bool plus, int& tm, int& slot) {
   const int nk = 2 * k + 1;
   const int r = mod_small(s, nk);
   if (r == 0) {
     tm = 0;
-    slot = 0;
+    slot = plus ? 0 : 1;
   } else if (r <= k) {
     tm = r;
     slot = plus ? 0 : 1;
@@ -654,9 +658,9 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
         }
         const double* rr = rch + (size_t)(t & 1) * CC + 4 * b;
         double* lt = late + (size_t)(t & 1) * CC + 4 * b;
-        if (t == 0) {
-          lt[0] = rr[0] - gp_r - gm_r;
-          lt[1] = rr[1] - gp_i - gm_i;
+        if (t == 0) {  // bin 0 of ring 0: + slot + the - tones collected in the - slot
+          lt[0] = rr[0] + rr[2] - gp_r - gm_r;
+          lt[1] = rr[1] + rr[3] - gp_i - gm_i;
           lt[2] = 0.0;
           lt[3] = 0.0;
         } else {
@@ -704,7 +708,7 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
           const int bl = c >> 2;
           if (k >= s - 1 || bl >= gm) return;  // ring s-1 is the chain
           const bool plus = (c & 2) == 0;
-          double gr = plus ? v0 : ss * v0, gi = plus ? v1 : ss * v1;
+          const double gr = plus ? v0 : ss * v0, gi = plus ? v1 : ss * v1;
           if (k == s - 2 && s - 3 >= SWEEP_PF_MIN) {
             // row 1 of order s-3 (ring s-2): its right-hand side was prefetched
             // before this correction, so the correction goes to every CTA's
@@ -722,17 +726,6 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
           }
           int tm, slot;
           corr_target(s, k, plus, tm, slot);
-          if (tm == 0) {
-            // s = 0 mod (2k+1): both tones land in bin 0 -- one reduction from the
-            // + lane (deterministic sum order, no racing pair of REDs).  The other
-            // tone of the same map is in lane ^ 1 (column c ^ 2); both lanes of the
-            // pair share (s, k), so they take this (rare) branch together.
-            const unsigned am = __activemask();
-            const double o0 = __shfl_xor_sync(am, v0, 1), o1 = __shfl_xor_sync(am, v1, 1);
-            if (!plus) return;
-            gr += ss * o0;
-            gi += ss * o1;
-          }
           // fire-and-forget reductions (RED.ADD.F64)
           double2* rp = Rt + (packed_pos(L, tm, k - tm) * 2 + slot) * G + bl;
           atomicAdd(&rp->x, -gr);
@@ -844,6 +837,16 @@ __global__ void __launch_bounds__(SWEEP_THREADS_ALL, 1) k_sweep(
           // small orders: aliases are dense, fetch again now that R is final
           if (gt == 0) operands_issue(s);
           operands_wait(s);
+          if (s == 0) {
+            // order 0: add the - slot (the -tone corrections of bin 0) into the + slot;
+            // gst columns are [+-][map][re, im], the - half starts at CC / 2
+            group_sync(SWEEP_BAR_B, SWEEP_NB);
+            double* g0 = gst;  // parity 0
+            for (int i = gt; i < L * (CC / 2); i += SWEEP_NB) {
+              const int r = i / (CC / 2), c = i - r * (CC / 2);
+              g0[(size_t)r * CC + c] += g0[(size_t)r * CC + c + CC / 2];
+            }
+          }
         }
         group_sync(SWEEP_BAR_B, SWEEP_NB);
         PROF_MARK(1);

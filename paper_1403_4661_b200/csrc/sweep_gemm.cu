@@ -158,9 +158,9 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
         }
         const int k = row, nk = 2 * k + 1, rr = s % nk;
         int tm, ts;
-        if (rr == 0) {
+        if (rr == 0) {  // bin 0: -tones into order 0's unused - slot (no racing REDs; folded at s = 0)
           tm = 0;
-          ts = 0;
+          ts = slot;
         } else if (rr <= k) {
           tm = rr;
           ts = slot;
@@ -168,23 +168,21 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
           tm = nk - rr;
           ts = slot ^ 1;
         }
-        if (rr == 0) {
-          // both tones land in bin 0: one reduction from the slot-0 lane
-          // (deterministic sum order instead of two racing REDs).  The other slot
-          // of the same (row, map) is in lane ^ 1 (column col ^ 2); both lanes
-          // share the row, so they take this (rare) branch together.
-          const unsigned am = __activemask();
-          const double or_ = __shfl_xor_sync(am, acc[i][j][0], 1), oi_ = __shfl_xor_sync(am, acc[i][j][1], 1);
-          if (slot) continue;
-          vr += sg * or_;
-          vi += sg * oi_;
-        }
         double2* rp = R + ((int64_t)b * npos + packed_pos(L, tm, k - tm)) * 2 + ts;
         atomicAdd(&rp->x, -vr);
         atomicAdd(&rp->y, -vi);
       }
     }
   }
+}
+
+// R[b][pos(0, k)][+] += R[b][pos(0, k)][-] for every ring k (plain layout).
+__global__ void k_fold_order0(int L, double2* __restrict__ R) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= L) return;
+  const int64_t npos = (int64_t)L * (L + 1) / 2;
+  double2* rp = R + ((int64_t)blockIdx.y * npos + k) * 2;  // pos(0, k) = k
+  rp[0] = make_double2(rp[0].x + rp[1].x, rp[0].y + rp[1].y);
 }
 
 template <int NS, int TM, int MAPS>
@@ -201,6 +199,10 @@ static cudaError_t sweep_gemm_run(osph_plan* p, int B, double2* flm) {
   const int ny = (B + MAPS - 1) / MAPS;
   for (int s = L - 1; s >= 0; --s) {
     const int n = L - s;
+    if (s == 0) {  // order 0: fold the - slot (bin-0 -tone corrections) into the + slot
+      k_fold_order0<<<dim3((L + 127) / 128, B), 128, 0, p->stream>>>(L, p->d_r);
+      p->launches++;
+    }
     k_sweep_gemm<0, NS, TM, MAPS><<<dim3((n + TM - 1) / TM, ny), SG_THREADS, smem, p->stream>>>(
         L, s, B, p->d_xt, p->d_xt_off, p->d_w, p->d_r, p->d_xbuf, flm);
     if (s >= 1)

@@ -22,7 +22,7 @@ void osph_set_error(const std::string& msg);
 
 static int64_t order_doubles(int L, int m, bool refine) {
   const int n = L - m;
-  return (int64_t)n * n + tile_size(n, n) * (refine ? 2 : 1) + tile_size(m, n) + 2 * bf_panel_doubles(n);
+  return (int64_t)n * n + tile_size(n, n) * (refine ? 2 : 1) + tile_size(m, n) + 4 * bf_panel_doubles(n);
 }
 
 #define W_TRY(expr)                                                                  \
@@ -115,6 +115,7 @@ int alloc_factor_storage(osph_plan* p) {
     if (rf) W_TRY(dalloc_w(&p->d_at, (size_t)tot[1]));
     W_TRY(dalloc_w(&p->d_pbelow, (size_t)tot[2]));
     W_TRY(dalloc_w(&p->d_bf_e, (size_t)tot[3]));
+    W_TRY(dalloc_w(&p->d_bf_e2, (size_t)tot[3]));
     W_TRY(dalloc_w(&p->d_bf_r, (size_t)(2 * tot[3])));  // two R buffers (alternating steps), zeroed once
     W_TRY(cudaMemsetAsync(p->d_bf_r, 0, sizeof(double) * (size_t)(2 * tot[3]), st));
     p->bf_r_half = tot[3];
@@ -161,6 +162,7 @@ int alloc_factor_storage(osph_plan* p) {
   if (rf) W_TRY(dalloc_w(&p->d_at, (size_t)mx[1]));
   W_TRY(dalloc_w(&p->d_pbelow, (size_t)mx[2]));
   W_TRY(dalloc_w(&p->d_bf_e, (size_t)mx[3]));
+  W_TRY(dalloc_w(&p->d_bf_e2, (size_t)mx[3]));
   W_TRY(dalloc_w(&p->d_bf_r, (size_t)(2 * mx[3])));
   W_TRY(cudaMemsetAsync(p->d_bf_r, 0, sizeof(double) * (size_t)(2 * mx[3]), st));
   p->bf_r_half = mx[3];

@@ -56,3 +56,21 @@ def test_factor_variants_bit_identical(tmp_path, L, B):
         got = run_variant(tmp_path, L, B, v, i)
         assert np.array_equal(got["flm"], base["flm"]), f"variant {v} differs: " \
             f"{np.abs(got['flm'] - base['flm']).max():.3e}"
+
+
+@pytest.mark.parametrize("L,B", [(256, 2), (512, 1), (2048, 1)])
+def test_paired_steps_match_single_steps(tmp_path, L, B):
+    """Paired (rank-128) breadth-first steps against rank-64 steps: the same elimination
+    in a different association order, so equal to rounding (L = 2048: on the orders the
+    peeling chain has not yet amplified, m >= L/2; DESIGN 6)."""
+    single = run_variant(tmp_path, L, B, {"OSPH_BF_PAIR": "0"}, "single")
+    paired = run_variant(tmp_path, L, B, {"OSPH_BF_PAIR": "1"}, "paired")
+    assert float(paired["rt_err"]) <= (1e-9 if L <= 512 else 0.12)
+    a, b = paired["flm"], single["flm"]
+    if L >= 2048:
+        ell = np.floor(np.sqrt(np.arange(L * L))).astype(np.int64)
+        m = np.abs(np.arange(L * L) - ell * ell - ell)
+        keep = m >= L // 2
+        a, b = a[:, keep], b[:, keep]
+    scale = max(1.0, float(np.abs(b).max()))
+    assert np.abs(a - b).max() <= 1e-11 * scale, f"{np.abs(a - b).max():.3e} vs scale {scale:.3e}"

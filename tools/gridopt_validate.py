@@ -1,0 +1,107 @@
+"""Check the GPU greedy's rank-one kappa against exact SVD kappa at sampled steps.
+
+    python tools/gridopt_validate.py L [grid file] [--steps m1,m2,...] [--top 8] [--others 8]
+
+gridopt.py picks ring m as the unassigned candidate t minimising the 2-norm
+condition number of the order-m block [r_t; A0] (the reference's greedy,
+sampling.py:217-278, which evaluates kappa by an SVD per candidate,
+blocks.py:75-85).  It evaluates kappa from the secular equation of a rank-one
+update of A0^T A0 instead.  For a committed grid (whose permutation fixes the
+state of the greedy at every step) this tool recomputes, at the sampled steps
+m, the rank-one kappa of every unassigned candidate and the exact kappa
+(torch.linalg.svdvals on the GPU) of the `top` best candidates by rank-one
+kappa plus `others` random candidates, and reports:
+  * whether the grid's pick is the exact-SVD argmin among the evaluated ones
+    (the reference's choice, up to its 1e-9 tie rule);
+  * the relative difference of the two kappas for the pick;
+  * the exact margin between the best and the second-best candidate.
+Writes a table on stdout (profiles/gridopt_validate_*.txt).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    import torch
+
+    import paper_1403_4661_b200 as osp
+    from paper_1403_4661_b200 import _lib, gridopt, sampling
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("L", type=int)
+    ap.add_argument("grid", nargs="?")
+    ap.add_argument("--steps", default=None)
+    ap.add_argument("--top", type=int, default=8)
+    ap.add_argument("--others", type=int, default=8)
+    args = ap.parse_args()
+    L = args.L
+    path = args.grid or ROOT / "tests" / "golden" / "grids" / f"grid-L{L}-uniform-condmin.txt"
+    grid = osp.load_grid(path)
+    perm = np.asarray(grid.permutation)
+    cands = sampling.equiangular_candidates(L)
+    equator = np.abs(cands - np.pi / 2.0)
+    steps = ([int(s) for s in args.steps.split(",")] if args.steps else
+             sorted({L - 2, (3 * L) // 4, L // 2, L // 4, L // 8, 64, 16, 2, 0}, reverse=True))
+    lib = _lib.load()
+    plan = osp.transform.Plan(cands, 1, 0)
+    buf = torch.empty((L, L), dtype=torch.float64, device="cuda")
+    rng = np.random.default_rng(0)
+    print(f"# gridopt validation: L={L}, grid {Path(path).name}; exact kappa = torch.linalg.svdvals (GPU)")
+    print(f"{'m':>6} {'cands':>6} {'pick':>6} {'pick=exact argmin':>18} {'kappa(pick)':>14} "
+          f"{'rel diff rank1/exact':>21} {'exact margin to 2nd':>20} {'max rel diff (evaluated)':>25}")
+    t0 = time.time()
+    all_ok = True
+    for m in steps:
+        if not 0 <= m <= L - 2:
+            continue
+        _lib.raise_for(lib.osph_legendre_block(plan.handle, m, ctypes.c_void_p(buf.data_ptr()), L, _lib.OSPH_DEVICE))
+        P = buf[: L - m].T  # (candidates, degrees)
+        chosen = torch.as_tensor(perm[m + 1:], device="cuda")
+        unassigned = np.array(sorted(set(range(L)) - set(perm[m + 1:].tolist())))
+        A0 = P.index_select(0, chosen)
+        d, V = torch.linalg.eigh(A0.T @ A0)
+        R = P.index_select(0, torch.as_tensor(unassigned, device="cuda"))
+        k1 = gridopt.rank_one_kappas(d, R @ V).cpu().numpy()
+        order = np.argsort(k1)
+        sel = list(order[: args.top])
+        rest = order[args.top:]
+        if len(rest):
+            sel += list(rng.choice(rest, size=min(args.others, len(rest)), replace=False))
+        pick = int(perm[m])
+        pick_i = int(np.nonzero(unassigned == pick)[0][0])
+        if pick_i not in sel:
+            sel.append(pick_i)
+        exact = {}
+        for i in sel:
+            A = torch.cat([P[int(unassigned[i])][None, :], A0], dim=0)
+            s = torch.linalg.svdvals(A)
+            exact[i] = float(s[0] / s[-1]) if float(s[-1]) > 0 else float("inf")
+        best = min(exact.values())
+        near = [i for i, v in exact.items() if v <= best * (1 + 1e-9)]
+        ref_pick = int(unassigned[min(near, key=lambda i: (equator[unassigned[i]], unassigned[i]))])
+        ok = ref_pick == pick
+        all_ok &= ok
+        ex = sorted(exact.values())
+        margin = (ex[1] - ex[0]) / ex[0] if len(ex) > 1 else float("nan")
+        rel = abs(k1[pick_i] - exact[pick_i]) / exact[pick_i]
+        maxrel = max(abs(k1[i] - exact[i]) / exact[i] for i in exact if np.isfinite(exact[i]))
+        print(f"{m:>6} {len(unassigned):>6} {pick:>6} {str(ok):>18} {exact[pick_i]:>14.6g} {rel:>21.3e} "
+              f"{margin:>20.3e} {maxrel:>25.3e}", flush=True)
+    plan.close()
+    print(f"# all picks equal the exact-SVD choice among the evaluated candidates: {all_ok} "
+          f"({time.time() - t0:.1f} s)")
+
+
+if __name__ == "__main__":
+    main()
