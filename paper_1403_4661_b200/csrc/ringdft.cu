@@ -91,14 +91,17 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_inverse_bluestein(
   const int n = 2 * k + 1;
   const int N = fft_n[k];
   const int logN = 31 - __clz(N);
-  double2* xs = sm + OSPH_SW_SMEM;  // Gr transforms of length N after the short-span twiddles
+  // Gr transforms of length N after the short-span twiddles: a size-N transform
+  // reads stage-table entries < N only, so the data start right after them
+  const int tw_cnt = min(N, OSPH_SW_SMEM);
+  double2* xs = sm + tw_cnt;
   load_stage_twiddles_smem(sm, logN, gsw);
   const StageTw twn{sm, gsw};
   const double2* chirp = chirp_all + chirp_off[k];
   const double2* bh = bhat_all + bhat_off[k] + N;  // inverse-direction kernel
   const int b_first = blockIdx.y * maps_per_block;
   const int b_last = min(B, b_first + maps_per_block);
-  const int Gmax = max(1, (smem_cplx - OSPH_SW_SMEM) >> logN);
+  const int Gmax = max(1, (smem_cplx - tw_cnt) >> logN);
   for (int b0 = b_first; b0 < b_last; b0 += Gmax) {
     const int Gr = min(Gmax, b_last - b0);
     for (int idx = threadIdx.x; idx < Gr * N; idx += blockDim.x) {  // map-fastest reads of G
@@ -218,7 +221,10 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_forward_bluestein(
   const int n = 2 * k + 1;
   const int N = fft_n[k];
   const int logN = 31 - __clz(N);
-  double2* xs = sm + OSPH_SW_SMEM;  // Gr transforms of length N after the short-span twiddles
+  // Gr transforms of length N after the short-span twiddles: a size-N transform
+  // reads stage-table entries < N only, so the data start right after them
+  const int tw_cnt = min(N, OSPH_SW_SMEM);
+  double2* xs = sm + tw_cnt;
   load_stage_twiddles_smem(sm, logN, gsw);
   const StageTw twn{sm, gsw};
   const double2* chirp = chirp_all + chirp_off[k];
@@ -226,7 +232,7 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_forward_bluestein(
   // maps [bofs, bend) of a batch of B (R keeps the batch stride B)
   const int b_first = bofs + blockIdx.y * maps_per_block;
   const int b_last = min(bend, b_first + maps_per_block);
-  const int Gmax = max(1, (smem_cplx - OSPH_SW_SMEM) >> logN);
+  const int Gmax = max(1, (smem_cplx - tw_cnt) >> logN);
   for (int b0 = b_first; b0 < b_last; b0 += Gmax) {
     const int Gr = min(Gmax, b_last - b0);
     for (int idx = threadIdx.x; idx < (Gr << logN); idx += blockDim.x) {  // contiguous ring reads per map

@@ -53,13 +53,8 @@ def _single(grid, samples, env=None, monkeypatch=None):
 
 
 @pytest.mark.parametrize("L,ndev", [(64, 2), (256, 3), (1024, 2)])
-def test_group_plan_chain_single_map(L, ndev, grid_of, monkeypatch, tmp_path):
-    if L == 1024:  # (refinement on, L > 512) grid from the GPU greedy, as the reference's make_grid would
-        from paper_1403_4661_b200 import gridopt
-
-        g = gridopt.make_grid(L, ordering=osp.Ordering.CONDITION_MINIMIZED, cache_dir=str(tmp_path))
-    else:
-        g = grid_of(L)
+def test_group_plan_chain_single_map(L, ndev, grid_of, monkeypatch):
+    g = grid_of(L)  # L = 1024: the GPU greedy's grid (refinement on for L > 512)
     rng = np.random.default_rng(L + ndev)
     flm = rng.standard_normal((1, L * L)) + 1j * rng.standard_normal((1, L * L))
     ref_s = osp.inverse_sht_batch(flm, g)

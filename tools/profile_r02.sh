@@ -12,11 +12,11 @@ cap() {  # name regex skip L B N
   timeout 900 ncu --set full $M --import-source on --clock-control none --kernel-name-base demangled -k regex:$2 -s $3 -c 1 \
     -o gpurun_out/$1 -f python tools/fwd_once.py $4 $5 $6 > gpurun_out/ncu_$1.log 2>&1
 }
-cap sweep_r02 'k_sweep<8>' 1 256 64 2
-cap synth_r02 'k_synth_dmma' 1 256 64 2
+cap sweep_r02 'k_sweep<\(int\)8>' 1 256 64 2
+cap synth_r02 'k_synth_dmma' 0 256 64 1
 cap ringinv_r02 'k_ring_inverse_bluestein\(' 0 256 64 1
 cap ringfwd_r02 'k_ring_forward_bluestein\(' 1 256 64 2
-cap bfu256_r02 'k_bf_update<false>' 6 256 64 2
-cap bfpair2048_r02 'k_bf_update_w<true>' 12 2048 1 1
-cap sweepgemm_r02 'k_sweep_gemm<0' 300 512 128 1
+cap bfu256_r02 'k_bf_update<\(bool\)0>' 6 256 64 2
+cap bfpair2048_r02 'k_bf_update_w<\(bool\)1>' 4 2048 1 1
+cap sweepgemm_r02 'k_sweep_gemm<\(int\)0' 300 512 128 1
 ls -la gpurun_out/*.ncu-rep
