@@ -50,3 +50,30 @@ def grid_of():
 @pytest.fixture
 def rng():
     return np.random.default_rng(20240901)
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _release_gpu_memory():
+    """Cached plans (get_plan) of one test module can hold tens of GB of factor
+    storage at L >= 2048; free them between modules so large-L tests see the
+    whole GPU, as a fresh process would."""
+    yield
+    if not has_gpu():
+        return
+    import torch
+
+    import paper_1403_4661_b200 as osp
+
+    osp.clear_plans()
+    torch.cuda.empty_cache()
+
+
+@pytest.fixture
+def fresh_gpu():
+    """Drop cached plans and torch's cached blocks before a large-L test."""
+    import torch
+
+    import paper_1403_4661_b200 as osp
+
+    osp.clear_plans()
+    torch.cuda.empty_cache()

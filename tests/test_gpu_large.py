@@ -86,7 +86,7 @@ def ref4096(golden):
     return golden("ref_L4096.npz")
 
 
-def test_L4096_forward_top_orders(ref4096, grid_of):
+def test_L4096_forward_top_orders(ref4096, grid_of, fresh_gpu):
     L4 = 4096
     grid = grid_of(L4)
     flm = config_coefficients(L4, np.random.default_rng(SEED + 5), spectrum="cmb")

@@ -77,7 +77,7 @@ def test_pivot_order_matches_lapack_getrf(L, ordering, grid_of):
 
 
 @pytest.mark.parametrize("L,orders", [(2048, [0, 1, 700, 2040]), (4096, [0, 1000, 3000, 4090])])
-def test_pivot_order_large_blocks(L, orders, grid_of, monkeypatch):
+def test_pivot_order_large_blocks(L, orders, grid_of, monkeypatch, fresh_gpu):
     """n up to 2048 (resident factor storage) and 4096 (windowed, 16-CTA clusters): our order
     is a partial-pivoting order of each block."""
     from oracle import optisph_oracle as O
@@ -237,7 +237,7 @@ def test_config3_shape_without_gemm_sweep(grid_of, monkeypatch):
 # device Legendre rows at L=4096: the reference's rescaling-range KATs
 
 
-def test_legendre_block_range_L4096():
+def test_legendre_block_range_L4096(fresh_gpu):
     import ctypes
 
     import torch
