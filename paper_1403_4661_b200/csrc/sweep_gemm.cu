@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
                                                            const int64_t* __restrict__ a_off,
                                                            const double* __restrict__ w_all, double2* __restrict__ R,
                                                            double2* __restrict__ xbuf, double2* __restrict__ flm) {
+  pdl_start();
   extern __shared__ __align__(16) unsigned char sg_raw[];
   using Stage = SgStage<TM, MAPS>;
   Stage* st = reinterpret_cast<Stage*>(sg_raw);
@@ -178,6 +179,7 @@ __global__ void __launch_bounds__(SG_THREADS) k_sweep_gemm(int L, int s, int B, 
 
 // R[b][pos(0, k)][+] += R[b][pos(0, k)][-] for every ring k (plain layout).
 __global__ void k_fold_order0(int L, double2* __restrict__ R) {
+  pdl_start();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= L) return;
   const int64_t npos = (int64_t)L * (L + 1) / 2;
@@ -200,14 +202,15 @@ static cudaError_t sweep_gemm_run(osph_plan* p, int B, double2* flm) {
   for (int s = L - 1; s >= 0; --s) {
     const int n = L - s;
     if (s == 0) {  // order 0: fold the - slot (bin-0 -tone corrections) into the + slot
-      k_fold_order0<<<dim3((L + 127) / 128, B), 128, 0, p->stream>>>(L, p->d_r);
+      launch_pdl(k_fold_order0, dim3((L + 127) / 128, B), dim3(128), 0, p->stream, L, p->d_r);
       p->launches++;
     }
-    k_sweep_gemm<0, NS, TM, MAPS><<<dim3((n + TM - 1) / TM, ny), SG_THREADS, smem, p->stream>>>(
-        L, s, B, p->d_xt, p->d_xt_off, p->d_w, p->d_r, p->d_xbuf, flm);
+    launch_pdl(k_sweep_gemm<0, NS, TM, MAPS>, dim3((n + TM - 1) / TM, ny), dim3(SG_THREADS), smem, p->stream, L, s,
+               B, (const double*)p->d_xt, (const int64_t*)p->d_xt_off, (const double*)p->d_w, p->d_r, p->d_xbuf, flm);
     if (s >= 1)
-      k_sweep_gemm<1, NS, TM, MAPS><<<dim3((s + TM - 1) / TM, ny), SG_THREADS, smem, p->stream>>>(
-          L, s, B, p->d_pbelow, p->d_pb_off, p->d_w, p->d_r, p->d_xbuf, flm);
+      launch_pdl(k_sweep_gemm<1, NS, TM, MAPS>, dim3((s + TM - 1) / TM, ny), dim3(SG_THREADS), smem, p->stream, L,
+                 s, B, (const double*)p->d_pbelow, (const int64_t*)p->d_pb_off, (const double*)p->d_w, p->d_r,
+                 p->d_xbuf, flm);
   }
   p->launches += 2 * L - 1;
   return cudaGetLastError();

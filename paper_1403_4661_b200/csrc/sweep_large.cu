@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(SL_THREADS) k_sweep_solve_t(int L, int s, int 
                                                               const double2* __restrict__ R,
                                                               double2* __restrict__ xbuf, double2* __restrict__ flm,
                                                               int64_t npos, int64_t p0, int accumulate) {
+  pdl_start();
   __shared__ double red[SL_THREADS / 32][8][4 * MB];
   const int n = L - s, nrt = (n + 7) >> 3;
   const int rt = blockIdx.x;
@@ -125,6 +126,7 @@ __global__ void __launch_bounds__(128) k_sweep_resid(int L, int s, int B, const 
                                                      const double2* __restrict__ pstart,
                                                      const double2* __restrict__ R, const double2* __restrict__ xbuf,
                                                      double2* __restrict__ rres) {
+  pdl_start();
   const int n = L - s;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
@@ -165,6 +167,7 @@ __global__ void __launch_bounds__(SL_THREADS) k_sweep_corr_t(int L, int s, int B
                                                              const int64_t* __restrict__ pb_off,
                                                              const double2* __restrict__ xbuf,
                                                              double2* __restrict__ R) {
+  pdl_start();
   __shared__ double red[SL_THREADS / 32][8][4 * MB];
   const int n = L - s, nrtpb = (s + 7) >> 3;
   const int rt = blockIdx.x;  // rings 8 rt .. 8 rt + 7 (< s)
@@ -262,6 +265,7 @@ __global__ void __launch_bounds__(SL_THREADS) k_sweep_resid_t(int L, int s, int 
                                                               const double2* __restrict__ R,
                                                               const double2* __restrict__ xbuf,
                                                               double2* __restrict__ rres) {
+  pdl_start();
   __shared__ double red[SL_THREADS / 32][8][4 * MB];
   const int n = L - s, nrt = (n + 7) >> 3;
   const int rt = blockIdx.x;  // rings s + 8 rt .. s + 8 rt + 7
@@ -336,41 +340,45 @@ cudaError_t launch_sweep_large_range(osph_plan* p, int B, double2* flm, int s_hi
   const int L = p->L;
   const int mb = B >= 2 ? 2 : 1;
   const int ymaps = (B + mb - 1) / mb;
+  // every launch of the chain: programmatic dependent launch (common.cuh)
+  const dim3 blk(SL_THREADS);
+  const double* xt = p->d_xt;
+  const double* wv = p->d_w;
+  const double* pbt = p->d_pbelow;
+  const double* at = p->d_at;
   for (int s = s_hi; s >= s_lo; --s) {
     const int n = L - s;
     const int64_t npos = (int64_t)L * (L + 1) / 2, p0 = packed_pos(L, s, 0);
+    const dim3 gn((n + 7) / 8, ymaps), gs((s + 7) / 8, ymaps);
     auto solve = [&](const double2* rhs, int64_t np, int64_t q0, int acc) {
       if (mb == 2)
-        k_sweep_solve_t<2><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(
-            L, s, B, p->d_xt, xt_off, p->d_w, rhs, p->d_xbuf, flm, np, q0, acc);
+        launch_pdl(k_sweep_solve_t<2>, gn, blk, 0, p->stream, L, s, B, xt, xt_off, wv, rhs, p->d_xbuf, flm, np, q0, acc);
       else
-        k_sweep_solve_t<1><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(
-            L, s, B, p->d_xt, xt_off, p->d_w, rhs, p->d_xbuf, flm, np, q0, acc);
+        launch_pdl(k_sweep_solve_t<1>, gn, blk, 0, p->stream, L, s, B, xt, xt_off, wv, rhs, p->d_xbuf, flm, np, q0, acc);
       p->launches++;
     };
     solve(p->d_r, npos, p0, 0);
     for (int rstep = 0; rstep < p->refine; ++rstep) {  // x += X (b - A x): fixed-precision refinement
+      const double2* r = p->d_r;
+      const double2* xb = p->d_xbuf;
       if (p->d_at) {  // stored block (tiled like X)
         if (mb == 2)
-          k_sweep_resid_t<2><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_at, xt_off, p->d_r,
-                                                                                   p->d_xbuf, p->d_rres);
+          launch_pdl(k_sweep_resid_t<2>, gn, blk, 0, p->stream, L, s, B, at, xt_off, r, xb, p->d_rres);
         else
-          k_sweep_resid_t<1><<<dim3((n + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_at, xt_off, p->d_r,
-                                                                                   p->d_xbuf, p->d_rres);
+          launch_pdl(k_sweep_resid_t<1>, gn, blk, 0, p->stream, L, s, B, at, xt_off, r, xb, p->d_rres);
       } else {
-        k_sweep_resid<<<dim3((n + 127) / 128, B), 128, 0, p->stream>>>(L, s, B, p->d_cos, p->d_rec, p->d_ls,
-                                                                        p->d_pstart, p->d_r, p->d_xbuf, p->d_rres);
+        launch_pdl(k_sweep_resid, dim3((n + 127) / 128, B), dim3(128), 0, p->stream, L, s, B, (const double*)p->d_cos,
+                   (const double2*)p->d_rec, (const int*)p->d_ls, (const double2*)p->d_pstart, r, xb, p->d_rres);
       }
       solve(p->d_rres, L, 0, 1);
       p->launches++;
     }
     if (s >= 1) {
+      const double2* xb = p->d_xbuf;
       if (mb == 2)
-        k_sweep_corr_t<2><<<dim3((s + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_pbelow, pb_off,
-                                                                                p->d_xbuf, p->d_r);
+        launch_pdl(k_sweep_corr_t<2>, gs, blk, 0, p->stream, L, s, B, pbt, pb_off, xb, p->d_r);
       else
-        k_sweep_corr_t<1><<<dim3((s + 7) / 8, ymaps), SL_THREADS, 0, p->stream>>>(L, s, B, p->d_pbelow, pb_off,
-                                                                                p->d_xbuf, p->d_r);
+        launch_pdl(k_sweep_corr_t<1>, gs, blk, 0, p->stream, L, s, B, pbt, pb_off, xb, p->d_r);
       p->launches++;
     }
   }
