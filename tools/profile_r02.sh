@@ -16,7 +16,7 @@ cap sweep_r02 'k_sweep<\(int\)8>' 1 256 64 2
 cap synth_r02 'k_synth_dmma' 0 256 64 1
 cap ringinv_r02 'k_ring_inverse_bluestein\(' 0 256 64 1
 cap ringfwd_r02 'k_ring_forward_bluestein\(' 1 256 64 2
-cap bfu256_r02 'k_bf_update<\(bool\)0>' 6 256 64 2
+cap bfu256_r02 'k_bf_update<\(bool\)1>' 2 256 64 2
 cap bfpair2048_r02 'k_bf_update_w<\(bool\)1>' 4 2048 1 1
 cap sweepgemm_r02 'k_sweep_gemm<\(int\)0' 300 512 128 1
 ls -la gpurun_out/*.ncu-rep
