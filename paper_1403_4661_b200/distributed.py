@@ -111,7 +111,8 @@ def device_bytes(ptr: int, nbytes: int, device: int):
 
 
 def shard_range(L: int, rank: int, world: int, mode: int) -> tuple[int, int, int, int]:
-    """(m_lo, m_hi, k_lo, k_hi) of `rank` (osph_shard_range)."""
+    """(m_lo, m_hi, k_lo, k_hi) of `rank` (osph_shard_range): orders [m_lo, m_hi]
+    (inclusive), rings [k_lo, k_hi)."""
     import ctypes
 
     v = [ctypes.c_int() for _ in range(4)]
@@ -132,7 +133,10 @@ class ShardedTransform:
     FACTOR_BUFFERS = (_lib.BUF_XT, _lib.BUF_PB, _lib.BUF_AT, _lib.BUF_U, _lib.BUF_W, _lib.BUF_BETA,
                       _lib.BUF_JSTAR, _lib.BUF_NORMS, _lib.BUF_STATUS)
 
-    def __init__(self, grid, max_batch: int = 1, mode: str = "chain", group=None, device: int | None = None):
+    def __init__(self, grid, max_batch: int = 1, mode: str = "chain", group=None, device: int | None = None,
+                 plan=None):
+        """`plan` (tests only): an object with the Plan methods used below whose
+        buffers live in host memory; `device` is then "cpu"."""
         import torch
         import torch.distributed as dist
 
@@ -145,11 +149,12 @@ class ShardedTransform:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.mode = mode
         self.cmode = _lib.SHARD_CHAIN if mode == "chain" else _lib.SHARD_FACTORS
-        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.cuda = device != "cpu"
+        self.device = device if not self.cuda else torch.cuda.current_device() if device is None else int(device)
         self.grid = grid
         self.L = grid.band_limit if hasattr(grid, "band_limit") else len(grid)
         thetas = getattr(grid, "thetas", grid)
-        self.plan = Plan(thetas, max_batch, self.device)
+        self.plan = Plan(thetas, max_batch, self.device) if plan is None else plan
         self.plan.shard(self.rank, self.world, self.cmode)
         self.ranges = [shard_range(self.L, r, self.world, self.cmode) for r in range(self.world)]
         self.nccl = dist.is_initialized() and dist.get_backend(group) == "nccl"
@@ -158,7 +163,24 @@ class ShardedTransform:
     def _sync_stream(self):
         import torch
 
-        self.plan.set_stream(_torch_stream(torch.cuda.current_stream(self.device)))
+        if self.cuda:
+            self.plan.set_stream(_torch_stream(torch.cuda.current_stream(self.device)))
+
+    def _synchronize(self):
+        import torch
+
+        if self.cuda:
+            torch.cuda.synchronize(self.device)
+
+    def _view(self, ptr: int, nbytes: int):
+        """uint8 tensor over a plan buffer (device memory; host memory for a test plan)."""
+        import ctypes
+
+        import torch
+
+        if self.cuda:
+            return device_bytes(ptr, nbytes, self.device)
+        return torch.frombuffer((ctypes.c_uint8 * nbytes).from_address(ptr), dtype=torch.uint8)
 
     def _bcast(self, view, src: int):
         """Broadcast a device byte view from rank `src` (NCCL in place; gloo via host)."""
@@ -170,7 +192,7 @@ class ShardedTransform:
         if self.nccl:
             dist.broadcast(view, src=src, group=self.group)
             return
-        torch.cuda.synchronize(self.device)
+        self._synchronize()
         host = view.cpu() if self.rank == src else torch.empty(view.numel(), dtype=torch.uint8)
         dist.broadcast(host, src=src, group=self.group)
         if self.rank != src:
@@ -183,7 +205,7 @@ class ShardedTransform:
         if self.nccl:
             dist.send(view, dst=dst, group=self.group)
         else:
-            torch.cuda.synchronize(self.device)
+            self._synchronize()
             dist.send(view.cpu(), dst=dst, group=self.group)
 
     def _recv(self, view, src: int):
@@ -235,7 +257,7 @@ class ShardedTransform:
                 for which in self.FACTOR_BUFFERS:
                     ptr, nbytes = plan.buffer(which, 0, m_lo, m_hi)
                     if nbytes:
-                        self._bcast(device_bytes(ptr, nbytes, self.device), q)
+                        self._bcast(self._view(ptr, nbytes), q)
             plan.forward_stage(_lib.STAGE_RINGS | _lib.STAGE_SWEEP, B, x.data_ptr(), flm.data_ptr(),
                                _lib.OSPH_DEVICE if check else _lib.OSPH_DEVICE | _lib.OSPH_ASYNC, check)
             return flm
@@ -244,7 +266,7 @@ class ShardedTransform:
         first = _lib.STAGE_RINGS | _lib.STAGE_FACTOR if self.rank == 0 else _lib.STAGE_FACTOR
         plan.forward_stage(first, B, x.data_ptr(), flm.data_ptr(), _lib.OSPH_DEVICE | _lib.OSPH_ASYNC)
         sp_ptr, sp_bytes = plan.buffer(_lib.BUF_SPECTRA, B)
-        spectra = device_bytes(sp_ptr, sp_bytes, self.device)
+        spectra = self._view(sp_ptr, sp_bytes)
         coeffs = flm.view(torch.uint8).reshape(-1)
         if self.rank > 0:  # spectra corrected by every higher order + the coefficients solved so far
             self._recv(spectra, self.rank - 1)
