@@ -182,6 +182,12 @@ def _cpu_init(grid_path):
     """Pool initializer: load the oracle and the grid once per worker process."""
     for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[k] = "1"
+    # a forked worker inherits BLAS pools already sized to every core: the env
+    # vars come too late for them, so cap them through the libraries' own API
+    # (one BLAS thread per process; 16 processes must not oversubscribe the host)
+    from threadpoolctl import threadpool_limits
+
+    _W["blas_limit"] = threadpool_limits(limits=1)
     from oracle import optisph_oracle as O
 
     _, _, thetas = O.load_grid_file(grid_path)

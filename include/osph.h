@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define OSPH_ABI_VERSION 2
+#define OSPH_ABI_VERSION 3
 
 /* return codes */
 #define OSPH_OK 0
@@ -50,6 +50,7 @@ extern "C" {
 #define OSPH_ERR_ILLCOND 2    /* per-order block numerically singular (IllConditionedSolveError) */
 #define OSPH_ERR_CUDA 3       /* CUDA runtime failure (no device, launch error, OOM) */
 #define OSPH_ERR_NCCL 4       /* inter-GPU exchange failed (peer copy / collective of a multi-GPU plan) */
+#define OSPH_ERR_ORDER 5      /* order / spin outside the band limit (OrderRangeError) */
 
 /* pointer kinds / flags for osph_inverse / osph_forward */
 #define OSPH_HOST 0   /* host pointers: the library copies in and out (pinned memory is fastest) */
@@ -207,6 +208,37 @@ int osph_forward_stage(osph_plan* plan, int stages, int B, const void* samples, 
 #define OSPH_BUF_STATUS 9 /* zero-pivot flags */
 #define OSPH_BUF_COUNT 10
 int osph_shard_buffer(osph_plan* plan, int which, int B, int m_lo, int m_hi, void** ptr, int64_t* bytes);
+
+/* ---- spin-weighted transforms ----
+ * spin_inverse_sht / spin_forward_sht (transform.py:474-533) on a
+ * single-device, unsharded plan; layouts as osph_inverse / osph_forward.
+ * spin = 0 IS the scalar path (osph_inverse / osph_forward, bit for bit);
+ * |spin| >= L -> OSPH_ERR_ORDER.  Coefficients with degree l < |spin| are
+ * ignored by the inverse and come back as exact zeros from the forward.  The
+ * forward solves, per order m = L-1..0, the +m and -m blocks
+ * 2pi sY_l(+-m)(theta_k), k >= m, l >= max(m, |spin|) separately (tall
+ * least-squares blocks for m < |spin|); their solution operators are built on
+ * the first forward of each spin (the plan keeps the two most recent spins) and
+ * stats->factor_seconds reports that build (0 once cached).  check != 0
+ * refuses a block whose condition estimate ||A||_1 ||X||_1 exceeds 2e14
+ * (failed_order = the signed order).  ptr_kind: OSPH_HOST or OSPH_DEVICE
+ * (| OSPH_ASYNC); OSPH_REAL is not accepted. */
+int osph_spin_inverse(osph_plan* plan, int spin, int B, const void* flm, void* samples, int ptr_kind);
+int osph_spin_forward(osph_plan* plan, int spin, int B, const void* samples, void* flm, int ptr_kind, int check,
+                      osph_stats* stats);
+
+/* spin_table(spin, m, grid.thetas, L) (legendre.py:276-306) on the device for
+ * all L plan rings: out[(l - lo) * ld + k] = sY_lm(theta_k, 0), l = lo..L-1,
+ * lo = max(|m|, |spin|) (m signed; ld >= L; values below 2^-500 returned as 0).
+ * lo >= L -> OSPH_ERR_ORDER.  ptr_kind must include OSPH_DEVICE. */
+int osph_spin_block(osph_plan* plan, int spin, int m, double* out, int64_t ld, int ptr_kind);
+
+/* Host-only: the constants the spin recurrence of (spin, m) starts from at
+ * degree j = max(|m|, |spin|) (legendre.py:233-262): the seed is
+ * scale * 2^offset * sin(theta/2)^exp_sin * cos(theta/2)^exp_cos, scale
+ * rounded from the exact rational as the reference's Fraction arithmetic.
+ * Any output pointer may be NULL.  No device needed. */
+int osph_spin_seed(int spin, int m, int* j, double* scale, int* offset, int* exp_sin, int* exp_cos);
 
 /* ABI version (OSPH_ABI_VERSION) -- lets bindings refuse a mismatched library. */
 int osph_abi_version(void);

@@ -437,3 +437,166 @@ def config_coefficients(L: int, rng, spectrum: str = "white", real: bool = False
         cl[nz] = 1.0 / (ells[nz] * (ells[nz] + 1.0))
         f = f * np.sqrt(cl)
     return f
+
+
+# ---------------------------------------------------------------------------
+# spin-weighted transforms (legendre.py:212-314, transform.py:474-533)
+
+_BIG = 2.0**500  # legendre.py:31-36
+_TINY = 2.0**-500
+_UP = 2.0**1000
+_DOWN = 2.0**-1000
+_SHIFT = 1000
+
+
+def spin_direct(spin: int, ell: int, m: int, theta: float) -> float:
+    """sY_lm(theta, 0) from the explicit Wigner-d sum (legendre.py:175-218); small l only."""
+    f = math.factorial
+    m_row, m_col = -m, -spin  # spin_direct evaluates d^l_{-m,-s}
+    if abs(m_row) > ell or abs(m_col) > ell:
+        return 0.0
+    ch, sh = math.cos(theta / 2.0), math.sin(theta / 2.0)
+    pref = math.sqrt(f(ell + m_row) * f(ell - m_row) * f(ell + m_col) * f(ell - m_col))
+    total = 0.0
+    for k in range(max(0, m_col - m_row), min(ell + m_col, ell - m_row) + 1):
+        num = ((-1.0) ** ((m_row - m_col + k) % 2) * ch ** (2 * ell + m_col - m_row - 2 * k)
+               * sh ** (m_row - m_col + 2 * k))
+        total += num / (f(ell + m_col - k) * f(k) * f(m_row - m_col + k) * f(ell - m_row - k))
+    return (-1.0) ** (m % 2) * math.sqrt((2 * ell + 1) / FOUR_PI) * pref * total
+
+
+def spin_seed_constants(spin: int, m: int):
+    """(j, scale, offset, exp_sin, exp_cos) of the spin seed at l = j = max(|m|, |spin|)
+    (legendre.py:233-262): scale = sign * sqrt(ratio2 / 2^shift2) * sqrt((2j+1)/4pi)
+    from the exact rational ratio2, offset = shift2 / 2."""
+    from fractions import Fraction
+
+    j = max(abs(m), abs(spin))
+    if j == 0:
+        return 0, 1.0 / math.sqrt(FOUR_PI), 0, 0, 0
+    k_lo = max(0, m - spin)
+    k_hi = min(j - spin, j + m)
+    assert k_lo == k_hi, "seed degree must sit at a corner of the d-matrix"
+    k = k_lo
+    exp_sin = spin - m + 2 * k
+    exp_cos = 2 * j - exp_sin
+    sign = -1.0 if (k + spin) % 2 else 1.0
+    f = math.factorial
+    numer = f(j - m) * f(j + m) * f(j - spin) * f(j + spin)
+    denom = f(j - spin - k) * f(k) * f(spin - m + k) * f(j + m - k)
+    ratio2 = Fraction(numer, denom * denom)
+    shift2 = ratio2.numerator.bit_length() - ratio2.denominator.bit_length()
+    if shift2 % 2:
+        shift2 -= 1
+    base = math.sqrt(float(ratio2 / Fraction(2) ** shift2))
+    scale = sign * base * math.sqrt((2 * j + 1) / FOUR_PI)
+    return j, scale, shift2 // 2, exp_sin, exp_cos
+
+
+def _rescale_small(mant, off):
+    lo = (np.abs(mant) < _TINY) & (mant != 0.0)
+    mant[lo] *= _UP
+    off[lo] -= _SHIFT
+
+
+def _rescale_pair(curr, prev, off):
+    hi = np.abs(curr) > _BIG
+    curr[hi] *= _DOWN
+    prev[hi] *= _DOWN
+    off[hi] += _SHIFT
+    lo = (np.abs(curr) < _TINY) & (np.abs(prev) < _TINY) & ((curr != 0.0) | (prev != 0.0))
+    curr[lo] *= _UP
+    prev[lo] *= _UP
+    off[lo] -= _SHIFT
+
+
+def spin_table(spin: int, m: int, thetas, L: int) -> np.ndarray:
+    """sY_lm(theta, 0) for l = max(|m|, |spin|)..L-1, shape (len(thetas), L - lo)
+    (legendre.py:276-314: exact-rational seed, rescaled three-term recurrence)."""
+    lo = max(abs(m), abs(spin))
+    if L < 1 or lo >= L:
+        raise ValueError(f"order {m}, spin {spin} invalid for band limit {L}")
+    thetas = np.atleast_1d(np.asarray(thetas, dtype=np.float64))
+    costh = np.cos(thetas)
+    out = np.empty((thetas.size, L - lo))
+    j, scale, off0, exp_sin, exp_cos = spin_seed_constants(spin, m)
+    mant = np.full(thetas.size, scale)
+    off = np.full(thetas.size, off0, dtype=np.int64)
+    ch, sh = np.cos(thetas / 2.0), np.sin(thetas / 2.0)
+    for _ in range(exp_sin):
+        mant *= sh
+        _rescale_small(mant, off)
+    for _ in range(exp_cos):
+        mant *= ch
+        _rescale_small(mant, off)
+    out[:, 0] = np.ldexp(mant, off)
+    prev = np.zeros_like(mant)
+    curr = mant
+    ms = float(m * spin)
+    for idx, ell in enumerate(range(lo, L - 1)):
+        if ell == 0:
+            nxt = math.sqrt(3.0) * costh * curr
+        else:
+            d = ell * math.sqrt(((ell + 1.0) ** 2 - m * m) * ((ell + 1.0) ** 2 - spin * spin) / (2 * ell + 3))
+            a = math.sqrt(2 * ell + 1.0) * ell * (ell + 1.0)
+            b = math.sqrt(2 * ell + 1.0) * ms
+            c = (ell + 1.0) * math.sqrt((ell * ell - m * m) * (ell * ell - spin * spin) / (2 * ell - 1.0))
+            nxt = ((a * costh - b) * curr - c * prev) / d
+        prev = curr
+        curr = nxt
+        _rescale_pair(curr, prev, off)
+        out[:, idx + 1] = np.ldexp(curr, off)
+    return out
+
+
+def spin_inverse_sht(flm: np.ndarray, thetas: np.ndarray, spin: int) -> np.ndarray:
+    """Spin-weighted synthesis (transform.py:474-496); degrees below |spin| ignored."""
+    thetas = np.asarray(thetas, dtype=np.float64)
+    L = thetas.size
+    flm = np.asarray(flm, dtype=np.complex128)
+    if abs(spin) >= L:
+        raise ValueError(f"spin {spin} invalid for band limit {L}")
+    if spin == 0:
+        return inverse_sht(flm, thetas)
+    g_plus = np.empty((L, L), dtype=np.complex128)
+    g_minus = np.empty((L, L), dtype=np.complex128)
+    for m in range(L):
+        lo = max(m, abs(spin))
+        ells = np.arange(lo, L)
+        g_plus[:, m] = TWO_PI * (spin_table(spin, m, thetas, L) @ flm[ells * ells + ells + m])
+        g_minus[:, m] = TWO_PI * (spin_table(spin, -m, thetas, L) @ flm[ells * ells + ells - m])
+    return rings_from_tones(g_plus, g_minus, L)
+
+
+def spin_forward_sht(samples: np.ndarray, thetas: np.ndarray, spin: int, check: bool = True) -> np.ndarray:
+    """Spin-weighted analysis by top-down peeling (transform.py:499-533): per order the
+    +m and -m blocks 2pi sY_l(+-m)(theta_k), k >= |m|, are solved separately (tall for
+    |m| < |spin|, least squares); degrees below |spin| come back zero."""
+    thetas = np.asarray(thetas, dtype=np.float64)
+    L = thetas.size
+    samples = np.asarray(samples, dtype=np.complex128)
+    if abs(spin) >= L:
+        raise ValueError(f"spin {spin} invalid for band limit {L}")
+    if spin == 0:
+        return forward_sht(samples, thetas, check=check)
+    coeffs = np.zeros(L * L, dtype=np.complex128)
+    buf = samples.copy()
+    roots = ring_roots_flat(L)
+    lib = _clib()
+    for m in range(L - 1, -1, -1):
+        lo = max(m, abs(spin))
+        tab_p = spin_table(spin, m, thetas, L)
+        tab_n = spin_table(spin, -m, thetas, L)
+        g_p = np.empty(L - m, dtype=np.complex128)
+        g_n = np.empty(L - m, dtype=np.complex128)
+        lib.oracle_peel_analyze(_p(buf), _p(roots), m, L, _p(g_p), _p(g_n))
+        f_p = solve_columns(TWO_PI * tab_p[m:], g_p[:, None], m, check=check)[:, 0]
+        f_n = f_p if m == 0 else solve_columns(TWO_PI * tab_n[m:], g_n[:, None], -m, check=check)[:, 0]
+        ells = np.arange(lo, L)
+        coeffs[ells * ells + ells + m] = f_p
+        if m:
+            coeffs[ells * ells + ells - m] = f_n
+            big_gp = np.ascontiguousarray(TWO_PI * (tab_p[:m] @ f_p))
+            big_gn = np.ascontiguousarray(TWO_PI * (tab_n[:m] @ f_n))
+            lib.oracle_peel_update(_p(buf), _p(roots), m, m, _p(big_gp), _p(big_gn))
+    return coeffs

@@ -41,6 +41,11 @@ from .transform import (
     inverse_sht,
     inverse_sht_batch,
     ring_analysis,
+    spin_forward_sht,
+    spin_forward_sht_batch,
+    spin_inverse_sht,
+    spin_inverse_sht_batch,
+    spin_table,
 )
 
 from . import distributed, experiments, fileio  # noqa: E402
@@ -56,7 +61,8 @@ __all__ = [
     "OrderRangeError", "Plan", "RingLongitudes", "SpatialSamples", "TransformStats", "candidates",
     "clear_plans", "equiangular_candidates", "forward_sht", "forward_sht_batch", "get_plan",
     "grid_from_permutation", "interleaved_grid", "inverse_sht", "inverse_sht_batch", "load_grid",
-    "ring_analysis", "ring_longitudes", "save_grid",
+    "ring_analysis", "ring_longitudes", "save_grid", "spin_forward_sht", "spin_forward_sht_batch",
+    "spin_inverse_sht", "spin_inverse_sht_batch", "spin_table",
 ]
 
 __version__ = "0.1.0"

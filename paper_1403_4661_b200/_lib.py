@@ -11,18 +11,18 @@ import ctypes
 import os
 from pathlib import Path
 
-from .errors import BandLimitError, DeviceError, IllConditionedSolveError
+from .errors import BandLimitError, DeviceError, IllConditionedSolveError, OrderRangeError
 
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libosph.so"
 
-OSPH_OK, OSPH_ERR_ARG, OSPH_ERR_ILLCOND, OSPH_ERR_CUDA, OSPH_ERR_NCCL = 0, 1, 2, 3, 4
+OSPH_OK, OSPH_ERR_ARG, OSPH_ERR_ILLCOND, OSPH_ERR_CUDA, OSPH_ERR_NCCL, OSPH_ERR_ORDER = 0, 1, 2, 3, 4, 5
 OSPH_HOST, OSPH_DEVICE, OSPH_ASYNC, OSPH_REAL = 0, 1, 2, 4
 SHARD_CHAIN, SHARD_FACTORS = 1, 2
 STAGE_RINGS, STAGE_FACTOR, STAGE_SWEEP = 1, 2, 4
 BUF_SPECTRA, BUF_XT, BUF_PB, BUF_AT, BUF_U, BUF_W, BUF_BETA, BUF_JSTAR, BUF_NORMS, BUF_STATUS, BUF_COUNT = range(11)
 SWEEP_KINDS = {0: "persistent", 1: "gemm", 2: "large", 3: "windowed"}
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class OsphStats(ctypes.Structure):
@@ -57,6 +57,11 @@ SIGNATURES = {
     "osph_last_sweep_kind": (_I, [_P]),
     "osph_plan_pivots": (_I, [_P, _P, _P]),
     "osph_last_stage_times": (_I, [_P, _P]),
+    "osph_spin_inverse": (_I, [_P, _I, _I, _P, _P, _I]),
+    "osph_spin_forward": (_I, [_P, _I, _I, _P, _P, _I, _I, ctypes.POINTER(OsphStats)]),
+    "osph_spin_block": (_I, [_P, _I, _I, _P, ctypes.c_int64, _I]),
+    "osph_spin_seed": (_I, [_I, _I, ctypes.POINTER(_I), ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I),
+                            ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "osph_last_error": (ctypes.c_char_p, []),
     "osph_abi_version": (_I, []),
 }
@@ -101,6 +106,8 @@ def raise_for(rc: int, stats: OsphStats | None = None) -> None:
         raise IllConditionedSolveError(order, kappa)
     if rc == OSPH_ERR_ARG:
         raise BandLimitError(msg) if "band" in msg or "batch" in msg else ValueError(msg)
+    if rc == OSPH_ERR_ORDER:
+        raise OrderRangeError(msg)
     if rc == OSPH_ERR_NCCL:
         raise DeviceError(f"libosph multi-GPU exchange failed: {msg}")
     raise DeviceError(f"libosph error {rc}: {msg}")

@@ -77,6 +77,7 @@ void plan_free(osph_plan* p) {
     cudaFree(p->d_inv_bluestein);
   }
   free_windows(p);
+  spin_free(p);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   delete p;
 }
@@ -168,6 +169,7 @@ int plan_create_one(int L, const double* thetas, int max_batch, int device, osph
   PLAN_TRY(cudaEventCreateWithFlags(&p->ev_sweep_done, cudaEventDisableTiming));
   cudaStream_t st = p->stream;
 
+  p->h_thetas.assign(thetas, thetas + L);
   std::vector<double> c(L), s(L);
   for (int k = 0; k < L; ++k) {
     c[k] = std::cos(thetas[k]);
@@ -295,11 +297,18 @@ int ensure_forward(osph_plan* p) {
   CUDA_TRY(dalloc(&p->d_w, nuw));
   CUDA_TRY(cudaMemsetAsync(p->d_u, 0, sizeof(double) * nuw, st));
   CUDA_TRY(cudaMemsetAsync(p->d_w, 0, sizeof(double) * nuw, st));
-  // teams of up to 4 maps: the last team's padding maps stay zero
-  CUDA_TRY(dalloc(&p->d_r, (size_t)L * (L + 1) * (B + 3)));
-  CUDA_TRY(cudaMemsetAsync(p->d_r, 0, sizeof(double2) * (size_t)L * (L + 1) * (B + 3), st));
+  if ((rc = ensure_spectra(p))) return rc;
   CUDA_TRY(cudaStreamSynchronize(st));
   p->fwd_ready = true;
+  return OSPH_OK;
+}
+
+// The ring spectra R (teams of up to 4 maps: the last team's padding maps stay zero).
+int ensure_spectra(osph_plan* p) {
+  if (p->d_r) return OSPH_OK;
+  const size_t n = (size_t)p->L * (p->L + 1) * (p->max_batch + 3);
+  CUDA_TRY(dalloc(&p->d_r, n));
+  CUDA_TRY(cudaMemsetAsync(p->d_r, 0, sizeof(double2) * n, p->stream));
   return OSPH_OK;
 }
 

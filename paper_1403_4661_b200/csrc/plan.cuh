@@ -35,6 +35,20 @@ struct FwdWindow {  // orders m_lo..m_hi, factored then swept together
   cudaEvent_t ev[4] = {};     // factor start/end, sweep start/end
 };
 
+struct SpinState {  // spin-weighted transforms of one spin s != 0 (spin.cu); u = signed order + L - 1
+  int s = 0;
+  int* d_ls = nullptr;          // [2L-1][L] first degree whose value is in the double range (L: none)
+  double2* d_pstart = nullptr;  // [2L-1][L] {sY_(ls-1), sY_ls} (true values)
+  double4* d_rec = nullptr;     // [2L-1][L] {alpha, beta, gamma, 0}: sY_(l+1) = (alpha x - beta) sY_l - gamma sY_(l-1)
+  double* d_x = nullptr;        // X_u = least-squares solution operator, row-major (L - lo) x (L - m)
+  std::vector<int64_t> h_x_off;  // [2L] offsets into d_x
+  int64_t* d_x_off = nullptr;
+  double* d_kappa = nullptr;     // [2L-1] ||A_u||_1 ||X_u||_1 (infinity: singular / non-finite)
+  std::vector<double> h_kappa;
+  bool factored = false;
+  double factor_seconds = 0.0;   // device time of the last factorisation (0 once cached)
+};
+
 struct osph_plan {
   int L = 0;
   int device = 0;
@@ -133,6 +147,9 @@ struct osph_plan {
   bool windowed = false;
   std::vector<FwdWindow> windows;  // descending in m
   float last_factor_ms = 0.f, last_sweep_ms = 0.f;
+  // spin-weighted transforms (spin.cu): the two most recently used spins
+  std::vector<SpinState*> spins;
+  double2* d_spin_xbuf = nullptr;  // [B][+-][L] solved coefficients of the current order
 
   // ---- per-call workspaces (sized for max_batch) ----
   double* d_fpack = nullptr;  // inverse: packed coefficients [pos(m,l)][4B]
@@ -203,8 +220,9 @@ int group_forward(osph_plan* p, int B, const void* samples, void* flm, int kind,
 cudaError_t launch_tables(osph_plan* p);
 cudaError_t launch_legendre_block(osph_plan* p, int m, double* out, int64_t ld);  // tables.cu
 cudaError_t launch_ring_inverse(osph_plan* p, int B, double2* samples);    // ringdft.cu
-// maps [bofs, bofs + nb) of a batch of B (nb < 0: all B)
-cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples, int bofs = 0, int nb = -1);  // ringdft.cu
+// maps [bofs, bofs + nb) of a batch of B (nb < 0: all B); plain: R in the [map][pos][+-] layout
+cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples, int bofs = 0, int nb = -1,
+                                bool plain = false);  // ringdft.cu
 cudaError_t launch_pack(osph_plan* p, int B, const double2* flm);          // synth.cu
 cudaError_t launch_synth(osph_plan* p, int B);                             // synth.cu
 cudaError_t launch_factor(osph_plan* p, cudaStream_t st = nullptr);  // factor.cu: every order, breadth-first
@@ -223,6 +241,8 @@ cudaError_t launch_sweep_large_range(osph_plan* p, int B, double2* flm, int s_hi
                                      const int64_t* pb_off);  // sweep_large.cu
 int discover_pivots(osph_plan* p);  // pivots.cu: the grid's pivot order (once per grid), host-blocking
 int alloc_factor_storage(osph_plan* p);                        // window.cu
+void spin_free(osph_plan* p);                                  // spin.cu
+int ensure_spectra(osph_plan* p);                              // plan.cu: the ring spectra buffer d_r
 void free_windows(osph_plan* p);                               // window.cu
 cudaError_t forward_windows(osph_plan* p, int B, double2* flm);  // window.cu: factor + sweep per window
 // window.cu, staged: factor window 0 only / sweep every window (factoring windows >= 1 before their sweep)

@@ -472,10 +472,10 @@ cudaError_t launch_ring_inverse(osph_plan* p, int B, double2* samples) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples, int bofs, int nb) {
+cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples, int bofs, int nb, bool plain) {
   const int L = p->L;
   if (nb < 0) nb = B;
-  int lgG = __builtin_ctz(sweep_maps_per_team(p, B));  // team-major R (common.cuh)
+  int lgG = plain ? 0 : __builtin_ctz(sweep_maps_per_team(p, B));  // team-major R (common.cuh)
   if (p->n_big_rings > 0) {
     int Li = L, Bi = B, mpb = 0, b0 = bofs, b1 = bofs + nb;
     const int* rings = p->d_bluestein_rings;

@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .errors import AliasingError, BandLimitError
+from .errors import AliasingError, BandLimitError, OrderRangeError
 
 TWO_PI = 2.0 * np.pi
 
@@ -201,6 +201,22 @@ class Plan:
     def inverse_raw(self, B: int, src: int, dst: int, kind: int) -> None:
         _lib.raise_for(self._lib.osph_inverse(self._h, B, ctypes.c_void_p(src), ctypes.c_void_p(dst), kind))
 
+    def spin_inverse_raw(self, spin: int, B: int, src: int, dst: int, kind: int) -> None:
+        _lib.raise_for(self._lib.osph_spin_inverse(self._h, int(spin), B, ctypes.c_void_p(src), ctypes.c_void_p(dst),
+                                                   kind))
+
+    def spin_forward_raw(self, spin: int, B: int, src: int, dst: int, kind: int, check: bool) -> _lib.OsphStats:
+        st = _lib.OsphStats()
+        rc = self._lib.osph_spin_forward(self._h, int(spin), B, ctypes.c_void_p(src), ctypes.c_void_p(dst), kind,
+                                         1 if check else 0, ctypes.byref(st))
+        _lib.raise_for(rc, st)
+        return st
+
+    def spin_block(self, spin: int, m: int, out_ptr: int, ld: int) -> None:
+        """osph_spin_block into a device buffer (degree-major, leading dimension ld >= L)."""
+        _lib.raise_for(self._lib.osph_spin_block(self._h, int(spin), int(m), ctypes.c_void_p(out_ptr), int(ld),
+                                                 _lib.OSPH_DEVICE))
+
     def forward_raw(self, B: int, src: int, dst: int, kind: int, check: bool) -> _lib.OsphStats:
         st = _lib.OsphStats()
         rc = self._lib.osph_forward(self._h, B, ctypes.c_void_p(src), ctypes.c_void_p(dst), kind,
@@ -271,9 +287,23 @@ def _check_out(out, shape, device=None):
         raise ValueError(f"out must be a writeable C-contiguous complex128 array of shape {tuple(shape)}")
 
 
-def _run(direction: str, data, grid, out=None, check: bool = True, device: int = 0, real: bool = False):
-    """Shared driver: numpy (host) or CUDA torch tensor (device) batches of shape (B, L^2)."""
+def _run(direction: str, data, grid, out=None, check: bool = True, device: int = 0, real: bool = False,
+         spin: int | None = None):
+    """Shared driver: numpy (host) or CUDA torch tensor (device) batches of shape (B, L^2).
+    ``spin`` not None: the spin-weighted transforms (osph_spin_*)."""
     L = grid.band_limit if hasattr(grid, "band_limit") else len(grid)
+
+    def call(plan, B, src, dst, kind):
+        if spin is not None:
+            if direction == "inverse":
+                plan.spin_inverse_raw(spin, B, src, dst, kind)
+                return None
+            return plan.spin_forward_raw(spin, B, src, dst, kind, check)
+        if direction == "inverse":
+            plan.inverse_raw(B, src, dst, kind)
+            return None
+        return plan.forward_raw(B, src, dst, kind, check)
+
     if _is_torch_cuda(data):
         import torch
 
@@ -291,11 +321,7 @@ def _run(direction: str, data, grid, out=None, check: bool = True, device: int =
         kind = _lib.OSPH_DEVICE | (_lib.OSPH_REAL if real else 0)
         with plan.lock:
             plan.set_stream(torch_stream_handle(torch.cuda.current_stream(x.device)))
-            if direction == "inverse":
-                plan.inverse_raw(B, x.data_ptr(), y.data_ptr(), kind)
-                return y, None
-            st = plan.forward_raw(B, x.data_ptr(), y.data_ptr(), kind, check)
-            return y, st
+            return y, call(plan, B, x.data_ptr(), y.data_ptr(), kind)
     x = np.ascontiguousarray(np.asarray(data, dtype=np.complex128))
     if x.ndim == 1:
         x = x.reshape(1, -1)
@@ -308,11 +334,7 @@ def _run(direction: str, data, grid, out=None, check: bool = True, device: int =
     kind = _lib.OSPH_HOST | (_lib.OSPH_REAL if real else 0)
     with plan.lock:
         plan.set_stream(None)
-        if direction == "inverse":
-            plan.inverse_raw(B, x.ctypes.data, y.ctypes.data, kind)
-            return y, None
-        st = plan.forward_raw(B, x.ctypes.data, y.ctypes.data, kind, check)
-        return y, st
+        return y, call(plan, B, x.ctypes.data, y.ctypes.data, kind)
 
 
 def inverse_sht_batch(flm, grid, out=None, device: int = 0, *, real: bool = False):
@@ -368,6 +390,87 @@ def forward_sht(samples: SpatialSamples, grid, *, method: str = "direct", check:
     flat = samples.flatten().reshape(1, -1)
     values = forward_sht_batch(flat, grid, check=check, stats=stats)[0]
     return HarmonicCoefficients(L, values)
+
+
+# ---------------------------------------------------------------------------
+# spin-weighted transforms (transform.py:474-533, legendre.py:276-306)
+
+
+def _check_spin(spin: int, L: int) -> int:
+    spin = int(spin)
+    if abs(spin) >= L:
+        raise OrderRangeError(f"spin {spin} invalid for band limit {L}")
+    return spin
+
+
+def spin_inverse_sht_batch(flm, grid, spin: int, out=None, device: int = 0):
+    """B maps of spin-weight ``spin``: flm (B, L^2) -> samples (B, L^2) (numpy or CUDA torch).
+    Degrees below |spin| are ignored; spin 0 is inverse_sht_batch."""
+    spin = _check_spin(spin, grid.band_limit)
+    return _run("inverse", flm, grid, out=out, device=device, spin=spin)[0]
+
+
+def spin_forward_sht_batch(samples, grid, spin: int, *, check: bool = True, stats: TransformStats | None = None,
+                           out=None, device: int = 0):
+    """B maps of spin-weight ``spin``: samples (B, L^2) -> coefficients (B, L^2);
+    degrees below |spin| come back as exact zeros.  The per-order solution
+    operators are built on the first call for a spin (stats.extra["factor_seconds"])."""
+    spin = _check_spin(spin, grid.band_limit)
+    y, st = _run("forward", samples, grid, out=out, check=check, device=device, spin=spin)
+    if stats is not None and st is not None:
+        stats.solve_seconds = st.solve_seconds
+        stats.orders = st.orders
+        stats.extra.update(factor_seconds=st.factor_seconds, sweep_seconds=st.sweep_seconds,
+                           total_seconds=st.total_seconds)
+    return y
+
+
+def spin_inverse_sht(coeffs: HarmonicCoefficients, grid, spin: int) -> SpatialSamples:
+    """Spin-weighted synthesis (transform.py:474-496).  Spin zero takes the scalar
+    path bit for bit; coefficients with degree below |spin| are ignored."""
+    L = grid.band_limit
+    _check_band_limits(coeffs.band_limit, L)
+    spin = _check_spin(spin, L)
+    if spin == 0:
+        return inverse_sht(coeffs, grid)
+    flat = spin_inverse_sht_batch(np.asarray(coeffs.values, dtype=np.complex128).reshape(1, -1), grid, spin)[0]
+    return SpatialSamples.from_flat(L, flat)
+
+
+def spin_forward_sht(samples: SpatialSamples, grid, spin: int, *, check: bool = True) -> HarmonicCoefficients:
+    """Spin-weighted analysis by the same top-down peeling (transform.py:499-533);
+    tall least-squares blocks for |m| < |spin|; degrees below |spin| come back zero."""
+    L = grid.band_limit
+    _check_band_limits(samples.band_limit, L)
+    spin = _check_spin(spin, L)
+    if spin == 0:
+        return forward_sht(samples, grid, check=check)
+    values = spin_forward_sht_batch(samples.flatten().reshape(1, -1), grid, spin, check=check)[0]
+    return HarmonicCoefficients(L, values)
+
+
+def spin_table(spin: int, m: int, thetas, band_limit: int, device: int = 0) -> np.ndarray:
+    """sY_lm(theta, 0) for l = max(|m|, |spin|)..L-1 at each theta in (0, pi]
+    (legendre.py:276-306), shape (len(thetas), L - lo), computed on the GPU
+    (osph_spin_block) in chunks of L co-latitudes."""
+    import torch
+
+    L = int(band_limit)
+    lo = max(abs(int(m)), abs(int(spin)))
+    if L < 1 or lo >= L:
+        raise OrderRangeError(f"order {m}, spin {spin} invalid for band limit {L}")
+    th = np.atleast_1d(np.asarray(thetas, dtype=np.float64))
+    out = np.empty((th.size, L - lo))
+    buf = torch.empty((L - lo, L), dtype=torch.float64, device=f"cuda:{device}")
+    for c0 in range(0, th.size, L):
+        chunk = th[c0:c0 + L]
+        padded = np.concatenate([chunk, np.full(L - chunk.size, np.pi / 2)])
+        plan = get_plan(padded, 1, device)
+        with plan.lock:
+            plan.set_stream(None)
+            plan.spin_block(spin, m, buf.data_ptr(), L)
+        out[c0:c0 + chunk.size] = buf.cpu().numpy().T[: chunk.size]
+    return out
 
 
 def ring_analysis(ring_values, m: int):
