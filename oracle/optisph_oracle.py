@@ -299,13 +299,14 @@ def condition_number(entries: np.ndarray) -> float:
     return float(sv[0] / sv[-1])
 
 
-def solve_columns(entries, rhs, order, *, rcond=SOLVE_RCOND, check=True):
-    """Real-split gelsy solve with rank check (blocks.py:88-116)."""
+def solve_columns(entries, rhs, order, *, rcond=SOLVE_RCOND, check=True, driver="gelsy"):
+    """Real-split gelsy solve with rank check (blocks.py:88-116).  ``driver`` other
+    than gelsy is for tests only (the spread between two least-squares solvers)."""
     rhs = np.atleast_2d(rhs.T).T
     stacked = np.empty((entries.shape[0], 2 * rhs.shape[1]))
     stacked[:, 0::2] = rhs.real
     stacked[:, 1::2] = rhs.imag
-    x, _, rank, _ = linalg.lstsq(entries, stacked, cond=rcond if check else None, lapack_driver="gelsy")
+    x, _, rank, _ = linalg.lstsq(entries, stacked, cond=rcond if check else None, lapack_driver=driver)
     if check and rank < entries.shape[1]:
         raise OracleIllConditioned(order, condition_number(entries))
     return x[:, 0::2] + 1j * x[:, 1::2]
@@ -568,7 +569,8 @@ def spin_inverse_sht(flm: np.ndarray, thetas: np.ndarray, spin: int) -> np.ndarr
     return rings_from_tones(g_plus, g_minus, L)
 
 
-def spin_forward_sht(samples: np.ndarray, thetas: np.ndarray, spin: int, check: bool = True) -> np.ndarray:
+def spin_forward_sht(samples: np.ndarray, thetas: np.ndarray, spin: int, check: bool = True,
+                     driver: str = "gelsy") -> np.ndarray:
     """Spin-weighted analysis by top-down peeling (transform.py:499-533): per order the
     +m and -m blocks 2pi sY_l(+-m)(theta_k), k >= |m|, are solved separately (tall for
     |m| < |spin|, least squares); degrees below |spin| come back zero."""
@@ -590,8 +592,9 @@ def spin_forward_sht(samples: np.ndarray, thetas: np.ndarray, spin: int, check: 
         g_p = np.empty(L - m, dtype=np.complex128)
         g_n = np.empty(L - m, dtype=np.complex128)
         lib.oracle_peel_analyze(_p(buf), _p(roots), m, L, _p(g_p), _p(g_n))
-        f_p = solve_columns(TWO_PI * tab_p[m:], g_p[:, None], m, check=check)[:, 0]
-        f_n = f_p if m == 0 else solve_columns(TWO_PI * tab_n[m:], g_n[:, None], -m, check=check)[:, 0]
+        f_p = solve_columns(TWO_PI * tab_p[m:], g_p[:, None], m, check=check, driver=driver)[:, 0]
+        f_n = f_p if m == 0 else solve_columns(TWO_PI * tab_n[m:], g_n[:, None], -m, check=check,
+                                               driver=driver)[:, 0]
         ells = np.arange(lo, L)
         coeffs[ells * ells + ells + m] = f_p
         if m:

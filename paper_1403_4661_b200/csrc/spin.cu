@@ -174,7 +174,10 @@ __device__ __forceinline__ double spin_step(const double4 r, double x, double p0
 // Start table: per (u, ring k) the reference's seed (scale * 2^offset times
 // sin(theta/2)^exp_sin cos(theta/2)^exp_cos, rescaled as legendre.py:265-270)
 // and the rescaled recurrence (legendre.py:221-231) up to the first degree
-// whose value is in the double range (offset 0); lower degrees are < 2^-500.
+// whose TRUE value ldexp(mantissa, offset) reaches 2^-500; lower degrees are
+// smaller and taken as zero.  Unlike the scalar seed, the offset may start
+// positive (the exact-rational scale carries 2^(shift2/2)), so the test is on
+// the value, not on offset == 0.
 __global__ void k_spin_start(int L, int s, const double* __restrict__ seed_scale, const int4* __restrict__ seed_int,
                              const double* __restrict__ costh, const double* __restrict__ ch,
                              const double* __restrict__ sh, const double4* __restrict__ rec, int* __restrict__ ls_tab,
@@ -204,7 +207,9 @@ __global__ void k_spin_start(int L, int s, const double* __restrict__ seed_scale
   int l = si.x;
   const double x = costh[k];
   const double4* rr = rec + (int64_t)u * L;
-  while (off != 0 && l < L - 1) {
+  // off > -1000 with |mant| <= 2^500 bounds the true value; ldexp is exact above 2^-1022
+  auto in_range = [&](double v) { return off > -2000 && fabs(ldexp(v, off)) >= OSPH_TINY; };
+  while (!in_range(curr) && l < L - 1) {
     const double nxt = spin_step(rr[l], x, prev, curr);
     prev = curr;
     curr = nxt;
@@ -220,8 +225,9 @@ __global__ void k_spin_start(int L, int s, const double* __restrict__ seed_scale
     ++l;
   }
   const int64_t t = (int64_t)u * L + k;
-  ls_tab[t] = off == 0 ? l : L;
-  pstart[t] = off == 0 ? make_double2(prev, curr) : make_double2(0.0, 0.0);
+  const bool ok = in_range(curr);
+  ls_tab[t] = ok ? l : L;
+  pstart[t] = ok ? make_double2(ldexp(prev, off), ldexp(curr, off)) : make_double2(0.0, 0.0);
 }
 
 // spin_table(s, mu, thetas, L) for all rings: out[(l - lo) * ld + k].

@@ -99,30 +99,41 @@ def test_spin_forward_matches_reference_per_order(ref, L, s):
 
     samples = ref[f"L{L}_s{s}_samples"]
     got = osp.spin_forward_sht_batch(samples[None], _grid(L), s)[0]
-    _per_order_ok(got, ref[f"L{L}_s{s}_fwd"], ref[f"L{L}_s{s}_flm"], L)
-    ell, _ = _orders(L)
+    want, flm = ref[f"L{L}_s{s}_fwd"], ref[f"L{L}_s{s}_flm"]
+    _per_order_ok(got, want, flm, L)
+    ell, m = _orders(L)
+    for am in range(L):  # per order no less accurate than the reference
+        sel = np.abs(m) == am
+        assert np.abs(got[sel] - flm[sel]).max() <= 10 * np.abs(want[sel] - flm[sel]).max() + 1e-11, am
     assert np.all(got[ell < abs(s)] == 0)  # degrees below |spin| come back exactly zero
 
 
 @pytest.mark.parametrize("s", [1, 2, -3])
 def test_spin_forward_least_squares_on_noise(ref, s):
     """Inconsistent samples: the tall blocks' least-squares solutions (gelsy in the
-    reference).  Per-order bar scaled by the reference's consistent-data
-    round-trip error at the same spin (the chain's amplification)."""
+    reference, Householder QR here).  Two error sources set the bar per order,
+    each taken at 10x: the spread between two LAPACK least-squares solvers
+    (gelsy vs gelsd) run through the same oracle sweep, and the sweep's own
+    amplification -- the oracle's round-trip error on consistent data of unit
+    size at this spin, relative to the order's coefficient magnitude."""
     import paper_1403_4661_b200 as osp
 
     L = 16
-    got = osp.spin_forward_sht_batch(ref[f"L16_s{s}_noise"][None], _grid(L), s)[0]
+    th = _grid(L).thetas
+    noise = ref[f"L16_s{s}_noise"]
+    got = osp.spin_forward_sht_batch(noise[None], _grid(L), s)[0]
     want = ref[f"L16_s{s}_noise_fwd"]
+    other = O.spin_forward_sht(noise, th, s, driver="gelsd")
     ell, m = _orders(L)
     rng = np.random.default_rng(9)
     flm = rng.standard_normal(L * L) + 1j * rng.standard_normal(L * L)
     flm[ell < abs(s)] = 0
-    th = _grid(L).thetas
     rt = O.spin_forward_sht(O.spin_inverse_sht(flm, th, s), th, s) - flm
     for am in range(L):
         sel = np.abs(m) == am
-        tol = max(1e-11, 100.0 * np.abs(rt[sel]).max()) * max(1.0, np.abs(want[sel]).max())
+        scale = max(1.0, np.abs(want[sel]).max())
+        spread = np.abs(other[sel] - want[sel]).max()
+        tol = max(1e-11 * scale, 10.0 * spread, 10.0 * np.abs(rt[sel]).max() * scale)
         assert np.abs(got[sel] - want[sel]).max() <= tol, am
 
 
@@ -226,7 +237,9 @@ def test_spin_L256_against_oracle(s):
     assert np.abs(got_inv - samples).max() <= 1e-12 * np.abs(samples).max()
     want = O.spin_forward_sht(samples, grid.thetas, s)
     got = osp.spin_forward_sht_batch(samples[None], grid, s)[0]
-    # high orders are well inside the reference's accuracy: a tight absolute bar there
-    hi = np.abs(m) >= L // 2
-    assert np.abs(got[hi] - want[hi]).max() <= 1e-11
     _per_order_ok(got, want, flm, L)
+    # and per order no less accurate than the reference (its round trip grows as m
+    # falls: 1e-11 at m = L/2 for s = 1, 1e22 for s = -2 on this grid)
+    for am in range(L):
+        sel = np.abs(m) == am
+        assert np.abs(got[sel] - flm[sel]).max() <= 10 * np.abs(want[sel] - flm[sel]).max() + 1e-11, am
