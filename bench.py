@@ -96,10 +96,10 @@ def flops(L: int, B: int) -> dict:
 # workload, summarised under profiles/ by tools/ncu_summary.py), bytes per launch
 
 NCU_PROFILES = {  # (stage, L, B) -> summary file (a multi-kernel stage sums its kernels of one call)
-    ("sweep", 256, 64): "sweep_r01d_full.txt",
-    ("factor", 256, 64): "launches_r01d_summary.txt",
+    ("sweep", 256, 64): "sweep_r02_full.txt",
+    ("factor", 256, 64): "launches_r02_c2_summary.txt",
     ("sweep", 512, 256): "sweepgemm_r01e_launches.txt",
-    ("factor", 2048, 1): "launches_bf2048_r01e_summary.txt",
+    ("factor", 2048, 1): "launches_r02_c4_summary.txt",
 }
 
 
