@@ -43,6 +43,9 @@ struct SpinState {  // spin-weighted transforms of one spin s != 0 (spin.cu); u 
   double* d_x = nullptr;        // X_u = least-squares solution operator, row-major (L - lo) x (L - m)
   std::vector<int64_t> h_x_off;  // [2L] offsets into d_x
   int64_t* d_x_off = nullptr;
+  double* d_pb = nullptr;        // Pb_u = 2pi sY_l(u)(theta_k), rings k < m, row-major m x (L - lo)
+  std::vector<int64_t> h_pb_off;  // [2L]
+  int64_t* d_pb_off = nullptr;
   double* d_kappa = nullptr;     // [2L-1] ||A_u||_1 ||X_u||_1 (infinity: singular / non-finite)
   std::vector<double> h_kappa;
   bool factored = false;

@@ -10,7 +10,8 @@
 //            DFTs (fold + Bluestein, ringdft.cu);
 //   forward  ring forward DFTs (plain spectra layout), then for m = L-1 .. 0:
 //            x_(+-m) = X_(+-m) g_(+-m) (k_spin_solve) and the corrections of
-//            the aliased bins of rings k < m (k_spin_corr) -- the peeling of
+//            the aliased bins of rings k < m, Pb_(+-m) x_(+-m) (k_spin_corr,
+//            Pb = the block's rows k < m, stored) -- the peeling of
 //            transform.py:513-533.
 // X_u is the least-squares solution operator of the block
 // A_u = 2pi sY_l(u)(theta_k), k = m..L-1, l = lo..L-1 -- square for m >= |s|,
@@ -282,6 +283,34 @@ __global__ void k_spin_gen(int L, int s, const int64_t* __restrict__ x_off, cons
   }
 }
 
+// The below-blocks Pb_u = 2pi sY_l(u)(theta_k), rings k < m (the corrections'
+// operand), row-major m x (L - lo): one thread per (u, ring).
+__global__ void k_spin_gen_below(int L, int s, const int64_t* __restrict__ pb_off, const double* __restrict__ costh,
+                                 const double4* __restrict__ rec, const int* __restrict__ ls_tab,
+                                 const double2* __restrict__ pstart, double* __restrict__ Pb) {
+  const int u = blockIdx.y;
+  const int mu = u - (L - 1), m = abs(mu), lo = max(m, abs(s));
+  const int nc = L - lo;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  double* row = Pb + pb_off[u] + (int64_t)k * nc;
+  const int64_t t = (int64_t)u * L + k;
+  const int ls = ls_tab[t];
+  for (int l = lo; l < min(ls, L); ++l) row[l - lo] = 0.0;
+  if (ls >= L) return;
+  double p0 = pstart[t].x, p1 = pstart[t].y;
+  const double x = costh[k];
+  const double4* rr = rec + (int64_t)u * L;
+  for (int l = ls; l < L; ++l) {
+    row[l - lo] = OSPH_TWO_PI * p1;
+    if (l + 1 < L) {
+      const double nxt = spin_step(rr[l], x, p0, p1);
+      p0 = p1;
+      p1 = nxt;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // per-order least-squares operators: Householder QR, one CTA per signed order
 
@@ -471,60 +500,61 @@ __global__ void __launch_bounds__(256) k_spin_solve(int L, int s, int m, int B, 
 }
 
 // Corrections of order m on the rings k < m (transform.py:527-532 through the
-// spectra): G_(+-m)(theta_k) = 2pi sum_l sY_l(+-m)(theta_k) x_l(+-m), subtracted
-// from the bins the tones e^(+-i m phi) alias to on ring k.  One thread per
-// (ring, map) writes both tones: single writer per bin (deterministic).
-__global__ void __launch_bounds__(128) k_spin_corr(int L, int s, int m, int B, const double* __restrict__ costh,
-                                                   const double4* __restrict__ rec, const int* __restrict__ ls_tab,
-                                                   const double2* __restrict__ pstart,
+// spectra): G_(+-m)(theta_k) = Pb_(+-m)[k, :] x_(+-m), subtracted from the bins
+// the tones e^(+-i m phi) alias to on ring k.  One warp per ring (lanes over
+// the degrees: coalesced Pb rows) and chunk of 4 maps; lane 0 writes both
+// tones of a map: single writer per bin (deterministic).
+#define CORR_MB 4
+__global__ void __launch_bounds__(256) k_spin_corr(int L, int s, int m, int B, const double* __restrict__ Pb,
+                                                   const int64_t* __restrict__ pb_off,
                                                    const double2* __restrict__ xbuf, double2* __restrict__ R) {
   pdl_start();
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  const int b = blockIdx.y;
-  if (k >= m || b >= B) return;
-  const int lo = max(m, abs(s));
-  const double x = costh[k];
-  double2 v[2];
+  const int k = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (k >= m) return;
+  const int lo = max(m, abs(s)), nc = L - lo;
+  const double* rp = Pb + pb_off[m + L - 1] + (int64_t)k * nc;
+  const double* rn = Pb + pb_off[-m + L - 1] + (int64_t)k * nc;
+  const int64_t npos = (int64_t)L * (L + 1) / 2;
+  const int nk = 2 * k + 1, rr = m % nk;
+  const int tm = rr == 0 ? 0 : (rr <= k ? rr : nk - rr);
+  const int slot_p = rr <= k ? 0 : 1;  // +m -> bin rr: (rr, +) if rr <= k else (nk - rr, -); -m the other slot
+  {
+    const int b0 = blockIdx.y * CORR_MB;
+    double a[CORR_MB][4];
 #pragma unroll
-  for (int sg = 0; sg < 2; ++sg) {
-    const int u = (sg ? -m : m) + L - 1;
-    const int64_t t = (int64_t)u * L + k;
-    const int ls = ls_tab[t];
-    double vr = 0.0, vi = 0.0;
-    if (ls < L) {
-      double p0 = pstart[t].x, p1 = pstart[t].y;
-      const double4* rr = rec + (int64_t)u * L;
-      const double2* xb = xbuf + ((int64_t)b * 2 + sg) * L - lo;
-      for (int l = ls; l < L; ++l) {
-        const double2 xv = xb[l];
-        vr = fma(p1, xv.x, vr);
-        vi = fma(p1, xv.y, vi);
-        if (l + 1 < L) {
-          const double nxt = spin_step(rr[l], x, p0, p1);
-          p0 = p1;
-          p1 = nxt;
+    for (int q = 0; q < CORR_MB; ++q) a[q][0] = a[q][1] = a[q][2] = a[q][3] = 0.0;
+    for (int l = lane; l < nc; l += 32) {
+      const double pp = __ldg(rp + l), pn = __ldg(rn + l);
+#pragma unroll
+      for (int q = 0; q < CORR_MB; ++q) {
+        if (b0 + q < B) {
+          const double2 xp = xbuf[((int64_t)(b0 + q) * 2 + 0) * L + l];
+          const double2 xn = xbuf[((int64_t)(b0 + q) * 2 + 1) * L + l];
+          a[q][0] = fma(pp, xp.x, a[q][0]);
+          a[q][1] = fma(pp, xp.y, a[q][1]);
+          a[q][2] = fma(pn, xn.x, a[q][2]);
+          a[q][3] = fma(pn, xn.y, a[q][3]);
         }
       }
     }
-    v[sg] = make_double2(OSPH_TWO_PI * vr, OSPH_TWO_PI * vi);
+#pragma unroll
+    for (int q = 0; q < CORR_MB; ++q) {
+      const double vpr = sp_warp_sum(a[q][0]), vpi = sp_warp_sum(a[q][1]);
+      const double vnr = sp_warp_sum(a[q][2]), vni = sp_warp_sum(a[q][3]);
+      if (lane == 0 && b0 + q < B) {
+        double2* e = R + ((int64_t)(b0 + q) * npos + packed_pos(L, tm, k - tm)) * 2;
+        if (rr == 0) {  // both tones land in bin 0 (stored at (0, k), + slot)
+          e->x -= vpr + vnr;
+          e->y -= vpi + vni;
+        } else {
+          e[slot_p].x -= vpr;
+          e[slot_p].y -= vpi;
+          e[1 - slot_p].x -= vnr;
+          e[1 - slot_p].y -= vni;
+        }
+      }
+    }
   }
-  const int64_t npos = (int64_t)L * (L + 1) / 2;
-  const int nk = 2 * k + 1, rr = m % nk;
-  double2* base = R + (int64_t)b * npos * 2;
-  if (rr == 0) {  // both tones land in bin 0 (stored at (0, k), + slot)
-    double2* e = base + packed_pos(L, 0, k) * 2;
-    e->x -= v[0].x + v[1].x;
-    e->y -= v[0].y + v[1].y;
-    return;
-  }
-  // +m -> bin rr, -m -> bin nk - rr; bin t <= k is (t, +), bin t > k is (nk - t, -)
-  const int tm = rr <= k ? rr : nk - rr;
-  const int slot_p = rr <= k ? 0 : 1;
-  double2* e = base + packed_pos(L, tm, k - tm) * 2;
-  e[slot_p].x -= v[0].x;
-  e[slot_p].y -= v[0].y;
-  e[1 - slot_p].x -= v[1].x;
-  e[1 - slot_p].y -= v[1].y;
 }
 
 // G_(+-m)(theta_k) = sum_l sY_l(+-m)(theta_k) f_l(+-m) in the ring kernels' layout
@@ -581,7 +611,7 @@ __global__ void __launch_bounds__(128) k_spin_synth(int L, int s, int B, const d
 
 static void spin_state_free(SpinState* st) {
   if (!st) return;
-  void* ptrs[] = {st->d_ls, st->d_pstart, st->d_rec, st->d_x, st->d_x_off, st->d_kappa};
+  void* ptrs[] = {st->d_ls, st->d_pstart, st->d_rec, st->d_x, st->d_x_off, st->d_pb, st->d_pb_off, st->d_kappa};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete st;
@@ -693,8 +723,17 @@ static int spin_factor(osph_plan* p, SpinState* st) {
     const int m = std::abs(u - (L - 1)), lo = std::max(m, as);
     st->h_x_off[u + 1] = st->h_x_off[u] + (int64_t)(L - lo) * (L - m);
   }
+  st->h_pb_off.assign(U + 1, 0);
+  for (int u = 0; u < U; ++u) {
+    const int m = std::abs(u - (L - 1)), lo = std::max(m, as);
+    st->h_pb_off[u + 1] = st->h_pb_off[u] + (int64_t)m * (L - lo);
+  }
   SP_TRY(cudaMalloc(&st->d_x, sizeof(double) * std::max<int64_t>(1, st->h_x_off[U])));
   SP_TRY(cudaMalloc(&st->d_x_off, sizeof(int64_t) * (U + 1)));
+  SP_TRY(cudaMalloc(&st->d_pb, sizeof(double) * std::max<int64_t>(1, st->h_pb_off[U])));
+  SP_TRY(cudaMalloc(&st->d_pb_off, sizeof(int64_t) * (U + 1)));
+  SP_TRY(cudaMemcpyAsync(st->d_pb_off, st->h_pb_off.data(), sizeof(int64_t) * (U + 1), cudaMemcpyHostToDevice,
+                         strm));
   SP_TRY(cudaMalloc(&st->d_kappa, sizeof(double) * U));
   SP_TRY(cudaMemcpyAsync(st->d_x_off, st->h_x_off.data(), sizeof(int64_t) * (U + 1), cudaMemcpyHostToDevice, strm));
   cudaEvent_t e0, e1;
@@ -703,6 +742,8 @@ static int spin_factor(osph_plan* p, SpinState* st) {
   SP_TRY(cudaEventRecord(e0, strm));
   k_spin_gen<<<dim3((L + 127) / 128, U), 128, 0, strm>>>(L, s, st->d_x_off, p->d_cos, st->d_rec, st->d_ls,
                                                          st->d_pstart, st->d_x);
+  k_spin_gen_below<<<dim3((L + 127) / 128, U), 128, 0, strm>>>(L, s, st->d_pb_off, p->d_cos, st->d_rec, st->d_ls,
+                                                               st->d_pstart, st->d_pb);
   SP_TRY(cudaGetLastError());
   // largest blocks first; waves of CTAs sized so the R scratch stays bounded
   std::vector<int> order(U);
@@ -899,9 +940,8 @@ extern "C" int osph_spin_forward(osph_plan* p, int spin, int B, const void* samp
                       p->d_spin_xbuf, out));
     p->launches++;
     if (m > 0) {
-      SP_TRY(launch_pdl(k_spin_corr, dim3((m + 127) / 128, B), dim3(128), 0, strm, L, spin, m, B,
-                        (const double*)p->d_cos, (const double4*)st->d_rec, (const int*)st->d_ls,
-                        (const double2*)st->d_pstart, (const double2*)p->d_spin_xbuf, p->d_r));
+      SP_TRY(launch_pdl(k_spin_corr, dim3((m + 7) / 8, (B + CORR_MB - 1) / CORR_MB), dim3(256), 0, strm, L, spin, m, B, (const double*)st->d_pb,
+                        (const int64_t*)st->d_pb_off, (const double2*)p->d_spin_xbuf, p->d_r));
       p->launches++;
     }
   }
