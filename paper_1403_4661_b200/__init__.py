@@ -45,7 +45,16 @@ from .transform import (
     spin_forward_sht_batch,
     spin_inverse_sht,
     spin_inverse_sht_batch,
-    spin_table,
+)
+from .legendre import LegendreColumn, SpinColumn, legendre_column, legendre_table, spin_column, spin_table
+from .blocks import (
+    CoefficientSlice,
+    GVector,
+    LegendreBlock,
+    block_for_thetas,
+    build_block,
+    condition_number,
+    solve,
 )
 
 from . import distributed, experiments, fileio  # noqa: E402
@@ -62,7 +71,9 @@ __all__ = [
     "clear_plans", "equiangular_candidates", "forward_sht", "forward_sht_batch", "get_plan",
     "grid_from_permutation", "interleaved_grid", "inverse_sht", "inverse_sht_batch", "load_grid",
     "ring_analysis", "ring_longitudes", "save_grid", "spin_forward_sht", "spin_forward_sht_batch",
-    "spin_inverse_sht", "spin_inverse_sht_batch", "spin_table",
+    "spin_inverse_sht", "spin_inverse_sht_batch", "spin_table", "spin_column", "SpinColumn", "legendre_table",
+    "legendre_column", "LegendreColumn", "LegendreBlock", "GVector", "CoefficientSlice", "block_for_thetas",
+    "build_block", "condition_number", "solve",
 ]
 
 __version__ = "0.1.0"

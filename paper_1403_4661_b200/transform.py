@@ -449,30 +449,6 @@ def spin_forward_sht(samples: SpatialSamples, grid, spin: int, *, check: bool = 
     return HarmonicCoefficients(L, values)
 
 
-def spin_table(spin: int, m: int, thetas, band_limit: int, device: int = 0) -> np.ndarray:
-    """sY_lm(theta, 0) for l = max(|m|, |spin|)..L-1 at each theta in (0, pi]
-    (legendre.py:276-306), shape (len(thetas), L - lo), computed on the GPU
-    (osph_spin_block) in chunks of L co-latitudes."""
-    import torch
-
-    L = int(band_limit)
-    lo = max(abs(int(m)), abs(int(spin)))
-    if L < 1 or lo >= L:
-        raise OrderRangeError(f"order {m}, spin {spin} invalid for band limit {L}")
-    th = np.atleast_1d(np.asarray(thetas, dtype=np.float64))
-    out = np.empty((th.size, L - lo))
-    buf = torch.empty((L - lo, L), dtype=torch.float64, device=f"cuda:{device}")
-    for c0 in range(0, th.size, L):
-        chunk = th[c0:c0 + L]
-        padded = np.concatenate([chunk, np.full(L - chunk.size, np.pi / 2)])
-        plan = get_plan(padded, 1, device)
-        with plan.lock:
-            plan.set_stream(None)
-            plan.spin_block(spin, m, buf.data_ptr(), L)
-        out[c0:c0 + chunk.size] = buf.cpu().numpy().T[: chunk.size]
-    return out
-
-
 def ring_analysis(ring_values, m: int):
     """Quadrature-exact Fourier pair of one ring at frequencies (+m, -m) (transform.py:115-131)."""
     values = np.ascontiguousarray(np.asarray(ring_values, dtype=np.complex128))
