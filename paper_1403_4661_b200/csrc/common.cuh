@@ -21,6 +21,10 @@
 #define OSPH_FFT_MAX 8192  // largest one-CTA FFT (complex double: 128 KB); 16384 runs on 2-CTA clusters
 #define OSPH_SW_SMEM 2048     // per-stage FFT twiddles kept in shared memory (spans < 1024)
 #define OSPH_SW_GLOBAL 16384  // global per-stage twiddle table: spans up to 4096 (N <= 16384)
+// Bluestein FFTs of up to OSPH_REG_FFT_MAX points run register-resident (fft_reg.cuh);
+// OSPH_RTW_SIZE: entries of their inter-pass twiddle tables (tables.cu k_reg_twiddles)
+#define OSPH_REG_FFT_MAX 1024
+#define OSPH_RTW_SIZE 1872
 
 // Position of (order m, ring/degree offset i) in order-major packed storage:
 // sum_{m'<m} (L - m') + i   (same packing as transform.py:268-291 offsets).

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -55,7 +56,7 @@ void plan_free(osph_plan* p) {
                   p->d_bluestein_rings, p->d_ainv_off, p->d_pb_off, p->d_ainv, p->d_pbelow, p->d_piv,
                   p->d_norms, p->d_kappa, p->d_status, p->d_jstar, p->d_beta, p->d_u, p->d_w, p->d_xt_off, p->d_xt,
                   p->d_fpack, p->d_g, p->d_r,
-                  p->d_in, p->d_out, p->d_sw, p->d_xbuf, p->d_rres, p->d_at, p->d_bf_off, p->d_bf_e, p->d_bf_e2, p->d_bf_r,
+                  p->d_in, p->d_out, p->d_sw, p->d_rtw, p->d_xbuf, p->d_rres, p->d_at, p->d_bf_off, p->d_bf_e, p->d_bf_e2, p->d_bf_r,
                   p->d_bf_d};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -199,17 +200,23 @@ int plan_create_one(int L, const double* thetas, int max_batch, int device, osph
   PLAN_TRY(dalloc(&p->d_tw, 8192));
   PLAN_TRY(dalloc(&p->d_roots, (size_t)(OSPH_DIRECT_MAX + 1) * (OSPH_DIRECT_MAX + 1) / 4 + 64));
   PLAN_TRY(dalloc(&p->d_sw, OSPH_SW_GLOBAL));
+  PLAN_TRY(dalloc(&p->d_rtw, OSPH_RTW_SIZE));
+  // OSPH_RING_REG=0: every Bluestein ring on the shared-memory transforms of fft.cuh (A/B measurements)
+  p->reg_fft_max = (getenv("OSPH_RING_REG") && atoi(getenv("OSPH_RING_REG")) == 0) ? 0 : OSPH_REG_FFT_MAX;
   for (int k = 0; k < L; ++k) {
     if (p->h_fft_n[k] > 2 * OSPH_FFT_MAX) p->dft_ok = false;
     if (p->h_fft_n[k] > OSPH_FFT_MAX) p->n_big_rings++;
   }
   if (!p->dft_ok) p->n_bluestein_rings = p->n_big_rings = 0;  // Legendre tables only (osph_legendre_block)
+  for (int k : brings)
+    if (p->dft_ok && p->h_fft_n[k] <= p->reg_fft_max) p->n_reg_rings++;
   // the inverse produces every ring until osph_plan_shard restricts it
   p->inv_nr = L;
   p->d_inv_ring_order = p->d_ring_order;
   p->d_inv_bluestein = p->d_bluestein_rings;
   p->inv_n_bluestein = p->n_bluestein_rings;
   p->inv_n_big = p->n_big_rings;
+  p->inv_n_reg = p->n_reg_rings;
   p->inv_direct_lo = 0;
   p->inv_direct_hi = p->n_direct_rings;
   p->own_k_lo = 0;
@@ -622,19 +629,24 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
     // only waits for the previous forward's sweep (the last reader of the factor
     // buffers) and runs on a side stream beside whatever precedes this call on
     // the plan stream (e.g. the inverse of the same batch) and the ring DFTs.
-    if (p->have_sweep_ev) {
+    // OSPH_FACTOR_INLINE=1 (diagnostics): the factorisation on the plan stream, so
+    // every stage is timed alone
+    static const bool inline_factor = getenv("OSPH_FACTOR_INLINE") && atoi(getenv("OSPH_FACTOR_INLINE"));
+    cudaStream_t sf = inline_factor ? st : p->s_in;
+    if (inline_factor) {
+    } else if (p->have_sweep_ev) {
       CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_sweep_done, 0));
     } else {
       CUDA_TRY(cudaEventRecord(p->ev_start, st));
       CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
     }
-    CUDA_TRY(cudaEventRecord(p->ev[6], p->s_in));
-    CUDA_TRY(launch_factor(p, p->s_in));
-    CUDA_TRY(cudaEventRecord(p->ev[7], p->s_in));
+    CUDA_TRY(cudaEventRecord(p->ev[6], sf));
+    CUDA_TRY(launch_factor(p, sf));
+    CUDA_TRY(cudaEventRecord(p->ev[7], sf));
     CUDA_TRY(cudaEventRecord(p->ev[4], st));
     CUDA_TRY(launch_ring_forward(p, B, (const double2*)samples));
     CUDA_TRY(cudaEventRecord(p->ev[5], st));
-    CUDA_TRY(cudaStreamWaitEvent(st, p->ev[7], 0));
+    if (!inline_factor) CUDA_TRY(cudaStreamWaitEvent(st, p->ev[7], 0));
   } else {
     // the factorisation needs no data: it runs while the samples are copied in,
     // and each chunk's ring DFTs start as soon as the chunk has landed

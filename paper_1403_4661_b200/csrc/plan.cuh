@@ -85,6 +85,10 @@ struct osph_plan {
   int n_direct_rings = 0;
   int n_big_rings = 0;  // rings with a 16384-point Bluestein FFT (2-CTA clusters; first in d_bluestein_rings)
   double2* d_sw = nullptr;  // [OSPH_SW_GLOBAL] per-stage FFT twiddles (fft.cuh)
+  double2* d_rtw = nullptr;  // [OSPH_RTW_SIZE] inter-pass twiddles of the register-resident FFTs (fft_reg.cuh)
+  int reg_fft_max = 0;       // rings with fft_n <= this run the register-resident kernels (kernel spectra in natural order)
+  int n_reg_rings = 0;       // how many: the LAST n_reg_rings entries of d_bluestein_rings (sorted largest first)
+  int inv_n_reg = 0;         // the same count for d_inv_bluestein
   bool dft_ok = true;  // every ring's Bluestein FFT fits one CTA (else: tables-only plan)
   // rings the INVERSE produces: all of them, or a chain shard's contiguous range
   // [own_k_lo, own_k_hi) (osph_plan_shard); the forward ring DFTs always cover all rings

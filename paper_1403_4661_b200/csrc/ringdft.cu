@@ -19,6 +19,7 @@
 #include <cstdlib>
 
 #include "fft.cuh"
+#include "fft_reg.cuh"
 #include "plan.cuh"
 
 namespace cg = cooperative_groups;
@@ -295,6 +296,244 @@ __global__ void __launch_bounds__(RING_THREADS) k_ring_forward_direct(int L, int
 static int maps_per_block_for(int B, int rings);
 
 // ---------------------------------------------------------------------------
+// Register-resident Bluestein rings (fft_reg.cuh): FFT sizes 256, 512, 1024.
+// A block is REG_WARPS warps; a group of T = N2 threads (a warp, or half a
+// warp) convolves one map's ring, so a block iteration covers
+// REG_WARPS * 32 / T maps.  Global accesses that are contiguous per map
+// (samples) go straight between registers and global memory, coalesced over
+// the group's lanes; the map-fastest arrays (G, R) are staged through the
+// group's exchange matrix by the whole block.
+// one 32-byte read-only load (sm_100: ld.global.nc.v4.f64); p is 32-byte aligned
+__device__ __forceinline__ double4 ldg_f64x4(const double* p) {
+  double4 v;
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];\n" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+}
+
+#define REG_WARPS 4
+#define REG_THREADS (REG_WARPS * 32)
+
+__device__ __forceinline__ int reg_rtw_offset(int N) { return N == 256 ? 0 : (N == 512 ? 272 : 816); }
+
+// Shared memory of a block: [TW: RS][H: N][chirp: N/2][one exchange matrix of RS entries per group].
+template <int N1, int N2>
+__device__ __forceinline__ double2* reg_stage_tables(double2* sm, int n, const double2* __restrict__ chirp,
+                                                     const double2* __restrict__ bh, const double2* __restrict__ rtw) {
+  using C = RegConv<N1, N2>;
+  for (int i = threadIdx.x; i < C::RS; i += blockDim.x) sm[i] = __ldg(rtw + reg_rtw_offset(C::N) + i);
+  for (int i = threadIdx.x; i < C::N; i += blockDim.x) sm[C::RS + i] = __ldg(bh + i);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sm[C::RS + C::N + i] = __ldg(chirp + i);
+  return sm + C::RS + C::N + C::N / 2;
+}
+
+template <int N1, int N2>
+__device__ __forceinline__ void ring_inverse_reg(int L, int B, int k, int b_first, int b_last, double2* sm,
+                                                 const double2* __restrict__ chirp, const double2* __restrict__ bh,
+                                                 const double2* __restrict__ rtw, const double* __restrict__ G,
+                                                 double2* __restrict__ samples) {
+  using C = RegConv<N1, N2>;
+  constexpr int GPW = 32 / C::T;  // groups (maps) per warp
+  const int n = 2 * k + 1;
+  const int nwarps = blockDim.x >> 5;
+  const int gmax = nwarps * GPW;
+  const double2* tw = sm;
+  const double2* hs = sm + C::RS;
+  const double2* cs = sm + C::RS + C::N;
+  double2* ys = reg_stage_tables<N1, N2>(sm, n, chirp, bh, rtw);
+  const int lane = threadIdx.x & 31, g = (threadIdx.x >> 5) * GPW + lane / C::T, tid = lane % C::T;
+  double2* Y = ys + C::RS * g;
+  // Fold.  The tones m = t (mod n) feed bin t with their + half and bin -t with their
+  // - half, so one thread per (residue t, map) reads both halves as ONE 32-byte load per
+  // tone and keeps two sums: P[t] (+ halves) and M[t] (- halves, sign (-1)^m, m >= 1),
+  // in increasing m (fixed order: bitwise reproducible).  Bin t = P[t] + M[-t mod n].
+  // P sits at Y[0..n), M at Y[n..2n) of the map's exchange matrix (2n <= N <= RS).
+  const int nres = min(n, L);  // residues that hold a tone
+  const int64_t mstride = (int64_t)L * 4 * B;
+  for (int b0 = b_first; b0 < b_last; b0 += gmax) {
+    const int Gr = min(gmax, b_last - b0);
+    const int items = Gr * nres;
+    const double* gbase = G + ((int64_t)k * 4 * B + 4 * b0);
+    if (n >= L) {  // one tone per residue: four independent loads in flight per thread
+      for (int i0 = threadIdx.x; i0 < items; i0 += 4 * blockDim.x) {
+        double4 q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int idx = i0 + u * blockDim.x;
+          if (idx < items) {
+            const int gg = idx % Gr, t = idx / Gr;
+            q[u] = ldg_f64x4(gbase + 4 * gg + t * mstride);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int idx = i0 + u * blockDim.x;
+          if (idx < items) {
+            const int gg = idx % Gr, t = idx / Gr;
+            double2* Yg = ys + C::RS * gg;
+            Yg[t] = make_double2(q[u].x, q[u].y);
+            Yg[n + t] = t == 0 ? make_double2(0.0, 0.0)
+                               : ((t & 1) ? make_double2(-q[u].z, -q[u].w) : make_double2(q[u].z, q[u].w));
+          }
+        }
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < items; idx += blockDim.x) {
+        const int gg = idx % Gr, t = idx / Gr;
+        const double* gk = gbase + 4 * gg;
+        double pr = 0.0, pi = 0.0, mr = 0.0, mi = 0.0;
+        for (int m = t; m < L; m += n) {
+          const double4 q = ldg_f64x4(gk + m * mstride);
+          pr += q.x;
+          pi += q.y;
+          if (m > 0) {
+            if (m & 1) {
+              mr -= q.z;
+              mi -= q.w;
+            } else {
+              mr += q.z;
+              mi += q.w;
+            }
+          }
+        }
+        double2* Yg = ys + C::RS * gg;
+        Yg[t] = make_double2(pr, pi);
+        Yg[n + t] = make_double2(mr, mi);
+      }
+    }
+    __syncthreads();
+    double2 v[N1];
+#pragma unroll
+    for (int n1 = 0; n1 < N1 / 2; ++n1) {
+      const int t = n1 * N2 + tid;
+      v[n1] = make_double2(0.0, 0.0);
+      if (t < n && g < Gr) {
+        const int r = t == 0 ? 0 : n - t;
+        const double2 a = t < nres ? Y[t] : make_double2(0.0, 0.0);
+        const double2 b = r < nres ? Y[n + r] : make_double2(0.0, 0.0);
+        v[n1] = cmul(cadd(a, b), cs[t]);
+      }
+    }
+    __syncwarp();
+    C::run(v, Y, tw, hs, tid);
+    if (g < Gr) {
+      double2* out = samples + (int64_t)(b0 + g) * L * L + (int64_t)k * k;
+#pragma unroll
+      for (int n1 = 0; n1 < N1 / 2; ++n1) {
+        const int t = n1 * N2 + tid;
+        if (t < n) out[t] = cmul(v[n1], cs[t]);
+      }
+    }
+    __syncthreads();  // the next iteration's fold overwrites the exchange matrices
+  }
+}
+
+__global__ void __launch_bounds__(REG_THREADS, 2) k_ring_inverse_reg(
+    int L, int B, int maps_per_block, const int* __restrict__ rings, const int* __restrict__ fft_n,
+    const int64_t* __restrict__ chirp_off, const int64_t* __restrict__ bhat_off, const double2* __restrict__ chirp_all,
+    const double2* __restrict__ bhat_all, const double2* __restrict__ rtw, const double* __restrict__ G,
+    double2* __restrict__ samples) {
+  extern __shared__ double2 sm[];
+  const int k = rings[blockIdx.x];
+  const int N = fft_n[k];
+  const double2* chirp = chirp_all + chirp_off[k];
+  const double2* bh = bhat_all + bhat_off[k] + N;  // inverse-direction kernel, natural order
+  const int b_first = blockIdx.y * maps_per_block;
+  const int b_last = min(B, b_first + maps_per_block);
+  if (N == 1024) ring_inverse_reg<32, 32>(L, B, k, b_first, b_last, sm, chirp, bh, rtw, G, samples);
+  else if (N == 512) ring_inverse_reg<32, 16>(L, B, k, b_first, b_last, sm, chirp, bh, rtw, G, samples);
+  else ring_inverse_reg<16, 16>(L, B, k, b_first, b_last, sm, chirp, bh, rtw, G, samples);
+}
+
+template <int N1, int N2>
+__device__ __forceinline__ void ring_forward_reg(int L, int k, int b_first, int b_last, int lgG, double2* sm,
+                                                 const double2* __restrict__ chirp, const double2* __restrict__ bh,
+                                                 const double2* __restrict__ rtw, const double2* __restrict__ samples,
+                                                 double2* __restrict__ R) {
+  using C = RegConv<N1, N2>;
+  constexpr int GPW = 32 / C::T;
+  const int n = 2 * k + 1;
+  const int nwarps = blockDim.x >> 5;
+  const int gmax = nwarps * GPW;
+  const double2* tw = sm;
+  const double2* hs = sm + C::RS;
+  const double2* cs = sm + C::RS + C::N;
+  double2* ys = reg_stage_tables<N1, N2>(sm, n, chirp, bh, rtw);
+  const int lane = threadIdx.x & 31, g = (threadIdx.x >> 5) * GPW + lane / C::T, tid = lane % C::T;
+  double2* Y = ys + C::RS * g;
+  const int64_t npos = (int64_t)L * (L + 1) / 2;
+  const double scale = OSPH_TWO_PI / (double)n;
+  __syncthreads();
+  for (int b0 = b_first; b0 < b_last; b0 += gmax) {
+    const int Gr = min(gmax, b_last - b0);
+    double2 v[N1];
+    {
+      const double2* in = samples + (int64_t)(b0 + min(g, Gr - 1)) * L * L + (int64_t)k * k;
+#pragma unroll
+      for (int n1 = 0; n1 < N1 / 2; ++n1) {  // contiguous ring reads per map
+        const int t = n1 * N2 + tid;
+        v[n1] = t < n ? cmul(__ldg(in + t), conj2(cs[t])) : make_double2(0.0, 0.0);
+      }
+    }
+    C::run(v, Y, tw, hs, tid);
+    __syncwarp();  // every lane has re-read Y before the spectrum overwrites it
+#pragma unroll
+    for (int n1 = 0; n1 < N1 / 2; ++n1) {
+      const int t = n1 * N2 + tid;
+      if (t < n) {
+        const double2 x = cmul(v[n1], conj2(cs[t]));
+        Y[t] = make_double2(scale * x.x, scale * x.y);
+      }
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < Gr * (k + 1); idx += blockDim.x) {  // map-fastest writes of R
+      const int gg = idx % Gr, m = idx / Gr;
+      const double2* X = ys + C::RS * gg;
+      const int64_t base = r_index(packed_pos(L, m, k - m), 0, b0 + gg, lgG, npos);
+      R[base] = X[m];
+      // order 0's - slot starts at zero and collects the sweep's -tone corrections that alias
+      // to bin 0 (see scatter_rhs_multi)
+      R[base + (1 << lgG)] = m == 0 ? make_double2(0.0, 0.0) : X[n - m];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(REG_THREADS, 2) k_ring_forward_reg(
+    int L, int B, int maps_per_block, const int* __restrict__ rings, const int* __restrict__ fft_n,
+    const int64_t* __restrict__ chirp_off, const int64_t* __restrict__ bhat_off, const double2* __restrict__ chirp_all,
+    const double2* __restrict__ bhat_all, const double2* __restrict__ rtw, const double2* __restrict__ samples,
+    double2* __restrict__ R, int bofs, int bend, int lgG) {
+  extern __shared__ double2 sm[];
+  const int k = rings[blockIdx.x];
+  const int N = fft_n[k];
+  const double2* chirp = chirp_all + chirp_off[k];
+  const double2* bh = bhat_all + bhat_off[k];  // forward-direction kernel, natural order
+  const int b_first = bofs + blockIdx.y * maps_per_block;
+  const int b_last = min(bend, b_first + maps_per_block);
+  if (N == 1024) ring_forward_reg<32, 32>(L, k, b_first, b_last, lgG, sm, chirp, bh, rtw, samples, R);
+  else if (N == 512) ring_forward_reg<32, 16>(L, k, b_first, b_last, lgG, sm, chirp, bh, rtw, samples, R);
+  else ring_forward_reg<16, 16>(L, k, b_first, b_last, lgG, sm, chirp, bh, rtw, samples, R);
+}
+
+// launch shape of the register-resident kernels: warps per block, maps per block, shared memory
+struct RegShape {
+  int threads, mpb;
+  size_t smem;
+};
+static RegShape reg_shape(int B, int nrings) {
+  int warps = REG_WARPS;
+  while (warps > 1 && (warps - 1) * 2 >= B) --warps;  // small batches: no idle warps (two maps per warp at N <= 512)
+  // twiddles, kernel spectrum, chirp + one exchange matrix per group; 512- and 256-point rings
+  // run two groups per warp
+  const size_t ent = std::max<size_t>((size_t)RegConv<32, 32>::RS * (1 + warps) + 1536,
+                                      (size_t)RegConv<32, 16>::RS * (1 + 2 * warps) + 768);
+  static const int waves = getenv("OSPH_RING_WAVES") ? atoi(getenv("OSPH_RING_WAVES")) : 4;
+  int mpb = 2 * warps;  // maps per block iteration of the half-warp classes
+  while (mpb < B && (int64_t)nrings * ((B + mpb - 1) / mpb) > (int64_t)148 * 2 * waves) mpb *= 2;
+  return {warps * 32, mpb, ent * sizeof(double2)};
+}
+
+// ---------------------------------------------------------------------------
 // Rings whose Bluestein FFT is N = 2M = 16384 points (n = 2k+1 > 4096, L > 2048):
 // one 2-CTA cluster per ring, each CTA holding M points.  Because n <= M the
 // upper half of the chirped input is zero, so the first (span-M) stage of the
@@ -451,7 +690,16 @@ cudaError_t launch_ring_inverse(osph_plan* p, int B, double2* samples) {
     cudaError_t e = launch_big((const void*)k_ring_inverse_bluestein2, p, B, p->inv_n_big, args);
     if (e != cudaSuccess) return e;
   }
-  const int nsmall = p->inv_n_bluestein - p->inv_n_big;
+  if (p->inv_n_reg > 0) {
+    const RegShape sh = reg_shape(B, p->inv_n_reg);
+    cudaFuncSetAttribute(k_ring_inverse_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem);
+    dim3 grid(p->inv_n_reg, (B + sh.mpb - 1) / sh.mpb);
+    k_ring_inverse_reg<<<grid, sh.threads, sh.smem, p->stream>>>(
+        L, B, sh.mpb, p->d_inv_bluestein + (p->inv_n_bluestein - p->inv_n_reg), p->d_fft_n, p->d_chirp_off,
+        p->d_bhat_off, p->d_chirp, p->d_bhat, p->d_rtw, p->d_g, samples);
+    p->launches++;
+  }
+  const int nsmall = p->inv_n_bluestein - p->inv_n_big - p->inv_n_reg;
   if (nsmall > 0) {
     const int mpb = maps_per_block_for(B, nsmall);
     const size_t smem = ring_smem(p);
@@ -484,7 +732,16 @@ cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples, int
     cudaError_t e = launch_big((const void*)k_ring_forward_bluestein2, p, nb, p->n_big_rings, args);
     if (e != cudaSuccess) return e;
   }
-  const int nsmall = p->n_bluestein_rings - p->n_big_rings;
+  if (p->n_reg_rings > 0) {
+    const RegShape sh = reg_shape(nb, p->n_reg_rings);
+    cudaFuncSetAttribute(k_ring_forward_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem);
+    dim3 grid(p->n_reg_rings, (nb + sh.mpb - 1) / sh.mpb);
+    k_ring_forward_reg<<<grid, sh.threads, sh.smem, p->stream>>>(
+        L, B, sh.mpb, p->d_bluestein_rings + (p->n_bluestein_rings - p->n_reg_rings), p->d_fft_n, p->d_chirp_off,
+        p->d_bhat_off, p->d_chirp, p->d_bhat, p->d_rtw, samples, p->d_r, bofs, bofs + nb, lgG);
+    p->launches++;
+  }
+  const int nsmall = p->n_bluestein_rings - p->n_big_rings - p->n_reg_rings;
   if (nsmall > 0) {
     const int mpb = maps_per_block_for(nb, nsmall);
     const size_t smem = ring_smem(p);

@@ -149,6 +149,26 @@ __global__ void k_stage_twiddles(double2* __restrict__ sw) {
   sw[2 * (h - 1) + h + pos] = make_double2(c, s);
 }
 
+// Inter-pass twiddles of the register-resident convolutions (fft_reg.cuh):
+// for N = N1 N2 the padded matrix TW[k1 (N2 + 1) + n2] = e^{-2 pi i k1 n2 / N}.
+// Classes: 256 = 16 x 16 at 0, 512 = 32 x 16 at 272, 1024 = 32 x 32 at 816.
+__global__ void k_reg_twiddles(double2* __restrict__ rtw) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= OSPH_RTW_SIZE) return;
+  int N1, N2, base;
+  if (i < 272) {
+    N1 = 16; N2 = 16; base = 0;
+  } else if (i < 816) {
+    N1 = 32; N2 = 16; base = 272;
+  } else {
+    N1 = 32; N2 = 32; base = 816;
+  }
+  const int r = i - base, k1 = r / (N2 + 1), n2 = r - k1 * (N2 + 1);
+  double s = 0.0, c = 1.0;
+  if (n2 < N2) sincospi(-2.0 * (double)(k1 * n2) / (double)(N1 * N2), &s, &c);
+  rtw[i] = make_double2(c, s);
+}
+
 __global__ void k_twiddles(double2* __restrict__ tw) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= OSPH_TW_SIZE / 2) return;
@@ -178,7 +198,7 @@ __global__ void k_bluestein_tables(int nrings, const int* __restrict__ rings, co
                                    const int64_t* __restrict__ chirp_off,
                                    const int64_t* __restrict__ bhat_off, const double2* __restrict__ tw,
                                    double2* __restrict__ chirp, double2* __restrict__ bhat,
-                                   double2* __restrict__ scratch) {
+                                   double2* __restrict__ scratch, int natural_max) {
   extern __shared__ double2 xs_sm[];
   for (int ri = blockIdx.x; ri < nrings; ri += gridDim.x) {
   const int k = rings[ri];
@@ -211,8 +231,10 @@ __global__ void k_bluestein_tables(int nrings, const int* __restrict__ rings, co
     fft_dit_smem(xs, N, logN, tw, false);
     const double inv = 1.0 / (double)N;
     double2* out = bhat + bhat_off[k] + (int64_t)dir * N;
-    for (int u = threadIdx.x; u < N; u += blockDim.x) {  // bit-reversed order (see bluestein_convolve)
-      const double2 v = xs[bitrev(u, logN)];
+    // bit-reversed order for the shared-memory transforms (bluestein_convolve), natural
+    // order for the register-resident ones (N <= natural_max, fft_reg.cuh)
+    for (int u = threadIdx.x; u < N; u += blockDim.x) {
+      const double2 v = xs[N <= natural_max ? u : bitrev(u, logN)];
       out[u] = make_double2(v.x * inv, v.y * inv);
     }
     __syncthreads();
@@ -261,6 +283,7 @@ cudaError_t launch_tables(osph_plan* p) {
   k_small_roots<<<ndirect, 64, 0, st>>>(ndirect, p->d_roots);
   if ((e = dbg_sync(st, "k_twiddles/k_small_roots")) != cudaSuccess) return e;
   k_stage_twiddles<<<OSPH_SW_GLOBAL / 2 / 256, 256, 0, st>>>(p->d_sw);
+  k_reg_twiddles<<<(OSPH_RTW_SIZE + 255) / 256, 256, 0, st>>>(p->d_rtw);
   if ((e = dbg_sync(st, "k_stage_twiddles")) != cudaSuccess) return e;
   const int nsmall = p->n_bluestein_rings - p->n_big_rings;
   if (nsmall > 0) {
@@ -271,7 +294,7 @@ cudaError_t launch_tables(osph_plan* p) {
     cudaFuncSetAttribute(k_bluestein_tables, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_bluestein_tables<<<nsmall, 256, smem, st>>>(nsmall, p->d_bluestein_rings + p->n_big_rings, p->d_fft_n,
                                                   p->d_chirp_off, p->d_bhat_off, p->d_tw, p->d_chirp, p->d_bhat,
-                                                  nullptr);
+                                                  nullptr, p->reg_fft_max);
   }
   if (p->n_big_rings > 0) {  // 16384-point kernel spectra: work arrays in global memory
     const int nb = std::min(p->n_big_rings, 296);
@@ -279,7 +302,7 @@ cudaError_t launch_tables(osph_plan* p) {
     if ((e = cudaMallocAsync(&scratch, sizeof(double2) * (size_t)nb * 2 * OSPH_FFT_MAX, st)) != cudaSuccess)
       return e;
     k_bluestein_tables<<<nb, 256, 0, st>>>(p->n_big_rings, p->d_bluestein_rings, p->d_fft_n, p->d_chirp_off,
-                                           p->d_bhat_off, p->d_tw, p->d_chirp, p->d_bhat, scratch);
+                                           p->d_bhat_off, p->d_tw, p->d_chirp, p->d_bhat, scratch, 0);
     cudaFreeAsync(scratch, st);
   }
   return cudaGetLastError();
