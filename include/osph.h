@@ -137,11 +137,14 @@ int osph_last_launch_count(const osph_plan* plan);
  *   OSPH_SWEEP_PERSISTENT  one persistent cluster kernel (sweep.cu; L <= 1024, teams resident)
  *   OSPH_SWEEP_GEMM        two whole-GPU DMMA GEMM launches per order (sweep_gemm.cu; large batches)
  *   OSPH_SWEEP_LARGE       two launches per order + refinement (sweep_large.cu; L > 1024)
- *   OSPH_SWEEP_WINDOWED    factor + large sweep window by window (window.cu; factors exceed HBM) */
+ *   OSPH_SWEEP_WINDOWED    factor + large sweep window by window (window.cu; factors exceed HBM)
+ *   OSPH_SWEEP_BLOCKED     orders peeled in blocks of 32: in-block aliasing resolved by a scalar
+ *                          recurrence, three batched DMMA GEMM launches per block (sweep_block.cu; batches) */
 #define OSPH_SWEEP_PERSISTENT 0
 #define OSPH_SWEEP_GEMM 1
 #define OSPH_SWEEP_LARGE 2
 #define OSPH_SWEEP_WINDOWED 3
+#define OSPH_SWEEP_BLOCKED 4
 int osph_last_sweep_kind(const osph_plan* plan);
 
 /* The grid's pivot order: perm[L(L+1)/2] (may be NULL), packed by order as
@@ -206,7 +209,8 @@ int osph_forward_stage(osph_plan* plan, int stages, int B, const void* samples, 
 #define OSPH_BUF_JSTAR 7  /* j*_m */
 #define OSPH_BUF_NORMS 8  /* ||A_m||_1, ||X_m||_1 (condition estimate) */
 #define OSPH_BUF_STATUS 9 /* zero-pivot flags */
-#define OSPH_BUF_COUNT 10
+#define OSPH_BUF_UT 10    /* coupling rows U_m of the blocked sweep, tiles */
+#define OSPH_BUF_COUNT 11
 int osph_shard_buffer(osph_plan* plan, int which, int B, int m_lo, int m_hi, void** ptr, int64_t* bytes);
 
 /* ---- spin-weighted transforms ----

@@ -20,8 +20,8 @@ OSPH_OK, OSPH_ERR_ARG, OSPH_ERR_ILLCOND, OSPH_ERR_CUDA, OSPH_ERR_NCCL, OSPH_ERR_
 OSPH_HOST, OSPH_DEVICE, OSPH_ASYNC, OSPH_REAL = 0, 1, 2, 4
 SHARD_CHAIN, SHARD_FACTORS = 1, 2
 STAGE_RINGS, STAGE_FACTOR, STAGE_SWEEP = 1, 2, 4
-BUF_SPECTRA, BUF_XT, BUF_PB, BUF_AT, BUF_U, BUF_W, BUF_BETA, BUF_JSTAR, BUF_NORMS, BUF_STATUS, BUF_COUNT = range(11)
-SWEEP_KINDS = {0: "persistent", 1: "gemm", 2: "large", 3: "windowed"}
+BUF_SPECTRA, BUF_XT, BUF_PB, BUF_AT, BUF_U, BUF_W, BUF_BETA, BUF_JSTAR, BUF_NORMS, BUF_STATUS, BUF_UT, BUF_COUNT = range(12)
+SWEEP_KINDS = {0: "persistent", 1: "gemm", 2: "large", 3: "windowed", 4: "blocked"}
 ABI_VERSION = 3
 
 

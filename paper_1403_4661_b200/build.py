@@ -19,7 +19,7 @@ from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
-SOURCES = ["plan.cu", "tables.cu", "ringdft.cu", "synth.cu", "factor.cu", "sweep.cu", "sweep_large.cu", "factor_bf.cu", "pivots.cu", "window.cu", "sweep_gemm.cu", "shard.cu", "spin.cu"]
+SOURCES = ["plan.cu", "tables.cu", "ringdft.cu", "synth.cu", "factor.cu", "sweep.cu", "sweep_large.cu", "factor_bf.cu", "pivots.cu", "window.cu", "sweep_gemm.cu", "sweep_block.cu", "shard.cu", "spin.cu"]
 OUT = HERE / "libosph.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 OBJ = CSRC / "build"  # git-ignored, gpurun-ignored (only libosph.so travels)

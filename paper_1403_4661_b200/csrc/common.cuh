@@ -52,6 +52,11 @@ __host__ __device__ __forceinline__ int64_t r_index(int64_t pos, int slot, int b
 // so one chunk of a contiguous row-tile range is one contiguous block (a
 // single bulk copy).  Padding rows / columns are zero.
 #define OSPH_TILE_KC 32
+// Blocked sweep (sweep_block.cu): orders are peeled in blocks of OSPH_SB_BLOCK; order s keeps
+// the coupling rows U_s[r, :] = Pb_s[s-1-r, :] X_s of the rings just below it, r < sb_rows(s)
+// (every ring below s for the final block s < OSPH_SB_BLOCK), tiled like X.
+#define OSPH_SB_BLOCK 32
+__host__ __device__ __forceinline__ int sb_rows(int s) { return s < OSPH_SB_BLOCK ? OSPH_SB_BLOCK : OSPH_SB_BLOCK / 2; }
 __host__ __device__ __forceinline__ int64_t tile_index(int r, int k, int nrt) {
   return ((((int64_t)(k >> 5)) * nrt + (r >> 3)) << 8) + ((k & 31) << 3) + (r & 7);
 }

@@ -621,6 +621,85 @@ __global__ void __launch_bounds__(BF_THREADS) k_bf_epilogue(int L, int m_first, 
   }
 }
 
+// ---- 4. coupling rows of the blocked sweep (sweep_block.cu):
+//   U_m[r, j] = Pb_m[m-1-r, :] . X_m[:, j],   r < min(sb_rows(m), m),  j < n  (natural ring order),
+// the response of ring m-1-r (a ring just below the block of order m) to entry j of order
+// m's right-hand side.  Thread = column j (its 8-row pieces of the tiled X are contiguous;
+// column 0, zeroed in the tiles, is w_m); the Pb rows are staged in shared memory and
+// broadcast.  Output tiled like X (8-row tiles, 32-column chunks).
+template <int J>
+__device__ __forceinline__ void bf_couple_rows(int L, int m, const double* __restrict__ Xt,
+                                               const double* __restrict__ Pb, const double* __restrict__ w,
+                                               double* __restrict__ Ut, double* pbs) {
+  const int n = L - m, nrt = (n + 7) >> 3, nrtpb = (m + 7) >> 3;
+  const int JJ = min(J, m);
+  const int cn = blockIdx.x * 128 + threadIdx.x;
+  double acc[J];
+#pragma unroll
+  for (int r = 0; r < J; ++r) acc[r] = 0.0;
+  const double* xcol = cn == 0 ? w : Xt + ((int64_t)(cn >> 5) * nrt << 8) + ((cn & 31) << 3);
+  const int xstride = cn == 0 ? 8 : 256;  // doubles between consecutive 8-row pieces
+  for (int i0 = 0; i0 < n; i0 += 128) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 128 * J; idx += 128) {  // pbs[i][r] = Pb[m-1-r, i0 + i]
+      const int r = idx % J, i = idx / J;
+      pbs[idx] = (r < JJ && i0 + i < n) ? __ldcg(Pb + tile_index(m - 1 - r, i0 + i, nrtpb)) : 0.0;
+    }
+    __syncthreads();
+    if (cn < n) {
+      const int imax = min(128, n - i0);
+      for (int i8 = 0; i8 < imax; i8 += 8) {
+        const double* xp = xcol + (int64_t)((i0 + i8) >> 3) * xstride;
+        double x[8];
+        if (cn == 0) {  // w_m is not padded
+#pragma unroll
+          for (int q = 0; q < 8; ++q) x[q] = (i0 + i8 + q < n) ? __ldcg(xp + q) : 0.0;
+        } else {  // rows past n are zero in the tiles
+#pragma unroll
+          for (int q = 0; q < 8; q += 2) {
+            const double2 v = __ldcg(reinterpret_cast<const double2*>(xp + q));
+            x[q] = v.x;
+            x[q + 1] = v.y;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double xv = x[q];
+          const double* pr = pbs + (i8 + q) * J;
+#pragma unroll
+          for (int r = 0; r < J; r += 2) {
+            const double2 pv = *reinterpret_cast<const double2*>(pr + r);
+            acc[r] = fma(pv.x, xv, acc[r]);
+            acc[r + 1] = fma(pv.y, xv, acc[r + 1]);
+          }
+        }
+      }
+    }
+  }
+  if (cn < n) {
+    double* out = Ut + (((int64_t)(cn >> 5) * (J / 8)) << 8) + ((cn & 31) << 3);
+#pragma unroll
+    for (int r = 0; r < J; ++r)
+      if (r < JJ) out[(r >> 3) * 256 + (r & 7)] = acc[r];
+  }
+}
+
+__global__ void __launch_bounds__(128) k_bf_couple(int L, int m_first, const int64_t* __restrict__ xt_off,
+                                                   const double* __restrict__ xt_all,
+                                                   const int64_t* __restrict__ pb_off,
+                                                   const double* __restrict__ pbelow, const double* __restrict__ w_all,
+                                                   const int64_t* __restrict__ ut_off, double* __restrict__ ut_all) {
+  __shared__ __align__(16) double pbs[128 * OSPH_SB_BLOCK];
+  const int m = m_first + blockIdx.y;
+  if (m == 0 || (int)blockIdx.x * 128 >= L - m) return;
+  const double* Xt = xt_all + __ldg(xt_off + m);
+  const double* Pb = pbelow + __ldg(pb_off + m);
+  const double* w = w_all + (size_t)m * uw_ld(L);
+  double* Ut = ut_all + __ldg(ut_off + m);
+  if (m < OSPH_SB_BLOCK) bf_couple_rows<OSPH_SB_BLOCK>(L, m, Xt, Pb, w, Ut, pbs);
+  else bf_couple_rows<OSPH_SB_BLOCK / 2>(L, m, Xt, Pb, w, Ut, pbs);
+}
+
 // ---- host side ------------------------------------------------------------
 
 // E / R panel storage of one order (doubles), for offset tables built by the plan.
@@ -892,6 +971,11 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
   k_bf_epilogue<<<dim3(8, cnt_all), BF_THREADS, 0, st>>>(L, m_first, o.ainv, p->d_ainv, p->d_piv, o.xt, p->d_xt,
                                                          o.pb, p->d_pbelow, p->d_u, p->d_w, p->d_beta, p->d_jstar);
   p->launches++;
+  if (p->d_ut && !p->windowed && L <= 1024) {  // resident plans: the coupling rows of the blocked sweep
+    k_bf_couple<<<dim3((L - m_first + 127) / 128, cnt_all), 128, 0, st>>>(L, m_first, o.xt, p->d_xt, o.pb, p->d_pbelow,
+                                                                       p->d_w, p->d_ut_off, p->d_ut);
+    p->launches++;
+  }
   return cudaGetLastError();
 }
 

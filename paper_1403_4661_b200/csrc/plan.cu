@@ -56,7 +56,7 @@ void plan_free(osph_plan* p) {
                   p->d_bluestein_rings, p->d_ainv_off, p->d_pb_off, p->d_ainv, p->d_pbelow, p->d_piv,
                   p->d_norms, p->d_kappa, p->d_status, p->d_jstar, p->d_beta, p->d_u, p->d_w, p->d_xt_off, p->d_xt,
                   p->d_fpack, p->d_g, p->d_r,
-                  p->d_in, p->d_out, p->d_sw, p->d_rtw, p->d_xbuf, p->d_rres, p->d_at, p->d_bf_off, p->d_bf_e, p->d_bf_e2, p->d_bf_r,
+                  p->d_in, p->d_out, p->d_sw, p->d_rtw, p->d_ut_off, p->d_ut, p->d_sb_x, p->d_sb_a, p->d_sb_g, p->d_sb_r2, p->d_xbuf, p->d_rres, p->d_at, p->d_bf_off, p->d_bf_e, p->d_bf_e2, p->d_bf_r,
                   p->d_bf_d};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -321,6 +321,7 @@ int ensure_spectra(osph_plan* p) {
 
 static int sweep_kind(const osph_plan* p) {
   if (p->windowed) return OSPH_SWEEP_WINDOWED;
+  if (p->sweep_blocked) return OSPH_SWEEP_BLOCKED;
   if (p->sweep_gemm) return OSPH_SWEEP_GEMM;
   if (p->sweep_large) return OSPH_SWEEP_LARGE;
   return OSPH_SWEEP_PERSISTENT;

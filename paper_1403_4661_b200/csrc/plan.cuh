@@ -127,6 +127,15 @@ struct osph_plan {
   std::vector<int64_t> h_xt_off;  // [L+1] offset of order m's 8-row-tiled inverse
   int64_t* d_xt_off = nullptr;
   double* d_xt = nullptr;         // X_m in 8-row tiles (sweep operand)
+  // blocked sweep (sweep_block.cu): coupling rows U_m (tiled), per-block scratch
+  std::vector<int64_t> h_ut_off;  // [L+1]
+  int64_t* d_ut_off = nullptr;
+  double* d_ut = nullptr;
+  double2* d_sb_x = nullptr;      // [block][B][+-][L] solved coefficients of a block of orders
+  double2* d_sb_a = nullptr;      // [block][32][B][+-] coupling products U_s g_s
+  double2* d_sb_g = nullptr;      // [block][16][B][+-] corrections of a block through the short rings k < 16
+  double2* d_sb_r2 = nullptr;     // opposite-tone corrections, laid out like R (zero between forward calls)
+  bool sweep_blocked = false;     // batches: orders peeled in blocks, three batched GEMM launches per block
   bool fwd_ready = false;        // forward buffers allocated
   bool piv_ready = false;        // d_piv holds the (grid-determined) pivot order of every order
   double pivot_seconds = 0.0;    // host wall time of this plan's pivot discovery (0: cached per grid)
@@ -237,6 +246,8 @@ cudaError_t launch_sweep(osph_plan* p, int B, double2* flm);               // sw
 int sweep_maps_per_team(osph_plan* p, int B);
 cudaError_t launch_sweep_large(osph_plan* p, int B, double2* flm);  // sweep_large.cu
 cudaError_t launch_sweep_gemm(osph_plan* p, int B, double2* flm);   // sweep_gemm.cu
+cudaError_t launch_sweep_blocked(osph_plan* p, int B, double2* flm);  // sweep_block.cu
+int ensure_sweep_blocked(osph_plan* p);                               // sweep_block.cu: scratch buffers
 cudaError_t launch_factor_bf(osph_plan* p, int m_first, int m_last, cudaStream_t st);  // factor_bf.cu
 cudaError_t bf_prepare(osph_plan* p, int m_first, int m_last, BfRange* r);               // factor_bf.cu
 cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffsets& o); // factor_bf.cu

@@ -219,6 +219,10 @@ static int buffer_span(osph_plan* p, int which, int B, int m_lo, int m_hi, void*
       *ptr = p->d_status + m_lo;
       *bytes = (int64_t)sizeof(int) * cnt;
       break;
+    case OSPH_BUF_UT:
+      *ptr = p->d_ut + p->h_ut_off[m_lo];
+      *bytes = (int64_t)sizeof(double) * (p->h_ut_off[m_hi + 1] - p->h_ut_off[m_lo]);
+      break;
     default:
       osph_set_error("unknown buffer id");
       return OSPH_ERR_ARG;
@@ -267,7 +271,7 @@ int forward_stage_enqueue(osph_plan* p, int stages, int B, const void* samples, 
     } else {
       if (p->shard_mode == OSPH_SHARD_FACTORS) SH_TRY(launch_kappa(p, st));  // norms gathered from every shard
       SH_TRY(launch_sweep(p, B, (double2*)flm));
-      p->last_sweep_kind = p->sweep_gemm ? OSPH_SWEEP_GEMM : p->sweep_large ? OSPH_SWEEP_LARGE : OSPH_SWEEP_PERSISTENT;
+      p->last_sweep_kind = p->sweep_blocked ? OSPH_SWEEP_BLOCKED : p->sweep_gemm ? OSPH_SWEEP_GEMM : p->sweep_large ? OSPH_SWEEP_LARGE : OSPH_SWEEP_PERSISTENT;
     }
     SH_TRY(cudaEventRecord(p->ev[9], st));
     SH_TRY(cudaEventRecord(p->ev_sweep_done, st));

@@ -936,6 +936,22 @@ int sweep_maps_per_team(osph_plan* p, int B) {
   const int KC = SWEEP_KC;
   if (p->sweep_cfg_B == B) return p->sweep_cfg[0];
   p->sweep_gemm = false;
+  p->sweep_blocked = false;
+  {
+    // batches: orders peeled in blocks of 32 with batched GEMM launches (sweep_block.cu);
+    // OSPH_SWEEP_BLOCKED=1 / 0 forces / forbids it
+    const char* eb = getenv("OSPH_SWEEP_BLOCKED");
+    const bool can = L <= 1024 && !p->windowed && p->d_ut && !getenv("OSPH_SWEEP_LARGE") &&
+                     !getenv("OSPH_SWEEP_GEMM") && !getenv("OSPH_SWEEP_NO_GEMM");
+    if (can && (eb ? atoi(eb) != 0 : B >= 16)) {
+      p->sweep_blocked = true;
+      p->sweep_large = false;
+      p->sweep_cfg_B = B;
+      p->sweep_cfg[0] = 1;
+      p->sweep_cfg[1] = p->sweep_cfg[2] = 0;
+      return 1;
+    }
+  }
   if (L > 1024 || p->windowed || getenv("OSPH_SWEEP_LARGE")) {  // the right-hand sides no longer fit the persistent kernel's smem
     p->sweep_large = true;
     p->sweep_cfg_B = B;
@@ -1035,6 +1051,10 @@ int sweep_maps_per_team(osph_plan* p, int B) {
 
 cudaError_t launch_sweep(osph_plan* p, int B, double2* flm) {
   const int g = sweep_maps_per_team(p, B), T = p->sweep_cfg[1], S = p->sweep_cfg[2];
+  if (p->sweep_blocked) {
+    if (ensure_sweep_blocked(p)) return cudaErrorMemoryAllocation;
+    return launch_sweep_blocked(p, B, flm);
+  }
   if (p->sweep_gemm) return launch_sweep_gemm(p, B, flm);
   if (p->sweep_large) return launch_sweep_large(p, B, flm);
   if (g == 4) return launch_sweep_cc<16>(p, B, 4, T, SWEEP_KC, S, flm);

@@ -123,6 +123,13 @@ int alloc_factor_storage(osph_plan* p) {
     // padding of the tiled operands stays zero forever (the kernels write only real entries)
     W_TRY(cudaMemsetAsync(p->d_pbelow, 0, sizeof(double) * (size_t)tot[2], st));
     W_TRY(cudaMemsetAsync(p->d_xt, 0, sizeof(double) * (size_t)tot[1], st));
+    // coupling rows of the blocked sweep (rows past the rings below s and padding stay zero)
+    p->h_ut_off.assign(L + 1, 0);
+    for (int m = 0; m < L; ++m) p->h_ut_off[m + 1] = p->h_ut_off[m] + tile_size(sb_rows(m), L - m);
+    W_TRY(cudaMalloc(&p->d_ut_off, sizeof(int64_t) * (L + 1)));
+    W_TRY(cudaMemcpy(p->d_ut_off, p->h_ut_off.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice));
+    W_TRY(dalloc_w(&p->d_ut, (size_t)p->h_ut_off[L]));
+    W_TRY(cudaMemsetAsync(p->d_ut, 0, sizeof(double) * (size_t)p->h_ut_off[L], st));
     return OSPH_OK;
   }
   // windows in descending m, each within the budget

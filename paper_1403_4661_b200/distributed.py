@@ -131,7 +131,7 @@ class ShardedTransform:
     """
 
     FACTOR_BUFFERS = (_lib.BUF_XT, _lib.BUF_PB, _lib.BUF_AT, _lib.BUF_U, _lib.BUF_W, _lib.BUF_BETA,
-                      _lib.BUF_JSTAR, _lib.BUF_NORMS, _lib.BUF_STATUS)
+                      _lib.BUF_JSTAR, _lib.BUF_NORMS, _lib.BUF_STATUS, _lib.BUF_UT)
 
     def __init__(self, grid, max_batch: int = 1, mode: str = "chain", group=None, device: int | None = None,
                  plan=None):

@@ -150,7 +150,8 @@ def _fresh_forward(grid, samples, real=False, env=None, monkeypatch=None):
 
 
 @pytest.mark.parametrize("env,want", [({}, "persistent"), ({"OSPH_SWEEP_LARGE": "1"}, "large"),
-                                      ({"OSPH_WINDOW_GB": "0.03"}, "windowed")])
+                                      ({"OSPH_WINDOW_GB": "0.03"}, "windowed"),
+                                      ({"OSPH_SWEEP_BLOCKED": "1"}, "blocked")])
 def test_sweep_variants_L256_reference(env, want, golden, grid_of, monkeypatch):
     """Config 2's grid and recipe through each sweep the library has, against the reference."""
     d = golden("ref_L256.npz")
@@ -164,27 +165,47 @@ def test_sweep_variants_L256_reference(env, want, golden, grid_of, monkeypatch):
         assert np.abs(f[i] - d[f"{recipe}_flm"]).max() <= tol_fwd(rt), recipe
 
 
-def test_sweep_variants_bitwise_deterministic(grid_of, monkeypatch):
-    """Config 2's shape (L=256, B=64): ten forward calls give the same bits (no racing REDs)."""
+@pytest.mark.parametrize("env,want", [({}, "blocked"), ({"OSPH_SWEEP_BLOCKED": "0"}, "persistent")])
+def test_sweep_variants_bitwise_deterministic(env, want, grid_of, monkeypatch):
+    """Config 2's shape (L=256, B=64): ten forward calls give the same bits (no racing reductions),
+    for the blocked sweep (the default for batches) and the persistent one."""
     import torch
 
+    from paper_1403_4661_b200 import _lib
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     g = grid_of(256)
     rng = np.random.default_rng(3)
     B = 64
     x = torch.from_numpy(rng.standard_normal((B, 256 * 256)) + 1j * rng.standard_normal((B, 256 * 256))).cuda()
-    first = osp.forward_sht_batch(x, g, check=False)
-    plan = osp.get_plan(g, B, 0)
-    assert plan.last_sweep_kind() == "persistent"
+    plan = osp.transform.Plan(g.thetas, B, 0)  # a fresh plan: the sweep is chosen per plan
+    out = [torch.empty_like(x) for _ in range(2)]
+    kind = _lib.OSPH_DEVICE
+    plan.forward_raw(B, x.data_ptr(), out[0].data_ptr(), kind, False)
+    assert plan.last_sweep_kind() == want
     for _ in range(9):
-        again = osp.forward_sht_batch(x, g, check=False)
-        assert torch.equal(again, first)
-    s0 = osp.inverse_sht_batch(x, g)  # the inverse too (short rings fold without atomics)
+        plan.forward_raw(B, x.data_ptr(), out[1].data_ptr(), kind, False)
+        assert torch.equal(out[1], out[0])
+    fw = out[0].clone()
+    plan.inverse_raw(B, x.data_ptr(), out[0].data_ptr(), kind)  # the inverse too (short rings fold without atomics)
     for _ in range(4):
-        assert torch.equal(osp.inverse_sht_batch(x, g), s0)
+        plan.inverse_raw(B, x.data_ptr(), out[1].data_ptr(), kind)
+        assert torch.equal(out[1], out[0])
+    plan.close()
+    if want == "persistent":  # both sweeps solve the same systems: agreement far inside the parity tolerance
+        monkeypatch.delenv("OSPH_SWEEP_BLOCKED")
+        plan2 = osp.transform.Plan(g.thetas, B, 0)
+        plan2.forward_raw(B, x.data_ptr(), out[1].data_ptr(), kind, False)
+        assert plan2.last_sweep_kind() == "blocked"
+        plan2.close()
+        assert (out[1] - fw).abs().max().item() <= 1e-11 * max(1.0, fw.abs().max().item())
 
 
-def test_config3_shape_gemm_sweep(golden, grid_of):
-    """BASELINE configs[2]: 256 real maps at L=512 (128 paired transforms) -> the GEMM sweep.
+@pytest.mark.parametrize("env,want", [({}, "blocked"), ({"OSPH_SWEEP_BLOCKED": "0"}, "gemm")])
+def test_config3_shape_gemm_sweep(env, want, golden, grid_of, monkeypatch):
+    """BASELINE configs[2]: 256 real maps at L=512 (128 paired transforms) -> the blocked sweep
+    (batched GEMM launches per block of orders; default) and the per-order GEMM sweep.
 
     Map 0 is the reference's own L=512 real-recipe map (fixture); every map's
     round trip and a sample of maps against the reference/oracle."""
@@ -193,6 +214,8 @@ def test_config3_shape_gemm_sweep(golden, grid_of):
     d = golden("ref_L512.npz")
     g = grid_of(512)
     L, B = 512, 256
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     rng = np.random.default_rng(31)
     flm = np.empty((B, L * L), dtype=np.complex128)
     flm[0] = d["flm"]
@@ -206,7 +229,7 @@ def test_config3_shape_gemm_sweep(golden, grid_of):
     assert np.abs(s[0] - d["samples"]).max() <= 1e-12 * max(1.0, np.abs(d["samples"]).max())
     f = np.empty_like(flm)
     plan.forward_raw(B, s.ctypes.data, f.ctypes.data, _lib.OSPH_HOST | _lib.OSPH_REAL, True)
-    assert plan.last_sweep_kind() == "gemm"
+    assert plan.last_sweep_kind() == want
     plan.close()
     rt = np.abs(d["fwd"] - d["flm"]).max()
     assert np.abs(f[0] - d["fwd"]).max() <= tol_fwd(rt)
@@ -228,7 +251,7 @@ def test_config3_shape_without_gemm_sweep(grid_of, monkeypatch):
     s = osp.inverse_sht_batch(flm, g, real=True)
     ref, kind0 = _fresh_forward(g, s, real=True)
     f, kind = _fresh_forward(g, s, real=True, env={"OSPH_SWEEP_NO_GEMM": "1"}, monkeypatch=monkeypatch)
-    assert kind0 == "gemm" and kind == "persistent"
+    assert kind0 == "blocked" and kind == "persistent"
     assert np.abs(f - flm).max() <= 1e-11
     assert np.abs(f - ref).max() <= 1e-12
 
