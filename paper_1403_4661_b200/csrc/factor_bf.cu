@@ -631,52 +631,70 @@ template <int J>
 __device__ __forceinline__ void bf_couple_rows(int L, int m, const double* __restrict__ Xt,
                                                const double* __restrict__ Pb, const double* __restrict__ w,
                                                double* __restrict__ Ut, double* pbs) {
+  // 128 threads = 32 columns x 4 row quarters: thread (column, quarter h) sums the 8-row
+  // pieces it = h, h + 4, ... of its column (next piece prefetched); the quarters are added
+  // in a fixed order by shuffles.
   const int n = L - m, nrt = (n + 7) >> 3, nrtpb = (m + 7) >> 3;
   const int JJ = min(J, m);
-  const int cn = blockIdx.x * 128 + threadIdx.x;
+  const int cl = threadIdx.x >> 2, h = threadIdx.x & 3;
+  const int cn = blockIdx.x * 32 + cl;
+  const bool colok = cn < n;
   double acc[J];
 #pragma unroll
   for (int r = 0; r < J; ++r) acc[r] = 0.0;
-  const double* xcol = cn == 0 ? w : Xt + ((int64_t)(cn >> 5) * nrt << 8) + ((cn & 31) << 3);
-  const int xstride = cn == 0 ? 8 : 256;  // doubles between consecutive 8-row pieces
+  const double* xcol = Xt + ((int64_t)(cn >> 5) * nrt << 8) + ((cn & 31) << 3);
+  auto fetch = [&](int it, double (&x)[8]) {  // rows 8 it .. 8 it + 7 of column cn
+    if (!colok || it >= nrt) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[q] = 0.0;
+    } else if (cn == 0) {  // the late ring's column is zero in the tiles: it is w_m (not padded)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[q] = (8 * it + q < n) ? __ldcg(w + 8 * it + q) : 0.0;
+    } else {  // rows past n are zero in the tiles
+#pragma unroll
+      for (int q = 0; q < 8; q += 2) {
+        const double2 v = __ldcg(reinterpret_cast<const double2*>(xcol + (int64_t)it * 256 + q));
+        x[q] = v.x;
+        x[q + 1] = v.y;
+      }
+    }
+  };
   for (int i0 = 0; i0 < n; i0 += 128) {
     __syncthreads();
     for (int idx = threadIdx.x; idx < 128 * J; idx += 128) {  // pbs[i][r] = Pb[m-1-r, i0 + i]
       const int r = idx % J, i = idx / J;
-      pbs[idx] = (r < JJ && i0 + i < n) ? __ldcg(Pb + tile_index(m - 1 - r, i0 + i, nrtpb)) : 0.0;
+      // two doubles of padding per 8-row piece: the four quarters of a warp read different banks
+      pbs[idx + 2 * (i >> 3)] = (r < JJ && i0 + i < n) ? __ldcg(Pb + tile_index(m - 1 - r, i0 + i, nrtpb)) : 0.0;
     }
     __syncthreads();
-    if (cn < n) {
-      const int imax = min(128, n - i0);
-      for (int i8 = 0; i8 < imax; i8 += 8) {
-        const double* xp = xcol + (int64_t)((i0 + i8) >> 3) * xstride;
-        double x[8];
-        if (cn == 0) {  // w_m is not padded
+    double xn[8];
+    fetch((i0 >> 3) + h, xn);
+#pragma unroll 1
+    for (int t = h; t < 16; t += 4) {  // 16 pieces of 8 rows per 128-row chunk
+      double x[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) x[q] = (i0 + i8 + q < n) ? __ldcg(xp + q) : 0.0;
-        } else {  // rows past n are zero in the tiles
+      for (int q = 0; q < 8; ++q) x[q] = xn[q];
+      fetch((i0 >> 3) + t + 4, xn);  // the first piece of the next chunk is fetched again there
 #pragma unroll
-          for (int q = 0; q < 8; q += 2) {
-            const double2 v = __ldcg(reinterpret_cast<const double2*>(xp + q));
-            x[q] = v.x;
-            x[q + 1] = v.y;
-          }
-        }
+      for (int q = 0; q < 8; ++q) {
+        const double* pr = pbs + (8 * t + q) * J + 2 * t;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const double xv = x[q];
-          const double* pr = pbs + (i8 + q) * J;
-#pragma unroll
-          for (int r = 0; r < J; r += 2) {
-            const double2 pv = *reinterpret_cast<const double2*>(pr + r);
-            acc[r] = fma(pv.x, xv, acc[r]);
-            acc[r + 1] = fma(pv.y, xv, acc[r + 1]);
-          }
+        for (int r = 0; r < J; r += 2) {
+          const double2 pv = *reinterpret_cast<const double2*>(pr + r);
+          acc[r] = fma(pv.x, x[q], acc[r]);
+          acc[r + 1] = fma(pv.y, x[q], acc[r + 1]);
         }
       }
     }
   }
-  if (cn < n) {
+#pragma unroll
+  for (int r = 0; r < J; ++r) {  // quarters 0 + 1 + 2 + 3, the same order on every lane
+    const double a1 = __shfl_xor_sync(0xffffffffu, acc[r], 1);
+    const double s01 = (h & 1) ? a1 + acc[r] : acc[r] + a1;
+    const double a2 = __shfl_xor_sync(0xffffffffu, s01, 2);
+    acc[r] = (h & 2) ? a2 + s01 : s01 + a2;
+  }
+  if (colok && h == 0) {
     double* out = Ut + (((int64_t)(cn >> 5) * (J / 8)) << 8) + ((cn & 31) << 3);
 #pragma unroll
     for (int r = 0; r < J; ++r)
@@ -689,9 +707,9 @@ __global__ void __launch_bounds__(128) k_bf_couple(int L, int m_first, const int
                                                    const int64_t* __restrict__ pb_off,
                                                    const double* __restrict__ pbelow, const double* __restrict__ w_all,
                                                    const int64_t* __restrict__ ut_off, double* __restrict__ ut_all) {
-  __shared__ __align__(16) double pbs[128 * OSPH_SB_BLOCK];
+  __shared__ __align__(16) double pbs[128 * OSPH_SB_BLOCK + 32];
   const int m = m_first + blockIdx.y;
-  if (m == 0 || (int)blockIdx.x * 128 >= L - m) return;
+  if (m == 0 || (int)blockIdx.x * 32 >= L - m) return;
   const double* Xt = xt_all + __ldg(xt_off + m);
   const double* Pb = pbelow + __ldg(pb_off + m);
   const double* w = w_all + (size_t)m * uw_ld(L);
@@ -972,7 +990,7 @@ cudaError_t bf_run(osph_plan* p, const BfRange& r, cudaStream_t st, const BfOffs
                                                          o.pb, p->d_pbelow, p->d_u, p->d_w, p->d_beta, p->d_jstar);
   p->launches++;
   if (p->d_ut && !p->windowed && L <= 1024) {  // resident plans: the coupling rows of the blocked sweep
-    k_bf_couple<<<dim3((L - m_first + 127) / 128, cnt_all), 128, 0, st>>>(L, m_first, o.xt, p->d_xt, o.pb, p->d_pbelow,
+    k_bf_couple<<<dim3((L - m_first + 31) / 32, cnt_all), 128, 0, st>>>(L, m_first, o.xt, p->d_xt, o.pb, p->d_pbelow,
                                                                        p->d_w, p->d_ut_off, p->d_ut);
     p->launches++;
   }

@@ -62,10 +62,11 @@ __device__ __forceinline__ void sb_target(int s, int k, int slot, int& tm, int& 
   }
 }
 
-template <int TM, int MAPS>
+template <int TM, int MAPS, bool MERGE = false>
 struct SbStage {
   double a[TM / 8][SB_KC][8];  // row tiles as stored: [k][row % 8]
   double b[MAPS][SB_KC][4];    // [map][k][+re, +im, -re, -im]
+  double b2[MERGE ? MAPS : 1][MERGE ? SB_KC : 1][4];  // MODE 2: the same rows of R2 (merged into R)
 };
 
 // One GEMM per order s = s_top - blockIdx.z of the block, CTA tile TM rows x MAPS maps.
@@ -81,13 +82,13 @@ __global__ void __launch_bounds__(SB_THREADS) k_sb_gemm(int L, int s_top, int m0
                                                         double2* __restrict__ out, double2* __restrict__ flm) {
   pdl_start();
   extern __shared__ __align__(16) unsigned char sb_raw[];
-  using Stage = SbStage<TM, MAPS>;
+  using Stage = SbStage<TM, MAPS, MODE == 2>;
   Stage* st = reinterpret_cast<Stage*>(sb_raw);
   const int z = blockIdx.z, s = s_top - z;
   const int n = L - s;
   const int M = MODE == 0 ? n : MODE == 1 ? s : min(sb_rows(s), s);  // output rows
   const int rt0 = blockIdx.x * (TM / 8);                            // first 8-row tile
-  if (rt0 * 8 >= M) return;
+  if (rt0 * 8 >= M && !(MODE == 2 && rt0 == 0)) return;  // MODE 2 also merges R2 into R: every order's rows
   const int nrt = MODE == 0 ? (n + 7) >> 3 : MODE == 1 ? (s + 7) >> 3 : sb_rows(s) >> 3;
   const int b0 = blockIdx.y * MAPS;
   const double* A = atiles + __ldg(a_off + s);
@@ -110,11 +111,13 @@ __global__ void __launch_bounds__(SB_THREADS) k_sb_gemm(int L, int s_top, int m0
       const int kk = c * SB_KC + k, b = b0 + mp;
       double* dst = &S.b[mp][k][2 * slot];
       if (kk < n && b < B) {
-        const double2* src = MODE == 1 ? xz + ((int64_t)b * 2 + slot) * L + kk
-                                       : R + ((int64_t)b * npos + p0 + kk) * 2 + slot;
+        const int64_t ri = ((int64_t)b * npos + p0 + kk) * 2 + slot;
+        const double2* src = MODE == 1 ? xz + ((int64_t)b * 2 + slot) * L + kk : R + ri;
         sb_cp16(dst, src);
+        if (MODE == 2) sb_cp16(&S.b2[mp][k][2 * slot], R2 + ri);
       } else {
         *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+        if (MODE == 2) *reinterpret_cast<double2*>(&S.b2[mp][k][2 * slot]) = make_double2(0.0, 0.0);
       }
     }
     sb_commit();
@@ -140,7 +143,26 @@ __global__ void __launch_bounds__(SB_THREADS) k_sb_gemm(int L, int s_top, int m0
     __syncthreads();  // chunk c visible to all; stage (c - 1) % NS free
     if (c + NS - 1 < nch) load((c + NS - 1) % NS, c + NS - 1);
     else sb_commit();
-    const Stage& S = st[c % NS];
+    Stage& S = st[c % NS];
+    if (MODE == 2) {
+      // The opposite-tone corrections of the blocks above wait in R2 (k_sb_gemm<1>): this
+      // launch visits every right-hand-side row of the block exactly once (grid.x = 1), so it
+      // adds them in -- R += R2, R2 = 0 in global memory for the solve that follows, and in
+      // the staged operand for its own products.
+      for (int i = tid; i < MAPS * SB_KC * 2; i += SB_THREADS) {
+        const int mp = i / (SB_KC * 2), rem = i % (SB_KC * 2), k = rem >> 1, slot = rem & 1;
+        const double2 v2 = *reinterpret_cast<const double2*>(&S.b2[mp][k][2 * slot]);
+        if (v2.x != 0.0 || v2.y != 0.0) {
+          double2* bp = reinterpret_cast<double2*>(&S.b[mp][k][2 * slot]);
+          const double2 v = make_double2(bp->x + v2.x, bp->y + v2.y);
+          *bp = v;
+          const int64_t ri = ((int64_t)(b0 + mp) * npos + p0 + c * SB_KC + k) * 2 + slot;
+          R[ri] = v;
+          R2[ri] = make_double2(0.0, 0.0);
+        }
+      }
+      __syncthreads();
+    }
 #pragma unroll
     for (int k0 = 0; k0 < SB_KC; k0 += 4) {
       double a[RB], b[2];
@@ -348,12 +370,13 @@ __global__ void __launch_bounds__(SB_THREADS) k_sb_chain(int L, int s_top, int m
 //  * the last blockIdx.y: the corrections the PREVIOUS block (orders pm0 .. ps_top) sent
 //    through the short rings k < 16 (several sources can meet in one bin there), gathered
 //    per target (tm <= k, tone) in descending source order, + tone before - tone.
-__global__ void __launch_bounds__(256) k_sb_combine(int L, int s_top, int m0, int ps_top, int pm0, int B,
+__global__ void __launch_bounds__(256) k_sb_combine(int L, int s_top, int m0, int ps_top, int pm0, int B, int nstream,
                                                     const double2* __restrict__ G16, double2* __restrict__ R,
                                                     double2* __restrict__ R2) {
   pdl_start();
   const int64_t npos = (int64_t)L * (L + 1) / 2;
-  if ((int)blockIdx.y < B) {  // map blockIdx.y: R += R2 over the block's rows
+  if ((int)blockIdx.y < nstream) {  // map blockIdx.y: R += R2 over the block's rows (nstream = B for one-order
+                                    // blocks only: otherwise the coupling launch k_sb_gemm<2> merges them)
     const int64_t p_lo = packed_pos(L, m0, 0) * 2, per = packed_pos(L, s_top + 1, 0) * 2 - p_lo;
     double2* rp = R + (int64_t)blockIdx.y * npos * 2 + p_lo;
     double2* r2 = R2 + (int64_t)blockIdx.y * npos * 2 + p_lo;
@@ -373,8 +396,8 @@ __global__ void __launch_bounds__(256) k_sb_combine(int L, int s_top, int m0, in
   // order (descending source order, + tone before - tone).
   constexpr int NT = (SB_B / 2) * (SB_B / 2 + 1) / 2 * 2;
   const int lane = threadIdx.x & 31;
-  const int64_t gblock = (int64_t)(blockIdx.y - B) * gridDim.x + blockIdx.x;  // gather blocks: rows B.. of the grid
-  const int64_t gblocks = (int64_t)(gridDim.y - B) * gridDim.x;
+  const int64_t gblock = (int64_t)(blockIdx.y - nstream) * gridDim.x + blockIdx.x;  // gather blocks: the grid's last rows
+  const int64_t gblocks = (int64_t)(gridDim.y - nstream) * gridDim.x;
   for (int64_t w = (gblock * blockDim.x + threadIdx.x) >> 5; w < (int64_t)NT * B; w += (gblocks * blockDim.x) >> 5) {
     const int b = (int)(w % B);
     int tt = (int)(w / B);
@@ -388,26 +411,30 @@ __global__ void __launch_bounds__(256) k_sb_combine(int L, int s_top, int m0, in
     const int tm = tt, nk = 2 * k + 1;
     if (tm >= pm0) continue;  // inside the previous block: resolved by its recurrence (warp-uniform)
     const int s = ps_top - lane;
-    double2 g[2] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0)};
+    // each source order sends at most one of its tones to this target (the + tone comes first
+    // in the reference's order, but the two never meet in one bin of the same source)
+    double2 g = make_double2(0.0, 0.0);
+    bool hit = false;
     if (s >= pm0 && s > k) {
       const int rr = s % nk;
       const bool same = rr <= k;
       const int stm = same ? rr : nk - rr;
       if (stm == tm) {
         const int slot = same ? ts : ts ^ 1;  // the tone of source s that lands on tone ts
-        g[slot] = __ldcg(G16 + (((int64_t)lane * (SB_B / 2) + k) * B + b) * 2 + slot);
+        g = __ldcg(G16 + (((int64_t)lane * (SB_B / 2) + k) * B + b) * 2 + slot);
+        hit = true;
       }
     }
+    unsigned mask = __ballot_sync(0xffffffffu, hit);
+    const bool any = mask != 0;
     double ax = 0.0, ay = 0.0;
-#pragma unroll
-    for (int src = 0; src < 32; ++src) {
-#pragma unroll
-      for (int slot = 0; slot < 2; ++slot) {
-        ax += __shfl_sync(0xffffffffu, g[slot].x, src);
-        ay += __shfl_sync(0xffffffffu, g[slot].y, src);
-      }
+    while (mask) {  // ascending lanes = descending source orders
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      ax += __shfl_sync(0xffffffffu, g.x, src);
+      ay += __shfl_sync(0xffffffffu, g.y, src);
     }
-    if (lane == 0 && (ax != 0.0 || ay != 0.0)) {
+    if (lane == 0 && any) {
       double2* rp = R + ((int64_t)b * npos + packed_pos(L, tm, k - tm)) * 2 + ts;
       const double2 r = *rp;
       *rp = make_double2(r.x - ax, r.y - ay);
@@ -449,7 +476,7 @@ static cudaError_t sweep_blocked_run(osph_plan* p, int B, double2* flm) {
   auto k_solve = k_sb_gemm<0, NS, TM, MAPS>;
   auto k_corr = k_sb_gemm<1, NS, TM, MAPS>;
   auto k_cpl = k_sb_gemm<2, 4, 32, 8>;  // at most 32 coupling rows per order: 32 x 8 maps per CTA
-  const size_t smem_cpl = 4 * sizeof(SbStage<32, 8>);
+  const size_t smem_cpl = 4 * sizeof(SbStage<32, 8, true>);
   if ((e = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess ||
       (e = cudaFuncSetAttribute(k_corr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess ||
       (e = cudaFuncSetAttribute(k_cpl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cpl)) != cudaSuccess)
@@ -475,7 +502,8 @@ static cudaError_t sweep_blocked_run(osph_plan* p, int B, double2* flm) {
       const int64_t per = (packed_pos(L, s_top + 1, 0) - packed_pos(L, m0, 0)) * 2;
       const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((per + 255) / 256, 32));
       const int gy = (272 * B / 8 + gx - 1) / gx;  // one warp per short-ring target (272 per map)
-      if ((e = launch_pdl(k_sb_combine, dim3(gx, B + gy), dim3(256), 0, st, L, s_top, m0, ps_top, pm0, B,
+      const int nstream = nb > 1 ? 0 : B;
+      if ((e = launch_pdl(k_sb_combine, dim3(gx, nstream + gy), dim3(256), 0, st, L, s_top, m0, ps_top, pm0, B, nstream,
                           (const double2*)p->d_sb_g, p->d_r, p->d_sb_r2)) != cudaSuccess)
         return e;
       p->launches++;
@@ -524,5 +552,7 @@ cudaError_t launch_sweep_blocked(osph_plan* p, int B, double2* flm) {
   static const int tile = getenv("OSPH_SB_TILE") ? atoi(getenv("OSPH_SB_TILE")) : 0;
   if (tile == 1) return sweep_blocked_run<4, 64, 4>(p, B, flm);
   if (tile == 2) return sweep_blocked_run<3, 128, 8>(p, B, flm);
+  if (tile == 3) return sweep_blocked_run<3, 128, 16>(p, B, flm);
+  if (tile == 4) return sweep_blocked_run<4, 64, 16>(p, B, flm);
   return sweep_blocked_run<4, 64, 8>(p, B, flm);
 }
