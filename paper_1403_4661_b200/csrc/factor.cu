@@ -17,6 +17,7 @@
 // (calibrated on the interleaved L=256 grid: gelsy first reports rank
 // deficiency at m=220 where this estimate is 3.0e14; m=221 gives 1.9e14).
 #include <algorithm>
+#include <cstdlib>
 
 #include "plan.cuh"
 
@@ -38,6 +39,15 @@ cudaError_t launch_kappa(osph_plan* p, cudaStream_t st) {
 
 // Every order in one breadth-first pass on `st` (the resident, non-windowed
 // forward; the windowed one runs bf_run per window in window.cu).
+//
+// Split (unsharded plans, L >= 128; OSPH_FACTOR_SPLIT=0 disables): the chain of
+// panel steps is latency-bound, and the orders >= L/2 (blocks of at most L/2
+// rows, ~6% of the flops, half of the panel steps) are the first the sweep
+// needs.  They run as their own range on a second stream beside the low
+// orders; `ev_fa` marks them done, so the blocked sweep starts on the high
+// orders while the low ones are still being factored.  `st` joins the second
+// stream before returning, so an event recorded on `st` after this call still
+// covers every order.
 cudaError_t launch_factor(osph_plan* p, cudaStream_t st) {
   const int L = p->L;
   cudaError_t e;
@@ -46,6 +56,28 @@ cudaError_t launch_factor(osph_plan* p, cudaStream_t st) {
   if ((e = cudaMemsetAsync(p->d_status, 0, sizeof(int) * L, st)) != cudaSuccess) return e;
   int lo, hi;
   own_orders(p, lo, hi);  // all orders, or this shard's block (OSPH_SHARD_FACTORS)
+  static const bool split_off = getenv("OSPH_FACTOR_SPLIT") && atoi(getenv("OSPH_FACTOR_SPLIT")) == 0;
+  p->fsplit_active = false;
+  p->sweep_late_ev = nullptr;
+  if (!split_off && !p->shard_mode && !p->windowed && lo == 0 && hi == L - 1 && L >= 128 && p->s_fa) {
+    const int split = ((L / 2) / OSPH_SB_BLOCK) * OSPH_SB_BLOCK;  // a block boundary of the blocked sweep
+    if (p->fsplit_m != split) {
+      if ((e = bf_prepare(p, split, L - 1, &p->bf_hi)) != cudaSuccess) return e;
+      if ((e = bf_prepare(p, 0, split - 1, &p->bf_lo)) != cudaSuccess) return e;
+      p->bf_hi.dbuf = p->d_bf_d + bf_diag_doubles(split);  // disjoint diagonal-block scratch
+      p->bf_lo.dbuf = p->d_bf_d;
+      p->fsplit_m = split;
+    }
+    const BfOffsets o{p->d_ainv_off, p->d_xt_off, p->d_pb_off, p->d_bf_off};
+    if ((e = cudaEventRecord(p->ev_fstart, st)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(p->s_fa, p->ev_fstart, 0)) != cudaSuccess) return e;
+    if ((e = bf_run(p, p->bf_hi, p->s_fa, o)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(p->ev_fa, p->s_fa)) != cudaSuccess) return e;
+    if ((e = bf_run(p, p->bf_lo, st, o)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(st, p->ev_fa, 0)) != cudaSuccess) return e;
+    p->fsplit_active = true;
+    return launch_kappa(p, st);
+  }
   if ((e = launch_factor_bf(p, lo, hi, st)) != cudaSuccess) return e;
   return launch_kappa(p, st);
 }

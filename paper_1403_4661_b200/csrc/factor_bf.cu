@@ -863,9 +863,9 @@ cudaError_t bf_step(osph_plan* p, const BfRange& r, int sidx, cudaStream_t st, c
     k_bf_rcopy<<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, rcur, o.bf);
     p->launches++;
   }
-  k_bf_diag_rows<<<d.cnt, 64, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_status);
+  k_bf_diag_rows<<<d.cnt, 64, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, (r.dbuf ? r.dbuf : p->d_bf_d), p->d_status);
   k_bf_panel_mma<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, r.d_tab + d.pre_panel, d.cnt, o.ainv,
-                                                     p->d_ainv, p->d_bf_d, p->d_bf_e, o.bf, rnext);
+                                                     p->d_ainv, (r.dbuf ? r.dbuf : p->d_bf_d), p->d_bf_e, o.bf, rnext);
   p->launches += 2;
   BfUpdArgs ua{L, m_first, j0, nullptr, d.cnt, o.ainv, p->d_ainv, p->d_bf_e, rcur, o.bf, rnext, nullptr, nullptr,
                -1, -1};
@@ -905,9 +905,9 @@ static cudaError_t bf_pair_step(osph_plan* p, const BfRange& r, int ps, cudaStre
   const int* tab = r.d_tab;
   const dim3 dgrid(d.cnt, (L - m_first + BF_RCHUNK - 1) / BF_RCHUNK);
   k_bf_rcopy<<<dgrid, BF_THREADS, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, R1, o.bf);                // 1
-  k_bf_diag_rows<<<d.cnt, 64, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, p->d_bf_d, p->d_status);     // 2
+  k_bf_diag_rows<<<d.cnt, 64, 0, st>>>(L, m_first, j0, o.ainv, p->d_ainv, (r.dbuf ? r.dbuf : p->d_bf_d), p->d_status);     // 2
   k_bf_panel_mma<<<d.n_panel, BF_THREADS, sm2, st>>>(L, m_first, j0, tab + d.pre_panel, d.cnt, o.ainv,  // 3
-                                                     p->d_ainv, p->d_bf_d, p->d_bf_e, o.bf, d.cnt2 ? R2 : nullptr);
+                                                     p->d_ainv, (r.dbuf ? r.dbuf : p->d_bf_d), p->d_bf_e, o.bf, d.cnt2 ? R2 : nullptr);
   p->launches += 3;
   if (d.cnt2 > 0) {
     BfUpdArgs u{L, m_first, j0, tab + d.pre_panel, d.cnt2, o.ainv, p->d_ainv, p->d_bf_e, R1, o.bf, nullptr,
@@ -918,9 +918,9 @@ static cudaError_t bf_pair_step(osph_plan* p, const BfRange& r, int ps, cudaStre
     u.rt_fixed = jt + 1;
     u.rnext = R2;
     if (d.n_row > 0) k_bf_update<false><<<d.n_row, BF_THREADS, sm2, st>>>(u);  // 5
-    k_bf_diag_rows<<<d.cnt2, 64, 0, st>>>(L, m_first, j0 + BF_NB, o.ainv, p->d_ainv, p->d_bf_d, p->d_status);  // 6
+    k_bf_diag_rows<<<d.cnt2, 64, 0, st>>>(L, m_first, j0 + BF_NB, o.ainv, p->d_ainv, (r.dbuf ? r.dbuf : p->d_bf_d), p->d_status);  // 6
     k_bf_panel_mma<<<d.n_panel2, BF_THREADS, sm2, st>>>(L, m_first, j0 + BF_NB, tab + d.pre_panel, d.cnt2,     // 7
-                                                        o.ainv, p->d_ainv, p->d_bf_d, p->d_bf_e2, o.bf, nullptr);
+                                                        o.ainv, p->d_ainv, (r.dbuf ? r.dbuf : p->d_bf_d), p->d_bf_e2, o.bf, nullptr);
     BfUpdArgs v{L, m_first, j0 + BF_NB, tab + d.pre_panel, d.cnt2, o.ainv, p->d_ainv, p->d_bf_e2, R2, o.bf,
                 nullptr, nullptr, nullptr, -1, jt};
     k_bf_update<false><<<d.n_panel2, BF_THREADS, sm2, st>>>(v);  // 8

@@ -70,6 +70,12 @@ void plan_free(osph_plan* p) {
   if (p->ev_out) cudaEventDestroy(p->ev_out);
   if (p->ev_sweep_done) cudaEventDestroy(p->ev_sweep_done);
   if (p->s_in) cudaStreamDestroy(p->s_in);
+  if (p->s_fa) cudaStreamDestroy(p->s_fa);
+  if (p->ev_fstart) cudaEventDestroy(p->ev_fstart);
+  if (p->ev_fa) cudaEventDestroy(p->ev_fa);
+  cudaFree(p->bf_full.d_tab);
+  cudaFree(p->bf_hi.d_tab);
+  cudaFree(p->bf_lo.d_tab);
   if (p->s_out) cudaStreamDestroy(p->s_out);
   cudaFree(p->d_z1);
   cudaFree(p->d_z2);
@@ -161,6 +167,9 @@ int plan_create_one(int L, const double* thetas, int max_batch, int device, osph
   if (getenv("OSPH_NO_STREAM_PRIORITY")) prio_hi = prio_lo;
   PLAN_TRY(cudaStreamCreateWithPriority(&p->s_in, cudaStreamNonBlocking, prio_hi));
   PLAN_TRY(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
+  PLAN_TRY(cudaStreamCreateWithPriority(&p->s_fa, cudaStreamNonBlocking, prio_hi));
+  PLAN_TRY(cudaEventCreateWithFlags(&p->ev_fstart, cudaEventDisableTiming));
+  PLAN_TRY(cudaEventCreateWithFlags(&p->ev_fa, cudaEventDisableTiming));
   for (int c = 0; c < osph_plan::kIoChunks; ++c) {
     PLAN_TRY(cudaEventCreateWithFlags(&p->ev_in[c], cudaEventDisableTiming));
     PLAN_TRY(cudaEventCreateWithFlags(&p->ev_done[c], cudaEventDisableTiming));
@@ -417,6 +426,20 @@ __global__ void k_unpair_flm(int B, int L, const double2* __restrict__ z, double
   }
 }
 
+// The sweep on `st` waits for the factorisation, recorded as ev[7] on a side stream.  The
+// blocked sweep of a split factorisation (factor.cu) waits only for the high orders now and
+// for the rest at its first block below the split (launch_sweep_blocked).
+static cudaError_t wait_factor_for_sweep(osph_plan* p, cudaStream_t st) {
+  p->sweep_late_ev = nullptr;
+  if (p->fsplit_active && p->sweep_blocked) {
+    cudaError_t e = cudaStreamWaitEvent(st, p->ev_fa, 0);
+    p->sweep_late_ev = p->ev[7];
+    p->sweep_late_m = p->fsplit_m;
+    return e;
+  }
+  return cudaStreamWaitEvent(st, p->ev[7], 0);
+}
+
 static int ensure_real(osph_plan* p) {
   if (p->d_z1) return OSPH_OK;
   const size_t n = (size_t)((p->max_batch + 1) / 2) * p->L * p->L;
@@ -487,7 +510,8 @@ static int forward_real(osph_plan* p, int B, const void* samples, void* flm, boo
   CUDA_TRY(cudaEventRecord(p->ev[4], st));
   CUDA_TRY(launch_ring_forward(p, Bp, p->d_z1));
   CUDA_TRY(cudaEventRecord(p->ev[5], st));
-  CUDA_TRY(cudaStreamWaitEvent(st, p->ev[7], 0));
+  if (p->windowed) CUDA_TRY(cudaStreamWaitEvent(st, p->ev[7], 0));
+  else CUDA_TRY(wait_factor_for_sweep(p, st));
   CUDA_TRY(cudaEventRecord(p->ev[8], st));
   if (p->windowed) CUDA_TRY(forward_windows(p, Bp, p->d_z2));
   else CUDA_TRY(launch_sweep(p, Bp, p->d_z2));
@@ -647,7 +671,7 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
     CUDA_TRY(cudaEventRecord(p->ev[4], st));
     CUDA_TRY(launch_ring_forward(p, B, (const double2*)samples));
     CUDA_TRY(cudaEventRecord(p->ev[5], st));
-    if (!inline_factor) CUDA_TRY(cudaStreamWaitEvent(st, p->ev[7], 0));
+    if (!inline_factor) CUDA_TRY(wait_factor_for_sweep(p, st));
   } else {
     // the factorisation needs no data: it runs while the samples are copied in,
     // and each chunk's ring DFTs start as soon as the chunk has landed

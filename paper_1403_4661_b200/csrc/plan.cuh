@@ -21,6 +21,7 @@ struct BfRange {  // work-item tables of one range of orders (factor_bf.cu)
   std::vector<BfStep> steps;
   std::vector<BfPairStep> psteps;
   int* d_tab = nullptr;
+  double* dbuf = nullptr;  // this range's diagonal-block inverses (nullptr: the plan's d_bf_d)
 };
 struct BfOffsets {  // per-order offsets (indexed by m) into the factor buffers
   const int64_t* ainv;
@@ -151,6 +152,16 @@ struct osph_plan {
   bool inv_ready = false;        // inverse buffers allocated
   // breadth-first factorisation (factor_bf.cu) of every order
   BfRange bf_full;               // the non-windowed range (every order)
+  // Split factorisation (factor.cu): orders >= fsplit_m on their own stream beside the rest, so the
+  // blocked sweep can start on the high orders (cheap to factor, first to be swept) while the low
+  // orders are still being factored.
+  BfRange bf_hi, bf_lo;
+  int fsplit_m = 0;              // 0: not split
+  cudaStream_t s_fa = nullptr;
+  cudaEvent_t ev_fstart = nullptr, ev_fa = nullptr;  // split start / high orders done
+  bool fsplit_active = false;    // the last launch_factor ran split
+  cudaEvent_t sweep_late_ev = nullptr;  // blocked sweep: wait for this event before the first block
+  int sweep_late_m = 0;                 //   that reaches below this order
   int num_sms = 0;
   bool need_norms = true;        // this call checks conditioning (check=True): factor kernels accumulate norms
   int64_t* d_bf_off = nullptr;   // [L+1] offsets of the E / R panels (NB x lde(n) per order)

@@ -498,6 +498,10 @@ static cudaError_t sweep_blocked_run(osph_plan* p, int B, double2* flm) {
     const int m0 = (s_top / SB_B) * SB_B;  // blocks start at multiples of 32
     const int nb = s_top - m0 + 1;
     const bool last = m0 == 0;
+    if (p->sweep_late_ev && m0 < p->sweep_late_m) {  // the low orders' factors (split factorisation)
+      if ((e = cudaStreamWaitEvent(st, p->sweep_late_ev, 0)) != cudaSuccess) return e;
+      p->sweep_late_ev = nullptr;
+    }
     if (ps_top >= 0) {  // corrections of the blocks above that were not reduced into R directly
       const int64_t per = (packed_pos(L, s_top + 1, 0) - packed_pos(L, m0, 0)) * 2;
       const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((per + 255) / 256, 32));
