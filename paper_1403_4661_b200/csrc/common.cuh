@@ -23,7 +23,7 @@
 #define OSPH_SW_GLOBAL 16384  // global per-stage twiddle table: spans up to 4096 (N <= 16384)
 // Bluestein FFTs of up to OSPH_REG_FFT_MAX points run register-resident (fft_reg.cuh);
 // OSPH_RTW_SIZE: entries of their inter-pass twiddle tables (tables.cu k_reg_twiddles)
-#define OSPH_REG_FFT_MAX 1024
+#define OSPH_REG_FFT_MAX 2048  // 2048 = two 1024-point convolutions (even / odd bins)
 #define OSPH_RTW_SIZE 1872
 
 // Position of (order m, ring/degree offset i) in order-major packed storage:

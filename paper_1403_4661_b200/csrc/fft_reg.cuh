@@ -116,10 +116,13 @@ struct RegConv {
   // matrix; TW[k1 LD + n2] = e^{-2 pi i k1 n2 / N}; H[k]: kernel spectrum,
   // natural order (any 1/N factor folded in), in shared memory like TW.  All
   // lanes of the warp call it.
+  // FULL: the input fills all N1 registers and every output is produced (the
+  // two half-size convolutions of a 2N-point Bluestein ring, ringdft.cu).
+  template <bool FULL = false>
   __device__ static __forceinline__ void run(double2 (&v)[N1], double2* Y, const double2* TW, const double2* H,
                                             int tid) {
     constexpr int L1 = rf_log2(N1), L2 = rf_log2(N2);
-    rf_dif<N1, false, true>(v);
+    rf_dif<N1, false, !FULL>(v);
 #pragma unroll
     for (int i = 0; i < N1; ++i) {
       const int k1 = rf_brev(i, L1);
@@ -142,6 +145,6 @@ struct RegConv {
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < N1; ++i) v[i] = Y[rf_brev(i, L1) * LD + tid];
-    rf_dit<N1, true, true>(v);
+    rf_dit<N1, true, !FULL>(v);
   }
 };

@@ -218,7 +218,10 @@ int plan_create_one(int L, const double* thetas, int max_batch, int device, osph
   }
   if (!p->dft_ok) p->n_bluestein_rings = p->n_big_rings = 0;  // Legendre tables only (osph_legendre_block)
   for (int k : brings)
-    if (p->dft_ok && p->h_fft_n[k] <= p->reg_fft_max) p->n_reg_rings++;
+    if (p->dft_ok && p->h_fft_n[k] <= p->reg_fft_max) {
+      p->n_reg_rings++;
+      if (p->h_fft_n[k] == 2048) p->n_reg2_rings++;
+    }
   // the inverse produces every ring until osph_plan_shard restricts it
   p->inv_nr = L;
   p->d_inv_ring_order = p->d_ring_order;
@@ -226,6 +229,7 @@ int plan_create_one(int L, const double* thetas, int max_batch, int device, osph
   p->inv_n_bluestein = p->n_bluestein_rings;
   p->inv_n_big = p->n_big_rings;
   p->inv_n_reg = p->n_reg_rings;
+  p->inv_n_reg2 = p->n_reg2_rings;
   p->inv_direct_lo = 0;
   p->inv_direct_hi = p->n_direct_rings;
   p->own_k_lo = 0;

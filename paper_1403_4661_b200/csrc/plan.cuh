@@ -90,6 +90,7 @@ struct osph_plan {
   int reg_fft_max = 0;       // rings with fft_n <= this run the register-resident kernels (kernel spectra in natural order)
   int n_reg_rings = 0;       // how many: the LAST n_reg_rings entries of d_bluestein_rings (sorted largest first)
   int inv_n_reg = 0;         // the same count for d_inv_bluestein
+  int n_reg2_rings = 0, inv_n_reg2 = 0;  // of those, the 2048-point rings (they lead the register-resident ones)
   bool dft_ok = true;  // every ring's Bluestein FFT fits one CTA (else: tables-only plan)
   // rings the INVERSE produces: all of them, or a chain shard's contiguous range
   // [own_k_lo, own_k_hi) (osph_plan_shard); the forward ring DFTs always cover all rings

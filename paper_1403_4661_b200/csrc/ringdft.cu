@@ -427,6 +427,158 @@ __device__ __forceinline__ void ring_inverse_reg(int L, int B, int k, int b_firs
   }
 }
 
+// FFT size 2048 (rings 513 <= n <= 1023): the input is zero beyond n < 1024, so the first
+// DIF stage splits the 2048-point transform into two 1024-point ones without any
+// arithmetic on the upper half -- even bins: FFT_1024(a), odd bins: FFT_1024(a W_2048^t) --
+// and the last DIT stage needs y_t = E_t + conj(W_2048^t) O_t for t < n only.  A PAIR of
+// warps owns one map's ring: warp 0 convolves a with the even half of the kernel spectrum,
+// warp 1 convolves a W^t with the odd half, applies conj(W^t) and hands its half over
+// through its exchange matrix.  Shared memory: [TW: RS][chirp: 1024][one matrix per warp];
+// the kernel spectrum halves (16 KB each, shared by every map) are read through L1.
+// tw16k[j] = e^{-2 pi i j / 16384}, so W_2048^t = tw16k[8 t].
+__device__ __forceinline__ void reg_pair_sync(int pair) {  // REG_WARPS = 4: two pairs, barriers 1 and 2
+  if (pair == 0) asm volatile("bar.sync 1, 64;\n" ::: "memory");
+  else asm volatile("bar.sync 2, 64;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void ring_inverse_reg2(int L, int B, int k, int b_first, int b_last, double2* sm,
+                                                  const double2* __restrict__ chirp, const double2* __restrict__ bh,
+                                                  const double2* __restrict__ rtw, const double2* __restrict__ tw16k,
+                                                  const double* __restrict__ G, double2* __restrict__ samples) {
+  using C = RegConv<32, 32>;
+  const int n = 2 * k + 1;
+  const int nwarps = blockDim.x >> 5, gmax = nwarps >> 1;  // maps per block iteration
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, pair = warp >> 1, half = warp & 1;
+  double2* tw = sm;
+  double2* cs = sm + C::RS;
+  double2* ys = sm + C::RS + 1024;
+  for (int i = threadIdx.x; i < C::RS; i += blockDim.x) tw[i] = __ldg(rtw + reg_rtw_offset(1024) + i);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) cs[i] = __ldg(chirp + i);
+  double2* YA = ys + C::RS * (2 * pair);      // P sums (fold), then warp 0's exchange matrix
+  double2* YB = ys + C::RS * (2 * pair + 1);  // M sums (fold), then warp 1's exchange matrix
+  double2* Y = half ? YB : YA;
+  const double2* H = bh + half * 1024;  // even / odd bins of the inverse-direction kernel spectrum
+  const int nres = min(n, L);
+  const int64_t mstride = (int64_t)L * 4 * B;
+  for (int b0 = b_first; b0 < b_last; b0 += gmax) {
+    const int Gr = min(gmax, b_last - b0);
+    const double* gbase = G + ((int64_t)k * 4 * B + 4 * b0);
+    for (int idx = threadIdx.x; idx < Gr * nres; idx += blockDim.x) {  // fold as ring_inverse_reg: P and M sums
+      const int gg = idx % Gr, t = idx / Gr;
+      double pr = 0.0, pi = 0.0, mr = 0.0, mi = 0.0;
+      for (int m = t; m < L; m += n) {
+        const double4 q = ldg_f64x4(gbase + 4 * gg + m * mstride);
+        pr += q.x;
+        pi += q.y;
+        if (m > 0) {
+          mr += (m & 1) ? -q.z : q.z;
+          mi += (m & 1) ? -q.w : q.w;
+        }
+      }
+      ys[C::RS * (2 * gg) + t] = make_double2(pr, pi);
+      ys[C::RS * (2 * gg + 1) + t] = make_double2(mr, mi);
+    }
+    __syncthreads();
+    double2 v[32];
+#pragma unroll
+    for (int n1 = 0; n1 < 32; ++n1) {
+      const int t = n1 * 32 + lane;
+      v[n1] = make_double2(0.0, 0.0);
+      if (t < n && pair < Gr) {
+        const int r = t == 0 ? 0 : n - t;
+        const double2 a = t < nres ? YA[t] : make_double2(0.0, 0.0);
+        const double2 b = r < nres ? YB[r] : make_double2(0.0, 0.0);
+        v[n1] = cmul(cadd(a, b), cs[t]);
+        if (half) v[n1] = cmul(v[n1], __ldg(tw16k + 8 * t));
+      }
+    }
+    reg_pair_sync(pair);  // both warps have read the fold sums
+    C::run<true>(v, Y, tw, H, lane);
+    __syncwarp();
+    if (half) {
+#pragma unroll
+      for (int n1 = 0; n1 < 32; ++n1) {
+        const int t = n1 * 32 + lane;
+        if (t < n) YB[t] = cmul(v[n1], conj2(__ldg(tw16k + 8 * t)));
+      }
+    }
+    reg_pair_sync(pair);
+    if (!half && pair < Gr) {
+      double2* out = samples + (int64_t)(b0 + pair) * L * L + (int64_t)k * k;
+#pragma unroll
+      for (int n1 = 0; n1 < 32; ++n1) {
+        const int t = n1 * 32 + lane;
+        if (t < n) out[t] = cmul(cadd(v[n1], YB[t]), cs[t]);
+      }
+    }
+    __syncthreads();  // the next iteration's fold overwrites the exchange matrices
+  }
+}
+
+__device__ __forceinline__ void ring_forward_reg2(int L, int k, int b_first, int b_last, int lgG, double2* sm,
+                                                  const double2* __restrict__ chirp, const double2* __restrict__ bh,
+                                                  const double2* __restrict__ rtw, const double2* __restrict__ tw16k,
+                                                  const double2* __restrict__ samples, double2* __restrict__ R) {
+  using C = RegConv<32, 32>;
+  const int n = 2 * k + 1;
+  const int nwarps = blockDim.x >> 5, gmax = nwarps >> 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, pair = warp >> 1, half = warp & 1;
+  double2* tw = sm;
+  double2* cs = sm + C::RS;
+  double2* ys = sm + C::RS + 1024;
+  for (int i = threadIdx.x; i < C::RS; i += blockDim.x) tw[i] = __ldg(rtw + reg_rtw_offset(1024) + i);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) cs[i] = __ldg(chirp + i);
+  double2* YA = ys + C::RS * (2 * pair);
+  double2* YB = ys + C::RS * (2 * pair + 1);
+  double2* Y = half ? YB : YA;
+  const double2* H = bh + half * 1024;  // forward-direction kernel spectrum, even / odd bins
+  const int64_t npos = (int64_t)L * (L + 1) / 2;
+  const double scale = OSPH_TWO_PI / (double)n;
+  __syncthreads();
+  for (int b0 = b_first; b0 < b_last; b0 += gmax) {
+    const int Gr = min(gmax, b_last - b0);
+    double2 v[32];
+    {
+      const double2* in = samples + (int64_t)(b0 + min(pair, Gr - 1)) * L * L + (int64_t)k * k;
+#pragma unroll
+      for (int n1 = 0; n1 < 32; ++n1) {
+        const int t = n1 * 32 + lane;
+        v[n1] = t < n ? cmul(__ldg(in + t), conj2(cs[t])) : make_double2(0.0, 0.0);
+        if (half && t < n) v[n1] = cmul(v[n1], __ldg(tw16k + 8 * t));
+      }
+    }
+    C::run<true>(v, Y, tw, H, lane);
+    __syncwarp();
+    if (half) {
+#pragma unroll
+      for (int n1 = 0; n1 < 32; ++n1) {
+        const int t = n1 * 32 + lane;
+        if (t < n) YB[t] = cmul(v[n1], conj2(__ldg(tw16k + 8 * t)));
+      }
+    }
+    reg_pair_sync(pair);
+    if (!half) {
+#pragma unroll
+      for (int n1 = 0; n1 < 32; ++n1) {
+        const int t = n1 * 32 + lane;
+        if (t < n) {
+          const double2 x = cmul(cadd(v[n1], YB[t]), conj2(cs[t]));
+          YA[t] = make_double2(scale * x.x, scale * x.y);
+        }
+      }
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < Gr * (k + 1); idx += blockDim.x) {  // map-fastest writes of R
+      const int gg = idx % Gr, m = idx / Gr;
+      const double2* X = ys + C::RS * (2 * gg);
+      const int64_t base = r_index(packed_pos(L, m, k - m), 0, b0 + gg, lgG, npos);
+      R[base] = X[m];
+      R[base + (1 << lgG)] = m == 0 ? make_double2(0.0, 0.0) : X[n - m];
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(REG_THREADS, 2) k_ring_inverse_reg(
     int L, int B, int maps_per_block, const int* __restrict__ rings, const int* __restrict__ fft_n,
     const int64_t* __restrict__ chirp_off, const int64_t* __restrict__ bhat_off, const double2* __restrict__ chirp_all,
@@ -515,6 +667,31 @@ __global__ void __launch_bounds__(REG_THREADS, 2) k_ring_forward_reg(
   else ring_forward_reg<16, 16>(L, k, b_first, b_last, lgG, sm, chirp, bh, rtw, samples, R);
 }
 
+// The 2048-point rings (their own launches: the code of the smaller classes stays lean).
+__global__ void __launch_bounds__(REG_THREADS, 2) k_ring_inverse_reg2(
+    int L, int B, int maps_per_block, const int* __restrict__ rings, const int64_t* __restrict__ chirp_off,
+    const int64_t* __restrict__ bhat_off, const double2* __restrict__ chirp_all, const double2* __restrict__ bhat_all,
+    const double2* __restrict__ rtw, const double2* __restrict__ tw16k, const double* __restrict__ G,
+    double2* __restrict__ samples) {
+  extern __shared__ double2 sm[];
+  const int k = rings[blockIdx.x];
+  const int b_first = blockIdx.y * maps_per_block;
+  ring_inverse_reg2(L, B, k, b_first, min(B, b_first + maps_per_block), sm, chirp_all + chirp_off[k],
+                    bhat_all + bhat_off[k] + 2048, rtw, tw16k, G, samples);
+}
+
+__global__ void __launch_bounds__(REG_THREADS, 2) k_ring_forward_reg2(
+    int L, int B, int maps_per_block, const int* __restrict__ rings, const int64_t* __restrict__ chirp_off,
+    const int64_t* __restrict__ bhat_off, const double2* __restrict__ chirp_all, const double2* __restrict__ bhat_all,
+    const double2* __restrict__ rtw, const double2* __restrict__ tw16k, const double2* __restrict__ samples,
+    double2* __restrict__ R, int bofs, int bend, int lgG) {
+  extern __shared__ double2 sm[];
+  const int k = rings[blockIdx.x];
+  const int b_first = bofs + blockIdx.y * maps_per_block;
+  ring_forward_reg2(L, k, b_first, min(bend, b_first + maps_per_block), lgG, sm, chirp_all + chirp_off[k],
+                    bhat_all + bhat_off[k], rtw, tw16k, samples, R);
+}
+
 // launch shape of the register-resident kernels: warps per block, maps per block, shared memory
 struct RegShape {
   int threads, mpb;
@@ -522,7 +699,7 @@ struct RegShape {
 };
 static RegShape reg_shape(int B, int nrings) {
   int warps = REG_WARPS;
-  while (warps > 1 && (warps - 1) * 2 >= B) --warps;  // small batches: no idle warps (two maps per warp at N <= 512)
+  while (warps > 2 && (warps - 2) * 2 >= B) warps -= 2;  // small batches: fewer idle warps; even (2048-class warp pairs)
   // twiddles, kernel spectrum, chirp + one exchange matrix per group; 512- and 256-point rings
   // run two groups per warp
   const size_t ent = std::max<size_t>((size_t)RegConv<32, 32>::RS * (1 + warps) + 1536,
@@ -690,12 +867,22 @@ cudaError_t launch_ring_inverse(osph_plan* p, int B, double2* samples) {
     cudaError_t e = launch_big((const void*)k_ring_inverse_bluestein2, p, B, p->inv_n_big, args);
     if (e != cudaSuccess) return e;
   }
-  if (p->inv_n_reg > 0) {
-    const RegShape sh = reg_shape(B, p->inv_n_reg);
+  if (p->inv_n_reg2 > 0) {  // 2048-point rings: the first inv_n_reg2 of the register-resident ones
+    const RegShape sh = reg_shape(B, p->inv_n_reg2);
+    cudaFuncSetAttribute(k_ring_inverse_reg2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem);
+    dim3 grid(p->inv_n_reg2, (B + sh.mpb - 1) / sh.mpb);
+    k_ring_inverse_reg2<<<grid, sh.threads, sh.smem, p->stream>>>(
+        L, B, sh.mpb, p->d_inv_bluestein + (p->inv_n_bluestein - p->inv_n_reg), p->d_chirp_off, p->d_bhat_off,
+        p->d_chirp, p->d_bhat, p->d_rtw, p->d_tw, p->d_g, samples);
+    p->launches++;
+  }
+  if (p->inv_n_reg - p->inv_n_reg2 > 0) {
+    const int nr = p->inv_n_reg - p->inv_n_reg2;
+    const RegShape sh = reg_shape(B, nr);
     cudaFuncSetAttribute(k_ring_inverse_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem);
-    dim3 grid(p->inv_n_reg, (B + sh.mpb - 1) / sh.mpb);
+    dim3 grid(nr, (B + sh.mpb - 1) / sh.mpb);
     k_ring_inverse_reg<<<grid, sh.threads, sh.smem, p->stream>>>(
-        L, B, sh.mpb, p->d_inv_bluestein + (p->inv_n_bluestein - p->inv_n_reg), p->d_fft_n, p->d_chirp_off,
+        L, B, sh.mpb, p->d_inv_bluestein + (p->inv_n_bluestein - nr), p->d_fft_n, p->d_chirp_off,
         p->d_bhat_off, p->d_chirp, p->d_bhat, p->d_rtw, p->d_g, samples);
     p->launches++;
   }
@@ -732,12 +919,22 @@ cudaError_t launch_ring_forward(osph_plan* p, int B, const double2* samples, int
     cudaError_t e = launch_big((const void*)k_ring_forward_bluestein2, p, nb, p->n_big_rings, args);
     if (e != cudaSuccess) return e;
   }
-  if (p->n_reg_rings > 0) {
-    const RegShape sh = reg_shape(nb, p->n_reg_rings);
+  if (p->n_reg2_rings > 0) {  // 2048-point rings: the first n_reg2_rings of the register-resident ones
+    const RegShape sh = reg_shape(nb, p->n_reg2_rings);
+    cudaFuncSetAttribute(k_ring_forward_reg2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem);
+    dim3 grid(p->n_reg2_rings, (nb + sh.mpb - 1) / sh.mpb);
+    k_ring_forward_reg2<<<grid, sh.threads, sh.smem, p->stream>>>(
+        L, B, sh.mpb, p->d_bluestein_rings + (p->n_bluestein_rings - p->n_reg_rings), p->d_chirp_off, p->d_bhat_off,
+        p->d_chirp, p->d_bhat, p->d_rtw, p->d_tw, samples, p->d_r, bofs, bofs + nb, lgG);
+    p->launches++;
+  }
+  if (p->n_reg_rings - p->n_reg2_rings > 0) {
+    const int nr = p->n_reg_rings - p->n_reg2_rings;
+    const RegShape sh = reg_shape(nb, nr);
     cudaFuncSetAttribute(k_ring_forward_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.smem);
-    dim3 grid(p->n_reg_rings, (nb + sh.mpb - 1) / sh.mpb);
+    dim3 grid(nr, (nb + sh.mpb - 1) / sh.mpb);
     k_ring_forward_reg<<<grid, sh.threads, sh.smem, p->stream>>>(
-        L, B, sh.mpb, p->d_bluestein_rings + (p->n_bluestein_rings - p->n_reg_rings), p->d_fft_n, p->d_chirp_off,
+        L, B, sh.mpb, p->d_bluestein_rings + (p->n_bluestein_rings - nr), p->d_fft_n, p->d_chirp_off,
         p->d_bhat_off, p->d_chirp, p->d_bhat, p->d_rtw, samples, p->d_r, bofs, bofs + nb, lgG);
     p->launches++;
   }

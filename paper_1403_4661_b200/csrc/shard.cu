@@ -126,12 +126,13 @@ extern "C" int osph_plan_shard(osph_plan* p, int rank, int nranks, int mode) {
   std::vector<int> ord, blu;
   for (int k : p->h_ring_order)
     if (k >= klo && k < khi) ord.push_back(k);
-  int nbig = 0, nreg = 0;
+  int nbig = 0, nreg = 0, nreg2 = 0;
   for (int k : p->h_bluestein_rings)  // largest first: the 16384-point rings lead, the register-resident ones trail
     if (k >= klo && k < khi) {
       blu.push_back(k);
       if (p->h_fft_n[k] > OSPH_FFT_MAX) ++nbig;
       if (p->h_fft_n[k] <= p->reg_fft_max) ++nreg;
+      if (p->h_fft_n[k] <= p->reg_fft_max && p->h_fft_n[k] == 2048) ++nreg2;
     }
   int* d_ord = nullptr;
   int* d_blu = nullptr;
@@ -145,6 +146,7 @@ extern "C" int osph_plan_shard(osph_plan* p, int rank, int nranks, int mode) {
   p->inv_n_bluestein = p->dft_ok ? (int)blu.size() : 0;
   p->inv_n_big = p->dft_ok ? nbig : 0;
   p->inv_n_reg = p->dft_ok ? nreg : 0;
+  p->inv_n_reg2 = p->dft_ok ? nreg2 : 0;
   p->inv_direct_lo = std::min(klo, p->n_direct_rings);
   p->inv_direct_hi = std::min(khi, p->n_direct_rings);
   p->inv_own_lists = true;

@@ -233,8 +233,11 @@ __global__ void k_bluestein_tables(int nrings, const int* __restrict__ rings, co
     double2* out = bhat + bhat_off[k] + (int64_t)dir * N;
     // bit-reversed order for the shared-memory transforms (bluestein_convolve), natural
     // order for the register-resident ones (N <= natural_max, fft_reg.cuh)
+    // (N = 2048: even bins then odd bins, the two 1024-point halves of ringdft.cu's 2048 class)
     for (int u = threadIdx.x; u < N; u += blockDim.x) {
-      const double2 v = xs[N <= natural_max ? u : bitrev(u, logN)];
+      int src = bitrev(u, logN);
+      if (N <= natural_max) src = N == 2048 ? (u < 1024 ? 2 * u : 2 * (u - 1024) + 1) : u;
+      const double2 v = xs[src];
       out[u] = make_double2(v.x * inv, v.y * inv);
     }
     __syncthreads();

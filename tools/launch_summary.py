@@ -4,7 +4,10 @@ Usage: python tools/launch_summary.py launches.csv "title line" > profiles/launc
 
 Prints per-kernel totals and the breadth-first factor chain of the LAST
 forward call (k_bf_generate .. k_bf_epilogue, plus k_kappa / k_bf_colnorm in
-between), whose DRAM bytes bench.py reads as the factor's roofline traffic.
+between) and the sweep stage after it, whose DRAM bytes bench.py reads as the
+roofline traffic of those stages.  With the split factorisation the two
+ranges interleave; capture launch lists with OSPH_FACTOR_SPLIT=0 so that one
+chain is contiguous.
 """
 import collections
 import csv
@@ -40,6 +43,8 @@ def main(path, title):
         i1 = i0
         while i1 < len(seq) and not seq[i1]["name"].startswith("k_bf_epilogue"):
             i1 += 1
+        while i1 + 1 < len(seq) and seq[i1 + 1]["name"].startswith(("k_bf_couple", "k_kappa")):
+            i1 += 1  # the coupling rows of the blocked sweep and the condition estimate close the chain
         chain = [x for x in seq[i0:i1 + 1] if x["name"].startswith(("k_bf_", "k_kappa"))]
         t = sum(x.get("gpu__time_duration.sum", 0.0) for x in chain)
         b = sum(x.get("dram__bytes_read.sum", 0.0) + x.get("dram__bytes_write.sum", 0.0) for x in chain)
@@ -47,6 +52,14 @@ def main(path, title):
         print(f"factor chain of one forward call (k_bf_* + k_kappa, serialised): {len(chain)} launches, "
               f"{t / 1e3:.1f} us, DRAM {b / 1e6:.1f} MB")
         print(f"factor_chain_dram_bytes {int(b)}")
+        # the sweep stage that follows this factor chain: every k_sb_* (blocked sweep) or
+        # k_sweep* launch up to the next non-sweep kernel after the ring DFTs
+        sw = [x for x in seq[i1 + 1:] if x["name"].startswith(("k_sb_", "void k_sb_", "void k_sweep", "k_fold_order0"))]
+        if sw:
+            t = sum(x.get("gpu__time_duration.sum", 0.0) for x in sw)
+            b = sum(x.get("dram__bytes_read.sum", 0.0) + x.get("dram__bytes_write.sum", 0.0) for x in sw)
+            print(f"sweep stage of the same forward call: {len(sw)} launches, {t / 1e3:.1f} us, DRAM {b / 1e6:.1f} MB")
+            print(f"sweep_stage_dram_bytes {int(b)}")
 
 
 if __name__ == "__main__":
