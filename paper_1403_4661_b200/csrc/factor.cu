@@ -40,14 +40,16 @@ cudaError_t launch_kappa(osph_plan* p, cudaStream_t st) {
 // Every order in one breadth-first pass on `st` (the resident, non-windowed
 // forward; the windowed one runs bf_run per window in window.cu).
 //
-// Split (unsharded plans, L >= 128; OSPH_FACTOR_SPLIT=0 disables): the chain of
-// panel steps is latency-bound, and the orders >= L/2 (blocks of at most L/2
-// rows, ~6% of the flops, half of the panel steps) are the first the sweep
-// needs.  They run as their own range on a second stream beside the low
-// orders; `ev_fa` marks them done, so the blocked sweep starts on the high
-// orders while the low ones are still being factored.  `st` joins the second
-// stream before returning, so an event recorded on `st` after this call still
-// covers every order.
+// Split (unsharded plans, L >= 128; OSPH_FACTOR_SPLIT=0 disables, =n sets the
+// number of ranges): the chain of panel steps is latency-bound, and the high
+// orders (small blocks: few panel steps, a few percent of the flops) are the
+// first the sweep needs.  The orders are cut into three (up to four) ranges at sweep
+// block boundaries; every range runs its own chain on its own stream, all
+// beside each other, and records an event when done, so the blocked sweep
+// starts on the high orders while the lower ranges are still being factored
+// (launch_sweep_blocked waits per range).  `st` runs the lowest range and joins
+// the other streams before returning, so an event recorded on `st` after this
+// call still covers every order.
 cudaError_t launch_factor(osph_plan* p, cudaStream_t st) {
   const int L = p->L;
   cudaError_t e;
@@ -56,25 +58,36 @@ cudaError_t launch_factor(osph_plan* p, cudaStream_t st) {
   if ((e = cudaMemsetAsync(p->d_status, 0, sizeof(int) * L, st)) != cudaSuccess) return e;
   int lo, hi;
   own_orders(p, lo, hi);  // all orders, or this shard's block (OSPH_SHARD_FACTORS)
-  static const bool split_off = getenv("OSPH_FACTOR_SPLIT") && atoi(getenv("OSPH_FACTOR_SPLIT")) == 0;
+  static const int split_env = getenv("OSPH_FACTOR_SPLIT") ? atoi(getenv("OSPH_FACTOR_SPLIT")) : -1;
   p->fsplit_active = false;
-  p->sweep_late_ev = nullptr;
-  if (!split_off && !p->shard_mode && !p->windowed && lo == 0 && hi == L - 1 && L >= 128 && p->s_fa) {
-    const int split = ((L / 2) / OSPH_SB_BLOCK) * OSPH_SB_BLOCK;  // a block boundary of the blocked sweep
-    if (p->fsplit_m != split) {
-      if ((e = bf_prepare(p, split, L - 1, &p->bf_hi)) != cudaSuccess) return e;
-      if ((e = bf_prepare(p, 0, split - 1, &p->bf_lo)) != cudaSuccess) return e;
-      p->bf_hi.dbuf = p->d_bf_d + bf_diag_doubles(split);  // disjoint diagonal-block scratch
-      p->bf_lo.dbuf = p->d_bf_d;
-      p->fsplit_m = split;
+  p->sweep_waits_ranges = false;
+  if (split_env != 0 && !p->shard_mode && !p->windowed && lo == 0 && hi == L - 1 && L >= 128 && p->s_f[0]) {
+    if (p->n_frng == 0) {
+      // boundaries at multiples of the sweep block, ranges of about L / n orders
+      // default three ranges (measured, config 2: 39.9k / 41.6k / 41.9k / 41.9k transforms/s with 1 / 2 / 3 / 4)
+      const int want = std::min<int>(osph_plan::kFactorRanges, split_env > 0 ? split_env : 3);
+      int n = 0, top = L - 1;
+      for (int r = 0; r < want && top >= 0; ++r) {
+        int first = r == want - 1 ? 0 : (((int64_t)L * (want - 1 - r) / want) / OSPH_SB_BLOCK) * OSPH_SB_BLOCK;
+        if (first > top) continue;
+        if ((e = bf_prepare(p, first, top, &p->bf_rng[n])) != cudaSuccess) return e;
+        p->bf_rng[n].dbuf = p->d_bf_d + bf_diag_doubles(first);  // disjoint diagonal-block scratch
+        ++n;
+        top = first - 1;
+      }
+      p->n_frng = n;
     }
+    const int n = p->n_frng;
     const BfOffsets o{p->d_ainv_off, p->d_xt_off, p->d_pb_off, p->d_bf_off};
     if ((e = cudaEventRecord(p->ev_fstart, st)) != cudaSuccess) return e;
-    if ((e = cudaStreamWaitEvent(p->s_fa, p->ev_fstart, 0)) != cudaSuccess) return e;
-    if ((e = bf_run(p, p->bf_hi, p->s_fa, o)) != cudaSuccess) return e;
-    if ((e = cudaEventRecord(p->ev_fa, p->s_fa)) != cudaSuccess) return e;
-    if ((e = bf_run(p, p->bf_lo, st, o)) != cudaSuccess) return e;
-    if ((e = cudaStreamWaitEvent(st, p->ev_fa, 0)) != cudaSuccess) return e;
+    for (int r = 0; r < n - 1; ++r) {
+      if ((e = cudaStreamWaitEvent(p->s_f[r], p->ev_fstart, 0)) != cudaSuccess) return e;
+      if ((e = bf_run(p, p->bf_rng[r], p->s_f[r], o)) != cudaSuccess) return e;
+      if ((e = cudaEventRecord(p->ev_f[r], p->s_f[r])) != cudaSuccess) return e;
+    }
+    if ((e = bf_run(p, p->bf_rng[n - 1], st, o)) != cudaSuccess) return e;
+    for (int r = 0; r < n - 1; ++r)
+      if ((e = cudaStreamWaitEvent(st, p->ev_f[r], 0)) != cudaSuccess) return e;
     p->fsplit_active = true;
     return launch_kappa(p, st);
   }

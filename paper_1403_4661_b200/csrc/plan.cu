@@ -70,12 +70,13 @@ void plan_free(osph_plan* p) {
   if (p->ev_out) cudaEventDestroy(p->ev_out);
   if (p->ev_sweep_done) cudaEventDestroy(p->ev_sweep_done);
   if (p->s_in) cudaStreamDestroy(p->s_in);
-  if (p->s_fa) cudaStreamDestroy(p->s_fa);
+  for (int r = 0; r < osph_plan::kFactorRanges; ++r) {
+    if (p->s_f[r]) cudaStreamDestroy(p->s_f[r]);
+    if (p->ev_f[r]) cudaEventDestroy(p->ev_f[r]);
+    cudaFree(p->bf_rng[r].d_tab);
+  }
   if (p->ev_fstart) cudaEventDestroy(p->ev_fstart);
-  if (p->ev_fa) cudaEventDestroy(p->ev_fa);
   cudaFree(p->bf_full.d_tab);
-  cudaFree(p->bf_hi.d_tab);
-  cudaFree(p->bf_lo.d_tab);
   if (p->s_out) cudaStreamDestroy(p->s_out);
   cudaFree(p->d_z1);
   cudaFree(p->d_z2);
@@ -167,9 +168,11 @@ int plan_create_one(int L, const double* thetas, int max_batch, int device, osph
   if (getenv("OSPH_NO_STREAM_PRIORITY")) prio_hi = prio_lo;
   PLAN_TRY(cudaStreamCreateWithPriority(&p->s_in, cudaStreamNonBlocking, prio_hi));
   PLAN_TRY(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
-  PLAN_TRY(cudaStreamCreateWithPriority(&p->s_fa, cudaStreamNonBlocking, prio_hi));
+  for (int r = 0; r < osph_plan::kFactorRanges - 1; ++r) {
+    PLAN_TRY(cudaStreamCreateWithPriority(&p->s_f[r], cudaStreamNonBlocking, prio_hi));
+    PLAN_TRY(cudaEventCreateWithFlags(&p->ev_f[r], cudaEventDisableTiming));
+  }
   PLAN_TRY(cudaEventCreateWithFlags(&p->ev_fstart, cudaEventDisableTiming));
-  PLAN_TRY(cudaEventCreateWithFlags(&p->ev_fa, cudaEventDisableTiming));
   for (int c = 0; c < osph_plan::kIoChunks; ++c) {
     PLAN_TRY(cudaEventCreateWithFlags(&p->ev_in[c], cudaEventDisableTiming));
     PLAN_TRY(cudaEventCreateWithFlags(&p->ev_done[c], cudaEventDisableTiming));
@@ -431,17 +434,11 @@ __global__ void k_unpair_flm(int B, int L, const double2* __restrict__ z, double
 }
 
 // The sweep on `st` waits for the factorisation, recorded as ev[7] on a side stream.  The
-// blocked sweep of a split factorisation (factor.cu) waits only for the high orders now and
-// for the rest at its first block below the split (launch_sweep_blocked).
+// blocked sweep of a split factorisation (factor.cu) waits range by range instead, each at
+// its first block of that range (launch_sweep_blocked; the lowest range's event is ev[7]).
 static cudaError_t wait_factor_for_sweep(osph_plan* p, cudaStream_t st) {
-  p->sweep_late_ev = nullptr;
-  if (p->fsplit_active && p->sweep_blocked) {
-    cudaError_t e = cudaStreamWaitEvent(st, p->ev_fa, 0);
-    p->sweep_late_ev = p->ev[7];
-    p->sweep_late_m = p->fsplit_m;
-    return e;
-  }
-  return cudaStreamWaitEvent(st, p->ev[7], 0);
+  p->sweep_waits_ranges = p->fsplit_active && p->sweep_blocked;
+  return p->sweep_waits_ranges ? cudaSuccess : cudaStreamWaitEvent(st, p->ev[7], 0);
 }
 
 static int ensure_real(osph_plan* p) {

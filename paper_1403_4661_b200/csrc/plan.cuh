@@ -153,16 +153,18 @@ struct osph_plan {
   bool inv_ready = false;        // inverse buffers allocated
   // breadth-first factorisation (factor_bf.cu) of every order
   BfRange bf_full;               // the non-windowed range (every order)
-  // Split factorisation (factor.cu): orders >= fsplit_m on their own stream beside the rest, so the
-  // blocked sweep can start on the high orders (cheap to factor, first to be swept) while the low
-  // orders are still being factored.
-  BfRange bf_hi, bf_lo;
-  int fsplit_m = 0;              // 0: not split
-  cudaStream_t s_fa = nullptr;
-  cudaEvent_t ev_fstart = nullptr, ev_fa = nullptr;  // split start / high orders done
-  bool fsplit_active = false;    // the last launch_factor ran split
-  cudaEvent_t sweep_late_ev = nullptr;  // blocked sweep: wait for this event before the first block
-  int sweep_late_m = 0;                 //   that reaches below this order
+  // Split factorisation (factor.cu): the orders are cut into ranges (high orders first);
+  // each range is its own latency-bound chain of panel steps on its own stream, so the
+  // blocked sweep can start on the high orders (cheap to factor, first to be swept) while the
+  // lower ranges are still being factored.  Range boundaries are sweep block boundaries.
+  static constexpr int kFactorRanges = 4;
+  BfRange bf_rng[kFactorRanges];            // [0] = the highest orders ... [n-1] = the lowest (on the caller's stream)
+  int n_frng = 0;                           // 0: not prepared
+  cudaStream_t s_f[kFactorRanges] = {};     // streams of ranges 0 .. n-2
+  cudaEvent_t ev_f[kFactorRanges] = {};     // range r done (r < n-1)
+  cudaEvent_t ev_fstart = nullptr;
+  bool fsplit_active = false;               // the last launch_factor ran split
+  bool sweep_waits_ranges = false;          // blocked sweep: wait for each range's event at its first block
   int num_sms = 0;
   bool need_norms = true;        // this call checks conditioning (check=True): factor kernels accumulate norms
   int64_t* d_bf_off = nullptr;   // [L+1] offsets of the E / R panels (NB x lde(n) per order)

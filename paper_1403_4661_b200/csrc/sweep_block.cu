@@ -493,14 +493,16 @@ static cudaError_t sweep_blocked_run(osph_plan* p, int B, double2* flm) {
     return e;
   const int ny = (B + MAPS - 1) / MAPS;
   cudaStream_t st = p->stream;
-  int s_top = L - 1, ps_top = -1, pm0 = 0;
+  int s_top = L - 1, ps_top = -1, pm0 = 0, next_rng = 0;
   while (s_top >= 0) {
     const int m0 = (s_top / SB_B) * SB_B;  // blocks start at multiples of 32
     const int nb = s_top - m0 + 1;
     const bool last = m0 == 0;
-    if (p->sweep_late_ev && m0 < p->sweep_late_m) {  // the low orders' factors (split factorisation)
-      if ((e = cudaStreamWaitEvent(st, p->sweep_late_ev, 0)) != cudaSuccess) return e;
-      p->sweep_late_ev = nullptr;
+    // split factorisation: the factors of every range this block touches (ranges descend)
+    while (p->sweep_waits_ranges && next_rng < p->n_frng && p->bf_rng[next_rng].m_last >= m0) {
+      cudaEvent_t ev = next_rng == p->n_frng - 1 ? p->ev[7] : p->ev_f[next_rng];
+      if ((e = cudaStreamWaitEvent(st, ev, 0)) != cudaSuccess) return e;
+      ++next_rng;
     }
     if (ps_top >= 0) {  // corrections of the blocks above that were not reduced into R directly
       const int64_t per = (packed_pos(L, s_top + 1, 0) - packed_pos(L, m0, 0)) * 2;
@@ -547,6 +549,7 @@ static cudaError_t sweep_blocked_run(osph_plan* p, int B, double2* flm) {
     pm0 = m0;
     s_top = m0 - 1;
   }
+  p->sweep_waits_ranges = false;
   return cudaGetLastError();
 }
 
