@@ -222,8 +222,10 @@ static int buffer_span(osph_plan* p, int which, int B, int m_lo, int m_hi, void*
       *bytes = (int64_t)sizeof(int) * cnt;
       break;
     case OSPH_BUF_UT:
-      *ptr = p->d_ut + p->h_ut_off[m_lo];
-      *bytes = (int64_t)sizeof(double) * (p->h_ut_off[m_hi + 1] - p->h_ut_off[m_lo]);
+      if (p->d_ut) {
+        *ptr = p->d_ut + p->h_ut_off[m_lo];
+        *bytes = (int64_t)sizeof(double) * (p->h_ut_off[m_hi + 1] - p->h_ut_off[m_lo]);
+      }
       break;
     default:
       osph_set_error("unknown buffer id");

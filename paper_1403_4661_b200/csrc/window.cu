@@ -124,6 +124,7 @@ int alloc_factor_storage(osph_plan* p) {
     W_TRY(cudaMemsetAsync(p->d_pbelow, 0, sizeof(double) * (size_t)tot[2], st));
     W_TRY(cudaMemsetAsync(p->d_xt, 0, sizeof(double) * (size_t)tot[1], st));
     // coupling rows of the blocked sweep (rows past the rings below s and padding stay zero)
+    if (L > 1024) return OSPH_OK;  // the blocked sweep serves L <= 1024
     p->h_ut_off.assign(L + 1, 0);
     for (int m = 0; m < L; ++m) p->h_ut_off[m + 1] = p->h_ut_off[m] + tile_size(sb_rows(m), L - m);
     W_TRY(cudaMalloc(&p->d_ut_off, sizeof(int64_t) * (L + 1)));
