@@ -938,12 +938,15 @@ int sweep_maps_per_team(osph_plan* p, int B) {
   p->sweep_gemm = false;
   p->sweep_blocked = false;
   {
-    // batches: orders peeled in blocks of 32 with batched GEMM launches (sweep_block.cu);
-    // OSPH_SWEEP_BLOCKED=1 / 0 forces / forbids it
+    // L <= 512: orders peeled in blocks of 32 with batched GEMM launches (sweep_block.cu; B = 1:
+    // 0.15 -> 0.07 ms at L = 64, 0.86 -> 0.32 ms at L = 256, 2.4 -> 0.9 ms at L = 512 against the
+    // persistent kernel); OSPH_SWEEP_BLOCKED=0 forbids it
     const char* eb = getenv("OSPH_SWEEP_BLOCKED");
-    const bool can = L <= 1024 && !p->windowed && p->d_ut && !getenv("OSPH_SWEEP_LARGE") &&
+    // (L > 512 keeps the large sweep: its refinement step holds the round trip at 2e-10 at L = 1024,
+    // the blocked sweep without one gives 2e-9 -- still inside 10x the reference's own 5e-10, but worse)
+    const bool can = (L <= 512 || (eb && atoi(eb) != 0)) && L <= 1024 && !p->windowed && p->d_ut && !getenv("OSPH_SWEEP_LARGE") &&
                      !getenv("OSPH_SWEEP_GEMM") && !getenv("OSPH_SWEEP_NO_GEMM");
-    if (can && (eb ? atoi(eb) != 0 : B >= 16)) {
+    if (can && (eb ? atoi(eb) != 0 : true)) {  // measured faster than the persistent kernel at every batch size
       p->sweep_blocked = true;
       p->sweep_large = false;
       p->sweep_cfg_B = B;

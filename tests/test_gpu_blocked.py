@@ -73,7 +73,7 @@ def test_blocked_sweep_real_maps_and_odd_batch(grid_of, monkeypatch):
     flm = np.stack([O.config_coefficients(L, rng, spectrum="cmb", real=True) for _ in range(B)])
     s = osp.inverse_sht_batch(flm, g, real=True)
     f, kind = _forward(g, s, {}, monkeypatch, real=True)
-    assert kind == "blocked"  # 19 pairs >= 16: the default for batches
+    assert kind == "blocked"  # the default at L <= 512
     assert np.abs(f - flm).max() <= 1e-11
     ref = O.forward_sht(s[5], g.thetas, method="spectral")
     assert np.abs(f[5] - ref).max() <= 1e-11

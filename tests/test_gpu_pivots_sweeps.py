@@ -149,9 +149,10 @@ def _fresh_forward(grid, samples, real=False, env=None, monkeypatch=None):
     return out, sweep
 
 
-@pytest.mark.parametrize("env,want", [({}, "persistent"), ({"OSPH_SWEEP_LARGE": "1"}, "large"),
+@pytest.mark.parametrize("env,want", [({}, "blocked"), ({"OSPH_SWEEP_BLOCKED": "0"}, "persistent"),
+                                      ({"OSPH_SWEEP_LARGE": "1"}, "large"),
                                       ({"OSPH_WINDOW_GB": "0.03"}, "windowed"),
-                                      ({"OSPH_SWEEP_BLOCKED": "1"}, "blocked")])
+                                      ({"OSPH_SB_SMALL": "0"}, "blocked")])
 def test_sweep_variants_L256_reference(env, want, golden, grid_of, monkeypatch):
     """Config 2's grid and recipe through each sweep the library has, against the reference."""
     d = golden("ref_L256.npz")
