@@ -220,7 +220,8 @@ __global__ void __launch_bounds__(SB_THREADS) k_sb_gemm(int L, int s_top, int m0
         // (s' = -s mod 2k+1) once 2k+1 > 32, so the same-tone branch reduces into R and the
         // opposite-tone branch into R2 (added to R before the target's block starts,
         // k_sb_combine): every address takes at most one reduction per launch and the
-        // sums are bitwise reproducible.  Rings k < 16 go through `out` (k_sb_combine).
+        // sums are bitwise reproducible.  Rings k < 16 go through `out` (gathered by k_sb_combine
+        // before the final block, where all of their targets live).
         const int k = row;
         if (k < SB_B / 2) {
           out[(((int64_t)z * (SB_B / 2) + k) * B + b) * 2 + slot] = make_double2(vr, vi);
@@ -363,42 +364,41 @@ __global__ void __launch_bounds__(SB_THREADS) k_sb_chain(int L, int s_top, int m
   }
 }
 
-// Before a block (orders m0 .. s_top) starts:
-//  * blockIdx.y < gridDim.y - 1: its right-hand-side rows take the opposite-tone
-//    corrections collected in R2 (R += R2, R2 = 0; elementwise over the rows' contiguous
-//    range of every map);
-//  * the last blockIdx.y: the corrections the PREVIOUS block (orders pm0 .. ps_top) sent
-//    through the short rings k < 16 (several sources can meet in one bin there), gathered
-//    per target (tm <= k, tone) in descending source order, + tone before - tone.
-__global__ void __launch_bounds__(256) k_sb_combine(int L, int s_top, int m0, int ps_top, int pm0, int B, int nstream,
-                                                    const double2* __restrict__ G16, double2* __restrict__ R,
-                                                    double2* __restrict__ R2) {
+// R += R2 over the rows of a ONE-order block (orders m0 = s_top; otherwise the coupling
+// launch k_sb_gemm<2> merges them): grid (x, B), map blockIdx.y.
+__global__ void __launch_bounds__(256) k_sb_merge(int L, int s_top, int m0, double2* __restrict__ R,
+                                                  double2* __restrict__ R2) {
   pdl_start();
   const int64_t npos = (int64_t)L * (L + 1) / 2;
-  if ((int)blockIdx.y < nstream) {  // map blockIdx.y: R += R2 over the block's rows (nstream = B for one-order
-                                    // blocks only: otherwise the coupling launch k_sb_gemm<2> merges them)
-    const int64_t p_lo = packed_pos(L, m0, 0) * 2, per = packed_pos(L, s_top + 1, 0) * 2 - p_lo;
-    double2* rp = R + (int64_t)blockIdx.y * npos * 2 + p_lo;
-    double2* r2 = R2 + (int64_t)blockIdx.y * npos * 2 + p_lo;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per; i += (int64_t)gridDim.x * blockDim.x) {
-      const double2 v = r2[i];
-      if (v.x != 0.0 || v.y != 0.0) {
-        const double2 r = rp[i];
-        rp[i] = make_double2(r.x + v.x, r.y + v.y);
-        r2[i] = make_double2(0.0, 0.0);
-      }
+  const int64_t p_lo = packed_pos(L, m0, 0) * 2, per = packed_pos(L, s_top + 1, 0) * 2 - p_lo;
+  double2* rp = R + (int64_t)blockIdx.y * npos * 2 + p_lo;
+  double2* r2 = R2 + (int64_t)blockIdx.y * npos * 2 + p_lo;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = r2[i];
+    if (v.x != 0.0 || v.y != 0.0) {
+      const double2 r = rp[i];
+      rp[i] = make_double2(r.x + v.x, r.y + v.y);
+      r2[i] = make_double2(0.0, 0.0);
     }
-    return;
   }
-  if (ps_top < 0) return;
-  // One warp per target (ring k < 16, order tm <= k, tone ts, map b): 136 (k, tm) pairs x 2
-  // tones.  Lane = source order ps_top - lane; the matching corrections are summed in lane
-  // order (descending source order, + tone before - tone).
+}
+
+// Before the final block (orders < 32): the corrections every block above sent through the
+// short rings k < 16 (several sources can meet in one bin there; their targets, orders
+// tm <= k < 16, all belong to the final block).  k_sb_gemm<1> left them in G16, one slice of
+// [32 sources][16 rings][B][tone] per block.  One warp per target (ring k, order tm <= k,
+// tone ts, map b): 136 (k, tm) pairs x 2 tones; blocks from the top down, lane = source
+// order s_top - lane of the block; the matching corrections are summed in lane order
+// (descending source order; a source sends at most one of its tones to a target).
+__global__ void __launch_bounds__(256) k_sb_combine(int L, int B, const double2* __restrict__ G16,
+                                                    double2* __restrict__ R) {
+  pdl_start();
+  const int64_t npos = (int64_t)L * (L + 1) / 2;
   constexpr int NT = (SB_B / 2) * (SB_B / 2 + 1) / 2 * 2;
   const int lane = threadIdx.x & 31;
-  const int64_t gblock = (int64_t)(blockIdx.y - nstream) * gridDim.x + blockIdx.x;  // gather blocks: the grid's last rows
-  const int64_t gblocks = (int64_t)(gridDim.y - nstream) * gridDim.x;
-  for (int64_t w = (gblock * blockDim.x + threadIdx.x) >> 5; w < (int64_t)NT * B; w += (gblocks * blockDim.x) >> 5) {
+  const int64_t slice = (int64_t)SB_B * (SB_B / 2) * B * 2;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < (int64_t)NT * B;
+       w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int b = (int)(w % B);
     int tt = (int)(w / B);
     const int ts = tt & 1;
@@ -409,30 +409,32 @@ __global__ void __launch_bounds__(256) k_sb_combine(int L, int s_top, int m0, in
       ++k;
     }
     const int tm = tt, nk = 2 * k + 1;
-    if (tm >= pm0) continue;  // inside the previous block: resolved by its recurrence (warp-uniform)
-    const int s = ps_top - lane;
-    // each source order sends at most one of its tones to this target (the + tone comes first
-    // in the reference's order, but the two never meet in one bin of the same source)
-    double2 g = make_double2(0.0, 0.0);
-    bool hit = false;
-    if (s >= pm0 && s > k) {
-      const int rr = s % nk;
-      const bool same = rr <= k;
-      const int stm = same ? rr : nk - rr;
-      if (stm == tm) {
-        const int slot = same ? ts : ts ^ 1;  // the tone of source s that lands on tone ts
-        g = __ldcg(G16 + (((int64_t)lane * (SB_B / 2) + k) * B + b) * 2 + slot);
-        hit = true;
-      }
-    }
-    unsigned mask = __ballot_sync(0xffffffffu, hit);
-    const bool any = mask != 0;
     double ax = 0.0, ay = 0.0;
-    while (mask) {  // ascending lanes = descending source orders
-      const int src = __ffs(mask) - 1;
-      mask &= mask - 1;
-      ax += __shfl_sync(0xffffffffu, g.x, src);
-      ay += __shfl_sync(0xffffffffu, g.y, src);
+    bool any = false;
+    int blk = 0;
+    for (int s_top = L - 1; s_top >= SB_B; ++blk) {
+      const int m0 = (s_top / SB_B) * SB_B;
+      const int s = s_top - lane;
+      double2 g = make_double2(0.0, 0.0);
+      bool hit = false;
+      if (s >= m0 && s > k) {
+        const int rr = s % nk;
+        const bool same = rr <= k;
+        if ((same ? rr : nk - rr) == tm) {
+          const int slot = same ? ts : ts ^ 1;  // the tone of source s that lands on tone ts
+          g = __ldcg(G16 + blk * slice + (((int64_t)lane * (SB_B / 2) + k) * B + b) * 2 + slot);
+          hit = true;
+        }
+      }
+      unsigned mask = __ballot_sync(0xffffffffu, hit);
+      any |= mask != 0;
+      while (mask) {  // ascending lanes = descending source orders
+        const int src = __ffs(mask) - 1;
+        mask &= mask - 1;
+        ax += __shfl_sync(0xffffffffu, g.x, src);
+        ay += __shfl_sync(0xffffffffu, g.y, src);
+      }
+      s_top = m0 - 1;
     }
     if (lane == 0 && any) {
       double2* rp = R + ((int64_t)b * npos + packed_pos(L, tm, k - tm)) * 2 + ts;
@@ -459,7 +461,7 @@ int ensure_sweep_blocked(osph_plan* p) {
   cudaError_t e;
   if ((e = cudaMalloc(&p->d_sb_x, sizeof(double2) * SB_B * B * 2 * L)) != cudaSuccess ||
       (e = cudaMalloc(&p->d_sb_a, sizeof(double2) * SB_B * SB_B * B * 2)) != cudaSuccess ||
-      (e = cudaMalloc(&p->d_sb_g, sizeof(double2) * SB_B * (SB_B / 2) * B * 2)) != cudaSuccess ||
+      (e = cudaMalloc(&p->d_sb_g, sizeof(double2) * ((L + SB_B - 1) / SB_B) * SB_B * (SB_B / 2) * B * 2)) != cudaSuccess ||
       (e = cudaMalloc(&p->d_sb_r2, sizeof(double2) * nr2)) != cudaSuccess ||
       (e = cudaMemsetAsync(p->d_sb_r2, 0, sizeof(double2) * nr2, p->stream)) != cudaSuccess) {
     osph_set_error(std::string("blocked sweep buffers: ") + cudaGetErrorString(e));
@@ -493,7 +495,7 @@ static cudaError_t sweep_blocked_run(osph_plan* p, int B, double2* flm) {
     return e;
   const int ny = (B + MAPS - 1) / MAPS;
   cudaStream_t st = p->stream;
-  int s_top = L - 1, ps_top = -1, pm0 = 0, next_rng = 0;
+  int s_top = L - 1, ps_top = -1, next_rng = 0, blk = 0;
   while (s_top >= 0) {
     const int m0 = (s_top / SB_B) * SB_B;  // blocks start at multiples of 32
     const int nb = s_top - m0 + 1;
@@ -504,13 +506,16 @@ static cudaError_t sweep_blocked_run(osph_plan* p, int B, double2* flm) {
       if ((e = cudaStreamWaitEvent(st, ev, 0)) != cudaSuccess) return e;
       ++next_rng;
     }
-    if (ps_top >= 0) {  // corrections of the blocks above that were not reduced into R directly
+    if (ps_top >= 0 && nb == 1) {  // a one-order block has no coupling launch to merge R2 into R
       const int64_t per = (packed_pos(L, s_top + 1, 0) - packed_pos(L, m0, 0)) * 2;
       const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((per + 255) / 256, 32));
-      const int gy = (272 * B / 8 + gx - 1) / gx;  // one warp per short-ring target (272 per map)
-      const int nstream = nb > 1 ? 0 : B;
-      if ((e = launch_pdl(k_sb_combine, dim3(gx, nstream + gy), dim3(256), 0, st, L, s_top, m0, ps_top, pm0, B, nstream,
-                          (const double2*)p->d_sb_g, p->d_r, p->d_sb_r2)) != cudaSuccess)
+      if ((e = launch_pdl(k_sb_merge, dim3(gx, B), dim3(256), 0, st, L, s_top, m0, p->d_r, p->d_sb_r2)) != cudaSuccess)
+        return e;
+      p->launches++;
+    }
+    if (last && ps_top >= 0) {  // the short-ring corrections of every block above
+      if ((e = launch_pdl(k_sb_combine, dim3((272 * B + 7) / 8), dim3(256), 0, st, L, B, (const double2*)p->d_sb_g,
+                          p->d_r)) != cudaSuccess)
         return e;
       p->launches++;
     }
@@ -541,12 +546,13 @@ static cudaError_t sweep_blocked_run(osph_plan* p, int B, double2* flm) {
     if (!last) {  // the final block's corrections all land inside the block
       if ((e = launch_pdl(k_corr, dim3((s_top + TM - 1) / TM, ny, nb), dim3(SB_THREADS), smem, st, L, s_top, m0, B,
                           (const double*)p->d_pbelow, (const int64_t*)p->d_pb_off, (const double*)p->d_w, p->d_r,
-                          p->d_sb_r2, p->d_sb_x, p->d_sb_g, flm)) != cudaSuccess)
+                          p->d_sb_r2, p->d_sb_x, p->d_sb_g + (int64_t)blk * SB_B * (SB_B / 2) * B * 2, flm)) !=
+          cudaSuccess)
         return e;
       p->launches++;
     }
+    ++blk;
     ps_top = s_top;
-    pm0 = m0;
     s_top = m0 - 1;
   }
   p->sweep_waits_ranges = false;
