@@ -629,6 +629,7 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
   cudaStream_t st = p->stream;
   p->launches = 0;
   double2* out = host ? p->d_out : (double2*)flm;
+  bool halves = false;  // host buffers + blocked sweep: the batch is swept and copied out in two halves
   if (kind & OSPH_REAL) {
     if ((rc = forward_real(p, B, samples, flm, host))) return rc;
   } else if (p->windowed) {
@@ -689,15 +690,40 @@ extern "C" int osph_forward(osph_plan* p, int B, const void* samples, void* flm,
     CUDA_TRY(cudaEventRecord(p->ev[6], st));
     CUDA_TRY(launch_factor(p, st));
     CUDA_TRY(cudaEventRecord(p->ev[7], st));
+    // Blocked sweep, batches: two halves.  The first half's ring DFTs and sweep run while the
+    // second half is still being copied in, and its coefficients go back to the host while the
+    // second half is swept (PCIe is full duplex): the copies, not the kernels, bound this path.
+    sweep_maps_per_team(p, B);  // decides the sweep (and the layout of the spectra)
+    halves = p->sweep_blocked && nch == osph_plan::kIoChunks && B >= 16 && !ensure_sweep_blocked(p);
     for (int c = 0; c < nch; ++c) {
       const int b0 = (int)((int64_t)B * c / nch), b1 = (int)((int64_t)B * (c + 1) / nch);
       CUDA_TRY(cudaStreamWaitEvent(st, p->ev_in[c], 0));
       if (c == 0) CUDA_TRY(cudaEventRecord(p->ev[4], st));
       CUDA_TRY(launch_ring_forward(p, B, p->d_in, b0, b1 - b0));
+      if (halves && (c == nch / 2 - 1 || c == nch - 1)) {
+        const int h = c == nch - 1;
+        const int hb0 = h ? (int)((int64_t)B * (nch / 2) / nch) : 0, hb1 = h ? B : (int)((int64_t)B * (nch / 2) / nch);
+        const size_t off = (size_t)hb0 * L * L, hbytes = sizeof(double2) * (size_t)(hb1 - hb0) * L * L;
+        if (h == 0) CUDA_TRY(cudaEventRecord(p->ev[8], st));
+        const int nl = p->launches;
+        CUDA_TRY(launch_sweep_blocked(p, hb1 - hb0, p->d_out + off, hb0));
+        (void)nl;
+        CUDA_TRY(cudaEventRecord(p->ev_done[h], st));
+        CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->ev_done[h], 0));
+        CUDA_TRY(cudaMemcpyAsync((double2*)flm + off, p->d_out + off, hbytes, cudaMemcpyDeviceToHost, p->s_out));
+      }
     }
     CUDA_TRY(cudaEventRecord(p->ev[5], st));
+    if (halves) {
+      p->last_sweep_kind = OSPH_SWEEP_BLOCKED;
+      CUDA_TRY(cudaEventRecord(p->ev[9], st));
+      CUDA_TRY(cudaEventRecord(p->ev_sweep_done, st));
+      p->have_sweep_ev = true;
+      CUDA_TRY(cudaEventRecord(p->ev_out, p->s_out));
+      CUDA_TRY(cudaStreamWaitEvent(st, p->ev_out, 0));  // the plan stream covers the whole call
+    }
   }
-  if (!(kind & OSPH_REAL) && !p->windowed) {
+  if (!(kind & OSPH_REAL) && !p->windowed && !halves) {
     CUDA_TRY(cudaEventRecord(p->ev[8], st));
     CUDA_TRY(launch_sweep(p, B, out));
     p->last_sweep_kind = sweep_kind(p);

@@ -260,7 +260,8 @@ cudaError_t launch_sweep(osph_plan* p, int B, double2* flm);               // sw
 int sweep_maps_per_team(osph_plan* p, int B);
 cudaError_t launch_sweep_large(osph_plan* p, int B, double2* flm);  // sweep_large.cu
 cudaError_t launch_sweep_gemm(osph_plan* p, int B, double2* flm);   // sweep_gemm.cu
-cudaError_t launch_sweep_blocked(osph_plan* p, int B, double2* flm);  // sweep_block.cu
+// sweep_block.cu; maps b0 .. b0 + B - 1 of the spectra, flm = the first of those maps
+cudaError_t launch_sweep_blocked(osph_plan* p, int B, double2* flm, int b0 = 0);
 int ensure_sweep_blocked(osph_plan* p);                               // sweep_block.cu: scratch buffers
 cudaError_t launch_factor_bf(osph_plan* p, int m_first, int m_last, cudaStream_t st);  // factor_bf.cu
 cudaError_t bf_prepare(osph_plan* p, int m_first, int m_last, BfRange* r);               // factor_bf.cu

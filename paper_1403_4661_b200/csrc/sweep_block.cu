@@ -471,8 +471,11 @@ int ensure_sweep_blocked(osph_plan* p) {
 }
 
 template <int NS, int TM, int MAPS>
-static cudaError_t sweep_blocked_run(osph_plan* p, int B, double2* flm) {
+static cudaError_t sweep_blocked_run(osph_plan* p, int B, double2* flm, int b0) {
   const int L = p->L;
+  // maps b0 .. b0 + B - 1 of the spectra (plain layout [map][pos][+-]); flm is already the first map's
+  double2* const Rb = p->d_r + (int64_t)b0 * L * (L + 1);
+  double2* const R2b = p->d_sb_r2 + (int64_t)b0 * L * (L + 1);
   const size_t smem = NS * sizeof(SbStage<TM, MAPS>);
   cudaError_t e;
   auto k_solve = k_sb_gemm<0, NS, TM, MAPS>;
@@ -509,44 +512,44 @@ static cudaError_t sweep_blocked_run(osph_plan* p, int B, double2* flm) {
     if (ps_top >= 0 && nb == 1) {  // a one-order block has no coupling launch to merge R2 into R
       const int64_t per = (packed_pos(L, s_top + 1, 0) - packed_pos(L, m0, 0)) * 2;
       const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((per + 255) / 256, 32));
-      if ((e = launch_pdl(k_sb_merge, dim3(gx, B), dim3(256), 0, st, L, s_top, m0, p->d_r, p->d_sb_r2)) != cudaSuccess)
+      if ((e = launch_pdl(k_sb_merge, dim3(gx, B), dim3(256), 0, st, L, s_top, m0, Rb, R2b)) != cudaSuccess)
         return e;
       p->launches++;
     }
     if (last && ps_top >= 0) {  // the short-ring corrections of every block above
       if ((e = launch_pdl(k_sb_combine, dim3((272 * B + 7) / 8), dim3(256), 0, st, L, B, (const double2*)p->d_sb_g,
-                          p->d_r)) != cudaSuccess)
+                          Rb)) != cudaSuccess)
         return e;
       p->launches++;
     }
     if (nb > 1) {
       if ((e = launch_pdl(k_cpl, dim3(1, (B + 7) / 8, nb), dim3(SB_THREADS), smem_cpl, st, L, s_top, m0, B,
-                          (const double*)p->d_ut, (const int64_t*)p->d_ut_off, (const double*)p->d_w, p->d_r,
-                          p->d_sb_r2, p->d_sb_x, p->d_sb_a, flm)) != cudaSuccess)
+                          (const double*)p->d_ut, (const int64_t*)p->d_ut_off, (const double*)p->d_w, Rb,
+                          R2b, p->d_sb_x, p->d_sb_a, flm)) != cudaSuccess)
         return e;
       if (last)
         e = launch_pdl(k_sb_chain<32>, dim3((B + 1) / 2), dim3(SB_THREADS), chain_smem(32), st, L, s_top, m0, B,
-                       (const double*)p->d_ut, (const int64_t*)p->d_ut_off, (const double2*)p->d_sb_a, p->d_r);
+                       (const double*)p->d_ut, (const int64_t*)p->d_ut_off, (const double2*)p->d_sb_a, Rb);
       else
         e = launch_pdl(k_sb_chain<16>, dim3((B + 3) / 4), dim3(SB_THREADS), chain_smem(16), st, L, s_top, m0, B,
-                       (const double*)p->d_ut, (const int64_t*)p->d_ut_off, (const double2*)p->d_sb_a, p->d_r);
+                       (const double*)p->d_ut, (const int64_t*)p->d_ut_off, (const double2*)p->d_sb_a, Rb);
       if (e != cudaSuccess) return e;
       p->launches += 2;
     }
     if (last) {  // order 0: fold the - slot (bin-0 -tone corrections) into the + slot
-      if ((e = launch_pdl(k_sb_fold_order0, dim3((L + 127) / 128, B), dim3(128), 0, st, L, p->d_r)) != cudaSuccess)
+      if ((e = launch_pdl(k_sb_fold_order0, dim3((L + 127) / 128, B), dim3(128), 0, st, L, Rb)) != cudaSuccess)
         return e;
       p->launches++;
     }
     if ((e = launch_pdl(k_solve, dim3((L - m0 + TM - 1) / TM, ny, nb), dim3(SB_THREADS), smem, st, L, s_top, m0, B,
-                        (const double*)p->d_xt, (const int64_t*)p->d_xt_off, (const double*)p->d_w, p->d_r,
-                        p->d_sb_r2, p->d_sb_x, p->d_sb_g, flm)) != cudaSuccess)
+                        (const double*)p->d_xt, (const int64_t*)p->d_xt_off, (const double*)p->d_w, Rb,
+                        R2b, p->d_sb_x, p->d_sb_g, flm)) != cudaSuccess)
       return e;
     p->launches++;
     if (!last) {  // the final block's corrections all land inside the block
       if ((e = launch_pdl(k_corr, dim3((s_top + TM - 1) / TM, ny, nb), dim3(SB_THREADS), smem, st, L, s_top, m0, B,
-                          (const double*)p->d_pbelow, (const int64_t*)p->d_pb_off, (const double*)p->d_w, p->d_r,
-                          p->d_sb_r2, p->d_sb_x, p->d_sb_g + (int64_t)blk * SB_B * (SB_B / 2) * B * 2, flm)) !=
+                          (const double*)p->d_pbelow, (const int64_t*)p->d_pb_off, (const double*)p->d_w, Rb,
+                          R2b, p->d_sb_x, p->d_sb_g + (int64_t)blk * SB_B * (SB_B / 2) * B * 2, flm)) !=
           cudaSuccess)
         return e;
       p->launches++;
@@ -561,12 +564,12 @@ static cudaError_t sweep_blocked_run(osph_plan* p, int B, double2* flm) {
 
 // CTA tile shapes (OSPH_SB_TILE=rows x maps): 64x4 as the per-order GEMM sweep, 64x8 halves
 // the L2 reads of the A operands.
-cudaError_t launch_sweep_blocked(osph_plan* p, int B, double2* flm) {
+cudaError_t launch_sweep_blocked(osph_plan* p, int B, double2* flm, int b0) {
   static const int tile = getenv("OSPH_SB_TILE") ? atoi(getenv("OSPH_SB_TILE")) : 0;
   static const int small_b = getenv("OSPH_SB_SMALL") ? atoi(getenv("OSPH_SB_SMALL")) : 8;  // 64 x 4-map tiles up to this batch (10-20% faster there)
-  if (tile == 1 || (tile == 0 && B <= small_b)) return sweep_blocked_run<4, 64, 4>(p, B, flm);
-  if (tile == 2) return sweep_blocked_run<3, 128, 8>(p, B, flm);
-  if (tile == 3) return sweep_blocked_run<3, 128, 16>(p, B, flm);
-  if (tile == 4) return sweep_blocked_run<4, 64, 16>(p, B, flm);
-  return sweep_blocked_run<4, 64, 8>(p, B, flm);
+  if (tile == 1 || (tile == 0 && B <= small_b)) return sweep_blocked_run<4, 64, 4>(p, B, flm, b0);
+  if (tile == 2) return sweep_blocked_run<3, 128, 8>(p, B, flm, b0);
+  if (tile == 3) return sweep_blocked_run<3, 128, 16>(p, B, flm, b0);
+  if (tile == 4) return sweep_blocked_run<4, 64, 16>(p, B, flm, b0);
+  return sweep_blocked_run<4, 64, 8>(p, B, flm, b0);
 }
