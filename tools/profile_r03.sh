@@ -6,7 +6,7 @@
 mkdir -p gpurun_out
 M="--metrics sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_tensor_subpipe_dmma.sum"
 OSPH_FACTOR_SPLIT=0 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 4000 --csv \
-  --log-file gpurun_out/launches_r03_c2.csv python bench.py --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_l2.log 2>&1
+  --log-file gpurun_out/launches_r03_c2.csv python tools/fwd_once.py 256 64 2 > gpurun_out/ncu_l2.log 2>&1
 OSPH_FACTOR_SPLIT=0 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 4000 --csv \
   --log-file gpurun_out/launches_r03_c3.csv python tools/fwd_once.py 512 128 1 > gpurun_out/ncu_l3.log 2>&1
 cap() {  # name regex skip L B N
