@@ -1,5 +1,5 @@
-// sweep_block.cu -- the order-peeling sweep for batches, peeled a BLOCK of
-// orders at a time.
+// sweep_block.cu -- the order-peeling sweep, peeled a BLOCK of orders at a time
+// (the default at L <= 512, for every batch size).
 //
 // Reference recurrence (pkg/src/optisph/transform.py:441-463): for
 // s = L-1 .. 0 solve order s, then subtract its aliases from every ring k < s.
@@ -16,17 +16,27 @@
 // g_s the right-hand side corrected by every order ABOVE the block and d_s the
 // in-block corrections it has received -- a scalar recurrence over the block
 // (k_sb_chain) that needs only the small products a_s = U_s g_s.  A block is
-//   1. a_s = U_s g_s                 one GEMM launch over every order of the block
-//   2. the scalar recurrence; R[s][j] -= d_s[j]
-//   3. x_s = X_s g~_s                one GEMM launch (-> flm and the block's x buffer)
-//   4. G_s = Pb_s x_s, rings k < s   one GEMM launch (-> the block's correction buffer)
-//   5. R[target] -= G                one thread per (ring, map), sources in a fixed order
+//   1. a_s = U_s g_s                 k_sb_gemm<2>, one launch over every order of the block
+//                                    (it also merges the pending R2 into R, see below)
+//   2. the scalar recurrence; R[s][j] -= d_s[j]                        k_sb_chain
+//   3. x_s = X_s g~_s                k_sb_gemm<0>, one launch (-> flm and the block's x buffer)
+//   4. G_s = Pb_s x_s, rings k < s   k_sb_gemm<1>, one launch, reduced straight into the
+//                                    right-hand sides of the orders below the block
 // instead of two launches per order: the L sequential steps of the reference
 // loop become L/32 block steps of whole-GPU fp64 tensor-core GEMMs
-// (mma.sync m8n8k4 -> DMMA.8x8x4).  Step 5 applies the corrections of a block
-// without atomics, in a fixed order per target: bitwise reproducible.  The
-// final block (orders < 32) keeps every ring below each order in U_s, so all of
-// its aliases (any tm, including bin 0) are resolved by the recurrence.
+// (mma.sync m8n8k4 -> DMMA.8x8x4).
+//
+// Bitwise reproducibility.  Inside one launch of step 4 (32 consecutive orders)
+// two corrections can meet in one bin of a ring k >= 16 only as a same-tone /
+// opposite-tone pair (s' = -s mod 2k+1, since 2k+1 > 32).  The same-tone branch
+// reduces into R, the opposite-tone branch into a second array R2 that the
+// next visit of those rows adds in: every address takes at most one reduction
+// per launch and launches are ordered.  The short rings k < 16 (where several
+// sources can meet) are written out and gathered per target in a fixed order
+// by k_sb_combine before the final block, where all of their targets live.
+//
+// The final block (orders < 32) keeps every ring below each order in U_s, so
+// all of its aliases (any tm, including bin 0) are resolved by the recurrence.
 // Blocks start at multiples of 32, so a block with m0 >= 32 has no in-block
 // alias other than the principal one (the next alias of order m is >= 3m+1).
 #include <algorithm>
