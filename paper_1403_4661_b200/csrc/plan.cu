@@ -453,9 +453,49 @@ static dim3 pair_grid(int pairs, int64_t n) {
   return dim3((unsigned)std::min<int64_t>((n + 255) / 256, 1184), (unsigned)pairs);
 }
 
+// Host buffers, real maps: the batch goes through in chunks of whole pairs -- chunk c's
+// H2D copy (s_in), pairing + transform + unpairing (plan stream) and D2H copy (s_out) are
+// chained by events, so the copies of neighbouring chunks overlap the kernels in both
+// directions (the copies, 2 x 16 B L^2 per real map and direction, bound this path).
+static int inverse_real_host_chunked(osph_plan* p, int B, const void* flm, void* samples) {
+  const int L = p->L;
+  const int64_t n = (int64_t)L * L;
+  cudaStream_t st = p->stream;
+  const int npairs = (B + 1) / 2, nch = std::min(npairs, osph_plan::kIoChunks);
+  CUDA_TRY(cudaEventRecord(p->ev_start, st));
+  CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
+  CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->ev_start, 0));
+  for (int c = 0; c < nch; ++c) {
+    const int q0 = (int)((int64_t)npairs * c / nch), q1 = (int)((int64_t)npairs * (c + 1) / nch);  // pairs
+    const int b0 = 2 * q0, b1 = std::min(B, 2 * q1), bc = b1 - b0, qc = q1 - q0;
+    const size_t off = (size_t)b0 * n, zoff = (size_t)q0 * n, cb = sizeof(double2) * (size_t)bc * n;
+    CUDA_TRY(cudaMemcpyAsync(p->d_in + off, (const double2*)flm + off, cb, cudaMemcpyHostToDevice, p->s_in));
+    CUDA_TRY(cudaEventRecord(p->ev_in[c], p->s_in));
+    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_in[c], 0));
+    k_pair_flm<<<pair_grid(qc, n), 256, 0, st>>>(bc, n, p->d_in + off, p->d_z1 + zoff);
+    if (c == 0) CUDA_TRY(cudaEventRecord(p->ev[0], st));
+    CUDA_TRY(launch_pack(p, qc, p->d_z1 + zoff));
+    if (c == 0) CUDA_TRY(cudaEventRecord(p->ev[1], st));
+    CUDA_TRY(launch_synth(p, qc));
+    if (c == 0) CUDA_TRY(cudaEventRecord(p->ev[2], st));
+    CUDA_TRY(launch_ring_inverse(p, qc, p->d_z2 + zoff));
+    k_unpair_samples<<<pair_grid(qc, n), 256, 0, st>>>(bc, n, p->d_z2 + zoff, p->d_out + off);
+    CUDA_TRY(cudaGetLastError());
+    p->launches += 2;
+    CUDA_TRY(cudaEventRecord(p->ev_done[c], st));
+    CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->ev_done[c], 0));
+    CUDA_TRY(cudaMemcpyAsync((double2*)samples + off, p->d_out + off, cb, cudaMemcpyDeviceToHost, p->s_out));
+  }
+  CUDA_TRY(cudaEventRecord(p->ev[3], st));
+  CUDA_TRY(cudaEventRecord(p->ev_out, p->s_out));
+  CUDA_TRY(cudaStreamWaitEvent(st, p->ev_out, 0));  // the plan stream covers the whole call
+  return OSPH_OK;
+}
+
 static int inverse_real(osph_plan* p, int B, const void* flm, void* samples, bool host) {
   int rc;
   if ((rc = ensure_real(p))) return rc;
+  if (host && p->own_k_lo == 0 && p->own_k_hi == p->L) return inverse_real_host_chunked(p, B, flm, samples);
   const int L = p->L, Bp = (B + 1) / 2;
   const int64_t n = (int64_t)L * L;
   const size_t bytes = sizeof(double2) * (size_t)B * n;
@@ -482,9 +522,69 @@ static int inverse_real(osph_plan* p, int B, const void* flm, void* samples, boo
   return OSPH_OK;
 }
 
+// Host buffers, real maps, blocked sweep: chunks of whole pairs are copied in (s_in) while the
+// factorisation runs; each chunk is paired and ring-transformed as it lands; the batch is
+// swept, unpaired and copied out (s_out) in two halves, so the first half's coefficients cross
+// PCIe while the second half is swept.
+static int forward_real_host_chunked(osph_plan* p, int B, const void* samples, void* flm) {
+  const int L = p->L;
+  const int64_t n = (int64_t)L * L;
+  cudaStream_t st = p->stream;
+  const int npairs = (B + 1) / 2, nch = osph_plan::kIoChunks;
+  CUDA_TRY(cudaEventRecord(p->ev_start, st));
+  CUDA_TRY(cudaStreamWaitEvent(p->s_in, p->ev_start, 0));
+  CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->ev_start, 0));
+  for (int c = 0; c < nch; ++c) {
+    const int q0 = (int)((int64_t)npairs * c / nch), q1 = (int)((int64_t)npairs * (c + 1) / nch);
+    const int b0 = 2 * q0, b1 = std::min(B, 2 * q1);
+    const size_t off = (size_t)b0 * n, cb = sizeof(double2) * (size_t)(b1 - b0) * n;
+    CUDA_TRY(cudaMemcpyAsync(p->d_in + off, (const double2*)samples + off, cb, cudaMemcpyHostToDevice, p->s_in));
+    CUDA_TRY(cudaEventRecord(p->ev_in[c], p->s_in));
+  }
+  CUDA_TRY(cudaEventRecord(p->ev[6], st));
+  CUDA_TRY(launch_factor(p, st));
+  CUDA_TRY(cudaEventRecord(p->ev[7], st));
+  for (int c = 0; c < nch; ++c) {
+    const int q0 = (int)((int64_t)npairs * c / nch), q1 = (int)((int64_t)npairs * (c + 1) / nch);
+    const int b0 = 2 * q0, b1 = std::min(B, 2 * q1), bc = b1 - b0, qc = q1 - q0;
+    const size_t off = (size_t)b0 * n, zoff = (size_t)q0 * n;
+    CUDA_TRY(cudaStreamWaitEvent(st, p->ev_in[c], 0));
+    k_pair_samples<<<pair_grid(qc, n), 256, 0, st>>>(bc, n, p->d_in + off, p->d_z1 + zoff);
+    p->launches++;
+    if (c == 0) CUDA_TRY(cudaEventRecord(p->ev[4], st));
+    CUDA_TRY(launch_ring_forward(p, npairs, p->d_z1, q0, qc));
+    if (c == nch / 2 - 1 || c == nch - 1) {
+      const int h = c == nch - 1;
+      const int hq0 = h ? (int)((int64_t)npairs * (nch / 2) / nch) : 0, hq1 = h ? npairs : (int)((int64_t)npairs * (nch / 2) / nch);
+      const int hb0 = 2 * hq0, hb1 = std::min(B, 2 * hq1);
+      const size_t hoff = (size_t)hb0 * n, hz = (size_t)hq0 * n, hbytes = sizeof(double2) * (size_t)(hb1 - hb0) * n;
+      if (h == 0) CUDA_TRY(cudaEventRecord(p->ev[8], st));
+      CUDA_TRY(launch_sweep_blocked(p, hq1 - hq0, p->d_z2 + hz, hq0));
+      k_unpair_flm<<<pair_grid(hq1 - hq0, n), 256, 0, st>>>(hb1 - hb0, L, p->d_z2 + hz, p->d_out + hoff);
+      CUDA_TRY(cudaGetLastError());
+      p->launches++;
+      CUDA_TRY(cudaEventRecord(p->ev_done[h], st));
+      CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->ev_done[h], 0));
+      CUDA_TRY(cudaMemcpyAsync((double2*)flm + hoff, p->d_out + hoff, hbytes, cudaMemcpyDeviceToHost, p->s_out));
+    }
+  }
+  CUDA_TRY(cudaEventRecord(p->ev[5], st));
+  p->last_sweep_kind = OSPH_SWEEP_BLOCKED;
+  CUDA_TRY(cudaEventRecord(p->ev[9], st));
+  CUDA_TRY(cudaEventRecord(p->ev_sweep_done, st));
+  p->have_sweep_ev = true;
+  CUDA_TRY(cudaEventRecord(p->ev_out, p->s_out));
+  CUDA_TRY(cudaStreamWaitEvent(st, p->ev_out, 0));
+  return OSPH_OK;
+}
+
 static int forward_real(osph_plan* p, int B, const void* samples, void* flm, bool host) {
   int rc;
   if ((rc = ensure_real(p))) return rc;
+  if (host && !p->windowed && (B + 1) / 2 >= 4 * osph_plan::kIoChunks) {
+    sweep_maps_per_team(p, (B + 1) / 2);  // decides the sweep (and the layout of the spectra)
+    if (p->sweep_blocked && !ensure_sweep_blocked(p)) return forward_real_host_chunked(p, B, samples, flm);
+  }
   const int L = p->L, Bp = (B + 1) / 2;
   const int64_t n = (int64_t)L * L;
   const size_t bytes = sizeof(double2) * (size_t)B * n;
