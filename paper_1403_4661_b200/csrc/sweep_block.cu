@@ -347,29 +347,30 @@ __global__ void __launch_bounds__(SB_THREADS) k_sb_chain(int L, int s_top, int m
     }
     group_sync();  // delta of the next order complete
   }
-  // apply R[s][j] -= delta_s[j]: independent read-modify-writes, eight in flight per thread
+  // apply R[s][j] -= delta_s[j]: independent read-modify-writes, sixteen in flight per thread.
+  // Thread rl owns entry j = rl of every order; in a block above the final one order z can
+  // only have received corrections in entries j <= (z - 1) / 2.
   if (b < B) {
-    const int total = nb * JR;
-    for (int i0 = rl; i0 < total; i0 += 8 * JR) {
-      double* rp[8];
-      double d[8], v[8];
+    const int z_lo = JR == SB_B / 2 ? 2 * rl + 1 : 0;
+    for (int z0 = z_lo; z0 < nb; z0 += 16) {
+      int64_t ri[16];
+      double d[16], v[16];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int i = i0 + q * JR;
-        rp[q] = nullptr;
+      for (int q = 0; q < 16; ++q) {
+        const int z = z0 + q, m = s_top - z;
+        ri[q] = -1;
         d[q] = 0.0;
-        if (i < total) {
-          const int z = i / JR, j = i - z * JR, m = s_top - z;
-          d[q] = delta[(size_t)i * 4 + c4];
-          if (j < L - m && d[q] != 0.0)
-            rp[q] = reinterpret_cast<double*>(R + ((int64_t)b * npos + packed_pos(L, m, j)) * 2 + slot) + comp;
+        if (z < nb && rl < L - m) {
+          d[q] = delta[((size_t)z * JR + rl) * 4 + c4];
+          if (d[q] != 0.0) ri[q] = (((int64_t)b * npos + packed_pos(L, m, rl)) * 2 + slot) * 2 + comp;
         }
       }
+      double* Rd = reinterpret_cast<double*>(R);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = rp[q] ? __ldcg(rp[q]) : 0.0;
+      for (int q = 0; q < 16; ++q) v[q] = ri[q] >= 0 ? __ldcg(Rd + ri[q]) : 0.0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (rp[q]) *rp[q] = v[q] - d[q];
+      for (int q = 0; q < 16; ++q)
+        if (ri[q] >= 0) Rd[ri[q]] = v[q] - d[q];
     }
   }
 }
