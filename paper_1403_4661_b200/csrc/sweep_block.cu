@@ -573,14 +573,11 @@ static cudaError_t sweep_blocked_run(osph_plan* p, int B, double2* flm, int b0) 
   return cudaGetLastError();
 }
 
-// CTA tile shapes (OSPH_SB_TILE=rows x maps): 64x4 as the per-order GEMM sweep, 64x8 halves
-// the L2 reads of the A operands.
+// CTA tile: 64 rows x 8 maps; 64 x 4 maps for small batches (10-20% faster up to B = 8;
+// OSPH_SB_SMALL=b moves the threshold).  Measured and removed: 128 x 8, 128 x 16 and 64 x 16
+// maps (config 2 sweep 0.85 / 0.79 / 0.79 vs 0.71 ms at the time; DESIGN 12).
 cudaError_t launch_sweep_blocked(osph_plan* p, int B, double2* flm, int b0) {
-  static const int tile = getenv("OSPH_SB_TILE") ? atoi(getenv("OSPH_SB_TILE")) : 0;
-  static const int small_b = getenv("OSPH_SB_SMALL") ? atoi(getenv("OSPH_SB_SMALL")) : 8;  // 64 x 4-map tiles up to this batch (10-20% faster there)
-  if (tile == 1 || (tile == 0 && B <= small_b)) return sweep_blocked_run<4, 64, 4>(p, B, flm, b0);
-  if (tile == 2) return sweep_blocked_run<3, 128, 8>(p, B, flm, b0);
-  if (tile == 3) return sweep_blocked_run<3, 128, 16>(p, B, flm, b0);
-  if (tile == 4) return sweep_blocked_run<4, 64, 16>(p, B, flm, b0);
+  static const int small_b = getenv("OSPH_SB_SMALL") ? atoi(getenv("OSPH_SB_SMALL")) : 8;
+  if (B <= small_b) return sweep_blocked_run<4, 64, 4>(p, B, flm, b0);
   return sweep_blocked_run<4, 64, 8>(p, B, flm, b0);
 }

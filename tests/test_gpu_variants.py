@@ -3,7 +3,8 @@
 The breadth-first update runs on 64 x 64 or 128 x 64 tiles (chosen by L,
 forced by OSPH_BF_UPD_ROWS), and the next step's R panel is either handed
 off by the panel and update kernels or copied by its own launch
-(OSPH_BF_RFUSE=0).  Every variant performs the same DMMA chain per element,
+(OSPH_BF_RFUSE=0); the orders are factored as one chain or as several
+ranges on their own streams (OSPH_FACTOR_SPLIT).  Every variant performs the same DMMA chain per element,
 so the forward output must not change by a single bit.  The switches are
 read once per process, so each variant runs in a subprocess; the default
 result is also checked against the round-trip bar of the other parity tests.
@@ -35,7 +36,9 @@ np.savez(out, flm=flm, rt_err=np.abs(rt - flm).max())
 """
 
 VARIANTS = [{}, {"OSPH_BF_UPD_ROWS": "64"}, {"OSPH_BF_UPD_ROWS": "128"}, {"OSPH_BF_RFUSE": "0"},
-            {"OSPH_BF_UPD_ROWS": "128", "OSPH_BF_RFUSE": "0"}]
+            {"OSPH_BF_UPD_ROWS": "128", "OSPH_BF_RFUSE": "0"},
+            # the factorisation as one chain / four order ranges on their own streams (default three)
+            {"OSPH_FACTOR_SPLIT": "0"}, {"OSPH_FACTOR_SPLIT": "4"}]
 
 
 def run_variant(tmp_path, L, B, env_extra, tag):
