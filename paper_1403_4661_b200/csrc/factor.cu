@@ -79,13 +79,16 @@ cudaError_t launch_factor(osph_plan* p, cudaStream_t st) {
     }
     const int n = p->n_frng;
     const BfOffsets o{p->d_ainv_off, p->d_xt_off, p->d_pb_off, p->d_bf_off};
+    // Enqueue the longest chain first (the lowest orders: most panel steps): the host needs a few
+    // microseconds per launch, and every range queued ahead of it would delay the chain the
+    // sweep waits for last.
     if ((e = cudaEventRecord(p->ev_fstart, st)) != cudaSuccess) return e;
-    for (int r = 0; r < n - 1; ++r) {
+    if ((e = bf_run(p, p->bf_rng[n - 1], st, o)) != cudaSuccess) return e;
+    for (int r = n - 2; r >= 0; --r) {
       if ((e = cudaStreamWaitEvent(p->s_f[r], p->ev_fstart, 0)) != cudaSuccess) return e;
       if ((e = bf_run(p, p->bf_rng[r], p->s_f[r], o)) != cudaSuccess) return e;
       if ((e = cudaEventRecord(p->ev_f[r], p->s_f[r])) != cudaSuccess) return e;
     }
-    if ((e = bf_run(p, p->bf_rng[n - 1], st, o)) != cudaSuccess) return e;
     for (int r = 0; r < n - 1; ++r)
       if ((e = cudaStreamWaitEvent(st, p->ev_f[r], 0)) != cudaSuccess) return e;
     p->fsplit_active = true;
